@@ -1,0 +1,232 @@
+/*
+ * cacheprune.h -- C-ABI of the B200-native CachePrune hot path (arxiv 2605.23640).
+ *
+ * The library implements token-granular, privacy-masked KV reuse:
+ *   cp_index_insert     -- store reusable segments in the shared KV pool
+ *                          (§4.3.5 KV Pool: storage format, dedup, LRU;
+ *                           L403-405 §3.3 selective sharing: a masked token is never stored)
+ *   cp_match_spans      -- find stored segments inside incoming prompts
+ *                          (§4.2.2 C2: rolling-hash prefix filter + verification;
+ *                           L724-727 §4.3.1: plan with zero placeholders)
+ *   cp_gather_rerotate  -- copy the matched K/V rows into the request's paged KV cache and re-rotate
+ *                          moved keys by the RoPE position delta (placement: PAPER.md L518, L726,
+ *                          L781; RoPE: the paper is silent -- DESIGN.md readings R#11-14)
+ *   cp_score_deviation  -- per-token inter-minus-intra attention score and top-rho selection of the
+ *                          tokens to recompute (§4.2.1 C1 Step 3; rho = 25%, L1032)
+ *
+ * Conventions (all calls):
+ *   - Pointers are DEVICE pointers unless the name ends in _h (host).  The caller owns every buffer,
+ *     including the workspaces handed to cp_index_create; the library never allocates device memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *     asynchronous on that stream; outputs are valid once the stream reaches them.  All calls on one
+ *     index must be ordered by the caller (single writer, multiple readers: SPEC.md L351, L423).
+ *   - Errors: argument errors detectable on the host return a negative cp_status synchronously with
+ *     no side effects.  Errors detectable only on the device (a sensitive token inside an insert
+ *     span, a request longer than the configured maximum, a full candidate buffer) are written to a
+ *     sticky device error word; while it is set every later kernel of every call on that index is a
+ *     no-op, and the insert that raised it changed nothing.  cp_index_last_error() synchronizes,
+ *     returns and clears it.
+ *   - Positions are 0-based.  Token ids are int32 >= 0.  Masks are uint8 (1 = sensitive).
+ *   - Hashing: p = 2^61-1, base B = 2 + splitmix64(hash_seed) mod (p-3) ("random base";
+ *     DESIGN.md R#1), tokenval = id + 1 (R#2).  Use the same hash_seed on every rank.
+ */
+#ifndef CACHEPRUNE_H
+#define CACHEPRUNE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CP_OK = 0,
+    CP_ERR_INVALID_ARG = -1,     /* bad argument (host) or bad span range (device)             */
+    CP_ERR_SENSITIVE_SPAN = -2,  /* an insert span covers a mask-1 token         */
+    CP_ERR_SPAN_TOO_SHORT = -3,  /* an insert span is shorter than window_len    */
+    CP_ERR_CAPACITY = -4,        /* span longer than the budget / max_span_len, buffers full  */
+    CP_ERR_CUDA = -5,            /* a CUDA runtime call failed                                  */
+    CP_ERR_UNSUPPORTED = -6      /* configuration or mode not built (e.g. CP_SCORE_KVDEV)      */
+} cp_status;
+
+enum { CP_FP32 = 0, CP_BF16 = 1 };                 /* KV storage dtype                          */
+enum { CP_ROPE_NEOX = 0, CP_ROPE_GPTJ = 1 };       /* pairs (i, i+d/2) | (2i, 2i+1)  (R#12)      */
+enum { CP_MATCH_NO_TOUCH = 1 };                    /* cp_match_spans flags                       */
+enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2 }; /* cp_gather_rerotate flags (R#14)         */
+enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
+enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
+enum { CP_PLAN_UNCOVERED = 0, CP_PLAN_REUSED = 1, CP_PLAN_RECOMPUTE = 2 };              /* plan codes     */
+
+typedef struct cp_index cp_index;                  /* opaque host handle */
+
+/* Index configuration.  num_layers / num_kv_heads are THIS shard's geometry. */
+typedef struct {
+    int32_t  window_len;            /* prefix-filter window = minimum segment length, 128 */
+    int32_t  block_size;            /* tokens per page, pool and caller caches; must be 16 (R#23)       */
+    uint64_t hash_seed;             /* seeds the random hash base B                             */
+    int32_t  num_layers, num_kv_heads, head_dim;
+    int32_t  layer_offset, head_offset;   /* position of this shard (diagnostics only)                */
+    int32_t  dtype;                 /* CP_FP32 | CP_BF16                                                 */
+    int32_t  rope_style;            /* CP_ROPE_NEOX | CP_ROPE_GPTJ                                       */
+    double   rope_theta;            /* 500000 (Llama-3), 10000 (toy)                                     */
+    int64_t  pool_capacity_tokens;  /* LRU budget in tokens (R#21)                              */
+    int32_t  max_entries;           /* live-entry slots (>= capacity/window_len + max_spans_per_insert + 1) */
+    int32_t  max_span_len;          /* longest storable segment                                          */
+    int32_t  max_req_tokens;        /* longest request accepted by cp_match_spans (<= 10240)             */
+    int32_t  max_batch_reqs;        /* most requests per match / insert call                             */
+    int64_t  max_batch_tokens;      /* most tokens per match / insert call                               */
+    int32_t  max_spans_per_insert;  /* most spans per insert call                                        */
+} cp_config;
+
+enum { CP_WS_POOL_K = 0, CP_WS_POOL_V = 1, CP_WS_META = 2, CP_WS_SCRATCH = 3, CP_WS_COUNT = 4 };
+
+/* Fill sizes_h[CP_WS_COUNT] with the byte size of each workspace the caller must allocate
+ * (device memory, 256-byte aligned).  Pool K/V layout: [num_layers][num_pages][16][H][d] dtype. */
+cp_status cp_index_workspace(const cp_config* cfg_h, size_t* sizes_h);
+
+/* Physical pool pages for cfg: ceil((capacity + max_span_len)/16) + ceil(capacity/window_len) + 1,
+ * enough that the token budget, not the page count, always decides eviction. */
+int64_t cp_pool_num_pages(const cp_config* cfg_h);
+int32_t cp_max_pages_per_entry(const cp_config* cfg_h);
+
+/* Create an empty index inside caller-allocated workspaces ws_h[CP_WS_COUNT] (device pointers).
+ * Initializes the free-page FIFO to ascending page ids and an empty hash table on `stream`. */
+cp_status cp_index_create(const cp_config* cfg_h, void* const* ws_h, void* stream, cp_index** out_h);
+cp_status cp_index_destroy(cp_index* idx);
+
+/* A CSR batch of requests. */
+typedef struct {
+    int32_t        num_reqs;
+    int64_t        total_tokens;
+    const int32_t* tokens;          /* [total_tokens]                                                 */
+    const int64_t* offsets;         /* [num_reqs + 1], offsets[0] = 0                                 */
+    const uint8_t* mask;            /* [total_tokens] 1 = sensitive; NULL allowed for match (R#9)    */
+    int32_t        max_req_len;     /* host hint: longest request in the batch (0 = cfg max)         */
+} cp_batch;
+
+/* A paged KV cache in vLLM NHD layout: per layer a K and a V tensor [num_blocks][16][H][d]. */
+typedef struct {
+    void* const*   k_layers_h;      /* host array [num_layers] of device pointers                    */
+    void* const*   v_layers_h;
+    const int32_t* block_tables;    /* [num_reqs][max_blocks_per_req] block ids                      */
+    int32_t        max_blocks_per_req;
+} cp_paged_kv;
+
+/*
+ * Insert `num_spans` segments (request span_req[s], positions [span_begin[s], +span_len[s])) of
+ * the writer batch, in input order, at logical time `logical_time`.  Per span: DUPLICATE (an equal
+ * live segment exists: refresh its last_used), else DROPPED_CONTAINED (a live segment strictly
+ * contains it), else stored -- removing every live segment it strictly contains (SUPERSEDED) --
+ * on pages taken from the FIFO head, with its K/V rows copied from writer_kv unrotated; then LRU
+ * eviction by (last_used, id) while live tokens exceed the budget (R#20-22).
+ * recompute_bits: packed LSB-first per span starting at word bits_word_offsets[s] (device arrays;
+ * NULL = no recompute marks).  out_entry_id[s]: the stored / duplicate / containing entry id.
+ * Device errors (no side effects): CP_ERR_INVALID_ARG (range), CP_ERR_SPAN_TOO_SHORT,
+ * CP_ERR_CAPACITY (len > budget or > max_span_len), CP_ERR_SENSITIVE_SPAN -- the first failing
+ * span in input order decides the code.
+ */
+cp_status cp_index_insert(cp_index* idx, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
+                          int32_t num_spans, const int32_t* span_req, const int32_t* span_begin,
+                          const int32_t* span_len, const uint32_t* recompute_bits,
+                          const int64_t* bits_word_offsets, uint64_t logical_time,
+                          int32_t* out_entry_id, int32_t* out_outcome, void* stream);
+
+/* Outputs of cp_match_spans (all device buffers owned by the caller). */
+typedef struct {
+    int32_t  max_hits;              /* capacity; must be >= sum_r floor(n_r / window_len)            */
+    int32_t* num_hits;              /* [1]                                                            */
+    int32_t* req_hit_offsets;       /* [num_reqs + 1]                                                 */
+    int32_t* hit_req;               /* [max_hits] request index                                       */
+    int32_t* hit_entry;             /* [max_hits] entry id                                            */
+    int32_t* hit_slot;              /* [max_hits] pool slot of the entry (consumed by the gather)     */
+    int32_t* hit_dst;               /* [max_hits] first request position covered                     */
+    int32_t* hit_len;               /* [max_hits] entry length                                        */
+    int32_t* hit_delta;             /* [max_hits] RoPE delta = hit_dst - entry origin (R#11)          */
+    uint8_t* plan;                  /* [total_tokens] CP_PLAN_* per position                         */
+    int32_t* req_covered;           /* [num_reqs] positions covered by hits                           */
+    int32_t* req_recompute;         /* [num_reqs] covered positions marked for recompute              */
+    int32_t* req_candidates;        /* [num_reqs] prefix-filter candidates c                 */
+} cp_hits;
+
+/*
+ * Match every request against the index (a snapshot for the call): each (k, entry e) with
+ * request[k..k+m_e) equal to e's tokens (and, if a reader mask is given, no mask-1 position in the
+ * range) is a verified candidate; hits are assembled greedily left to right, longest first, then
+ * smaller id (R#7).  Accepted hits touch last_used[e] = max(last_used[e], logical_time) unless
+ * CP_MATCH_NO_TOUCH.  Device error: a request longer than cfg.max_req_tokens, or max_hits exceeded.
+ */
+cp_status cp_match_spans(cp_index* idx, const cp_batch* readers_h, uint64_t logical_time,
+                         int32_t flags, const cp_hits* out_h, void* stream);
+
+/*
+ * For every hit h and token t < hit_len[h] at request position q = hit_dst[h] + t, and every
+ * (layer, head) of the shard: V_dst[q] <- V_pool[e][t] (bit copy); K_dst[q] <- R(delta) K_pool[e][t]
+ * (fp32 products with cos/sin of delta*theta_i evaluated in fp64; delta == 0 is a bit copy).  With
+ * CP_ZERO_RECOMPUTE, plan-2 positions get +0.0 in K and V (zero placeholders); with
+ * CP_ZERO_UNCOVERED, plan-0 positions are zeroed too.  `hits` is the struct cp_match_spans wrote
+ * (only num_hits, hit_* and plan are read).  readers_h must be the batch that was matched.
+ */
+cp_status cp_gather_rerotate(cp_index* idx, const cp_batch* readers_h, const cp_hits* hits_h,
+                             const cp_paged_kv* dst_kv_h, int32_t flags, void* stream);
+
+/*
+ * Recompute scores and top-rho selection for `num_spans` spans.  Span s uses the
+ * final-layer attention attn_h[s] (device, fp32 [heads_h[s]][n_h[s]][n_h[s]] row-major), span
+ * [span_l_h[s], span_r_h[s]] (inclusive).  For i in the span, with q(x) = trunc(x * 2^40) (R#17):
+ *   score(i) = sum_heads ( sum_{j < l} q(A[i][j]) - sum_{l <= j <= i} q(A[i][j]) )
+ * out_scores (device int64) receives m_s scores from score_offsets_h[s]; out_bits (device uint32)
+ * receives ceil(m_s/32) words from bits_word_offsets_h[s]: the first ceil(rho_num*m/rho_den) tokens in
+ * (score desc, index asc) order get bit 1 (R#15-16).  max_m bounds m_s (<= 16384).
+ * mode CP_SCORE_KVDEV (CacheBlend deviation) returns CP_ERR_UNSUPPORTED in this build.
+ */
+cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, const int32_t* n_h,
+                             const int32_t* heads_h, const int32_t* span_l_h, const int32_t* span_r_h,
+                             int32_t rho_num, int32_t rho_den, int32_t mode, int32_t max_m,
+                             int64_t* out_scores, const int64_t* score_offsets_h,
+                             uint32_t* out_bits, const int64_t* bits_word_offsets_h, void* stream);
+
+/* ---- test / diagnostic exports ------------------------------------------------------------- */
+
+/* Prefix hashes of every request: out_h (device u64) gets n_r + 1 values per request starting at
+ * offsets[r] + r (h[0] = 0, h[k] = h[k-1]*B + tokenval(t_k) mod p). */
+cp_status cp_hash_prefix(const cp_batch* batch_h, uint64_t hash_seed, uint64_t* out_h, void* stream);
+
+/* Host copy of the live entries, sorted by id.  Arrays are caller-allocated HOST buffers with room
+ * for cfg.max_entries entries (pages: max_pages_per_entry each; tokens/recompute: max_span_len each;
+ * fifo: cp_pool_num_pages).  Optional arrays may be NULL.  Synchronizes the stream. */
+typedef struct {
+    int32_t   num_live;
+    int32_t   next_id;
+    int64_t   live_tokens;
+    int32_t   fifo_count;
+    int32_t   error;
+    int32_t*  id;
+    int32_t*  len;
+    int32_t*  origin_pos;
+    uint64_t* prefix_hash;
+    uint64_t* full_hash;
+    uint64_t* last_used;
+    uint8_t*  digest;               /* [32] per entry */
+    int32_t*  pages;                /* [max_pages_per_entry] per entry */
+    int32_t*  tokens;               /* [max_span_len] per entry, optional */
+    uint8_t*  recompute;            /* [max_span_len] per entry, optional */
+    int32_t*  fifo;                 /* free pages in pop order, optional */
+} cp_snapshot;
+cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
+
+/* Synchronizes, returns and clears the sticky device error word (CP_OK if none). */
+cp_status cp_index_last_error(cp_index* idx, void* stream);
+
+/* Hash base B of an index (diagnostic). */
+uint64_t cp_index_hash_base(const cp_index* idx);
+
+/* Number of kernels this library launched since load (evidence for gpu_launches). */
+uint64_t cp_kernel_launch_count(void);
+
+const char* cp_status_string(cp_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CACHEPRUNE_H */

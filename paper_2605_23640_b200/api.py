@@ -1,0 +1,283 @@
+"""Thin Python front-end over the C-ABI (include/cacheprune.h): argument marshalling only.
+
+Every step of the hot path runs in libcacheprune.so kernels; torch supplies
+device memory (workspaces, batches, paged caches) and streams.  Names follow
+the C-ABI: insert / match_spans / gather_rerotate / score_deviation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class IndexConfig:
+    num_layers: int
+    num_kv_heads: int
+    head_dim: int
+    dtype: str = "bf16"                  # "bf16" | "fp32"
+    rope_theta: float = 500000.0
+    rope_style: str = "neox"
+    window_len: int = 128
+    block_size: int = 16
+    hash_seed: int = 42
+    pool_capacity_tokens: int = 1 << 20
+    max_entries: int = 8192
+    max_span_len: int = 2048
+    max_req_tokens: int = 10240
+    max_batch_reqs: int = 1024
+    max_batch_tokens: int = 1 << 21
+    max_spans_per_insert: int = 4096
+    layer_offset: int = 0
+    head_offset: int = 0
+
+    def c(self) -> L.CpConfig:
+        return L.CpConfig(self.window_len, self.block_size, self.hash_seed, self.num_layers, self.num_kv_heads,
+                          self.head_dim, self.layer_offset, self.head_offset,
+                          L.CP_BF16 if self.dtype == "bf16" else L.CP_FP32,
+                          L.CP_ROPE_GPTJ if self.rope_style == "gptj" else L.CP_ROPE_NEOX,
+                          float(self.rope_theta), self.pool_capacity_tokens, self.max_entries, self.max_span_len,
+                          self.max_req_tokens, self.max_batch_reqs, self.max_batch_tokens, self.max_spans_per_insert)
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.dtype == "bf16" else torch.float32
+
+
+@dataclass
+class DeviceBatch:
+    tokens: torch.Tensor                  # int32 [T]
+    offsets: torch.Tensor                 # int64 [R+1]
+    mask: Optional[torch.Tensor]          # uint8 [T] or None
+    max_req_len: int = 0
+
+    @property
+    def num_reqs(self) -> int:
+        return int(self.offsets.numel() - 1)
+
+    @property
+    def total_tokens(self) -> int:
+        return int(self.tokens.numel())
+
+    def c(self, with_mask: bool = True) -> L.CpBatch:
+        return L.CpBatch(self.num_reqs, self.total_tokens, _ptr(self.tokens), _ptr(self.offsets),
+                         _ptr(self.mask) if (with_mask and self.mask is not None) else None, int(self.max_req_len))
+
+    @staticmethod
+    def from_numpy(tokens, offsets, mask, device="cuda", pin: bool = False) -> "DeviceBatch":
+        import numpy as np
+        lens = np.diff(offsets)
+        t = torch.from_numpy(np.ascontiguousarray(tokens, dtype=np.int32))
+        o = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
+        m = None if mask is None else torch.from_numpy(np.ascontiguousarray(mask, dtype=np.uint8))
+        return DeviceBatch(t.to(device), o.to(device), None if m is None else m.to(device),
+                           int(lens.max()) if len(lens) else 0)
+
+
+@dataclass
+class PagedKV:
+    k: List[torch.Tensor]                 # per layer [num_blocks, 16, H, d]
+    v: List[torch.Tensor]
+    block_tables: torch.Tensor            # int32 [R, max_blocks]
+    _keep: list = field(default_factory=list)
+
+    def c(self) -> L.CpPagedKV:
+        kp = (C.c_void_p * len(self.k))(*[t.data_ptr() for t in self.k])
+        vpp = (C.c_void_p * len(self.v))(*[t.data_ptr() for t in self.v])
+        self._keep = [kp, vpp]
+        return L.CpPagedKV(C.cast(kp, C.POINTER(C.c_void_p)), C.cast(vpp, C.POINTER(C.c_void_p)),
+                           _ptr(self.block_tables), int(self.block_tables.shape[1]))
+
+    @staticmethod
+    def allocate(num_layers, num_blocks, H, d, dtype, block_tables, device="cuda", zero=True) -> "PagedKV":
+        mk = torch.zeros if zero else torch.empty
+        k = [mk((num_blocks, 16, H, d), dtype=dtype, device=device) for _ in range(num_layers)]
+        v = [mk((num_blocks, 16, H, d), dtype=dtype, device=device) for _ in range(num_layers)]
+        return PagedKV(k, v, block_tables.to(device=device, dtype=torch.int32).contiguous())
+
+
+class Hits:
+    """Device output buffers of cp_match_spans."""
+
+    def __init__(self, max_hits: int, num_reqs: int, total_tokens: int, device="cuda"):
+        z = lambda n, dt=torch.int32: torch.zeros(max(int(n), 1), dtype=dt, device=device)
+        self.max_hits = int(max_hits)
+        self.num_hits = z(1)
+        self.req_hit_offsets = z(num_reqs + 1)
+        self.hit_req, self.hit_entry, self.hit_slot = z(max_hits), z(max_hits), z(max_hits)
+        self.hit_dst, self.hit_len, self.hit_delta = z(max_hits), z(max_hits), z(max_hits)
+        self.plan = z(total_tokens, torch.uint8)
+        self.req_covered, self.req_recompute, self.req_candidates = z(num_reqs), z(num_reqs), z(num_reqs)
+
+    def c(self) -> L.CpHits:
+        return L.CpHits(self.max_hits, *[_ptr(t) for t in (
+            self.num_hits, self.req_hit_offsets, self.hit_req, self.hit_entry, self.hit_slot, self.hit_dst,
+            self.hit_len, self.hit_delta, self.plan, self.req_covered, self.req_recompute, self.req_candidates)])
+
+    def to_host(self) -> dict:
+        n = int(self.num_hits.item())
+        out = {k: getattr(self, k)[:n].cpu().numpy() for k in
+               ("hit_req", "hit_entry", "hit_slot", "hit_dst", "hit_len", "hit_delta")}
+        out["num_hits"] = n
+        for k in ("req_hit_offsets", "plan", "req_covered", "req_recompute", "req_candidates"):
+            out[k] = getattr(self, k).cpu().numpy()
+        return out
+
+
+class KVIndex:
+    """A shared KV pool + its prefix index on one GPU (one shard of layers/heads)."""
+
+    def __init__(self, cfg: IndexConfig, device="cuda", stream=None):
+        self.cfg, self.device = cfg, torch.device(device)
+        self._c = cfg.c()
+        lib = L.lib()
+        sizes = (C.c_size_t * L.CP_WS_COUNT)()
+        L.check(lib.cp_index_workspace(C.byref(self._c), sizes), "cp_index_workspace")
+        self.ws_sizes = [int(s) for s in sizes]
+        # 256-B aligned byte workspaces (torch's caching allocator returns >= 512-B aligned blocks)
+        self.ws = [torch.empty(max(s, 256), dtype=torch.uint8, device=self.device) for s in self.ws_sizes]
+        ptrs = (C.c_void_p * L.CP_WS_COUNT)(*[t.data_ptr() for t in self.ws])
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(lib.cp_index_create(C.byref(self._c), ptrs, _stream(stream), C.byref(h)), "cp_index_create")
+        self.h = h
+        self.num_pages = int(lib.cp_pool_num_pages(C.byref(self._c)))
+        self.max_pages_per_entry = int(lib.cp_max_pages_per_entry(C.byref(self._c)))
+        self.B = int(lib.cp_index_hash_base(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                L.lib().cp_index_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # --- pool views (for tests / diagnostics) ---
+    def pool_views(self):
+        c = self.cfg
+        shape = (c.num_layers, self.num_pages, 16, c.num_kv_heads, c.head_dim)
+        n = 1
+        for s in shape:
+            n *= s
+        k = self.ws[0][: n * (4 if c.dtype == "fp32" else 2)].view(c.torch_dtype).view(shape)
+        v = self.ws[1][: n * (4 if c.dtype == "fp32" else 2)].view(c.torch_dtype).view(shape)
+        return k, v
+
+    def insert(self, writers: DeviceBatch, writer_kv: PagedKV, span_req, span_begin, span_len,
+               recompute_bits=None, bits_word_offsets=None, t: int = 0, stream=None):
+        S = int(span_req.numel())
+        out_id = torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device)
+        out_oc = torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device)
+        wb, kv = writers.c(), writer_kv.c()
+        rc = L.lib().cp_index_insert(self.h, C.byref(wb), C.byref(kv), S, _ptr(span_req), _ptr(span_begin),
+                                     _ptr(span_len), _ptr(recompute_bits), _ptr(bits_word_offsets), int(t),
+                                     _ptr(out_id), _ptr(out_oc), _stream(stream))
+        L.check(rc, "cp_index_insert")
+        return out_id[:S], out_oc[:S]
+
+    def match_spans(self, readers: DeviceBatch, t: int = 0, no_touch: bool = False, use_mask: bool = True,
+                    hits: Optional[Hits] = None, stream=None) -> Hits:
+        if hits is None:
+            hits = Hits(readers.total_tokens // self.cfg.window_len + readers.num_reqs + 1, readers.num_reqs,
+                        readers.total_tokens, self.device)
+        rb, hc = readers.c(use_mask), hits.c()
+        rc = L.lib().cp_match_spans(self.h, C.byref(rb), int(t), L.CP_MATCH_NO_TOUCH if no_touch else 0,
+                                    C.byref(hc), _stream(stream))
+        L.check(rc, "cp_match_spans")
+        return hits
+
+    def gather_rerotate(self, readers: DeviceBatch, hits: Hits, dst_kv: PagedKV,
+                        zero_recompute: bool = True, zero_uncovered: bool = False, stream=None):
+        flags = (L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0)
+        rb, hc, kv = readers.c(), hits.c(), dst_kv.c()
+        L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
+                "cp_gather_rerotate")
+
+    def last_error(self, stream=None) -> int:
+        return int(L.lib().cp_index_last_error(self.h, _stream(stream)))
+
+    def snapshot(self, with_tokens: bool = True, stream=None) -> dict:
+        import numpy as np
+        c = self.cfg
+        S, MP, ML = c.max_entries, self.max_pages_per_entry, c.max_span_len
+        arr = {
+            "id": np.zeros(S, np.int32), "len": np.zeros(S, np.int32), "origin_pos": np.zeros(S, np.int32),
+            "prefix_hash": np.zeros(S, np.uint64), "full_hash": np.zeros(S, np.uint64),
+            "last_used": np.zeros(S, np.uint64), "digest": np.zeros(S * 32, np.uint8),
+            "pages": np.zeros(S * MP, np.int32), "fifo": np.zeros(self.num_pages, np.int32),
+        }
+        if with_tokens:
+            arr["tokens"] = np.zeros(S * ML, np.int32)
+            arr["recompute"] = np.zeros(S * ML, np.uint8)
+        ptr = lambda k: arr[k].ctypes.data_as(C.c_void_p) if k in arr else None
+        snap = L.CpSnapshot(0, 0, 0, 0, 0, ptr("id"), ptr("len"), ptr("origin_pos"), ptr("prefix_hash"),
+                            ptr("full_hash"), ptr("last_used"), ptr("digest"), ptr("pages"), ptr("tokens"),
+                            ptr("recompute"), ptr("fifo"))
+        L.check(L.lib().cp_index_snapshot(self.h, C.byref(snap), _stream(stream)), "cp_index_snapshot")
+        n = snap.num_live
+        out = dict(num_live=n, next_id=snap.next_id, live_tokens=snap.live_tokens, fifo_count=snap.fifo_count,
+                   error=snap.error, fifo=arr["fifo"][:snap.fifo_count].copy(), entries=[])
+        for q in range(n):
+            ln = int(arr["len"][q])
+            e = dict(id=int(arr["id"][q]), len=ln, origin_pos=int(arr["origin_pos"][q]),
+                     prefix_hash=int(arr["prefix_hash"][q]), full_hash=int(arr["full_hash"][q]),
+                     last_used=int(arr["last_used"][q]), digest=arr["digest"][32 * q:32 * q + 32].tobytes(),
+                     pages=arr["pages"][q * MP:q * MP + (ln + 15) // 16].copy())
+            if with_tokens:
+                e["tokens"] = arr["tokens"][q * ML:q * ML + ln].copy()
+                e["recompute"] = arr["recompute"][q * ML:q * ML + ln].astype(bool)
+            out["entries"].append(e)
+        return out
+
+
+def score_deviation(attn: Sequence[torch.Tensor], n: Sequence[int], heads: Sequence[int], span_l: Sequence[int],
+                    span_r: Sequence[int], rho_num: int = 1, rho_den: int = 4, out_scores=None, out_bits=None,
+                    stream=None, mode: int = L.CP_SCORE_INTER_INTRA):
+    """Recompute scores + top-rho bits for spans (cp_score_deviation).  Returns (scores, bits,
+    score_offsets, bits_word_offsets); scores int64 concatenated, bits uint32 (as int32 storage)."""
+    S = len(span_l)
+    ms = [int(r) - int(l) + 1 for l, r in zip(span_l, span_r)]
+    so = [0]
+    bo = [0]
+    for m in ms:
+        so.append(so[-1] + m)
+        bo.append(bo[-1] + (m + 31) // 32)
+    dev = attn[0].device if S else torch.device("cuda")
+    if out_scores is None:
+        out_scores = torch.zeros(max(so[-1], 1), dtype=torch.int64, device=dev)
+    if out_bits is None:
+        out_bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=dev)
+    A = (C.c_void_p * max(S, 1))(*[a.data_ptr() for a in attn])
+    arr32 = lambda xs: (C.c_int32 * max(S, 1))(*[int(x) for x in xs])
+    arr64 = lambda xs: (C.c_int64 * max(len(xs), 1))(*[int(x) for x in xs])
+    rc = L.lib().cp_score_deviation(S, A, arr32(n), arr32(heads), arr32(span_l), arr32(span_r), rho_num, rho_den,
+                                    mode, max(ms) if ms else 1, _ptr(out_scores), arr64(so[:-1] or [0]),
+                                    _ptr(out_bits), arr64(bo[:-1] or [0]), _stream(stream))
+    L.check(rc, "cp_score_deviation")
+    return out_scores, out_bits, so, bo
+
+
+def hash_prefix(batch: DeviceBatch, hash_seed: int, stream=None) -> torch.Tensor:
+    out = torch.zeros(batch.total_tokens + batch.num_reqs, dtype=torch.int64, device=batch.tokens.device)
+    rb = batch.c(False)
+    L.check(L.lib().cp_hash_prefix(C.byref(rb), int(hash_seed), _ptr(out), _stream(stream)), "cp_hash_prefix")
+    return out
+
+
+def kernel_launch_count() -> int:
+    return int(L.lib().cp_kernel_launch_count())

@@ -1,0 +1,341 @@
+// cp_gather.cu -- N2 fused gather + RoPE re-rotation (placement: PAPER.md L518, L726-727, L781;
+// RoPE: DESIGN.md readings R#11-14, the paper never mentions position handling).
+//
+// Work list: a hit list (req, slot, dst, len, delta) is cut into chunks of CP_GATHER_CHUNK tokens by
+// k_rows_prep (block 0: scan + chunk list; every block: per-hit cos/sin table, angles in fp64).
+// k_rows: persistent grid, static round-robin over items (chunk, layer).  Per item, 32 threads
+// resolve the token rows (pool page via the entry's page list, destination block via the block
+// table, plan code), then the CTA streams the rows with 128-bit loads (ld.global.nc, L1 no-allocate)
+// and 128-bit streaming stores.  A "task" moves one 16-B vector of K at element i, its NeoX partner
+// at i + d/2, and the same two vectors of V; K is rotated in fp32 registers:
+//     K'[i] = K[i] c - K[i+d/2] s,   K'[i+d/2] = K[i+d/2] c + K[i] s,   (c, s) = (cos, sin)(delta theta_i)
+// V and delta == 0 rows are bit copies; recompute rows become +0.0 (zero placeholders).
+// dir 1 (insert copy-in) moves writer rows into pool pages unrotated with the same engine.
+#include "cp_internal.cuh"
+#include <algorithm>
+#include <cstring>
+
+namespace {
+
+constexpr int kRowsThreads = 256;
+constexpr int kUnroll = 4;
+constexpr int kPrepThreads = 512;
+
+struct RowsArgs {
+    DevHeader* hdr;
+    int dir;
+    const int32_t* count;
+    const int32_t *l_req, *l_slot, *l_dst, *l_len, *l_delta;
+    int64_t list_cap;
+    const int64_t* req_off; const uint8_t* plan;
+    const int32_t* block_tables; int32_t max_blocks;
+    char* paged_k[CP_MAX_LAYERS]; char* paged_v[CP_MAX_LAYERS];
+    char* pool_k; char* pool_v; int64_t P;
+    const int32_t* slot_pages; int32_t MP;
+    int32_t L, H, d; double theta; int32_t flags; int32_t gptj;
+    int32_t* chunk_hit; int32_t* chunk_t0; int64_t CH;
+    float2* hit_cs; int64_t cs_hits;
+};
+
+// block 0: chunk list; all blocks: cos/sin per (hit, pair index) in fp64 -> fp32
+__global__ void __launch_bounds__(kPrepThreads) k_rows_prep(RowsArgs a) {
+    __shared__ int s_scan[kPrepThreads / 32 + 1];
+    __shared__ int s_carry;
+    if (cp_err_set(a.hdr)) return;
+    const int nh = *a.count;
+    if (nh > a.list_cap || nh > a.cs_hits) { if (blockIdx.x == 0 && threadIdx.x == 0) cp_raise(a.hdr, CP_ERR_CAPACITY); return; }
+    const int half = a.d / 2;
+    if (a.dir == 0) {
+        const int64_t npairs = (int64_t)nh * half;
+        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npairs; q += (int64_t)gridDim.x * blockDim.x) {
+            const int hh = (int)(q / half), i = (int)(q % half);
+            const int delta = a.l_delta[hh];
+            if (delta == 0) continue;
+            const double th = pow(a.theta, -2.0 * (double)i / (double)a.d);
+            double s, c;
+            sincos((double)delta * th, &s, &c);
+            a.hit_cs[q] = make_float2((float)c, (float)s);
+        }
+    }
+    if (blockIdx.x != 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nh; b0 += kPrepThreads) {
+        const int hh = b0 + tid;
+        const int v = hh < nh ? (a.l_len[hh] + CP_GATHER_CHUNK - 1) / CP_GATHER_CHUNK : 0;
+        int inc = v;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_scan[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            int x = lane < kPrepThreads / 32 ? s_scan[lane] : 0, xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            if (lane < kPrepThreads / 32) s_scan[lane] = xi - x;
+            if (lane == 31) s_scan[kPrepThreads / 32] = xi;
+        }
+        __syncthreads();
+        const int start = s_carry + s_scan[wid] + inc - v;
+        if (start + v > a.CH) cp_raise(a.hdr, CP_ERR_CAPACITY);
+        else for (int c = 0; c < v; ++c) { a.chunk_hit[start + c] = hh; a.chunk_t0[start + c] = c * CP_GATHER_CHUNK; }
+        __syncthreads();
+        if (tid == 0) s_carry += s_scan[kPrepThreads / 32];
+        __syncthreads();
+    }
+    if (tid == 0) a.hdr->n_chunks = s_carry;
+}
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { static constexpr int N = 4; };
+template <> struct Vec<__nv_bfloat16> { static constexpr int N = 8; };
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ void unpack(const uint4& v, float* f, float) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y); f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+}
+__device__ __forceinline__ uint4 pack(const float* f, float) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+}
+__device__ __forceinline__ void unpack(const uint4& v, float* f, __nv_bfloat16) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { f[2 * i] = __uint_as_float(w[i] << 16); f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u); }
+}
+__device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);   // RNE
+        w[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename T, bool GPTJ>
+__global__ void __launch_bounds__(kRowsThreads) k_rows(RowsArgs a) {
+    constexpr int VEC = Vec<T>::N;
+    __shared__ int64_t s_src[CP_GATHER_CHUNK], s_dst[CP_GATHER_CHUNK];
+    __shared__ int s_code[CP_GATHER_CHUNK];
+    __shared__ float2 s_cs[256];
+    if (cp_err_set(a.hdr)) return;
+    const int nchunks = a.hdr->n_chunks;
+    const int64_t items = (int64_t)nchunks * a.L;
+    const int tid = threadIdx.x;
+    const int rowE = a.H * a.d;                        // elements per token row
+    const int half = a.d / 2;
+    const int hv = half / VEC;                          // vectors per half head
+    const int tpr = rowE / (2 * VEC);                   // tasks per token row
+    const bool zero_rec = (a.flags & CP_ZERO_RECOMPUTE) != 0;
+    const int64_t pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int c = (int)(item / a.L), l = (int)(item % a.L);
+        const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
+        const int len = a.l_len[hh];
+        const int ntok = min(CP_GATHER_CHUNK, len - t0);
+        const int r = a.l_req[hh], k = a.l_dst[hh], slot = a.l_slot[hh];
+        const int delta = a.dir == 0 ? a.l_delta[hh] : 0;
+        if (tid < ntok) {
+            const int t = t0 + tid;
+            const int q = k + t;                                           // position in the request
+            const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
+            const int blk = a.block_tables[(int64_t)r * a.max_blocks + (q >> 4)];
+            const int64_t pool_row = ((int64_t)page * CP_BLOCK + (t & 15)) * rowE;
+            const int64_t paged_row = ((int64_t)blk * CP_BLOCK + (q & 15)) * rowE;
+            if (a.dir == 0) { s_src[tid] = pool_row; s_dst[tid] = paged_row; s_code[tid] = a.plan[a.req_off[r] + q]; }
+            else { s_src[tid] = paged_row; s_dst[tid] = pool_row; s_code[tid] = CP_PLAN_REUSED; }
+        }
+        if (delta != 0) for (int i = tid; i < half; i += kRowsThreads) s_cs[i] = a.hit_cs[(int64_t)hh * half + i];
+        __syncthreads();
+        const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
+        const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
+        T* dstK = (T*)(a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T));
+        T* dstV = (T*)(a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T));
+        const int ntask = ntok * tpr;
+        for (int base = 0; base < ntask; base += kRowsThreads * kUnroll) {
+            uint4 klo[kUnroll], khi[kUnroll], vlo[kUnroll], vhi[kUnroll];
+            int64_t so[kUnroll], dso[kUnroll];
+            int code[kUnroll], i0[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int task = base + u * kRowsThreads + tid;
+                code[u] = -1;
+                if (task < ntask) {
+                    const int g = task / tpr, j = task - g * tpr;
+                    int lo;
+                    if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; i0[u] = sub * VEC; }
+                    else { lo = j * 2 * VEC; i0[u] = (lo % a.d) / 2; }
+                    const int hi = GPTJ ? lo + VEC : lo + half;
+                    code[u] = s_code[g];
+                    so[u] = s_src[g] + lo; dso[u] = s_dst[g] + lo;
+                    const int64_t shi = s_src[g] + hi;
+                    if (!(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
+                        klo[u] = ld_stream(srcK + so[u]); khi[u] = ld_stream(srcK + shi);
+                        vlo[u] = ld_stream(srcV + so[u]); vhi[u] = ld_stream(srcV + shi);
+                    }
+                    dso[u] = dso[u];
+                    so[u] = hi - lo;                                   // reuse: offset of the partner
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                if (code[u] < 0) continue;
+                T* dk = dstK + dso[u];
+                T* dv = dstV + dso[u];
+                const int poff = (int)so[u];
+                if (code[u] == CP_PLAN_RECOMPUTE && zero_rec) {
+                    const uint4 z = make_uint4(0, 0, 0, 0);
+                    st_stream(dk, z); st_stream(dk + poff, z); st_stream(dv, z); st_stream(dv + poff, z);
+                    continue;
+                }
+                if (delta != 0) {
+                    float x[VEC], y[VEC];
+                    unpack(klo[u], x, T()); unpack(khi[u], y, T());
+                    if (!GPTJ) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const float2 cs = s_cs[i0[u] + e];
+                            const float xo = fmaf(x[e], cs.x, -y[e] * cs.y);
+                            const float yo = fmaf(y[e], cs.x, x[e] * cs.y);
+                            x[e] = xo; y[e] = yo;
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < VEC; e += 2) {
+                            const float2 c0 = s_cs[i0[u] + e / 2];
+                            const float2 c1 = s_cs[i0[u] + VEC / 2 + e / 2];
+                            const float x0 = fmaf(x[e], c0.x, -x[e + 1] * c0.y), x1 = fmaf(x[e + 1], c0.x, x[e] * c0.y);
+                            const float y0 = fmaf(y[e], c1.x, -y[e + 1] * c1.y), y1 = fmaf(y[e + 1], c1.x, y[e] * c1.y);
+                            x[e] = x0; x[e + 1] = x1; y[e] = y0; y[e + 1] = y1;
+                        }
+                    }
+                    klo[u] = pack(x, T()); khi[u] = pack(y, T());
+                }
+                st_stream(dk, klo[u]); st_stream(dk + poff, khi[u]);
+                st_stream(dv, vlo[u]); st_stream(dv + poff, vhi[u]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// CP_ZERO_UNCOVERED: zero K and V rows of plan-0 positions (one CTA per (token block of 32, layer))
+template <typename T>
+__global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int32_t R, int64_t total) {
+    __shared__ int64_t s_dst[32];
+    __shared__ int s_on[32];
+    if (cp_err_set(a.hdr)) return;
+    const int rowE = a.H * a.d;
+    const int64_t nblk = (total + 31) / 32;
+    const int64_t items = nblk * a.L;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t b = item / a.L;
+        const int l = (int)(item % a.L);
+        if (threadIdx.x < 32) {
+            const int64_t g = b * 32 + threadIdx.x;
+            s_on[threadIdx.x] = 0;
+            if (g < total && a.plan[g] == CP_PLAN_UNCOVERED) {
+                int lo = 0, hi = R - 1;
+                while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.req_off[mid] <= g) lo = mid; else hi = mid - 1; }
+                const int q = (int)(g - a.req_off[lo]);
+                const int blk = a.block_tables[(int64_t)lo * a.max_blocks + (q >> 4)];
+                s_dst[threadIdx.x] = ((int64_t)blk * CP_BLOCK + (q & 15)) * rowE;
+                s_on[threadIdx.x] = 1;
+            }
+        }
+        __syncthreads();
+        constexpr int VEC = Vec<T>::N;
+        const int vpr = rowE / VEC;
+        for (int task = threadIdx.x; task < 32 * vpr; task += blockDim.x) {
+            const int g = task / vpr, v = task - g * vpr;
+            if (!s_on[g]) continue;
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            st_stream((T*)a.paged_k[l] + s_dst[g] + v * VEC, z);
+            st_stream((T*)a.paged_v[l] + s_dst[g] + v * VEC, z);
+        }
+        __syncthreads();
+    }
+}
+
+int g_rows_grid = 0;
+int rows_grid() {
+    if (!g_rows_grid) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_rows_grid = sms * 4;
+    }
+    return g_rows_grid;
+}
+
+}  // namespace
+
+cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int32_t* l_req, const int32_t* l_slot,
+                         const int32_t* l_dst, const int32_t* l_len, const int32_t* l_delta, int64_t list_cap,
+                         const int64_t* req_off, const uint8_t* plan, const cp_paged_kv* kv, int32_t flags,
+                         cudaStream_t st) {
+    RowsArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.hdr = x->hdr; a.dir = dir; a.count = d_count;
+    a.l_req = l_req; a.l_slot = l_slot; a.l_dst = l_dst; a.l_len = l_len; a.l_delta = l_delta;
+    a.list_cap = list_cap; a.req_off = req_off; a.plan = plan;
+    a.block_tables = kv->block_tables; a.max_blocks = kv->max_blocks_per_req;
+    for (int l = 0; l < x->cfg.num_layers; ++l) {
+        a.paged_k[l] = (char*)kv->k_layers_h[l]; a.paged_v[l] = (char*)kv->v_layers_h[l];
+        if (!a.paged_k[l] || !a.paged_v[l]) return CP_ERR_INVALID_ARG;
+    }
+    a.pool_k = x->pool_k; a.pool_v = x->pool_v; a.P = x->P; a.slot_pages = x->slot_pages; a.MP = x->MP;
+    a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim; a.theta = x->cfg.rope_theta;
+    a.flags = flags; a.gptj = x->cfg.rope_style == CP_ROPE_GPTJ;
+    a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH;
+    a.hit_cs = x->hit_cs; a.cs_hits = x->CS_HITS;
+    if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;
+    k_rows_prep<<<dir == 0 ? 148 : 1, kPrepThreads, 0, st>>>(a);
+    CP_COUNT_LAUNCH();
+    const int grid = rows_grid();
+    const bool bf16 = x->cfg.dtype == CP_BF16;
+    if (bf16) {
+        if (a.gptj) k_rows<__nv_bfloat16, true><<<grid, kRowsThreads, 0, st>>>(a);
+        else k_rows<__nv_bfloat16, false><<<grid, kRowsThreads, 0, st>>>(a);
+    } else {
+        if (a.gptj) k_rows<float, true><<<grid, kRowsThreads, 0, st>>>(a);
+        else k_rows<float, false><<<grid, kRowsThreads, 0, st>>>(a);
+    }
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}
+
+extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp_hits* h, const cp_paged_kv* kv,
+                                        int32_t flags, void* stream) {
+    if (!x || !b || !h || !kv) return CP_ERR_INVALID_ARG;
+    if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables || !b->offsets) return CP_ERR_INVALID_ARG;
+    if (!h->num_hits || !h->hit_req || !h->hit_slot || !h->hit_dst || !h->hit_len || !h->hit_delta || !h->plan)
+        return CP_ERR_INVALID_ARG;
+    if (b->num_reqs < 0 || b->num_reqs > x->cfg.max_batch_reqs) return CP_ERR_INVALID_ARG;
+    if (b->num_reqs == 0) return CP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    cp_status s = cp_launch_rows(x, 0, h->num_hits, h->hit_req, h->hit_slot, h->hit_dst, h->hit_len, h->hit_delta,
+                                 h->max_hits, b->offsets, h->plan, kv, flags, st);
+    if (s != CP_OK) return s;
+    if (flags & CP_ZERO_UNCOVERED) {
+        RowsArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.hdr = x->hdr; a.req_off = b->offsets; a.plan = h->plan;
+        a.block_tables = kv->block_tables; a.max_blocks = kv->max_blocks_per_req;
+        for (int l = 0; l < x->cfg.num_layers; ++l) { a.paged_k[l] = (char*)kv->k_layers_h[l]; a.paged_v[l] = (char*)kv->v_layers_h[l]; }
+        a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim;
+        if (x->cfg.dtype == CP_BF16) k_zero_uncovered<__nv_bfloat16><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, b->total_tokens);
+        else k_zero_uncovered<float><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, b->total_tokens);
+        CP_COUNT_LAUNCH();
+        if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    }
+    return CP_OK;
+}

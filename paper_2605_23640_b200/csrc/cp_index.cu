@@ -1,0 +1,1035 @@
+// cp_index.cu -- index lifecycle and cp_index_insert (§4.3.5 KV Pool).
+//
+// Insert pipeline (one call, stream ordered; the sequential semantics of DESIGN.md R#20-22 are
+// reproduced exactly: spans are applied in input order):
+//   k_ins_validate  warp per span: range / length / budget / mask checks (no side effects on error)
+//   k_ins_hash      warp per span: prefix (first w) and full polynomial hashes; batch prefix table
+//   k_ins_scan      CTA per haystack (new span or live entry): rolling windows probe the batch table
+//                   and (for new spans) the pool's prefix table -> containment candidates
+//   k_ins_verify    warp per candidate: exact token comparison
+//   k_ins_commit    one CTA: Duplicate -> Contained -> Supersede -> store -> LRU evict, in order
+//   k_ins_delete / k_ins_publish  table tombstones / inserts, token + bit store, SHA-256 digests
+//   copy-in         cp_launch_rows(dir = 1): writer paged KV -> pool pages (no rotation)
+#include "cp_internal.cuh"
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+std::atomic<unsigned long long> g_cp_launches{0};
+
+namespace {
+
+constexpr int kValThreads = 256;
+constexpr int kScanThreads = 256;
+constexpr int kCommitThreads = 1024;
+constexpr int kCommitRecCap = 8192;
+
+int64_t next_pow2(int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; }
+int ilog2(int64_t v) { int l = 0; while ((1LL << l) < v) ++l; return l; }
+size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
+
+uint64_t host_splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+uint64_t host_mulmod(uint64_t a, uint64_t b) {
+    unsigned __int128 x = (unsigned __int128)a * b;
+    uint64_t lo = (uint64_t)x & CP_PMOD, hi = (uint64_t)(x >> 61);
+    uint64_t r = lo + hi;
+    r = (r & CP_PMOD) + (r >> 61);
+    return r >= CP_PMOD ? r - CP_PMOD : r;
+}
+
+struct Layout {
+    int64_t P; int32_t MP, S; int64_t T; int logT;
+    int64_t HS, CH, CS_HITS; int32_t MS; int64_t MAXC, BT; int logBT;
+    size_t meta_off[20]; size_t meta_size;
+    size_t scr_off[32]; size_t scr_size;
+};
+
+bool valid_cfg(const cp_config* c) {
+    if (!c) return false;
+    if (c->window_len < 1 || c->block_size != CP_BLOCK) return false;
+    if (c->num_layers < 1 || c->num_layers > CP_MAX_LAYERS || c->num_kv_heads < 1 || c->head_dim < 2) return false;
+    if (c->dtype != CP_FP32 && c->dtype != CP_BF16) return false;
+    const int vec = c->dtype == CP_FP32 ? 4 : 8;
+    if (c->rope_style == CP_ROPE_NEOX) { if ((c->head_dim / 2) % vec != 0 || c->head_dim % 2) return false; }
+    else if (c->rope_style == CP_ROPE_GPTJ) { if (c->head_dim % (2 * vec) != 0) return false; }
+    else return false;
+    if (c->head_dim > 512) return false;
+    if (c->pool_capacity_tokens < c->window_len) return false;
+    if (c->max_entries < 1 || c->max_entries > 131072) return false;
+    if (c->max_span_len < c->window_len || c->max_span_len > 65535) return false;
+    if (c->max_req_tokens < 1 || c->max_req_tokens > CP_MAX_MATCH_TOKENS) return false;
+    if (c->max_batch_reqs < 1 || c->max_batch_tokens < 1 || c->max_spans_per_insert < 1) return false;
+    if (c->max_spans_per_insert > 16384) return false;
+    if (!(c->rope_theta > 0)) return false;
+    return true;
+}
+
+void compute_layout(const cp_config* c, Layout* L) {
+    L->P = cp_pool_num_pages(c);
+    L->MP = cp_max_pages_per_entry(c);
+    L->S = c->max_entries;
+    L->T = next_pow2(std::max<int64_t>(64, 4LL * L->S));
+    L->logT = ilog2(L->T);
+    const int64_t S = L->S, P = L->P, MP = L->MP;
+    size_t o = 0, i = 0;
+    auto put = [&](size_t bytes) { L->meta_off[i++] = o; o += al(bytes); };
+    put(sizeof(DevHeader));                  // 0 hdr
+    put(4 * S); put(4 * S); put(4 * S); put(1 * S);          // 1 id 2 len 3 origin 4 state
+    put(8 * S); put(8 * S); put(8 * S);                      // 5 prefix 6 full 7 last
+    put(32 * S);                                             // 8 digest
+    put(4 * S * MP);                                         // 9 pages
+    put(4 * P);                                              // 10 fifo
+    put(4 * S);                                              // 11 slot stack
+    put(4 * CP_BLOCK * P);                                   // 12 page tokens
+    put(2 * P);                                              // 13 page bits
+    put(sizeof(HEntry) * L->T);                              // 14 htab
+    put(8 * (size_t)(c->max_span_len + 1));                  // 15 pow table
+    L->meta_size = o;
+    // scratch
+    L->HS = c->max_batch_tokens / c->window_len + c->max_batch_reqs + 1;
+    L->MS = c->max_spans_per_insert;
+    L->CH = c->max_batch_tokens / CP_GATHER_CHUNK + std::max<int64_t>(L->HS, L->MS) + 1;
+    L->CS_HITS = std::max<int64_t>(L->HS, L->MS);
+    L->MAXC = 16LL * L->MS + 4096;
+    L->BT = next_pow2(std::max<int64_t>(64, 4LL * L->MS));
+    L->logBT = ilog2(L->BT);
+    o = 0; i = 0;
+    auto sput = [&](size_t bytes) { L->scr_off[i++] = o; o += al(bytes); };
+    for (int k = 0; k < 5; ++k) sput(4 * L->HS);             // 0-4 sp_entry sp_slot sp_dst sp_len sp_delta
+    sput(4 * (size_t)c->max_batch_reqs);                     // 5 req_cnt
+    sput(4 * L->CH); sput(4 * L->CH);                        // 6 chunk_hit 7 chunk_t0
+    sput(sizeof(float2) * L->CS_HITS * (size_t)(c->head_dim / 2));   // 8 hit_cs
+    sput(8 * (size_t)L->MS); sput(8 * (size_t)L->MS);        // 9 span_pre 10 span_full
+    sput(sizeof(HEntry) * L->BT);                            // 11 btab
+    sput(sizeof(Cand) * L->MAXC);                            // 12 cand
+    sput(4 * (size_t)(L->MS + 1));                           // 13 rel_off
+    sput(8 * (size_t)(2 * L->MAXC));                         // 14 rel_rec (int2)
+    sput(4 * (size_t)L->MS);                                 // 15 new_slot
+    sput(4 * (size_t)(S + L->MS));                           // 16 removed
+    for (int k = 0; k < 5; ++k) sput(4 * (size_t)L->MS);     // 17-21 cp_req cp_slot cp_dst cp_len cp_delta
+    sput(4 * (size_t)L->MS);                                 // 22 out_tmp
+    L->scr_size = o;
+}
+
+// ------------------------------------------------------------------------------------------
+// kernels: initialisation
+// ------------------------------------------------------------------------------------------
+__global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, int32_t* fifo, int32_t* slot_stack,
+                       HEntry* htab, int64_t P, int32_t S, int64_t T) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < P; i += nt) fifo[i] = (int32_t)i;                 // FIFO: ascending page ids (R#22)
+    for (int64_t i = tid; i < S; i += nt) { slot_id[i] = -1; slot_state[i] = CP_SLOT_FREE; slot_stack[i] = S - 1 - (int32_t)i; }
+    for (int64_t i = tid; i < T; i += nt) { htab[i].key = CP_EMPTY_KEY; htab[i].slot = -1; }
+    if (tid == 0) {
+        hdr->error = 0; hdr->next_id = 0; hdr->num_live = 0; hdr->fifo_head = 0; hdr->fifo_count = (int32_t)P;
+        hdr->slot_free_top = S; hdr->match_done = 0; hdr->table_used = 0; hdr->live_tokens = 0;
+        hdr->first_err = CP_NO_ERR_KEY; hdr->rebuild = 0; hdr->n_cand = 0; hdr->n_copy = 0; hdr->n_removed = 0;
+        hdr->n_chunks = 0; hdr->n_new_live = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// kernels: insert
+// ------------------------------------------------------------------------------------------
+struct InsArgs {
+    DevHeader* hdr;
+    const int32_t* tokens; const int64_t* offsets; const uint8_t* mask; int32_t num_reqs;
+    int32_t S; const int32_t* span_req; const int32_t* span_begin; const int32_t* span_len;
+    const uint32_t* bits; const int64_t* bits_off;
+    uint64_t t; int32_t w; uint64_t B; int64_t capacity; int32_t max_span_len;
+    int32_t* out_id; int32_t* out_oc;
+    // index
+    int32_t nslots; int64_t P; int32_t MP;
+    int32_t* slot_id; int32_t* slot_len; int32_t* slot_origin; uint8_t* slot_state;
+    unsigned long long* slot_prefix; unsigned long long* slot_full; unsigned long long* slot_last;
+    uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
+    int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; int logT; int64_t T; const unsigned long long* pw;
+    // scratch
+    unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
+    Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed;
+    int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
+};
+
+// error codes are ordered per span: range -> too short -> capacity -> sensitive (same order as the oracle)
+__device__ __forceinline__ int32_t code_of(int k) {
+    return k == 0 ? CP_ERR_INVALID_ARG : k == 1 ? CP_ERR_SPAN_TOO_SHORT : k == 2 ? CP_ERR_CAPACITY : CP_ERR_SENSITIVE_SPAN;
+}
+
+__global__ void k_ins_validate(InsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { a.hdr->n_cand = 0; a.hdr->n_copy = 0; a.hdr->n_removed = 0; a.hdr->n_new_live = 0; }
+    // clear the batch prefix table
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.BT; i += (int64_t)gridDim.x * blockDim.x) {
+        a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = -1;
+    }
+    if (cp_err_set(a.hdr)) return;
+    for (int s = warp; s < a.S; s += nwarps) {
+        const int r = a.span_req[s];
+        int bad = -1;
+        if (r < 0 || r >= a.num_reqs) bad = 0;
+        int64_t b = a.span_begin[s], m = a.span_len[s], n = 0;
+        if (bad < 0) {
+            n = a.offsets[r + 1] - a.offsets[r];
+            if (b < 0 || m < 0 || b + m > n) bad = 0;
+            else if (m < a.w) bad = 1;
+            else if (m > a.capacity || m > a.max_span_len) bad = 2;
+        }
+        if (bad < 0) {
+            const uint8_t* mk = a.mask + a.offsets[r] + b;
+            int any = 0;
+            for (int64_t k = lane; k < m; k += 32) any |= mk[k];
+            if (__any_sync(0xffffffffu, any)) bad = 3;
+        }
+        if (bad >= 0 && lane == 0) atomicMin(&a.hdr->first_err, ((unsigned long long)s << 32) | (unsigned)bad);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.hdr->slot_free_top < a.S)
+        atomicMin(&a.hdr->first_err, ((unsigned long long)0x7FFFFFFF << 32) | 2u);
+}
+
+// warp per span: prefix hash (first w tokens) and full hash; insert into the batch prefix table
+__global__ void k_ins_hash(InsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    for (int s = warp; s < a.S; s += nwarps) {
+        const int32_t* tau = a.tokens + a.offsets[a.span_req[s]] + a.span_begin[s];
+        const int m = a.span_len[s];
+        // lane folds a contiguous chunk; combine with B^(tokens after the chunk)
+        auto fold = [&](int len) -> uint64_t {
+            const int c = (len + 31) / 32;
+            const int c0 = min(len, lane * c), c1 = min(len, c0 + c);
+            uint64_t h = 0;
+            for (int i = c0; i < c1; ++i) h = cp_addmod(cp_mulmod(h, a.B), cp_tokval(tau[i]));
+            uint64_t v = cp_mulmod(h, a.pw[len - c1]);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) v = cp_addmod(v, __shfl_xor_sync(0xffffffffu, v, off));
+            return v;
+        };
+        const uint64_t pre = fold(a.w), full = fold(m);
+        if (lane == 0) {
+            a.span_pre[s] = pre; a.span_full[s] = full;
+            uint32_t pos = cp_hpos(pre, a.logBT);
+            while (true) {
+                unsigned long long prev = atomicCAS(&a.btab[pos].key, CP_EMPTY_KEY, (unsigned long long)pre);
+                if (prev == CP_EMPTY_KEY) { a.btab[pos].slot = s; break; }
+                pos = (pos + 1) & (uint32_t)(a.BT - 1);
+            }
+        }
+    }
+}
+
+// token fetch helpers
+__device__ __forceinline__ int32_t slot_token(const InsArgs& a, int slot, int t) {
+    const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
+    return a.page_tokens[(int64_t)page * CP_BLOCK + (t & 15)];
+}
+__device__ __forceinline__ const int32_t* span_tokens(const InsArgs& a, int j) {
+    return a.tokens + a.offsets[a.span_req[j]] + a.span_begin[j];
+}
+
+__device__ __forceinline__ void push_cand(const InsArgs& a, int hay, int needle, int off) {
+    int i = atomicAdd(&a.hdr->n_cand, 1);
+    if (i < a.MAXC) { a.cand[i].hay = hay; a.cand[i].needle = needle; a.cand[i].off = off; a.cand[i].ok = 0; }
+    else cp_raise(a.hdr, CP_ERR_CAPACITY);
+}
+
+// items [0, S): new span j as haystack (needles: other new spans via btab, live entries via htab)
+// items [S, S + nslots): live slot as haystack (needles: new spans via btab)
+__global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a) {
+    extern __shared__ uint64_t sm[];
+    __shared__ uint64_t wtmp[2 * (kScanThreads / 32)];
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    const int64_t items = (int64_t)a.S + a.nslots;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int m;
+        bool is_new = it < a.S;
+        int id = is_new ? (int)it : (int)(it - a.S);
+        if (is_new) m = a.span_len[id];
+        else {
+            if (a.slot_state[id] != CP_SLOT_LIVE) continue;
+            m = a.slot_len[id];
+        }
+        if (is_new) {
+            const int32_t* tau = span_tokens(a, id);
+            cp_block_prefix_hash<kScanThreads>([&](int i) { return tau[i]; }, m, a.B, sm, wtmp);
+        } else {
+            cp_block_prefix_hash<kScanThreads>([&](int i) { return slot_token(a, id, i); }, m, a.B, sm, wtmp);
+        }
+        const uint64_t Bw = a.pw[a.w];
+        for (int o = threadIdx.x; o + a.w <= m; o += blockDim.x) {
+            const uint64_t W = cp_subhash(sm, o, a.w, Bw);
+            // needles among new spans
+            uint32_t pos = cp_hpos(W, a.logBT);
+            while (true) {
+                const unsigned long long key = a.btab[pos].key;
+                if (key == CP_EMPTY_KEY) break;
+                if (key == W) {
+                    const int j = a.btab[pos].slot;
+                    const int mj = a.span_len[j];
+                    if (!(is_new && j == id) && o + mj <= m &&
+                        cp_subhash(sm, o, mj, a.pw[mj]) == a.span_full[j])
+                        push_cand(a, is_new ? -1 - id : id, -1 - j, o);
+                }
+                pos = (pos + 1) & (uint32_t)(a.BT - 1);
+            }
+            if (!is_new) continue;
+            // needles among live pool entries
+            pos = cp_hpos(W, a.logT);
+            while (true) {
+                const unsigned long long key = a.htab[pos].key;
+                if (key == CP_EMPTY_KEY) break;
+                if (key == W) {
+                    const int e = a.htab[pos].slot;
+                    const int me = a.slot_len[e];
+                    if (o + me <= m && cp_subhash(sm, o, me, a.pw[me]) == a.slot_full[e])
+                        push_cand(a, -1 - id, e, o);
+                }
+                pos = (pos + 1) & (uint32_t)(a.T - 1);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// warp per candidate: exact token comparison of needle vs haystack[off, off + len(needle))
+__global__ void k_ins_verify(InsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    const int nc = min((int64_t)a.hdr->n_cand, a.MAXC);
+    for (int c = warp; c < nc; c += nwarps) {
+        const Cand cd = a.cand[c];
+        const int nm = cd.needle < 0 ? a.span_len[-1 - cd.needle] : a.slot_len[cd.needle];
+        int bad = 0;
+        for (int t = lane; t < nm; t += 32) {
+            const int32_t x = cd.needle < 0 ? span_tokens(a, -1 - cd.needle)[t] : slot_token(a, cd.needle, t);
+            const int32_t y = cd.hay < 0 ? span_tokens(a, -1 - cd.hay)[cd.off + t] : slot_token(a, cd.hay, cd.off + t);
+            bad |= (x != y);
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) a.cand[c].ok = !bad;
+    }
+}
+
+enum { REL_EQ = 0, REL_CONTAINER = 1, REL_CONTAINED = 2 };
+constexpr int kMaxSupersede = 1024;
+
+struct CommitSmem {                  // byte offsets of the dynamic shared-memory carve-up
+    size_t snew, soff, srec, total;
+    __host__ __device__ CommitSmem(int nslots, int S) {
+        snew = ((size_t)nslots + 15) & ~(size_t)15;
+        soff = snew + 4 * (size_t)S;
+        srec = (soff + 4 * ((size_t)S + 1) + 15) & ~(size_t)15;
+        total = srec + 8 * (size_t)kCommitRecCap;
+    }
+};
+
+// block-wide exclusive scan of v[0..n) in shared memory (in place); returns the total
+template <int NT>
+__device__ int block_excl_scan(int32_t* v, int n, int32_t* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c = (n + NT - 1) / NT, c0 = min(n, tid * c), c1 = min(n, c0 + c);
+    int loc = 0;
+    for (int i = c0; i < c1; ++i) loc += v[i];
+    int inc = loc;
+    for (int off = 1; off < 32; off <<= 1) { int y = __shfl_up_sync(0xffffffffu, inc, off); if (lane >= off) inc += y; }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int x = lane < NT / 32 ? wsum[lane] : 0, xi = x;
+        for (int off = 1; off < 32; off <<= 1) { int y = __shfl_up_sync(0xffffffffu, xi, off); if (lane >= off) xi += y; }
+        if (lane < NT / 32) wsum[lane] = xi - x;
+        if (lane == 31) wsum[NT / 32] = xi;
+    }
+    __syncthreads();
+    int run = wsum[wid] + inc - loc;
+    for (int i = c0; i < c1; ++i) { int t = v[i]; v[i] = run; run += t; }
+    const int total = wsum[NT / 32];
+    __syncthreads();
+    return total;
+}
+
+// One CTA applies the spans in input order (exact sequential semantics of R#20-22).
+// sflag bit 0: live; bit 1: stored by this call.
+__global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
+    extern __shared__ __align__(16) unsigned char smc[];
+    const int tid = threadIdx.x;
+    const CommitSmem lay(a.nslots, a.S);
+    uint8_t* sflag = smc;
+    int32_t* snew = (int32_t*)(smc + lay.snew);
+    int32_t* soff = (int32_t*)(smc + lay.soff);
+    int2* srec = (int2*)(smc + lay.srec);
+    __shared__ int s_abort, s_nrec, s_j, s_store_slot, s_npg, s_pop_head, s_nrm, s_need;
+    __shared__ long long s_live_tokens;
+    __shared__ int s_fifo_head, s_fifo_count, s_next_id, s_free_top, s_num_live, s_nremoved;
+    __shared__ int s_rm[kMaxSupersede];
+    __shared__ int s_rm_base[kMaxSupersede + 1];
+    __shared__ unsigned long long s_red_key[kCommitThreads / 32];
+    __shared__ int s_red_slot[kCommitThreads / 32];
+    __shared__ int32_t s_wsum[kCommitThreads / 32 + 1];
+
+    if (tid == 0) {
+        s_abort = 0;
+        if (cp_err_set(a.hdr)) s_abort = 1;
+        else if (a.hdr->first_err != CP_NO_ERR_KEY) {
+            const unsigned code = (unsigned)(a.hdr->first_err & 0xffffffffu);
+            cp_raise(a.hdr, code_of((int)code));
+            s_abort = 1;
+        } else if (a.hdr->n_cand > a.MAXC) {
+            cp_raise(a.hdr, CP_ERR_CAPACITY);
+            s_abort = 1;
+        }
+        a.hdr->first_err = CP_NO_ERR_KEY;
+    }
+    __syncthreads();
+    if (s_abort) {
+        for (int j = tid; j < a.S; j += blockDim.x) { a.out_id[j] = -1; a.out_oc[j] = -1; a.out_tmp[j] = -1; }
+        return;
+    }
+    // ---- load state
+    for (int i = tid; i < a.nslots; i += blockDim.x) sflag[i] = a.slot_state[i] == CP_SLOT_LIVE ? 1 : 0;
+    for (int j = tid; j < a.S; j += blockDim.x) { snew[j] = -1; soff[j] = 0; }
+    if (tid == 0) {
+        soff[a.S] = 0;
+        s_live_tokens = a.hdr->live_tokens; s_fifo_head = a.hdr->fifo_head; s_fifo_count = a.hdr->fifo_count;
+        s_next_id = a.hdr->next_id; s_free_top = a.hdr->slot_free_top; s_num_live = a.hdr->num_live;
+        s_nremoved = 0;
+    }
+    __syncthreads();
+    // ---- relation CSR over new spans: (other, kind) records per span
+    const int nc = a.hdr->n_cand;
+    auto len_of = [&](int code) { return code < 0 ? a.span_len[-1 - code] : a.slot_len[code]; };
+    for (int c = tid; c < nc; c += blockDim.x) {
+        const Cand cd = a.cand[c];
+        if (!cd.ok) continue;
+        if (cd.needle < 0) atomicAdd(&soff[-1 - cd.needle], 1);
+        if (cd.hay < 0) atomicAdd(&soff[-1 - cd.hay], 1);
+    }
+    __syncthreads();
+    const int nrec = block_excl_scan<kCommitThreads>(soff, a.S + 1, s_wsum);
+    for (int j = tid; j <= a.S; j += blockDim.x) a.rel_off[j] = soff[j];
+    __syncthreads();
+    for (int c = tid; c < nc; c += blockDim.x) {
+        const Cand cd = a.cand[c];
+        if (!cd.ok) continue;
+        const bool eq = len_of(cd.needle) == len_of(cd.hay);
+        if (cd.needle < 0) {       // the new span (needle) occurs inside hay
+            const int p = atomicAdd(&soff[-1 - cd.needle], 1);
+            a.rel_rec[p] = make_int2(cd.hay, eq ? REL_EQ : REL_CONTAINER);
+        }
+        if (cd.hay < 0) {          // the new span (hay) contains needle
+            const int p = atomicAdd(&soff[-1 - cd.hay], 1);
+            a.rel_rec[p] = make_int2(cd.needle, eq ? REL_EQ : REL_CONTAINED);
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j <= a.S; j += blockDim.x) soff[j] = a.rel_off[j];
+    if (tid == 0) s_nrec = nrec;
+    __syncthreads();
+    const bool rec_in_smem = s_nrec <= kCommitRecCap;
+    if (rec_in_smem) for (int i = tid; i < s_nrec; i += blockDim.x) srec[i] = a.rel_rec[i];
+    __syncthreads();
+    const int2* rec = rec_in_smem ? srec : a.rel_rec;
+
+    auto resolve = [&](int code) -> int { return code >= 0 ? code : snew[-1 - code]; };
+    auto is_live = [&](int code) -> bool { const int s = resolve(code); return s >= 0 && (sflag[s] & 1); };
+
+    // remove s_rm[0..n): pages go to the FIFO tail in order (all threads)
+    auto remove_slots = [&](int n) {
+        __syncthreads();
+        const int total = s_rm_base[n];
+        for (int q = tid; q < total; q += blockDim.x) {
+            int lo = 0, hi = n - 1;                 // find r with s_rm_base[r] <= q < s_rm_base[r+1]
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rm_base[mid] <= q) lo = mid; else hi = mid - 1; }
+            const int slot = s_rm[lo];
+            a.fifo[(s_fifo_head + s_fifo_count + q) % a.P] = a.slot_pages[(int64_t)slot * a.MP + (q - s_rm_base[lo])];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int r = 0; r < n; ++r) {
+                const int slot = s_rm[r];
+                a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
+                sflag[slot] = 0;
+                s_live_tokens -= a.slot_len[slot];
+                s_num_live -= 1;
+            }
+            s_fifo_count += total;
+        }
+        __syncthreads();
+    };
+
+    int j0 = 0;
+    while (true) {
+        // ---- thread 0 runs ahead through spans that need no block-wide work
+        if (tid == 0) {
+            s_j = a.S; s_nrm = 0;
+            for (int j = j0; j < a.S; ++j) {
+                const int b = soff[j], e = soff[j + 1];
+                int dup = -1;
+                for (int q = b; q < e; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
+                if (dup >= 0) {
+                    a.slot_last[dup] = a.t;                      // Duplicate refreshes last_used (R#20)
+                    a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
+                    continue;
+                }
+                int cont = -1, cont_id = 0x7fffffff;
+                for (int q = b; q < e; ++q)
+                    if (rec[q].y == REL_CONTAINER && is_live(rec[q].x)) {
+                        const int s = resolve(rec[q].x);
+                        const int sid = a.slot_id[s];
+                        if (sid < cont_id) { cont_id = sid; cont = s; }
+                    }
+                if (cont >= 0) { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; continue; }
+                // store; first the live entries it strictly contains, ascending id
+                int n = 0;
+                for (int q = b; q < e; ++q)
+                    if (rec[q].y == REL_CONTAINED && is_live(rec[q].x)) {
+                        const int s = resolve(rec[q].x);
+                        bool seen = false;
+                        for (int z = 0; z < n; ++z) seen |= (s_rm[z] == s);
+                        if (!seen) {
+                            if (n < kMaxSupersede) s_rm[n++] = s;
+                            else cp_raise(a.hdr, CP_ERR_CAPACITY);
+                        }
+                    }
+                for (int x = 1; x < n; ++x)      // insertion sort by id
+                    for (int y = x; y > 0 && a.slot_id[s_rm[y]] < a.slot_id[s_rm[y - 1]]; --y) {
+                        const int tmp = s_rm[y]; s_rm[y] = s_rm[y - 1]; s_rm[y - 1] = tmp;
+                    }
+                s_rm_base[0] = 0;
+                for (int x = 0; x < n; ++x) s_rm_base[x + 1] = s_rm_base[x] + (a.slot_len[s_rm[x]] + CP_BLOCK - 1) / CP_BLOCK;
+                s_nrm = n;
+                s_j = j;
+                break;
+            }
+        }
+        __syncthreads();
+        const int j = s_j;
+        if (j >= a.S) break;
+        const int nrm = s_nrm;
+        if (nrm > 0) remove_slots(nrm);
+        // ---- store span j: id = next id, pages from the FIFO head (R#22)
+        if (tid == 0) {
+            const int m = a.span_len[j];
+            const int slot = a.slot_stack[--s_free_top];
+            const int id = s_next_id++;
+            const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
+            if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
+            s_store_slot = slot; s_npg = npg; s_pop_head = s_fifo_head;
+            s_fifo_head = (int)((s_fifo_head + npg) % a.P); s_fifo_count -= npg;
+            s_live_tokens += m; s_num_live += 1;
+            sflag[slot] = 3; snew[j] = slot;
+            a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_origin[slot] = a.span_begin[j];
+            a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j]; a.slot_last[slot] = a.t;
+            a.out_tmp[j] = slot; a.out_oc[j] = nrm > 0 ? CP_SUPERSEDED : CP_STORED;
+            s_need = s_live_tokens > a.capacity;
+        }
+        __syncthreads();
+        for (int i = tid; i < s_npg; i += blockDim.x)
+            a.slot_pages[(int64_t)s_store_slot * a.MP + i] = a.fifo[(s_pop_head + i) % a.P];
+        __syncthreads();
+        // ---- LRU eviction: victim = min (last_used, id) among live entries (R#21)
+        while (s_need) {
+            unsigned long long best_last = ~0ULL; int best_id = 0x7fffffff, best_slot = -1;
+            for (int s = tid; s < a.nslots; s += blockDim.x) {
+                if (!(sflag[s] & 1)) continue;
+                const unsigned long long lu = a.slot_last[s];
+                const int sid = a.slot_id[s];
+                if (lu < best_last || (lu == best_last && sid < best_id)) { best_last = lu; best_id = sid; best_slot = s; }
+            }
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long ol = __shfl_xor_sync(0xffffffffu, best_last, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, best_id, off);
+                const int os = __shfl_xor_sync(0xffffffffu, best_slot, off);
+                if (ol < best_last || (ol == best_last && oi < best_id)) { best_last = ol; best_id = oi; best_slot = os; }
+            }
+            if ((tid & 31) == 0) { s_red_key[tid >> 5] = best_last; s_red_slot[tid >> 5] = best_slot; s_wsum[tid >> 5] = best_id; }
+            __syncthreads();
+            if (tid == 0) {
+                int bs = -1, bi = 0x7fffffff; unsigned long long bl = ~0ULL;
+                for (int w = 0; w < kCommitThreads / 32; ++w) {
+                    if (s_red_slot[w] < 0) continue;
+                    if (s_red_key[w] < bl || (s_red_key[w] == bl && s_wsum[w] < bi)) { bl = s_red_key[w]; bi = s_wsum[w]; bs = s_red_slot[w]; }
+                }
+                s_rm[0] = bs; s_rm_base[0] = 0; s_rm_base[1] = (a.slot_len[bs] + CP_BLOCK - 1) / CP_BLOCK;
+            }
+            remove_slots(1);
+            if (tid == 0) s_need = s_live_tokens > a.capacity;
+            __syncthreads();
+        }
+        j0 = j + 1;
+    }
+    __syncthreads();
+    // ---- write back; removed slots return to the free stack; list the new entries to publish
+    if (tid == 0) {
+        for (int r = 0; r < s_nremoved; ++r) a.slot_stack[s_free_top++] = a.removed[r] & 0x7fffffff;
+        int nl = 0;
+        for (int j = 0; j < a.S; ++j) {
+            const int slot = snew[j];
+            if (slot >= 0 && (sflag[slot] & 1)) {
+                a.cp_req[nl] = a.span_req[j]; a.cp_slot[nl] = slot; a.cp_dst[nl] = a.span_begin[j];
+                a.cp_len[nl] = a.span_len[j]; a.cp_delta[nl] = j;       // cp_delta carries the span index
+                ++nl;
+            }
+        }
+        a.hdr->n_copy = nl; a.hdr->n_new_live = nl; a.hdr->n_removed = s_nremoved;
+        a.hdr->live_tokens = s_live_tokens; a.hdr->fifo_head = s_fifo_head; a.hdr->fifo_count = s_fifo_count;
+        a.hdr->next_id = s_next_id; a.hdr->slot_free_top = s_free_top; a.hdr->num_live = s_num_live;
+    }
+    __syncthreads();
+    for (int i = tid; i < a.nslots; i += blockDim.x) a.slot_state[i] = (sflag[i] & 1) ? CP_SLOT_LIVE : CP_SLOT_FREE;
+}
+
+// map the committed slot of each span to its entry id (parallel)
+__global__ void k_ins_outids(InsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.S; j += gridDim.x * blockDim.x) {
+        const int s = a.out_tmp[j];
+        a.out_id[j] = s >= 0 ? a.slot_id[s] : -1;
+    }
+}
+
+// tombstone prefix-table entries of removed pool entries (those that were in the table)
+__global__ void k_ins_delete(InsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    const int n = a.hdr->n_removed;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int code = a.removed[r];
+        if (code < 0) continue;               // stored and removed within this call: never published
+        const int slot = code;
+        const unsigned long long key = a.slot_prefix[slot];
+        uint32_t pos = cp_hpos(key, a.logT);
+        while (true) {
+            const unsigned long long k = a.htab[pos].key;
+            if (k == CP_EMPTY_KEY) break;
+            if (k == key && a.htab[pos].slot == slot) { a.htab[pos].key = CP_TOMB_KEY; break; }
+            pos = (pos + 1) & (uint32_t)(a.T - 1);
+        }
+    }
+}
+
+// SHA-256 (FIPS 180-4) over big-endian u64 token ids (R#6); one thread per entry
+__device__ const uint32_t kK256[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+
+__device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+__device__ void sha256_compress(uint32_t H[8], const uint32_t Win[16]) {
+    uint32_t W[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) W[i] = Win[i];
+    uint32_t a = H[0], b = H[1], c = H[2], d = H[3], e = H[4], f = H[5], g = H[6], h = H[7];
+#pragma unroll 16
+    for (int t = 0; t < 64; ++t) {
+        uint32_t wt;
+        if (t < 16) wt = W[t];
+        else {
+            const uint32_t w15 = W[(t - 15) & 15], w2 = W[(t - 2) & 15];
+            const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+            const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+            wt = W[t & 15] = W[t & 15] + s0 + W[(t - 7) & 15] + s1;
+        }
+        const uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t T1 = h + S1 + ch + kK256[t] + wt;
+        const uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        h = g; g = f; f = e; e = d + T1; d = c; c = b; b = a; a = T1 + S0 + mj;
+    }
+    H[0] += a; H[1] += b; H[2] += c; H[3] += d; H[4] += e; H[5] += f; H[6] += g; H[7] += h;
+}
+
+__device__ void sha256_tokens_dev(const int32_t* tau, int m, uint8_t* out) {
+    uint32_t H[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    uint32_t W[16];
+    const int full = m / 8;
+    for (int b = 0; b < full; ++b) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t v = tau[8 * b + i];
+            W[2 * i] = (uint32_t)((uint64_t)v >> 32); W[2 * i + 1] = (uint32_t)(uint64_t)v;
+        }
+        sha256_compress(H, W);
+    }
+    const int rem = m - 8 * full;
+    for (int i = 0; i < 16; ++i) W[i] = 0;
+    for (int i = 0; i < rem; ++i) {
+        const int64_t v = tau[8 * full + i];
+        W[2 * i] = (uint32_t)((uint64_t)v >> 32); W[2 * i + 1] = (uint32_t)(uint64_t)v;
+    }
+    W[2 * rem] = 0x80000000u;
+    const uint64_t bits = (uint64_t)m * 64ULL;
+    if (2 * rem + 1 > 14) {
+        sha256_compress(H, W);
+        for (int i = 0; i < 16; ++i) W[i] = 0;
+    }
+    W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits;
+    sha256_compress(H, W);
+    for (int i = 0; i < 8; ++i) {
+        out[4 * i] = (uint8_t)(H[i] >> 24); out[4 * i + 1] = (uint8_t)(H[i] >> 16);
+        out[4 * i + 2] = (uint8_t)(H[i] >> 8); out[4 * i + 3] = (uint8_t)H[i];
+    }
+}
+
+// publish new live entries: prefix table insert, token + recompute-bit store, digest
+__global__ void k_ins_publish(InsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    const int n = a.hdr->n_new_live;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int q = warp; q < n; q += nwarps) {
+        const int slot = a.cp_slot[q], j = a.cp_delta[q], m = a.cp_len[q];
+        const int32_t* tau = span_tokens(a, j);
+        for (int t = lane; t < m; t += 32) {
+            const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
+            a.page_tokens[(int64_t)page * CP_BLOCK + (t & 15)] = tau[t];
+        }
+        const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
+        for (int pg = lane; pg < npg; pg += 32) {
+            uint32_t v = 0;
+            if (a.bits) {
+                for (int z = 0; z < CP_BLOCK && pg * CP_BLOCK + z < m; ++z) {
+                    const int t = pg * CP_BLOCK + z;
+                    v |= ((a.bits[a.bits_off[j] + (t >> 5)] >> (t & 31)) & 1u) << z;
+                }
+            }
+            a.page_bits[a.slot_pages[(int64_t)slot * a.MP + pg]] = (uint16_t)v;
+        }
+        if (lane == 0) {
+            sha256_tokens_dev(tau, m, a.slot_digest + (int64_t)slot * 32);
+            const unsigned long long key = a.slot_prefix[slot];
+            uint32_t pos = cp_hpos(key, a.logT);
+            while (true) {
+                const unsigned long long k = a.htab[pos].key;
+                if (k == CP_EMPTY_KEY || k == CP_TOMB_KEY) {
+                    if (atomicCAS(&a.htab[pos].key, k, key) == k) {
+                        a.htab[pos].slot = slot;
+                        if (k == CP_EMPTY_KEY) atomicAdd(&a.hdr->table_used, 1);
+                        break;
+                    }
+                    continue;
+                }
+                pos = (pos + 1) & (uint32_t)(a.T - 1);
+            }
+        }
+    }
+}
+
+// rebuild the prefix table when tombstones accumulate (live + tombstones > T/2)
+__global__ void k_rebuild_check(DevHeader* hdr, int64_t T) {
+    hdr->rebuild = (hdr->error == 0 && (int64_t)hdr->table_used * 2 > T) ? 1 : 0;
+}
+__global__ void k_rebuild_clear(DevHeader* hdr, HEntry* htab, int64_t T) {
+    if (!hdr->rebuild) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x) {
+        htab[i].key = CP_EMPTY_KEY; htab[i].slot = -1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) hdr->table_used = 0;
+}
+__global__ void k_rebuild_fill(DevHeader* hdr, HEntry* htab, int logT, int64_t T, const uint8_t* state,
+                               const unsigned long long* prefix, int32_t nslots) {
+    if (!hdr->rebuild) return;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
+        if (state[s] != CP_SLOT_LIVE) continue;
+        const unsigned long long key = prefix[s];
+        uint32_t pos = cp_hpos(key, logT);
+        while (true) {
+            if (atomicCAS(&htab[pos].key, CP_EMPTY_KEY, key) == CP_EMPTY_KEY) { htab[pos].slot = s; atomicAdd(&hdr->table_used, 1); break; }
+            pos = (pos + 1) & (uint32_t)(T - 1);
+        }
+    }
+}
+
+// cp_hash_prefix: one CTA per request, chunks of 8192 tokens with a carried running hash
+__device__ uint64_t powmod_dev(uint64_t b, int e) {
+    uint64_t p = 1;
+    while (e) { if (e & 1) p = cp_mulmod(p, b); b = cp_mulmod(b, b); e >>= 1; }
+    return p;
+}
+__global__ void __launch_bounds__(256) k_hash_prefix(const int32_t* tokens, const int64_t* offsets, uint64_t B,
+                                                     uint64_t* out) {
+    extern __shared__ uint64_t sm[];
+    __shared__ uint64_t wtmp[16];
+    __shared__ uint64_t s_carry;
+    const int r = blockIdx.x;
+    const int64_t o = offsets[r];
+    const int n = (int)(offsets[r + 1] - o);
+    const int32_t* t = tokens + o;
+    uint64_t* dst = out + o + r;                       // n + 1 values for request r
+    if (threadIdx.x == 0) { dst[0] = 0; s_carry = 0; }
+    __syncthreads();
+    for (int base = 0; base < n; base += 8192) {
+        const int len = min(8192, n - base);
+        cp_block_prefix_hash<256>([&](int i) { return t[base + i]; }, len, B, sm, wtmp);
+        const uint64_t carry = s_carry;
+        for (int i = threadIdx.x + 1; i <= len; i += blockDim.x)
+            dst[base + i] = cp_addmod(cp_mulmod(carry, powmod_dev(B, i)), sm[i]);
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = dst[base + len];
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C-ABI
+// ==========================================================================================
+extern "C" {
+
+int64_t cp_pool_num_pages(const cp_config* c) {
+    if (!c || c->window_len < 1) return -1;
+    const int64_t cap = c->pool_capacity_tokens;
+    return (cap + c->max_span_len + CP_BLOCK - 1) / CP_BLOCK + (cap + c->window_len - 1) / c->window_len + 1;
+}
+
+int32_t cp_max_pages_per_entry(const cp_config* c) {
+    if (!c) return -1;
+    return (c->max_span_len + CP_BLOCK - 1) / CP_BLOCK;
+}
+
+cp_status cp_index_workspace(const cp_config* cfg, size_t* sizes) {
+    if (!valid_cfg(cfg) || !sizes) return CP_ERR_INVALID_ARG;
+    Layout L;
+    compute_layout(cfg, &L);
+    const size_t elem = cfg->dtype == CP_FP32 ? 4 : 2;
+    const size_t pool = (size_t)cfg->num_layers * L.P * CP_BLOCK * cfg->num_kv_heads * cfg->head_dim * elem;
+    sizes[CP_WS_POOL_K] = al(pool);
+    sizes[CP_WS_POOL_V] = al(pool);
+    sizes[CP_WS_META] = L.meta_size;
+    sizes[CP_WS_SCRATCH] = L.scr_size;
+    return CP_OK;
+}
+
+cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, cp_index** out) {
+    if (!valid_cfg(cfg) || !ws || !out) return CP_ERR_INVALID_ARG;
+    for (int i = 0; i < CP_WS_COUNT; ++i) if (!ws[i] || ((uintptr_t)ws[i] & 255)) return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    Layout L;
+    compute_layout(cfg, &L);
+    cp_index* x = new cp_index();
+    std::memset(x, 0, sizeof(*x));
+    x->cfg = *cfg;
+    cp_index_workspace(cfg, x->ws);
+    x->P = L.P; x->MP = L.MP; x->S = L.S; x->T = L.T; x->logT = L.logT;
+    x->B = 2 + host_splitmix64(cfg->hash_seed) % (CP_PMOD - 3);
+    x->elem = cfg->dtype == CP_FP32 ? 4 : 2;
+    x->pool_k = (char*)ws[CP_WS_POOL_K]; x->pool_v = (char*)ws[CP_WS_POOL_V];
+    x->meta = (char*)ws[CP_WS_META]; x->scratch = (char*)ws[CP_WS_SCRATCH];
+    char* m = x->meta;
+    x->hdr = (DevHeader*)(m + L.meta_off[0]);
+    x->slot_id = (int32_t*)(m + L.meta_off[1]); x->slot_len = (int32_t*)(m + L.meta_off[2]);
+    x->slot_origin = (int32_t*)(m + L.meta_off[3]); x->slot_state = (uint8_t*)(m + L.meta_off[4]);
+    x->slot_prefix = (unsigned long long*)(m + L.meta_off[5]); x->slot_full = (unsigned long long*)(m + L.meta_off[6]);
+    x->slot_last = (unsigned long long*)(m + L.meta_off[7]); x->slot_digest = (uint8_t*)(m + L.meta_off[8]);
+    x->slot_pages = (int32_t*)(m + L.meta_off[9]); x->fifo = (int32_t*)(m + L.meta_off[10]);
+    x->slot_stack = (int32_t*)(m + L.meta_off[11]); x->page_tokens = (int32_t*)(m + L.meta_off[12]);
+    x->page_bits = (uint16_t*)(m + L.meta_off[13]); x->htab = (HEntry*)(m + L.meta_off[14]);
+    x->pw = (unsigned long long*)(m + L.meta_off[15]);
+    char* s = x->scratch;
+    x->HS = L.HS; x->CH = L.CH; x->CS_HITS = L.CS_HITS; x->MS = L.MS; x->MAXC = L.MAXC; x->BT = L.BT; x->logBT = L.logBT;
+    x->sp_entry = (int32_t*)(s + L.scr_off[0]); x->sp_slot = (int32_t*)(s + L.scr_off[1]);
+    x->sp_dst = (int32_t*)(s + L.scr_off[2]); x->sp_len = (int32_t*)(s + L.scr_off[3]);
+    x->sp_delta = (int32_t*)(s + L.scr_off[4]); x->req_cnt = (int32_t*)(s + L.scr_off[5]);
+    x->chunk_hit = (int32_t*)(s + L.scr_off[6]); x->chunk_t0 = (int32_t*)(s + L.scr_off[7]);
+    x->hit_cs = (float2*)(s + L.scr_off[8]);
+    x->span_pre = (unsigned long long*)(s + L.scr_off[9]); x->span_full = (unsigned long long*)(s + L.scr_off[10]);
+    x->btab = (HEntry*)(s + L.scr_off[11]); x->cand = (Cand*)(s + L.scr_off[12]);
+    x->rel_off = (int32_t*)(s + L.scr_off[13]); x->rel_rec = (int32_t*)(s + L.scr_off[14]);
+    x->new_slot = (int32_t*)(s + L.scr_off[15]); x->removed = (int32_t*)(s + L.scr_off[16]);
+    x->cp_req = (int32_t*)(s + L.scr_off[17]); x->cp_slot = (int32_t*)(s + L.scr_off[18]);
+    x->cp_dst = (int32_t*)(s + L.scr_off[19]); x->cp_len = (int32_t*)(s + L.scr_off[20]);
+    x->cp_delta = (int32_t*)(s + L.scr_off[21]); x->out_tmp = (int32_t*)(s + L.scr_off[22]);
+    // power table B^k, k = 0..max_span_len (host, exact)
+    std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
+    pw[0] = 1;
+    for (size_t k = 1; k < pw.size(); ++k) pw[k] = host_mulmod(pw[k - 1], x->B);
+    x->Bw = pw[(size_t)cfg->window_len];
+    if (cudaMemcpyAsync(x->pw, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
+    k_init<<<592, 256, 0, st>>>(x->hdr, x->slot_id, x->slot_state, x->fifo, x->slot_stack, x->htab, x->P, x->S, x->T);
+    CP_COUNT_LAUNCH();
+    if (cudaGetLastError() != cudaSuccess) { delete x; return CP_ERR_CUDA; }
+    if (cudaStreamSynchronize(st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
+    // opt-in shared memory for the large kernels
+    cudaFuncSetAttribute(k_ins_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_ins_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_hash_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    *out = x;
+    return CP_OK;
+}
+
+cp_status cp_index_destroy(cp_index* x) {
+    if (!x) return CP_ERR_INVALID_ARG;
+    delete x;
+    return CP_OK;
+}
+
+uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
+
+uint64_t cp_kernel_launch_count(void) { return g_cp_launches.load(); }
+
+const char* cp_status_string(cp_status s) {
+    switch (s) {
+        case CP_OK: return "CP_OK";
+        case CP_ERR_INVALID_ARG: return "CP_ERR_INVALID_ARG";
+        case CP_ERR_SENSITIVE_SPAN: return "CP_ERR_SENSITIVE_SPAN";
+        case CP_ERR_SPAN_TOO_SHORT: return "CP_ERR_SPAN_TOO_SHORT";
+        case CP_ERR_CAPACITY: return "CP_ERR_CAPACITY";
+        case CP_ERR_CUDA: return "CP_ERR_CUDA";
+        case CP_ERR_UNSUPPORTED: return "CP_ERR_UNSUPPORTED";
+    }
+    return "CP_ERR_UNKNOWN";
+}
+
+cp_status cp_index_last_error(cp_index* x, void* stream) {
+    if (!x) return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t e = 0;
+    CP_CUDA_CHECK(cudaStreamSynchronize(st));
+    CP_CUDA_CHECK(cudaMemcpy(&e, &x->hdr->error, 4, cudaMemcpyDeviceToHost));
+    const int32_t z = 0;
+    CP_CUDA_CHECK(cudaMemcpy(&x->hdr->error, &z, 4, cudaMemcpyHostToDevice));
+    return (cp_status)e;
+}
+
+cp_status cp_index_snapshot(cp_index* x, cp_snapshot* o, void* stream) {
+    if (!x || !o) return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    CP_CUDA_CHECK(cudaStreamSynchronize(st));
+    DevHeader h;
+    CP_CUDA_CHECK(cudaMemcpy(&h, x->hdr, sizeof(h), cudaMemcpyDeviceToHost));
+    const int S = x->S;
+    std::vector<int32_t> sid(S), slen(S), sorg(S), spages((size_t)S * x->MP);
+    std::vector<uint8_t> sstate(S), sdig((size_t)S * 32);
+    std::vector<unsigned long long> spre(S), sfull(S), slast(S);
+    CP_CUDA_CHECK(cudaMemcpy(sid.data(), x->slot_id, 4 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(slen.data(), x->slot_len, 4 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(sorg.data(), x->slot_origin, 4 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(sstate.data(), x->slot_state, S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(spre.data(), x->slot_prefix, 8 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(sfull.data(), x->slot_full, 8 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(slast.data(), x->slot_last, 8 * S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(sdig.data(), x->slot_digest, 32 * (size_t)S, cudaMemcpyDeviceToHost));
+    CP_CUDA_CHECK(cudaMemcpy(spages.data(), x->slot_pages, 4 * (size_t)S * x->MP, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> ptok;
+    std::vector<uint16_t> pbits;
+    if (o->tokens || o->recompute) {
+        ptok.resize((size_t)x->P * CP_BLOCK);
+        pbits.resize((size_t)x->P);
+        CP_CUDA_CHECK(cudaMemcpy(ptok.data(), x->page_tokens, 4 * ptok.size(), cudaMemcpyDeviceToHost));
+        CP_CUDA_CHECK(cudaMemcpy(pbits.data(), x->page_bits, 2 * pbits.size(), cudaMemcpyDeviceToHost));
+    }
+    std::vector<int> order;
+    for (int s = 0; s < S; ++s) if (sstate[s] == CP_SLOT_LIVE) order.push_back(s);
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return sid[a] < sid[b]; });
+    o->num_live = (int32_t)order.size(); o->next_id = h.next_id; o->live_tokens = h.live_tokens;
+    o->fifo_count = h.fifo_count; o->error = h.error;
+    const int ML = x->cfg.max_span_len;
+    for (size_t q = 0; q < order.size(); ++q) {
+        const int s = order[q];
+        if (o->id) o->id[q] = sid[s];
+        if (o->len) o->len[q] = slen[s];
+        if (o->origin_pos) o->origin_pos[q] = sorg[s];
+        if (o->prefix_hash) o->prefix_hash[q] = spre[s];
+        if (o->full_hash) o->full_hash[q] = sfull[s];
+        if (o->last_used) o->last_used[q] = slast[s];
+        if (o->digest) std::memcpy(o->digest + 32 * q, &sdig[(size_t)s * 32], 32);
+        if (o->pages) std::memcpy(o->pages + (size_t)q * x->MP, &spages[(size_t)s * x->MP], 4 * (size_t)x->MP);
+        for (int t = 0; t < slen[s] && (o->tokens || o->recompute); ++t) {
+            const int page = spages[(size_t)s * x->MP + t / CP_BLOCK];
+            if (o->tokens) o->tokens[(size_t)q * ML + t] = ptok[(size_t)page * CP_BLOCK + t % CP_BLOCK];
+            if (o->recompute) o->recompute[(size_t)q * ML + t] = (pbits[page] >> (t % CP_BLOCK)) & 1;
+        }
+    }
+    if (o->fifo) {
+        std::vector<int32_t> f((size_t)x->P);
+        CP_CUDA_CHECK(cudaMemcpy(f.data(), x->fifo, 4 * f.size(), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < h.fifo_count; ++i) o->fifo[i] = f[(size_t)((h.fifo_head + i) % x->P)];
+    }
+    return CP_OK;
+}
+
+cp_status cp_hash_prefix(const cp_batch* b, uint64_t hash_seed, uint64_t* out, void* stream) {
+    if (!b || !out || b->num_reqs < 0) return CP_ERR_INVALID_ARG;
+    if (b->num_reqs == 0) return CP_OK;
+    if (!b->tokens || !b->offsets) return CP_ERR_INVALID_ARG;
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_hash_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024); attr = true; }
+    const uint64_t B = 2 + host_splitmix64(hash_seed) % (CP_PMOD - 3);
+    k_hash_prefix<<<b->num_reqs, 256, 8 * 8193, (cudaStream_t)stream>>>(b->tokens, b->offsets, B, out);
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}
+
+cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
+                          const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
+                          const uint32_t* bits, const int64_t* bits_off, uint64_t t,
+                          int32_t* out_id, int32_t* out_oc, void* stream) {
+    if (!x || !wb || !kv) return CP_ERR_INVALID_ARG;
+    if (num_spans < 0 || num_spans > x->MS) return CP_ERR_INVALID_ARG;
+    if (num_spans == 0) return CP_OK;
+    if (!span_req || !span_begin || !span_len || !out_id || !out_oc) return CP_ERR_INVALID_ARG;
+    if (!wb->tokens || !wb->offsets || !wb->mask) return CP_ERR_INVALID_ARG;          // writer mask required
+    if (wb->num_reqs < 1 || wb->num_reqs > x->cfg.max_batch_reqs || wb->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
+    if ((bits == nullptr) != (bits_off == nullptr)) return CP_ERR_INVALID_ARG;
+    if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables) return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    InsArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.hdr = x->hdr; a.tokens = wb->tokens; a.offsets = wb->offsets; a.mask = wb->mask; a.num_reqs = wb->num_reqs;
+    a.S = num_spans; a.span_req = span_req; a.span_begin = span_begin; a.span_len = span_len;
+    a.bits = bits; a.bits_off = bits_off; a.t = t; a.w = x->cfg.window_len; a.B = x->B;
+    a.capacity = x->cfg.pool_capacity_tokens; a.max_span_len = x->cfg.max_span_len;
+    a.out_id = out_id; a.out_oc = out_oc;
+    a.nslots = x->S; a.P = x->P; a.MP = x->MP;
+    a.slot_id = x->slot_id; a.slot_len = x->slot_len; a.slot_origin = x->slot_origin; a.slot_state = x->slot_state;
+    a.slot_prefix = x->slot_prefix; a.slot_full = x->slot_full; a.slot_last = x->slot_last;
+    a.slot_digest = x->slot_digest; a.slot_pages = x->slot_pages; a.fifo = x->fifo; a.slot_stack = x->slot_stack;
+    a.page_tokens = x->page_tokens; a.page_bits = x->page_bits; a.htab = x->htab; a.logT = x->logT; a.T = x->T;
+    a.pw = x->pw;
+    a.span_pre = x->span_pre; a.span_full = x->span_full; a.btab = x->btab; a.logBT = x->logBT; a.BT = x->BT;
+    a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
+    a.new_slot = x->new_slot; a.removed = x->removed;
+    a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
+    a.out_tmp = x->out_tmp;
+
+    const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
+    k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    const int64_t items = (int64_t)num_spans + x->S;
+    const size_t scan_smem = 8 * ((size_t)x->cfg.max_span_len + 1);
+    k_ins_scan<<<(int)std::min<int64_t>(items, 148 * 6), kScanThreads, scan_smem, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_verify<<<148 * 4, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    const size_t csm = CommitSmem(x->S, num_spans).total;
+    if (csm > 200 * 1024) return CP_ERR_UNSUPPORTED;
+    k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_delete<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_publish<<<std::max(1, std::min(1184, (num_spans + 7) / 8)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_rebuild_check<<<1, 1, 0, st>>>(x->hdr, x->T); CP_COUNT_LAUNCH();
+    k_rebuild_clear<<<256, 256, 0, st>>>(x->hdr, x->htab, x->T); CP_COUNT_LAUNCH();
+    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->S); CP_COUNT_LAUNCH();
+    if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    // copy the writer KV rows of the published entries into their pool pages
+    return cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
+                          x->MS, wb->offsets, nullptr, kv, 0, st);
+}
+
+}  // extern "C"

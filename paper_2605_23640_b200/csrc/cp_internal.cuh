@@ -1,0 +1,192 @@
+// cp_internal.cuh -- private declarations of libcacheprune (not part of the C-ABI).
+//
+// Device layout of an index (all inside caller-owned workspaces, see cp_index_workspace):
+//   POOL_K / POOL_V : [L][P][16][H][d] dtype             (pool pages, per layer)
+//   META            : DevHeader + slot-indexed entry table + page-indexed token/bit store
+//                     + free-page FIFO + free-slot stack + prefix hash table + power table
+//   SCRATCH         : per-call temporaries of match / gather / insert (union)
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <atomic>
+#include "../../include/cacheprune.h"
+
+#define CP_PMOD ((((uint64_t)1) << 61) - 1)
+#define CP_EMPTY_KEY (~0ULL)
+#define CP_TOMB_KEY (~0ULL - 1ULL)
+#define CP_BLOCK 16
+#define CP_MAX_LAYERS 128
+#define CP_GATHER_CHUNK 32          // tokens per gather work item
+#define CP_MAX_MATCH_TOKENS 10240   // per request, limited by shared memory (20 B / token)
+#define CP_NO_ERR_KEY (~0ULL)
+
+// slot states
+#define CP_SLOT_FREE 0
+#define CP_SLOT_LIVE 1
+
+struct HEntry {                      // open-addressing multi-value table entry (16 B)
+    unsigned long long key;          // prefix hash; CP_EMPTY_KEY / CP_TOMB_KEY are never valid hashes (< p)
+    int32_t slot;
+    int32_t pad;
+};
+
+struct DevHeader {                   // first 256 B of META
+    int32_t error;                   // sticky cp_status (0 = none)
+    int32_t next_id;
+    int32_t num_live;
+    int32_t fifo_head;
+    int32_t fifo_count;
+    int32_t slot_free_top;           // number of entries on the free-slot stack
+    uint32_t match_done;             // last-block ticket of the matcher
+    int32_t table_used;              // live + tombstone entries in the prefix table
+    long long live_tokens;
+    unsigned long long first_err;    // insert validation: min((span << 32) | code index)
+    int32_t rebuild;                 // prefix table needs a rebuild
+    int32_t n_cand;                  // insert: candidate relations found
+    int32_t n_copy;                  // insert: entries to copy in
+    int32_t n_removed;               // insert: slots removed this call
+    int32_t n_chunks;                // gather/copy: work chunks
+    int32_t n_new_live;
+    int32_t pad[46];
+};
+static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
+
+// candidate relation found by the insert scans: needle's tokens occur in haystack at offset
+struct Cand {
+    int32_t hay;      // >= 0: pool slot;  < 0: new span (-1 - j)
+    int32_t needle;   // >= 0: pool slot;  < 0: new span (-1 - j)
+    int32_t off;
+    int32_t ok;       // set by verification
+};
+
+struct cp_index {
+    cp_config cfg;
+    int64_t P;           // physical pages
+    int32_t MP;          // max pages per entry
+    int32_t S;           // slots
+    int64_t T;           // prefix-table entries (pow2)
+    int32_t logT;
+    uint64_t B, Bw;      // base and B^w
+    int32_t elem;        // bytes per element
+    // workspaces
+    char* pool_k; char* pool_v; char* meta; char* scratch;
+    size_t ws[CP_WS_COUNT];
+    // META arrays
+    DevHeader* hdr;
+    int32_t* slot_id; int32_t* slot_len; int32_t* slot_origin; uint8_t* slot_state;
+    unsigned long long* slot_prefix; unsigned long long* slot_full; unsigned long long* slot_last;
+    uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
+    int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; unsigned long long* pw;
+    // SCRATCH (match)
+    int64_t HS;          // sparse hit capacity
+    int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;
+    // SCRATCH (gather / copy-in work lists)
+    int64_t CH;          // chunk capacity
+    int32_t *chunk_hit, *chunk_t0;
+    float2* hit_cs;      // [hits][d/2] cos/sin
+    int64_t CS_HITS;     // hits capacity of hit_cs
+    // SCRATCH (insert)
+    int32_t MS;          // max spans
+    int64_t MAXC;        // candidate capacity
+    int64_t BT; int32_t logBT;
+    unsigned long long *span_pre, *span_full;
+    HEntry* btab;
+    Cand* cand;
+    int32_t *rel_off, *rel_rec;    // CSR per span of relation records (other << 2 | kind)
+    int32_t *new_slot, *removed, *cp_req, *cp_slot, *cp_dst, *cp_len, *cp_delta, *out_tmp;
+};
+
+// ---- launch bookkeeping -------------------------------------------------------------------
+extern std::atomic<unsigned long long> g_cp_launches;
+#define CP_COUNT_LAUNCH() (g_cp_launches.fetch_add(1, std::memory_order_relaxed))
+#define CP_CUDA_CHECK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return CP_ERR_CUDA; } while (0)
+
+// ---- host launchers shared across translation units ---------------------------------------
+// Copy or gather rows between a paged cache and the pool. dir 0: pool -> paged (gather, rotate by
+// delta, plan codes honoured); dir 1: paged -> pool (copy-in, no rotation).  The hit-like list
+// (req, slot, dst, len, delta) and its count live in device memory.
+cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int32_t* l_req,
+                         const int32_t* l_slot, const int32_t* l_dst, const int32_t* l_len,
+                         const int32_t* l_delta, int64_t list_cap, const int64_t* req_off,
+                         const uint8_t* plan, const cp_paged_kv* kv, int32_t flags, cudaStream_t st);
+
+// ---- device helpers ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t cp_mulmod(uint64_t a, uint64_t b) {
+    // a, b < p = 2^61-1.  a*b = hi*2^64 + lo, 2^64 = 8 * 2^61 = 8 (mod p).
+    uint64_t lo = a * b;
+    uint64_t hi = __umul64hi(a, b);
+    uint64_t r = (lo & CP_PMOD) + (lo >> 61) + (hi << 3);
+    r = (r & CP_PMOD) + (r >> 61);
+    return r >= CP_PMOD ? r - CP_PMOD : r;
+}
+__device__ __forceinline__ uint64_t cp_addmod(uint64_t a, uint64_t b) {
+    uint64_t r = a + b;
+    return r >= CP_PMOD ? r - CP_PMOD : r;
+}
+__device__ __forceinline__ uint64_t cp_submod(uint64_t a, uint64_t b) {
+    return a >= b ? a - b : a + CP_PMOD - b;
+}
+__device__ __forceinline__ uint64_t cp_tokval(int32_t t) { return (uint64_t)(int64_t)t + 1ULL; }
+
+// substring hash of positions [k, k+m) from a prefix array h[0..n]
+__device__ __forceinline__ uint64_t cp_subhash(const uint64_t* h, int k, int m, uint64_t Bm) {
+    return cp_submod(h[k + m], cp_mulmod(h[k], Bm));
+}
+
+__device__ __forceinline__ uint32_t cp_hpos(uint64_t key, int logT) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ULL) >> (64 - logT));
+}
+
+// Block-wide prefix hashes h[0..n] of tokens tok(i), i < n, into shared memory `sh` (n+1 values).
+// Parallel scan of (hash, B^len) pairs: (h1,p1) o (h2,p2) = (h1*p2 + h2, p1*p2).  `wtmp` must hold
+// 2 * (NT/32) u64 in shared memory.  Ends with __syncthreads().
+template <int NT, typename F>
+__device__ void cp_block_prefix_hash(F tok, int n, uint64_t B, uint64_t* sh, uint64_t* wtmp) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c = (n + NT - 1) / NT;
+    const int c0 = min(n, tid * c), c1 = min(n, c0 + c);
+    uint64_t hh = 0, pp = 1;
+    for (int i = c0; i < c1; ++i) { hh = cp_addmod(cp_mulmod(hh, B), cp_tokval(tok(i))); pp = cp_mulmod(pp, B); }
+    // warp inclusive scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        uint64_t h2 = __shfl_up_sync(0xffffffffu, hh, off);
+        uint64_t p2 = __shfl_up_sync(0xffffffffu, pp, off);
+        if (lane >= off) { hh = cp_addmod(cp_mulmod(h2, pp), hh); pp = cp_mulmod(p2, pp); }
+    }
+    if (lane == 31) { wtmp[2 * wid] = hh; wtmp[2 * wid + 1] = pp; }
+    __syncthreads();
+    if (wid == 0) {
+        constexpr int NW = NT / 32;
+        uint64_t wh = lane < NW ? wtmp[2 * lane] : 0, wp = lane < NW ? wtmp[2 * lane + 1] : 1;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            uint64_t h2 = __shfl_up_sync(0xffffffffu, wh, off);
+            uint64_t p2 = __shfl_up_sync(0xffffffffu, wp, off);
+            if (lane >= off) { wh = cp_addmod(cp_mulmod(h2, wp), wh); wp = cp_mulmod(p2, wp); }
+        }
+        // exclusive
+        uint64_t eh = __shfl_up_sync(0xffffffffu, wh, 1), ep = __shfl_up_sync(0xffffffffu, wp, 1);
+        if (lane == 0) { eh = 0; ep = 1; }
+        if (lane < NW) { wtmp[2 * lane] = eh; wtmp[2 * lane + 1] = ep; }
+    }
+    __syncthreads();
+    // thread exclusive prefix = warp_excl o lane_excl
+    uint64_t lh = __shfl_up_sync(0xffffffffu, hh, 1), lp = __shfl_up_sync(0xffffffffu, pp, 1);
+    if (lane == 0) { lh = 0; lp = 1; }
+    uint64_t weh = wtmp[2 * wid];
+    uint64_t start = cp_addmod(cp_mulmod(weh, lp), lh);
+    (void)lp;
+    uint64_t cur = start;
+    if (tid == 0) sh[0] = 0;
+    for (int i = c0; i < c1; ++i) { cur = cp_addmod(cp_mulmod(cur, B), cp_tokval(tok(i))); sh[i + 1] = cur; }
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool cp_err_set(const DevHeader* hdr) {
+    return *((volatile const int32_t*)&hdr->error) != 0;
+}
+__device__ __forceinline__ void cp_raise(DevHeader* hdr, int32_t code) {
+    atomicCAS(&hdr->error, 0, code);
+}

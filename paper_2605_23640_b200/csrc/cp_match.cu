@@ -1,0 +1,290 @@
+// cp_match.cu -- N1 span matcher (§4.2.2 C2; plan codes L724-727 §4.3.1).
+//
+// One CTA per request (512 threads):
+//   1. prefix hashes h[0..n] of the request by a block-wide scan of (hash, B^len) pairs
+//   2. every thread slides its windows W[k] = h[k+w] - h[k] B^w and probes the pool's prefix hash
+//      table (open addressing, 16-B entries, L2 resident) -- the prefix filter;
+//      each probe hit is a candidate (counted: c of P:L697) and gets the O(1) full-length hash
+//      pre-check against the entry's full hash
+//   3. one warp per surviving candidate compares the tokens exactly (and the reader mask, R#9);
+//      exact comparison replaces the paper's SHA-256 equality (R#5): same result, no collision risk
+//   4. warp 0 assembles hits greedily left to right with ballot scans (R#7).  The pool is
+//      containment-free (R#20), so at most one verified entry starts at any position k.
+//   5. hits -> sparse per-request scratch, LRU touch (atomicMax), plan codes + stats
+//   6. the last CTA to finish (ticket) scans the per-request hit counts and compacts the hits
+//      into the caller's dense arrays -- no extra launch, no host round trip.
+#include "cp_internal.cuh"
+#include <algorithm>
+#include <cstring>
+
+namespace {
+
+constexpr int kNT = 512;
+
+struct MatchArgs {
+    DevHeader* hdr;
+    const int32_t* tokens; const int64_t* offsets; const uint8_t* mask; int32_t R;
+    unsigned long long t; int32_t no_touch;
+    int32_t w; uint64_t B; uint64_t Bw; const unsigned long long* pw;
+    const HEntry* htab; int logT; int64_t T;
+    const int32_t* slot_id; const int32_t* slot_len; const int32_t* slot_origin;
+    const unsigned long long* slot_full; unsigned long long* slot_last;
+    const int32_t* slot_pages; int32_t MP; const int32_t* page_tokens; const uint16_t* page_bits;
+    int32_t nmax;                      // shared memory is sized for requests of <= nmax tokens
+    int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;
+    int32_t max_hits; int32_t* num_hits; int32_t* req_hit_offsets;
+    int32_t *hit_req, *hit_entry, *hit_slot, *hit_dst, *hit_len, *hit_delta;
+    uint8_t* plan; int32_t *req_covered, *req_recompute, *req_candidates;
+};
+
+struct MatchSmem {
+    size_t h, vslot, tok, clist, hk, hs, hm, total;
+    __host__ __device__ MatchSmem(int nmax, int w) {
+        const int hmax = nmax / w + 1;
+        h = 0;
+        vslot = h + 8 * ((size_t)nmax + 1);
+        tok = vslot + 4 * (size_t)nmax;
+        clist = tok + 4 * (size_t)nmax;
+        hk = clist + 4 * (size_t)nmax;
+        hs = hk + 4 * (size_t)hmax;
+        hm = hs + 4 * (size_t)hmax;
+        total = hm + 4 * (size_t)hmax;
+    }
+};
+
+__device__ __forceinline__ HEntry ld_entry(const HEntry* p) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    HEntry e;
+    e.key = v.x;
+    e.slot = (int32_t)(v.y & 0xffffffffu);
+    e.pad = 0;
+    return e;
+}
+
+__global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ uint64_t wtmp[2 * (kNT / 32)];
+    __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last;
+    __shared__ int s_scan[kNT / 32 + 1];
+    const MatchSmem L(a.nmax, a.w);
+    uint64_t* h = (uint64_t*)(sm + L.h);
+    int32_t* vslot = (int32_t*)(sm + L.vslot);
+    int32_t* tok = (int32_t*)(sm + L.tok);
+    int32_t* clist = (int32_t*)(sm + L.clist);
+    int32_t* hk = (int32_t*)(sm + L.hk);
+    int32_t* hs = (int32_t*)(sm + L.hs);
+    int32_t* hm = (int32_t*)(sm + L.hm);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int r = blockIdx.x;
+    const int64_t off = a.offsets[r];
+    const int n = (int)(a.offsets[r + 1] - off);
+    const bool skip = cp_err_set(a.hdr) || n > a.nmax;
+    if (tid == 0 && !cp_err_set(a.hdr) && n > a.nmax) cp_raise(a.hdr, CP_ERR_INVALID_ARG);
+    if (tid == 0) { s_nc = 0; s_cands = 0; s_nh = 0; s_cov = 0; s_rec = 0; }
+    int nh = 0;
+    if (!skip) {
+        // ---- 1. tokens + prefix hashes
+        for (int i = tid; i < n; i += kNT) tok[i] = a.tokens[off + i];
+        __syncthreads();
+        cp_block_prefix_hash<kNT>([&](int i) { return tok[i]; }, n, a.B, h, wtmp);
+        const int nw = n - a.w + 1;                  // number of windows (may be <= 0)
+        for (int k = tid; k < nw; k += kNT) vslot[k] = -1;
+        __syncthreads();
+        // ---- 2. rolling windows -> prefix filter -> O(1) full-hash pre-check
+        int my_cands = 0;
+        for (int k = tid; k < nw; k += kNT) {
+            const uint64_t W = cp_subhash(h, k, a.w, a.Bw);
+            uint32_t pos = cp_hpos(W, a.logT);
+            int best = -1, best_m = 0, best_id = 0;
+            while (true) {
+                const HEntry e = ld_entry(a.htab + pos);
+                if (e.key == CP_EMPTY_KEY) break;
+                if (e.key == W) {
+                    ++my_cands;
+                    const int m = __ldg(a.slot_len + e.slot);
+                    if (k + m <= n && cp_subhash(h, k, m, __ldg(a.pw + m)) == __ldg(a.slot_full + e.slot)) {
+                        const int id = __ldg(a.slot_id + e.slot);
+                        if (best < 0 || m > best_m || (m == best_m && id < best_id)) { best = e.slot; best_m = m; best_id = id; }
+                    }
+                }
+                pos = (pos + 1) & (uint32_t)(a.T - 1);
+            }
+            if (best >= 0) {
+                vslot[k] = best;
+                clist[atomicAdd(&s_nc, 1)] = k;
+            }
+        }
+        // warp-aggregated candidate count
+        for (int o = 16; o; o >>= 1) my_cands += __shfl_xor_sync(0xffffffffu, my_cands, o);
+        if (lane == 0 && my_cands) atomicAdd(&s_cands, my_cands);
+        __syncthreads();
+        // ---- 3. exact verification, one warp per candidate
+        const int nc = s_nc;
+        const uint8_t* mk = a.mask ? a.mask + off : nullptr;
+        for (int c = wid; c < nc; c += kNT / 32) {
+            const int k = clist[c];
+            const int slot = vslot[k];
+            const int m = __ldg(a.slot_len + slot);
+            const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+            int bad = 0;
+            for (int i = lane; i < m; i += 32) {
+                const int32_t et = __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15));
+                bad |= (et != tok[k + i]);
+                if (mk) bad |= mk[k + i];
+            }
+            if (__any_sync(0xffffffffu, bad) && lane == 0) vslot[k] = -1;
+        }
+        __syncthreads();
+        // ---- 4. greedy left-to-right assembly (warp 0)
+        if (wid == 0) {
+            int cursor = 0;
+            while (cursor < nw) {
+                const int k = cursor + lane;
+                const int v = k < nw ? vslot[k] : -1;
+                const unsigned bal = __ballot_sync(0xffffffffu, v >= 0);
+                if (!bal) { cursor += 32; continue; }
+                const int f = __ffs(bal) - 1;
+                const int kk = cursor + f;
+                const int slot = __shfl_sync(0xffffffffu, v, f);
+                const int m = __ldg(a.slot_len + slot);
+                if (lane == 0) { hk[nh] = kk; hs[nh] = slot; hm[nh] = m; }
+                ++nh;
+                cursor = kk + m;
+            }
+            if (lane == 0) s_nh = nh;
+        }
+        __syncthreads();
+        nh = s_nh;
+        // ---- 5. sparse hits + LRU touch
+        const int64_t base = off / a.w + r;
+        for (int i = tid; i < nh; i += kNT) {
+            const int slot = hs[i];
+            a.sp_entry[base + i] = __ldg(a.slot_id + slot);
+            a.sp_slot[base + i] = slot;
+            a.sp_dst[base + i] = hk[i];
+            a.sp_len[base + i] = hm[i];
+            a.sp_delta[base + i] = hk[i] - __ldg(a.slot_origin + slot);      // R#11
+            if (!a.no_touch) atomicMax(a.slot_last + slot, a.t);
+        }
+        // ---- plan codes (0 uncovered / 1 reused / 2 recompute) and stats
+        int cov = 0, rec = 0;
+        for (int q = tid; q < n; q += kNT) {
+            uint8_t code = CP_PLAN_UNCOVERED;
+            int lo = 0, hi = nh - 1, found = -1;
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                if (hk[mid] <= q) { found = mid; lo = mid + 1; } else hi = mid - 1;
+            }
+            if (found >= 0 && q < hk[found] + hm[found]) {
+                const int tt = q - hk[found];
+                const int page = __ldg(a.slot_pages + (int64_t)hs[found] * a.MP + (tt >> 4));
+                const int bit = (__ldg(a.page_bits + page) >> (tt & 15)) & 1;
+                code = bit ? CP_PLAN_RECOMPUTE : CP_PLAN_REUSED;
+                ++cov; rec += bit;
+            }
+            a.plan[off + q] = code;
+        }
+        for (int o = 16; o; o >>= 1) { cov += __shfl_xor_sync(0xffffffffu, cov, o); rec += __shfl_xor_sync(0xffffffffu, rec, o); }
+        if (lane == 0) { atomicAdd(&s_cov, cov); atomicAdd(&s_rec, rec); }
+        __syncthreads();
+        if (tid == 0) {
+            a.req_cnt[r] = nh;
+            a.req_covered[r] = s_cov; a.req_recompute[r] = s_rec; a.req_candidates[r] = s_cands;
+        }
+    } else if (tid == 0) {
+        a.req_cnt[r] = 0;
+    }
+    // ---- 6. last CTA: scan counts and compact into the dense output
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(&a.hdr->match_done, 1u) == (unsigned)(a.R - 1));
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (cp_err_set(a.hdr)) return;
+    // exclusive scan over R counts in chunks of kNT
+    int carry = 0;
+    for (int b0 = 0; b0 < a.R; b0 += kNT) {
+        const int i = b0 + tid;
+        const int v = i < a.R ? *((volatile int32_t*)&a.req_cnt[i]) : 0;
+        int inc = v;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_scan[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            int x = lane < kNT / 32 ? s_scan[lane] : 0, xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            if (lane < kNT / 32) s_scan[lane] = xi - x;
+            if (lane == 31) s_scan[kNT / 32] = xi;
+        }
+        __syncthreads();
+        if (i < a.R) a.req_hit_offsets[i] = carry + s_scan[wid] + inc - v;
+        carry += s_scan[kNT / 32];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        a.req_hit_offsets[a.R] = carry;
+        if (carry > a.max_hits) cp_raise(a.hdr, CP_ERR_CAPACITY);
+        else *a.num_hits = carry;
+        a.hdr->match_done = 0;
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (carry > a.max_hits) return;
+    for (int rr = wid; rr < a.R; rr += kNT / 32) {
+        const int cnt = *((volatile int32_t*)&a.req_cnt[rr]);
+        const int dst0 = a.req_hit_offsets[rr];
+        const int64_t src0 = a.offsets[rr] / a.w + rr;
+        for (int i = lane; i < cnt; i += 32) {
+            a.hit_req[dst0 + i] = rr;
+            a.hit_entry[dst0 + i] = *((volatile int32_t*)&a.sp_entry[src0 + i]);
+            a.hit_slot[dst0 + i] = *((volatile int32_t*)&a.sp_slot[src0 + i]);
+            a.hit_dst[dst0 + i] = *((volatile int32_t*)&a.sp_dst[src0 + i]);
+            a.hit_len[dst0 + i] = *((volatile int32_t*)&a.sp_len[src0 + i]);
+            a.hit_delta[dst0 + i] = *((volatile int32_t*)&a.sp_delta[src0 + i]);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, int32_t flags, const cp_hits* o,
+                                    void* stream) {
+    if (!x || !b || !o) return CP_ERR_INVALID_ARG;
+    if (b->num_reqs < 0 || b->num_reqs > x->cfg.max_batch_reqs || b->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
+    if (!o->num_hits || !o->req_hit_offsets || !o->hit_req || !o->hit_entry || !o->hit_slot || !o->hit_dst ||
+        !o->hit_len || !o->hit_delta || !o->plan || !o->req_covered || !o->req_recompute || !o->req_candidates)
+        return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (b->num_reqs == 0) {
+        CP_CUDA_CHECK(cudaMemsetAsync(o->num_hits, 0, 4, st));
+        CP_CUDA_CHECK(cudaMemsetAsync(o->req_hit_offsets, 0, 4, st));
+        return CP_OK;
+    }
+    if (!b->tokens || !b->offsets) return CP_ERR_INVALID_ARG;
+    int nmax = b->max_req_len > 0 ? std::min(b->max_req_len, x->cfg.max_req_tokens) : x->cfg.max_req_tokens;
+    nmax = std::max(nmax, 1);
+    MatchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.hdr = x->hdr; a.tokens = b->tokens; a.offsets = b->offsets; a.mask = b->mask; a.R = b->num_reqs;
+    a.t = t; a.no_touch = (flags & CP_MATCH_NO_TOUCH) ? 1 : 0;
+    a.w = x->cfg.window_len; a.B = x->B; a.Bw = x->Bw; a.pw = x->pw;
+    a.htab = x->htab; a.logT = x->logT; a.T = x->T;
+    a.slot_id = x->slot_id; a.slot_len = x->slot_len; a.slot_origin = x->slot_origin; a.slot_full = x->slot_full;
+    a.slot_last = x->slot_last; a.slot_pages = x->slot_pages; a.MP = x->MP; a.page_tokens = x->page_tokens;
+    a.page_bits = x->page_bits; a.nmax = nmax;
+    a.sp_entry = x->sp_entry; a.sp_slot = x->sp_slot; a.sp_dst = x->sp_dst; a.sp_len = x->sp_len;
+    a.sp_delta = x->sp_delta; a.req_cnt = x->req_cnt;
+    a.max_hits = o->max_hits; a.num_hits = o->num_hits; a.req_hit_offsets = o->req_hit_offsets;
+    a.hit_req = o->hit_req; a.hit_entry = o->hit_entry; a.hit_slot = o->hit_slot; a.hit_dst = o->hit_dst;
+    a.hit_len = o->hit_len; a.hit_delta = o->hit_delta; a.plan = o->plan;
+    a.req_covered = o->req_covered; a.req_recompute = o->req_recompute; a.req_candidates = o->req_candidates;
+    const size_t smem = MatchSmem(nmax, a.w).total;
+    static int attr_set = 0;
+    if (!attr_set) { cudaFuncSetAttribute(k_match, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024); attr_set = 1; }
+    if (smem > 210 * 1024) return CP_ERR_UNSUPPORTED;
+    CP_CUDA_CHECK(cudaMemsetAsync(&x->hdr->match_done, 0, 4, st));
+    k_match<<<b->num_reqs, kNT, smem, st>>>(a);
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}

@@ -1,0 +1,207 @@
+// cp_score.cu -- N3 recompute score + top-rho selection (§4.2.1 C1 Step 3;
+// rho = 25% default).  The paper computes the per-token inter/intra sums from a summed-area
+// table on the CPU after copying the attention matrix off the GPU (L770, 383 ms at 10K tokens,
+// L1201); here the attention never leaves HBM: the row sums are streamed directly.
+//
+//   k_score_rows : one warp per span row i; reads A_h[i][0..i] (fp32, 128-bit loads where aligned),
+//                  accumulates q(x) = trunc(x * 2^40) in int64 (R#17: exact and order independent,
+//                  so the GPU and the oracle agree bit for bit) with sign + for j < l*, - for j >= l*.
+//   k_score_topk : one CTA per span; 8-pass MSB radix select of the k-th largest score
+//                  (k = ceil(rho_num*m/rho_den), R#15), then ties at the threshold go to the smaller
+//                  index (R#16) via a block scan; bits packed LSB-first.
+#include "cp_internal.cuh"
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+constexpr int kSpansPerLaunch = 256;
+constexpr int kRowThreads = 256;
+constexpr int kTopkThreads = 1024;
+
+struct SpanDesc {
+    const float* A;
+    int32_t n, heads, l, r;
+    int64_t score_off, bits_off, row_begin;
+};
+
+struct ScoreArgs {
+    SpanDesc sp[kSpansPerLaunch];
+    int32_t nsp;
+    int64_t total_rows;
+    int32_t rho_num, rho_den;
+    long long* scores;
+    uint32_t* bits;
+};
+
+// q(x) = trunc(x * 2^40) computed exactly from the fp32 bit pattern (|x| < 2^23)
+__device__ __forceinline__ long long fixq(float x) {
+    const uint32_t b = __float_as_uint(x);
+    const int e = (int)((b >> 23) & 0xffu);
+    if (e == 0) return 0;                           // zero / subnormal: |x| 2^40 < 1
+    const unsigned long long mant = (unsigned long long)((b & 0x7fffffu) | 0x800000u);   // x = mant 2^(e-150)
+    const int sh = e - 110;                         // (e - 150) + 40
+    unsigned long long v;
+    if (sh >= 0) v = mant << min(sh, 39);
+    else v = (sh > -64) ? (mant >> (-sh)) : 0ULL;
+    return (b >> 31) ? -(long long)v : (long long)v;
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t gr = warp; gr < a.total_rows; gr += nwarps) {
+        int lo = 0, hi = a.nsp - 1;
+        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
+        const SpanDesc& s = a.sp[lo];
+        const int i = s.l + (int)(gr - s.row_begin);
+        const int l = s.l;
+        long long acc = 0;
+        for (int h = 0; h < s.heads; ++h) {
+            const float* row = s.A + ((int64_t)h * s.n + i) * (int64_t)s.n;
+            const int cnt = i + 1;                                   // causal: columns 0..i
+            const int mis = (int)((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
+            const int head = min(cnt, mis ? 4 - mis : 0);             // scalars until 16-B aligned
+            if (lane < head) { const long long v = fixq(__ldg(row + lane)); acc += lane < l ? v : -v; }
+            const int nvec = (cnt - head) >> 2;
+            const float4* v4 = reinterpret_cast<const float4*>(row + head);
+            for (int q = lane; q < nvec; q += 32) {
+                float4 f;
+                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "l"(v4 + q));
+                const int j = head + 4 * q;
+                const long long a0 = fixq(f.x), a1 = fixq(f.y), a2 = fixq(f.z), a3 = fixq(f.w);
+                acc += (j < l ? a0 : -a0) + (j + 1 < l ? a1 : -a1) + (j + 2 < l ? a2 : -a2) + (j + 3 < l ? a3 : -a3);
+            }
+            const int tail0 = head + 4 * nvec;
+            if (tail0 + lane < cnt) { const int j = tail0 + lane; const long long v = fixq(__ldg(row + j)); acc += j < l ? v : -v; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.scores[s.score_off + (i - l)] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_score_topk(const ScoreArgs a) {
+    extern __shared__ __align__(16) unsigned char smt[];
+    __shared__ int hist[256];
+    __shared__ int s_digit, s_rem;
+    __shared__ int s_wsum[kTopkThreads / 32 + 1];
+    const SpanDesc& s = a.sp[blockIdx.x];
+    const int m = s.r - s.l + 1;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long* key = (unsigned long long*)smt;
+    uint8_t* sel = (uint8_t*)(smt + 8 * (size_t)m);
+    const long long kk = ((long long)a.rho_num * m + a.rho_den - 1) / a.rho_den;
+    const int nwords = (m + 31) / 32;
+    uint32_t* bits = a.bits + s.bits_off;
+    if (kk <= 0 || kk >= m) {
+        const uint32_t fill = kk <= 0 ? 0u : 0xffffffffu;
+        for (int w = tid; w < nwords; w += blockDim.x) {
+            const int nb = min(32, m - 32 * w);
+            bits[w] = nb == 32 ? fill : (fill & ((1u << nb) - 1u));
+        }
+        return;
+    }
+    for (int i = tid; i < m; i += blockDim.x) key[i] = (unsigned long long)a.scores[s.score_off + i] ^ (1ULL << 63);
+    unsigned long long prefix = 0, pmask = 0;
+    if (tid == 0) s_rem = (int)kk;
+    __syncthreads();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < m; i += blockDim.x)
+            if ((key[i] & pmask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 255], 1);
+        __syncthreads();
+        if (tid == 0) {
+            int cum = 0, rem = s_rem, dg = 0;
+            for (int b = 255; b >= 0; --b) {
+                if (cum + hist[b] >= rem) { dg = b; rem -= cum; break; }
+                cum += hist[b];
+            }
+            s_digit = dg; s_rem = rem;
+        }
+        __syncthreads();
+        prefix |= (unsigned long long)s_digit << shift;
+        pmask |= 0xFFULL << shift;
+        __syncthreads();
+    }
+    const unsigned long long T = prefix;
+    const int take_eq = s_rem;                      // keys equal to T to select, smallest index first
+    // rank among equals: chunked block scan
+    const int c = (m + kTopkThreads - 1) / kTopkThreads, c0 = min(m, tid * c), c1 = min(m, c0 + c);
+    int loc = 0;
+    for (int i = c0; i < c1; ++i) loc += key[i] == T;
+    int inc = loc;
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+    if (lane == 31) s_wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int x = lane < kTopkThreads / 32 ? s_wsum[lane] : 0, xi = x;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+        if (lane < kTopkThreads / 32) s_wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    int rank = s_wsum[wid] + inc - loc;
+    for (int i = c0; i < c1; ++i) {
+        const bool eq = key[i] == T;
+        sel[i] = key[i] > T || (eq && rank < take_eq);
+        rank += eq;
+    }
+    __syncthreads();
+    for (int w = tid; w < nwords; w += blockDim.x) {
+        uint32_t v = 0;
+        for (int b = 0; b < 32 && 32 * w + b < m; ++b) v |= (uint32_t)sel[32 * w + b] << b;
+        bits[w] = v;
+    }
+}
+
+}  // namespace
+
+extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, const int32_t* n_h,
+                                        const int32_t* heads_h, const int32_t* l_h, const int32_t* r_h,
+                                        int32_t rho_num, int32_t rho_den, int32_t mode, int32_t max_m,
+                                        int64_t* out_scores, const int64_t* score_off_h, uint32_t* out_bits,
+                                        const int64_t* bits_off_h, void* stream) {
+    if (mode == CP_SCORE_KVDEV) return CP_ERR_UNSUPPORTED;
+    if (mode != CP_SCORE_INTER_INTRA) return CP_ERR_INVALID_ARG;
+    if (num_spans < 0 || rho_den <= 0 || rho_num < 0 || rho_num > rho_den || max_m < 1 || max_m > 16384) return CP_ERR_INVALID_ARG;
+    if (num_spans == 0) return CP_OK;
+    if (!attn_h || !n_h || !heads_h || !l_h || !r_h || !out_scores || !score_off_h || !out_bits || !bits_off_h)
+        return CP_ERR_INVALID_ARG;
+    for (int s = 0; s < num_spans; ++s) {
+        if (!attn_h[s] || n_h[s] < 1 || heads_h[s] < 1 || l_h[s] < 0 || r_h[s] < l_h[s] || r_h[s] >= n_h[s]) return CP_ERR_INVALID_ARG;
+        if (r_h[s] - l_h[s] + 1 > max_m) return CP_ERR_INVALID_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t smem = 9 * (size_t)max_m + 16;
+    static size_t attr = 0;
+    if (smem > attr) {
+        if (cudaFuncSetAttribute(k_score_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 * 1024)) != cudaSuccess)
+            return CP_ERR_CUDA;
+        attr = smem;
+    }
+    std::vector<ScoreArgs> args(1);
+    for (int s0 = 0; s0 < num_spans; s0 += kSpansPerLaunch) {
+        ScoreArgs& a = args[0];
+        std::memset(&a, 0, sizeof(a));
+        a.nsp = std::min(kSpansPerLaunch, num_spans - s0);
+        int64_t rows = 0;
+        for (int q = 0; q < a.nsp; ++q) {
+            const int s = s0 + q;
+            a.sp[q] = SpanDesc{attn_h[s], n_h[s], heads_h[s], l_h[s], r_h[s], score_off_h[s], bits_off_h[s], rows};
+            rows += r_h[s] - l_h[s] + 1;
+        }
+        a.total_rows = rows; a.rho_num = rho_num; a.rho_den = rho_den;
+        a.scores = (long long*)out_scores; a.bits = out_bits;
+        const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 8);
+        k_score_rows<<<grid, kRowThreads, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_score_topk<<<a.nsp, kTopkThreads, smem, st>>>(a);
+        CP_COUNT_LAUNCH();
+        if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    }
+    return CP_OK;
+}

@@ -1,0 +1,222 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (north star): bit exact for hashes, entry tables, page lists, hits, plan codes, recompute
+bits and gathered V; re-rotated K within max-abs 2e-2 (bf16) or 1e-5 relative (fp32).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle.oracle as O  # noqa: E402
+from synth.gen import Batch, Geometry, make_workload, pack_batches  # noqa: E402
+from tests.harness import Case, ParityReport, run_round_parity  # noqa: E402
+
+
+def _assert(res):
+    assert res["ok"], res["notes"]
+
+
+def test_toy_config1_all_rounds():
+    case = Case(make_workload(1))
+    res = run_round_parity(case)
+    _assert(res)
+    assert res["moved_hits"] > 0 and res["covered"] > 0
+
+
+def test_toy_gptj_and_no_reader_mask():
+    wl = make_workload(1, seed=11)
+    wl.geometry.rope_style = "gptj"
+    case = Case(wl, use_reader_mask=False)
+    _assert(run_round_parity(case))
+
+
+def test_msmarco_config2_reduced():
+    case = Case(make_workload(2, scale=0.125), sample_reqs=4, sample_layers=[0, 17, 31])
+    res = run_round_parity(case, score=True)
+    _assert(res)
+    assert res["covered"] / res["tokens"] > 0.9
+
+
+def test_msmarco_config2_full_size_sampled():
+    """Config 2 at its full size in the bench's launch configuration; sampled KV rows."""
+    case = Case(make_workload(2), sample_reqs=2, sample_layers=[0, 31])
+    wb, rb = case.wl.rounds[0]
+    rep = ParityReport()
+    case.insert(wb, rep)
+    case.score_parity(wb, rep, max_spans=24)
+    case.match_and_gather(rb, rep, check_kv=True)
+    assert rep.ok, rep.notes[:10]
+
+
+def test_multidoc_config3_reduced():
+    wl = make_workload(3, scale=0.08)
+    case = Case(wl, sample_reqs=3, sample_layers=[0, 31])
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]
+    assert rep.stats["moved_hits"] > 0
+
+
+def test_70b_layer_shard_config4_reduced():
+    """Config 4 geometry (80 layers), one layer shard of 10 layers as one rank holds it."""
+    wl = make_workload(4, scale=0.05)
+    case = Case(wl, layer_range=(70, 80), sample_reqs=2, sample_layers=[0, 9])
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]
+
+
+def test_70b_head_shard():
+    wl = make_workload(4, scale=0.03)
+    case = Case(wl, layer_range=(0, 4), head_range=(3, 4), sample_reqs=2)
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]
+
+
+def test_churn_config5_reduced_with_eviction():
+    """Config 5 shape with a small token budget so LRU eviction, duplicates and supersedes happen."""
+    wl = make_workload(5, scale=0.02)          # 1 batch... scale rounds up below
+    from synth.gen import churn_workload
+    wl = churn_workload(batches=4, per_batch=24, corpus=60, capacity_tokens=9000,
+                        geometry=Geometry(2, 2, 64, "bf16", 500000.0))
+    case = Case(wl, sample_reqs=3)
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.match_and_gather(rb, rep)
+        case.insert(wb, rep)
+    assert rep.ok, rep.notes[:10]
+    assert rep.stats["duplicate"] > 0
+
+
+def test_supersede_and_contained():
+    g = Geometry(1, 1, 16, "fp32", 10000.0, window_len=8)
+    rng = np.random.default_rng(0)
+    base = rng.integers(1000, 2000, 400).astype(np.int32)
+
+    def wb(begin, end, wid):
+        t = base[begin:end]
+        return Batch(tokens=t.copy(), offsets=np.array([0, len(t)], np.int64), mask=np.zeros(len(t), np.uint8),
+                     writer_ids=np.array([wid], np.int64), span_req=np.zeros(1, np.int32),
+                     span_begin=np.zeros(1, np.int32), span_len=np.array([len(t)], np.int32))
+    from synth.gen import Workload
+    rounds = [(wb(50, 150, 0), wb(0, 300, 100)), (wb(0, 300, 1), wb(0, 300, 101)),
+              (wb(60, 120, 2), wb(0, 300, 102)), (wb(0, 300, 3), wb(0, 300, 103))]
+    wl = Workload("edge", g, rounds, pool_capacity_tokens=10000, max_span_len=512)
+    case = Case(wl)
+    res = run_round_parity(case, score=False)
+    _assert(res)
+
+
+def test_errors_have_no_side_effects():
+    case = Case(make_workload(1))
+    wb, rb = case.wl.rounds[0]
+    rep = ParityReport()
+    case.insert(wb, rep)
+    before = case.dev.snapshot()
+    bad = Batch(tokens=wb.tokens, offsets=wb.offsets, mask=wb.mask, writer_ids=wb.writer_ids,
+                span_req=np.array([0, 0], np.int32), span_begin=np.array([0, 120], np.int32),
+                span_len=np.array([128, 20], np.int32))
+    case.insert(bad, rep)                      # span 1 covers PII1 -> CP_ERR_SENSITIVE_SPAN on both sides
+    after = case.dev.snapshot()
+    assert rep.ok, rep.notes
+    assert [e["id"] for e in after["entries"]] == [e["id"] for e in before["entries"]]
+    assert after["fifo_count"] == before["fifo_count"] and after["next_id"] == before["next_id"]
+
+
+def test_empty_short_and_max_requests():
+    g = Geometry(2, 1, 32, "bf16", 500000.0)
+    rng = np.random.default_rng(5)
+    long_req = rng.integers(1000, 50000, 10240).astype(np.int32)
+    w = Batch(tokens=long_req[3000:5000].copy(), offsets=np.array([0, 2000], np.int64),
+              mask=np.zeros(2000, np.uint8), writer_ids=np.array([0], np.int64),
+              span_req=np.zeros(1, np.int32), span_begin=np.zeros(1, np.int32), span_len=np.array([2000], np.int32))
+    parts = [Batch(tokens=np.zeros(0, np.int32), offsets=np.array([0, 0], np.int64), mask=np.zeros(0, np.uint8),
+                   writer_ids=np.array([1], np.int64)),
+             Batch(tokens=long_req[3000:3100].copy(), offsets=np.array([0, 100], np.int64),
+                   mask=np.zeros(100, np.uint8), writer_ids=np.array([2], np.int64)),
+             Batch(tokens=long_req, offsets=np.array([0, 10240], np.int64), mask=np.zeros(10240, np.uint8),
+                   writer_ids=np.array([3], np.int64))]
+    from synth.gen import Workload
+    wl = Workload("edge2", g, [(w, pack_batches(parts))], pool_capacity_tokens=100000, max_span_len=2048)
+    case = Case(wl)
+    res = run_round_parity(case, score=False)
+    _assert(res)
+    assert res["hits"] == 1
+
+
+def test_identical_unmasked_prompt_is_prefix_reuse():
+    g = Geometry(2, 2, 64, "bf16", 500000.0)
+    rng = np.random.default_rng(7)
+    p = rng.integers(1000, 100000, 700).astype(np.int32)
+    mk = lambda wid, spans: Batch(tokens=p.copy(), offsets=np.array([0, 700], np.int64), mask=np.zeros(700, np.uint8),
+                                  writer_ids=np.array([wid], np.int64), span_req=np.zeros(len(spans), np.int32),
+                                  span_begin=np.array([s[0] for s in spans], np.int32),
+                                  span_len=np.array([s[1] for s in spans], np.int32))
+    from synth.gen import Workload
+    wl = Workload("prefix", g, [(mk(0, [(0, 700)]), mk(1, []))], pool_capacity_tokens=10000, max_span_len=1024)
+    case = Case(wl, rho=(0, 4))
+    rep = ParityReport()
+    case.insert(wl.rounds[0][0], rep)
+    case.match_and_gather(wl.rounds[0][1], rep)
+    assert rep.ok, rep.notes
+    assert rep.stats["hits"] == 1 and rep.stats["covered"] == 700 and rep.stats["moved_hits"] == 0
+
+
+def test_hash_prefix_matches_oracle():
+    import paper_2605_23640_b200 as cp
+    rng = np.random.default_rng(3)
+    lens = [0, 1, 5, 300, 8192, 9000]
+    toks = [rng.integers(0, 128256, n).astype(np.int32) for n in lens]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    db = cp.DeviceBatch.from_numpy(np.concatenate(toks), offs, None)
+    out = cp.hash_prefix(db, 42).cpu().numpy().view(np.uint64)
+    B = O.hash_base(42)
+    for r, t in enumerate(toks):
+        exp = O.prefix_hashes(t, B)
+        got = out[offs[r] + r: offs[r] + r + lens[r] + 1]
+        assert np.array_equal(got, exp), r
+
+
+def test_determinism_two_runs():
+    outs = []
+    for _ in range(2):
+        case = Case(make_workload(2, scale=0.05), sample_reqs=1, sample_layers=[0])
+        rep = ParityReport()
+        wb, rb = case.wl.rounds[0]
+        case.insert(wb, rep)
+        db = case._dev_batch(rb)
+        hits = case.dev.match_spans(db, 99)
+        outs.append((case.dev.snapshot(), hits.to_host()))
+    (s0, h0), (s1, h1) = outs
+    assert [e["pages"].tolist() for e in s0["entries"]] == [e["pages"].tolist() for e in s1["entries"]]
+    for k in ("hit_entry", "hit_dst", "hit_delta", "plan"):
+        assert np.array_equal(h0[k], h1[k])
+
+
+def test_score_edge_cases():
+    import paper_2605_23640_b200 as cp
+    rng = np.random.default_rng(1)
+    mats, ns, ls, rs = [], [], [], []
+    for n, l, r in [(1, 0, 0), (5, 0, 4), (33, 1, 32), (257, 100, 256), (1000, 3, 999), (130, 0, 129)]:
+        A = np.tril(rng.uniform(0, 1, (n, n))).astype(np.float32)
+        A /= A.sum(1, keepdims=True)
+        mats.append(torch.from_numpy(A).cuda()); ns.append(n); ls.append(l); rs.append(r)
+    A = np.eye(64, dtype=np.float32)                       # all-tie case
+    mats.append(torch.from_numpy(A).cuda()); ns.append(64); ls.append(10); rs.append(39)
+    for num, den in [(1, 4), (0, 4), (4, 4), (1, 10), (3, 7)]:
+        sc, bits, so, bo = cp.score_deviation(mats, ns, [1] * len(ns), ls, rs, num, den)
+        sc, bits = sc.cpu().numpy(), bits.cpu().numpy().view(np.uint32)
+        for q in range(len(ns)):
+            m = rs[q] - ls[q] + 1
+            osc, ob = O.score(mats[q].cpu().numpy(), ls[q], rs[q], num, den)
+            assert np.array_equal(sc[so[q]:so[q] + m], osc)
+            assert np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob), (q, num, den)

@@ -511,3 +511,10 @@ int32_t orc_score(const float* A, int64_t n, int32_t heads, int32_t l, int32_t r
     free(v);
     return ORC_OK;
 }
+
+/* Re-rotate `nrows` consecutive rows (plain loop over orc_rerotate_row). */
+void orc_rerotate_rows(const float* xin, int64_t nrows, int32_t H, int32_t d, int32_t gptj, double theta_base,
+                       int64_t delta, int32_t out_bf16, float* out) {
+    for (int64_t r = 0; r < nrows; ++r)
+        orc_rerotate_row(xin + r * (int64_t)H * d, H, d, gptj, theta_base, delta, out_bf16, out + r * (int64_t)H * d);
+}

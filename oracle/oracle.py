@@ -60,6 +60,7 @@ def lib():
             "orc_fifo_get": (None, [vp, vp]),
             "orc_rerotate_row": (None, [vp, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_score": (i32, [vp, i64, i32, i32, i32, i32, i32, vp, vp]),
+            "orc_rerotate_rows": (None, [vp, i64, i32, i32, i32, C.c_double, i64, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -132,10 +133,8 @@ def rerotate_row(row, H: int, d: int, theta: float, delta: int, bf16: bool, gptj
 def rerotate_rows(rows, H, d, theta, delta, bf16, gptj=False) -> np.ndarray:
     rows = _c(rows, np.float32)
     out = np.empty_like(rows)
-    flat_in = rows.reshape(-1, H * d)
-    flat_out = out.reshape(-1, H * d)
-    for i in range(flat_in.shape[0]):
-        flat_out[i] = rerotate_row(flat_in[i], H, d, theta, delta, bf16, gptj)
+    n = rows.size // (H * d)
+    lib().orc_rerotate_rows(_p(rows), n, H, d, int(gptj), float(theta), int(delta), int(bf16), _p(out))
     return out
 
 

@@ -221,6 +221,9 @@ cp_status cp_index_last_error(cp_index* idx, void* stream);
 /* Hash base B of an index (diagnostic). */
 uint64_t cp_index_hash_base(const cp_index* idx);
 
+/* Select the gather kernel's (unroll, min-blocks) variant 0-3 (A/B measurement; default 0). */
+cp_status cp_set_gather_variant(int32_t variant);
+
 /* Number of kernels this library launched since load (evidence for gpu_launches). */
 uint64_t cp_kernel_launch_count(void);
 

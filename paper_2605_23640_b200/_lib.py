@@ -73,6 +73,7 @@ EXPORTS = {
     "cp_index_last_error": (i32, [vp, vp]),
     "cp_index_hash_base": (u64, [vp]),
     "cp_kernel_launch_count": (u64, []),
+    "cp_set_gather_variant": (i32, [i32]),
     "cp_status_string": (C.c_char_p, [i32]),
 }
 

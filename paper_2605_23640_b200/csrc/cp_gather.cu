@@ -13,12 +13,12 @@
 // dir 1 (insert copy-in) moves writer rows into pool pages unrotated with the same engine.
 #include "cp_internal.cuh"
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace {
 
 constexpr int kRowsThreads = 256;
-constexpr int kUnroll = 4;
 constexpr int kPrepThreads = 512;
 
 struct RowsArgs {
@@ -120,8 +120,8 @@ __device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16) {
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <typename T, bool GPTJ>
-__global__ void __launch_bounds__(kRowsThreads) k_rows(RowsArgs a) {
+template <typename T, bool GPTJ, bool CREG, int UNROLL, int MINB>
+__global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     constexpr int VEC = Vec<T>::N;
     __shared__ int64_t s_src[CP_GATHER_CHUNK], s_dst[CP_GATHER_CHUNK];
     __shared__ int s_code[CP_GATHER_CHUNK];
@@ -136,6 +136,14 @@ __global__ void __launch_bounds__(kRowsThreads) k_rows(RowsArgs a) {
     const int tpr = rowE / (2 * VEC);                   // tasks per token row
     const bool zero_rec = (a.flags & CP_ZERO_RECOMPUTE) != 0;
     const int64_t pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
+    // CREG (tpr divides the block): a thread's column task, and so its cos/sin, is fixed
+    constexpr bool creg = CREG;
+    auto task_geom = [&](int j, int& lo, int& hi, int& i0) {
+        if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; hi = lo + half; i0 = sub * VEC; }
+        else { lo = j * 2 * VEC; hi = lo + VEC; i0 = (lo % a.d) / 2; }
+    };
+    int lo_t = 0, hi_t = 0, i0_t = 0;
+    task_geom(tid % tpr, lo_t, hi_t, i0_t);
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int c = (int)(item / a.L), l = (int)(item % a.L);
         const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
@@ -153,65 +161,69 @@ __global__ void __launch_bounds__(kRowsThreads) k_rows(RowsArgs a) {
             if (a.dir == 0) { s_src[tid] = pool_row; s_dst[tid] = paged_row; s_code[tid] = a.plan[a.req_off[r] + q]; }
             else { s_src[tid] = paged_row; s_dst[tid] = pool_row; s_code[tid] = CP_PLAN_REUSED; }
         }
-        if (delta != 0) for (int i = tid; i < half; i += kRowsThreads) s_cs[i] = a.hit_cs[(int64_t)hh * half + i];
+        float2 csr[VEC];
+        if (delta != 0) {
+            const float2* tab = a.hit_cs + (int64_t)hh * half;
+            if (creg) {
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) csr[e] = tab[i0_t + e];
+            } else {
+                for (int i = tid; i < half; i += kRowsThreads) s_cs[i] = tab[i];
+            }
+        }
         __syncthreads();
         const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
         const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
         T* dstK = (T*)(a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T));
         T* dstV = (T*)(a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T));
         const int ntask = ntok * tpr;
-        for (int base = 0; base < ntask; base += kRowsThreads * kUnroll) {
-            uint4 klo[kUnroll], khi[kUnroll], vlo[kUnroll], vhi[kUnroll];
-            int64_t so[kUnroll], dso[kUnroll];
-            int code[kUnroll], i0[kUnroll];
+        for (int base = 0; base < ntask; base += kRowsThreads * UNROLL) {
+            uint4 klo[UNROLL], khi[UNROLL], vlo[UNROLL], vhi[UNROLL];
+            int gg[UNROLL], code[UNROLL];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < UNROLL; ++u) {
                 const int task = base + u * kRowsThreads + tid;
                 code[u] = -1;
                 if (task < ntask) {
-                    const int g = task / tpr, j = task - g * tpr;
-                    int lo;
-                    if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; i0[u] = sub * VEC; }
-                    else { lo = j * 2 * VEC; i0[u] = (lo % a.d) / 2; }
-                    const int hi = GPTJ ? lo + VEC : lo + half;
+                    const int g = task / tpr;
+                    int lo = lo_t, hi = hi_t, i0 = i0_t;
+                    if (!creg) task_geom(task - g * tpr, lo, hi, i0);
+                    gg[u] = creg ? g : task;
                     code[u] = s_code[g];
-                    so[u] = s_src[g] + lo; dso[u] = s_dst[g] + lo;
-                    const int64_t shi = s_src[g] + hi;
                     if (!(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
-                        klo[u] = ld_stream(srcK + so[u]); khi[u] = ld_stream(srcK + shi);
-                        vlo[u] = ld_stream(srcV + so[u]); vhi[u] = ld_stream(srcV + shi);
+                        const int64_t so = s_src[g];
+                        klo[u] = ld_stream(srcK + so + lo); khi[u] = ld_stream(srcK + so + hi);
+                        vlo[u] = ld_stream(srcV + so + lo); vhi[u] = ld_stream(srcV + so + hi);
                     }
-                    dso[u] = dso[u];
-                    so[u] = hi - lo;                                   // reuse: offset of the partner
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < UNROLL; ++u) {
                 if (code[u] < 0) continue;
-                T* dk = dstK + dso[u];
-                T* dv = dstV + dso[u];
-                const int poff = (int)so[u];
+                int lo = lo_t, hi = hi_t, i0 = i0_t, g = gg[u];
+                if (!creg) { g = gg[u] / tpr; task_geom(gg[u] - g * tpr, lo, hi, i0); }
+                const int64_t dof = s_dst[g];
+                T* dk = dstK + dof;
+                T* dv = dstV + dof;
                 if (code[u] == CP_PLAN_RECOMPUTE && zero_rec) {
                     const uint4 z = make_uint4(0, 0, 0, 0);
-                    st_stream(dk, z); st_stream(dk + poff, z); st_stream(dv, z); st_stream(dv + poff, z);
+                    st_stream(dk + lo, z); st_stream(dk + hi, z); st_stream(dv + lo, z); st_stream(dv + hi, z);
                     continue;
                 }
                 if (delta != 0) {
                     float x[VEC], y[VEC];
                     unpack(klo[u], x, T()); unpack(khi[u], y, T());
-                    if (!GPTJ) {
 #pragma unroll
-                        for (int e = 0; e < VEC; ++e) {
-                            const float2 cs = s_cs[i0[u] + e];
+                    for (int e = 0; e < VEC; ++e) {
+                        // NeoX: pair (x[e], y[e]) uses theta_{i0+e}; GPT-J: pairs inside x and inside y
+                        if (!GPTJ) {
+                            const float2 cs = creg ? csr[e] : s_cs[i0 + e];
                             const float xo = fmaf(x[e], cs.x, -y[e] * cs.y);
                             const float yo = fmaf(y[e], cs.x, x[e] * cs.y);
                             x[e] = xo; y[e] = yo;
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < VEC; e += 2) {
-                            const float2 c0 = s_cs[i0[u] + e / 2];
-                            const float2 c1 = s_cs[i0[u] + VEC / 2 + e / 2];
+                        } else if ((e & 1) == 0) {
+                            const float2 c0 = creg ? csr[e / 2] : s_cs[i0 + e / 2];
+                            const float2 c1 = creg ? csr[VEC / 2 + e / 2] : s_cs[i0 + VEC / 2 + e / 2];
                             const float x0 = fmaf(x[e], c0.x, -x[e + 1] * c0.y), x1 = fmaf(x[e + 1], c0.x, x[e] * c0.y);
                             const float y0 = fmaf(y[e], c1.x, -y[e + 1] * c1.y), y1 = fmaf(y[e + 1], c1.x, y[e] * c1.y);
                             x[e] = x0; x[e + 1] = x1; y[e] = y0; y[e + 1] = y1;
@@ -219,8 +231,8 @@ __global__ void __launch_bounds__(kRowsThreads) k_rows(RowsArgs a) {
                     }
                     klo[u] = pack(x, T()); khi[u] = pack(y, T());
                 }
-                st_stream(dk, klo[u]); st_stream(dk + poff, khi[u]);
-                st_stream(dv, vlo[u]); st_stream(dv + poff, vhi[u]);
+                st_stream(dk + lo, klo[u]); st_stream(dk + hi, khi[u]);
+                st_stream(dv + lo, vlo[u]); st_stream(dv + hi, vhi[u]);
             }
         }
         __syncthreads();
@@ -265,15 +277,46 @@ __global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int
     }
 }
 
-int g_rows_grid = 0;
-int rows_grid() {
-    if (!g_rows_grid) {
-        int dev = 0, sms = 148;
+int g_sms = 0;
+int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        g_rows_grid = sms * 4;
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
     }
-    return g_rows_grid;
+    return g_sms;
+}
+int rows_grid() { return sm_count() * 4; }
+
+// variant = (UNROLL, MINB): selectable with CP_GATHER_VARIANT for A/B measurement
+template <typename T, bool G, bool CR>
+cp_status launch_rows_c(const RowsArgs& a, int variant, cudaStream_t st) {
+    auto go = [&](auto kern) -> cp_status {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRowsThreads, 0);
+        const int grid = sm_count() * std::max(1, occ);
+        kern<<<grid, kRowsThreads, 0, st>>>(a);
+        return CP_OK;
+    };
+    switch (variant) {
+        case 1: return go(k_rows<T, G, CR, 2, 4>);
+        case 2: return go(k_rows<T, G, CR, 4, 2>);
+        case 3: return go(k_rows<T, G, CR, 8, 1>);
+        default: return go(k_rows<T, G, CR, 3, 2>);      // measured best on B200 (tools/gather_ab.py)
+    }
+}
+template <typename T, bool G>
+cp_status launch_rows_t(const RowsArgs& a, int variant, cudaStream_t st) {
+    constexpr int VEC = Vec<T>::N;
+    const int tpr = a.H * a.d / (2 * VEC);
+    return (kRowsThreads % tpr == 0) ? launch_rows_c<T, G, true>(a, variant, st) : launch_rows_c<T, G, false>(a, variant, st);
+}
+
+int g_variant = -1;
+int gather_variant() {
+    if (g_variant < 0) { const char* e = getenv("CP_GATHER_VARIANT"); g_variant = e ? atoi(e) : 0; }
+    return g_variant;
 }
 
 }  // namespace
@@ -300,17 +343,18 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;
     k_rows_prep<<<dir == 0 ? 148 : 1, kPrepThreads, 0, st>>>(a);
     CP_COUNT_LAUNCH();
-    const int grid = rows_grid();
     const bool bf16 = x->cfg.dtype == CP_BF16;
-    if (bf16) {
-        if (a.gptj) k_rows<__nv_bfloat16, true><<<grid, kRowsThreads, 0, st>>>(a);
-        else k_rows<__nv_bfloat16, false><<<grid, kRowsThreads, 0, st>>>(a);
-    } else {
-        if (a.gptj) k_rows<float, true><<<grid, kRowsThreads, 0, st>>>(a);
-        else k_rows<float, false><<<grid, kRowsThreads, 0, st>>>(a);
-    }
+    const int var = gather_variant();
+    if (bf16) { if (a.gptj) launch_rows_t<__nv_bfloat16, true>(a, var, st); else launch_rows_t<__nv_bfloat16, false>(a, var, st); }
+    else { if (a.gptj) launch_rows_t<float, true>(a, var, st); else launch_rows_t<float, false>(a, var, st); }
     CP_COUNT_LAUNCH();
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}
+
+extern "C" cp_status cp_set_gather_variant(int32_t v) {
+    if (v < 0 || v > 3) return CP_ERR_INVALID_ARG;
+    g_variant = v;
+    return CP_OK;
 }
 
 extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp_hits* h, const cp_paged_kv* kv,

@@ -124,7 +124,7 @@ __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, in
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < P; i += nt) fifo[i] = (int32_t)i;                 // FIFO: ascending page ids (R#22)
     for (int64_t i = tid; i < S; i += nt) { slot_id[i] = -1; slot_state[i] = CP_SLOT_FREE; slot_stack[i] = S - 1 - (int32_t)i; }
-    for (int64_t i = tid; i < T; i += nt) { htab[i].key = CP_EMPTY_KEY; htab[i].slot = -1; }
+    for (int64_t i = tid; i < T; i += nt) { htab[i].key = CP_EMPTY_KEY; htab[i].full = 0; htab[i].slot = -1; htab[i].len = 0; }
     if (tid == 0) {
         hdr->error = 0; hdr->next_id = 0; hdr->num_live = 0; hdr->fifo_head = 0; hdr->fifo_count = (int32_t)P;
         hdr->slot_free_top = S; hdr->match_done = 0; hdr->table_used = 0; hdr->live_tokens = 0;
@@ -167,7 +167,7 @@ __global__ void k_ins_validate(InsArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) { a.hdr->n_cand = 0; a.hdr->n_copy = 0; a.hdr->n_removed = 0; a.hdr->n_new_live = 0; }
     // clear the batch prefix table
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.BT; i += (int64_t)gridDim.x * blockDim.x) {
-        a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = -1;
+        a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = -1; a.btab[i].len = 0; a.btab[i].full = 0;
     }
     if (cp_err_set(a.hdr)) return;
     for (int s = warp; s < a.S; s += nwarps) {
@@ -214,15 +214,9 @@ __global__ void k_ins_hash(InsArgs a) {
             return v;
         };
         const uint64_t pre = fold(a.w), full = fold(m);
-        if (lane == 0) {
-            a.span_pre[s] = pre; a.span_full[s] = full;
-            uint32_t pos = cp_hpos(pre, a.logBT);
-            while (true) {
-                unsigned long long prev = atomicCAS(&a.btab[pos].key, CP_EMPTY_KEY, (unsigned long long)pre);
-                if (prev == CP_EMPTY_KEY) { a.btab[pos].slot = s; break; }
-                pos = (pos + 1) & (uint32_t)(a.BT - 1);
-            }
-        }
+        if (lane == 0) { a.span_pre[s] = pre; a.span_full[s] = full; }
+        HEntry v; v.key = pre; v.full = full; v.slot = s; v.len = m; v.pad = 0;
+        cp_warp_insert(a.btab, (uint32_t)(a.BT - 1), a.logBT, v, false);
     }
 }
 
@@ -264,36 +258,26 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a) {
             cp_block_prefix_hash<kScanThreads>([&](int i) { return slot_token(a, id, i); }, m, a.B, sm, wtmp);
         }
         const uint64_t Bw = a.pw[a.w];
-        for (int o = threadIdx.x; o + a.w <= m; o += blockDim.x) {
-            const uint64_t W = cp_subhash(sm, o, a.w, Bw);
-            // needles among new spans
-            uint32_t pos = cp_hpos(W, a.logBT);
-            while (true) {
-                const unsigned long long key = a.btab[pos].key;
-                if (key == CP_EMPTY_KEY) break;
-                if (key == W) {
-                    const int j = a.btab[pos].slot;
-                    const int mj = a.span_len[j];
-                    if (!(is_new && j == id) && o + mj <= m &&
-                        cp_subhash(sm, o, mj, a.pw[mj]) == a.span_full[j])
-                        push_cand(a, is_new ? -1 - id : id, -1 - j, o);
-                }
-                pos = (pos + 1) & (uint32_t)(a.BT - 1);
-            }
-            if (!is_new) continue;
-            // needles among live pool entries
-            pos = cp_hpos(W, a.logT);
-            while (true) {
-                const unsigned long long key = a.htab[pos].key;
-                if (key == CP_EMPTY_KEY) break;
-                if (key == W) {
-                    const int e = a.htab[pos].slot;
-                    const int me = a.slot_len[e];
-                    if (o + me <= m && cp_subhash(sm, o, me, a.pw[me]) == a.slot_full[e])
-                        push_cand(a, -1 - id, e, o);
-                }
-                pos = (pos + 1) & (uint32_t)(a.T - 1);
-            }
+        const int nwin = m - a.w + 1;
+        const int wbase = threadIdx.x & ~31;
+        for (int base = 0; base < nwin; base += blockDim.x) {
+            const int o = base + threadIdx.x;
+            const bool act = o < nwin;
+            const uint64_t W = act ? cp_subhash(sm, o, a.w, Bw) : 0;
+            // needles among new spans (batch table)
+            cp_warp_probe<false>(a.btab, (uint32_t)(a.BT - 1), a.logBT, W, act, [&](int owner, const HEntry& e) {
+                const int oo = base + wbase + owner;
+                const int j = e.slot, mj = e.len;
+                if (!(is_new && j == id) && oo + mj <= m && cp_subhash(sm, oo, mj, a.pw[mj]) == e.full)
+                    push_cand(a, is_new ? -1 - id : id, -1 - j, oo);
+            });
+            // needles among live pool entries (new-span haystacks only)
+            if (is_new)
+                cp_warp_probe<false>(a.htab, (uint32_t)(a.T - 1), a.logT, W, act, [&](int owner, const HEntry& e) {
+                    const int oo = base + wbase + owner;
+                    const int me = e.len;
+                    if (oo + me <= m && cp_subhash(sm, oo, me, a.pw[me]) == e.full) push_cand(a, -1 - id, e.slot, oo);
+                });
         }
         __syncthreads();
     }
@@ -598,21 +582,30 @@ __global__ void k_ins_outids(InsArgs a) {
     }
 }
 
-// tombstone prefix-table entries of removed pool entries (those that were in the table)
+// tombstone prefix-table entries of removed pool entries (those that were in the table); warp per slot
 __global__ void k_ins_delete(InsArgs a) {
     if (cp_err_set(a.hdr)) return;
     const int n = a.hdr->n_removed;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < n; r += nwarps) {
         const int code = a.removed[r];
         if (code < 0) continue;               // stored and removed within this call: never published
         const int slot = code;
         const unsigned long long key = a.slot_prefix[slot];
-        uint32_t pos = cp_hpos(key, a.logT);
+        uint32_t p0 = cp_hpos(key, a.logT);
         while (true) {
-            const unsigned long long k = a.htab[pos].key;
-            if (k == CP_EMPTY_KEY) break;
-            if (k == key && a.htab[pos].slot == slot) { a.htab[pos].key = CP_TOMB_KEY; break; }
-            pos = (pos + 1) & (uint32_t)(a.T - 1);
+            const uint32_t p = (p0 + lane) & (uint32_t)(a.T - 1);
+            const unsigned long long k = a.htab[p].key;
+            const bool hit = k == key && a.htab[p].slot == slot;
+            const unsigned empt = __ballot_sync(0xffffffffu, k == CP_EMPTY_KEY);
+            const unsigned hits = __ballot_sync(0xffffffffu, hit);
+            const int lim = empt ? __ffs(empt) - 1 : 32;
+            const unsigned before = lim == 32 ? hits : (hits & ((1u << lim) - 1u));
+            if (before) { if (lane == __ffs(before) - 1) a.htab[p].key = CP_TOMB_KEY; break; }
+            if (empt) break;
+            p0 = (p0 + 32) & (uint32_t)(a.T - 1);
         }
     }
 }
@@ -712,23 +705,10 @@ __global__ void k_ins_publish(InsArgs a) {
             }
             a.page_bits[a.slot_pages[(int64_t)slot * a.MP + pg]] = (uint16_t)v;
         }
-        if (lane == 0) {
-            sha256_tokens_dev(tau, m, a.slot_digest + (int64_t)slot * 32);
-            const unsigned long long key = a.slot_prefix[slot];
-            uint32_t pos = cp_hpos(key, a.logT);
-            while (true) {
-                const unsigned long long k = a.htab[pos].key;
-                if (k == CP_EMPTY_KEY || k == CP_TOMB_KEY) {
-                    if (atomicCAS(&a.htab[pos].key, k, key) == k) {
-                        a.htab[pos].slot = slot;
-                        if (k == CP_EMPTY_KEY) atomicAdd(&a.hdr->table_used, 1);
-                        break;
-                    }
-                    continue;
-                }
-                pos = (pos + 1) & (uint32_t)(a.T - 1);
-            }
-        }
+        if (lane == 0) sha256_tokens_dev(tau, m, a.slot_digest + (int64_t)slot * 32);
+        HEntry v; v.key = a.slot_prefix[slot]; v.full = a.slot_full[slot]; v.slot = slot; v.len = m; v.pad = 0;
+        const bool fresh = cp_warp_insert(a.htab, (uint32_t)(a.T - 1), a.logT, v, true);
+        if (fresh && lane == 0) atomicAdd(&a.hdr->table_used, 1);
     }
 }
 
@@ -739,21 +719,22 @@ __global__ void k_rebuild_check(DevHeader* hdr, int64_t T) {
 __global__ void k_rebuild_clear(DevHeader* hdr, HEntry* htab, int64_t T) {
     if (!hdr->rebuild) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x) {
-        htab[i].key = CP_EMPTY_KEY; htab[i].slot = -1;
+        htab[i].key = CP_EMPTY_KEY; htab[i].slot = -1; htab[i].len = 0; htab[i].full = 0;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) hdr->table_used = 0;
 }
 __global__ void k_rebuild_fill(DevHeader* hdr, HEntry* htab, int logT, int64_t T, const uint8_t* state,
-                               const unsigned long long* prefix, int32_t nslots) {
+                               const unsigned long long* prefix, const unsigned long long* full,
+                               const int32_t* len, int32_t nslots) {
     if (!hdr->rebuild) return;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int s = warp; s < nslots; s += nwarps) {
         if (state[s] != CP_SLOT_LIVE) continue;
-        const unsigned long long key = prefix[s];
-        uint32_t pos = cp_hpos(key, logT);
-        while (true) {
-            if (atomicCAS(&htab[pos].key, CP_EMPTY_KEY, key) == CP_EMPTY_KEY) { htab[pos].slot = s; atomicAdd(&hdr->table_used, 1); break; }
-            pos = (pos + 1) & (uint32_t)(T - 1);
-        }
+        HEntry v; v.key = prefix[s]; v.full = full[s]; v.slot = s; v.len = len[s]; v.pad = 0;
+        cp_warp_insert(htab, (uint32_t)(T - 1), logT, v, false);
+        if (lane == 0) atomicAdd(&hdr->table_used, 1);
     }
 }
 
@@ -1021,11 +1002,11 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     if (csm > 200 * 1024) return CP_ERR_UNSUPPORTED;
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_delete<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_publish<<<std::max(1, std::min(1184, (num_spans + 7) / 8)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_rebuild_check<<<1, 1, 0, st>>>(x->hdr, x->T); CP_COUNT_LAUNCH();
     k_rebuild_clear<<<256, 256, 0, st>>>(x->hdr, x->htab, x->T); CP_COUNT_LAUNCH();
-    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->S); CP_COUNT_LAUNCH();
+    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->slot_full, x->slot_len, x->S); CP_COUNT_LAUNCH();
     if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     // copy the writer KV rows of the published entries into their pool pages
     return cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,

@@ -25,11 +25,14 @@
 #define CP_SLOT_FREE 0
 #define CP_SLOT_LIVE 1
 
-struct HEntry {                      // open-addressing multi-value table entry (16 B)
+struct __align__(32) HEntry {        // open-addressing multi-value table entry (32 B)
     unsigned long long key;          // prefix hash; CP_EMPTY_KEY / CP_TOMB_KEY are never valid hashes (< p)
-    int32_t slot;
-    int32_t pad;
+    unsigned long long full;         // full-length hash of the entry (the O(1) pre-check needs no extra load)
+    int32_t slot;                    // pool slot (or batch span index for the insert's batch table)
+    int32_t len;                     // entry length
+    unsigned long long pad;
 };
+static_assert(sizeof(HEntry) == 32, "HEntry must be 32 B");
 
 struct DevHeader {                   // first 256 B of META
     int32_t error;                   // sticky cp_status (0 = none)
@@ -182,6 +185,87 @@ __device__ void cp_block_prefix_hash(F tok, int n, uint64_t B, uint64_t* sh, uin
     if (tid == 0) sh[0] = 0;
     for (int i = c0; i < c1; ++i) { cur = cp_addmod(cp_mulmod(cur, B), cp_tokval(tok(i))); sh[i + 1] = cur; }
     __syncthreads();
+}
+
+
+// ---- hash-table probing ----------------------------------------------------------------------
+__device__ __forceinline__ HEntry cp_ld_entry(const HEntry* p) {
+    const ulonglong4 v = *reinterpret_cast<const ulonglong4*>(p);
+    HEntry e;
+    e.key = v.x; e.full = v.y; e.slot = (int32_t)(v.z & 0xffffffffu); e.len = (int32_t)(v.z >> 32); e.pad = 0;
+    return e;
+}
+__device__ __forceinline__ HEntry cp_ldg_entry(const HEntry* p) {
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    HEntry e;
+    e.key = a.x; e.full = a.y; e.slot = (int32_t)(b.x & 0xffffffffu); e.len = (int32_t)(b.x >> 32); e.pad = 0;
+    return e;
+}
+
+// Warp-level multi-value probe.  Every lane may carry one key (`active`).  Short chains are
+// walked per lane (up to kShort slots); lanes whose chain is longer (e.g. the hundreds of stored
+// segments that share one system-prompt window) are then served one at a time by the whole warp,
+// 32 consecutive entries per step with __ballot_sync.  on_match(owner_lane, entry) is invoked by
+// the lane that loaded a matching entry, in no particular order.  All 32 lanes must call it.
+template <bool LDG, typename F>
+__device__ __forceinline__ void cp_warp_probe(const HEntry* tab, uint32_t mask, int logT, uint64_t key,
+                                              bool active, F on_match) {
+    constexpr int kShort = 4;
+    const int lane = threadIdx.x & 31;
+    uint32_t pos = active ? cp_hpos(key, logT) : 0;
+    bool done = !active;
+    for (int s = 0; s < kShort && !done; ++s) {
+        const HEntry e = LDG ? cp_ldg_entry(tab + pos) : cp_ld_entry(tab + pos);
+        if (e.key == CP_EMPTY_KEY) { done = true; break; }
+        if (e.key == key) on_match(lane, e);
+        pos = (pos + 1) & mask;
+    }
+    unsigned pend = __ballot_sync(0xffffffffu, !done);
+    while (pend) {
+        const int owner = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const uint64_t k = __shfl_sync(0xffffffffu, key, owner);
+        uint32_t p0 = __shfl_sync(0xffffffffu, pos, owner);
+        while (true) {
+            const uint32_t p = (p0 + lane) & mask;
+            const HEntry e = LDG ? cp_ldg_entry(tab + p) : cp_ld_entry(tab + p);
+            const unsigned empt = __ballot_sync(0xffffffffu, e.key == CP_EMPTY_KEY);
+            const int lim = empt ? __ffs(empt) - 1 : 32;
+            if (lane < lim && e.key == k) on_match(owner, e);
+            if (empt) break;
+            p0 = (p0 + 32) & mask;
+        }
+    }
+}
+
+// Warp-cooperative insert of one entry (all lanes call with the same arguments): claims the first
+// EMPTY (or TOMB when allow_tomb) slot of the probe sequence with atomicCAS on the key.
+// Returns true (on every lane) if an EMPTY slot (not a tombstone) was consumed.
+__device__ __forceinline__ bool cp_warp_insert(HEntry* tab, uint32_t mask, int logT, const HEntry& val,
+                                               bool allow_tomb) {
+    const int lane = threadIdx.x & 31;
+    uint32_t p0 = cp_hpos(val.key, logT);
+    while (true) {
+        const uint32_t p = (p0 + lane) & mask;
+        const unsigned long long k = *((volatile unsigned long long*)&tab[p].key);
+        unsigned cand = __ballot_sync(0xffffffffu, k == CP_EMPTY_KEY || (allow_tomb && k == CP_TOMB_KEY));
+        while (cand) {
+            const int l = __ffs(cand) - 1;
+            int won = 0, was_empty = 0;
+            if (lane == l) {
+                const unsigned long long prev = atomicCAS(&tab[p].key, k, val.key);
+                if (prev == k) {
+                    tab[p].full = val.full; tab[p].slot = val.slot; tab[p].len = val.len;
+                    won = 1; was_empty = (k == CP_EMPTY_KEY);
+                }
+            }
+            won = __shfl_sync(0xffffffffu, won, l);
+            if (won) return __shfl_sync(0xffffffffu, was_empty, l);
+            cand &= cand - 1;
+        }
+        p0 = (p0 + 32) & mask;
+    }
 }
 
 __device__ __forceinline__ bool cp_err_set(const DevHeader* hdr) {

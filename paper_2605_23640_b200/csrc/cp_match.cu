@@ -52,15 +52,6 @@ struct MatchSmem {
     }
 };
 
-__device__ __forceinline__ HEntry ld_entry(const HEntry* p) {
-    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
-    HEntry e;
-    e.key = v.x;
-    e.slot = (int32_t)(v.y & 0xffffffffu);
-    e.pad = 0;
-    return e;
-}
-
 __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ uint64_t wtmp[2 * (kNT / 32)];
@@ -90,29 +81,22 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         const int nw = n - a.w + 1;                  // number of windows (may be <= 0)
         for (int k = tid; k < nw; k += kNT) vslot[k] = -1;
         __syncthreads();
-        // ---- 2. rolling windows -> prefix filter -> O(1) full-hash pre-check
+        // ---- 2. rolling windows -> prefix filter -> O(1) full-hash pre-check (warp-level probing)
         int my_cands = 0;
-        for (int k = tid; k < nw; k += kNT) {
-            const uint64_t W = cp_subhash(h, k, a.w, a.Bw);
-            uint32_t pos = cp_hpos(W, a.logT);
-            int best = -1, best_m = 0, best_id = 0;
-            while (true) {
-                const HEntry e = ld_entry(a.htab + pos);
-                if (e.key == CP_EMPTY_KEY) break;
-                if (e.key == W) {
-                    ++my_cands;
-                    const int m = __ldg(a.slot_len + e.slot);
-                    if (k + m <= n && cp_subhash(h, k, m, __ldg(a.pw + m)) == __ldg(a.slot_full + e.slot)) {
-                        const int id = __ldg(a.slot_id + e.slot);
-                        if (best < 0 || m > best_m || (m == best_m && id < best_id)) { best = e.slot; best_m = m; best_id = id; }
-                    }
+        const int wbase = tid & ~31;
+        for (int base = 0; base < nw; base += kNT) {
+            const int k = base + tid;
+            const bool act = k < nw;
+            const uint64_t W = act ? cp_subhash(h, k, a.w, a.Bw) : 0;
+            cp_warp_probe<true>(a.htab, (uint32_t)(a.T - 1), a.logT, W, act, [&](int owner, const HEntry& e) {
+                ++my_cands;
+                const int kk = base + wbase + owner;
+                const int m = e.len;
+                if (kk + m <= n && cp_subhash(h, kk, m, __ldg(a.pw + m)) == e.full) {
+                    // containment-free pool: at most one true match starts at kk (first writer wins)
+                    if (atomicCAS(&vslot[kk], -1, e.slot) == -1) clist[atomicAdd(&s_nc, 1)] = kk;
                 }
-                pos = (pos + 1) & (uint32_t)(a.T - 1);
-            }
-            if (best >= 0) {
-                vslot[k] = best;
-                clist[atomicAdd(&s_nc, 1)] = k;
-            }
+            });
         }
         // warp-aggregated candidate count
         for (int o = 16; o; o >>= 1) my_cands += __shfl_xor_sync(0xffffffffu, my_cands, o);

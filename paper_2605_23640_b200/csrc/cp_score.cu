@@ -35,17 +35,34 @@ struct ScoreArgs {
     uint32_t* bits;
 };
 
-// q(x) = trunc(x * 2^40) computed exactly from the fp32 bit pattern (|x| < 2^23)
-__device__ __forceinline__ long long fixq(float x) {
-    const uint32_t b = __float_as_uint(x);
-    const int e = (int)((b >> 23) & 0xffu);
-    if (e == 0) return 0;                           // zero / subnormal: |x| 2^40 < 1
-    const unsigned long long mant = (unsigned long long)((b & 0x7fffffu) | 0x800000u);   // x = mant 2^(e-150)
-    const int sh = e - 110;                         // (e - 150) + 40
-    unsigned long long v;
-    if (sh >= 0) v = mant << min(sh, 39);
-    else v = (sh > -64) ? (mant >> (-sh)) : 0ULL;
-    return (b >> 31) ? -(long long)v : (long long)v;
+// q(x) = trunc(x * 2^40): the fp32 product by a power of two is exact (no FTZ), and cvt.rzi.s64
+// truncates toward zero exactly like the oracle's (int64_t)((double)x * 2^40).
+__device__ __forceinline__ long long q40(float x) { return __float2ll_rz(x * 1099511627776.0f); }
+
+__device__ __forceinline__ float4 ld_nc4(const float4* p) {
+    float4 f;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "l"(p));
+    return f;
+}
+
+// warp-strided sum of q(p[0..cnt)) with 128-bit loads on the aligned body
+__device__ __forceinline__ long long warp_qsum(const float* p, int cnt, int lane) {
+    if (cnt <= 0) return 0;
+    long long acc = 0;
+    const int mis = (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
+    const int head = min(cnt, mis ? 4 - mis : 0);
+    if (lane < head) acc += q40(__ldg(p + lane));
+    const int nvec = (cnt - head) >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(p + head);
+#pragma unroll 4
+    for (int q = lane; q < nvec; q += 32) {
+        const float4 f = ld_nc4(v4 + q);
+        acc += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
+    }
+    const int t0 = head + 4 * nvec;
+    if (t0 + lane < cnt) acc += q40(__ldg(p + t0 + lane));
+    return acc;
 }
 
 __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
@@ -62,21 +79,8 @@ __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
         for (int h = 0; h < s.heads; ++h) {
             const float* row = s.A + ((int64_t)h * s.n + i) * (int64_t)s.n;
             const int cnt = i + 1;                                   // causal: columns 0..i
-            const int mis = (int)((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
-            const int head = min(cnt, mis ? 4 - mis : 0);             // scalars until 16-B aligned
-            if (lane < head) { const long long v = fixq(__ldg(row + lane)); acc += lane < l ? v : -v; }
-            const int nvec = (cnt - head) >> 2;
-            const float4* v4 = reinterpret_cast<const float4*>(row + head);
-            for (int q = lane; q < nvec; q += 32) {
-                float4 f;
-                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                             : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "l"(v4 + q));
-                const int j = head + 4 * q;
-                const long long a0 = fixq(f.x), a1 = fixq(f.y), a2 = fixq(f.z), a3 = fixq(f.w);
-                acc += (j < l ? a0 : -a0) + (j + 1 < l ? a1 : -a1) + (j + 2 < l ? a2 : -a2) + (j + 3 < l ? a3 : -a3);
-            }
-            const int tail0 = head + 4 * nvec;
-            if (tail0 + lane < cnt) { const int j = tail0 + lane; const long long v = fixq(__ldg(row + j)); acc += j < l ? v : -v; }
+            acc += warp_qsum(row, min(l, cnt), lane);                // inter: j < l*
+            acc -= warp_qsum(row + l, cnt - l, lane);                // intra: l* <= j <= i
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

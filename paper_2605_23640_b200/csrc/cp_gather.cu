@@ -34,30 +34,17 @@ struct RowsArgs {
     const int32_t* slot_pages; int32_t MP;
     int32_t L, H, d; double theta; int32_t flags; int32_t gptj;
     int32_t* chunk_hit; int32_t* chunk_t0; int64_t CH;
+    long long* row_src; long long* row_dst;
     float2* hit_cs; int64_t cs_hits;
 };
 
-// block 0: chunk list; all blocks: cos/sin per (hit, pair index) in fp64 -> fp32
+// k_rows_prep (one block): chunk list = scan of ceil(len/32) over the hit list
 __global__ void __launch_bounds__(kPrepThreads) k_rows_prep(RowsArgs a) {
     __shared__ int s_scan[kPrepThreads / 32 + 1];
     __shared__ int s_carry;
     if (cp_err_set(a.hdr)) return;
     const int nh = *a.count;
-    if (nh > a.list_cap || nh > a.cs_hits) { if (blockIdx.x == 0 && threadIdx.x == 0) cp_raise(a.hdr, CP_ERR_CAPACITY); return; }
-    const int half = a.d / 2;
-    if (a.dir == 0) {
-        const int64_t npairs = (int64_t)nh * half;
-        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npairs; q += (int64_t)gridDim.x * blockDim.x) {
-            const int hh = (int)(q / half), i = (int)(q % half);
-            const int delta = a.l_delta[hh];
-            if (delta == 0) continue;
-            const double th = pow(a.theta, -2.0 * (double)i / (double)a.d);
-            double s, c;
-            sincos((double)delta * th, &s, &c);
-            a.hit_cs[q] = make_float2((float)c, (float)s);
-        }
-    }
-    if (blockIdx.x != 0) return;
+    if (nh > a.list_cap || nh > a.cs_hits) { if (threadIdx.x == 0) cp_raise(a.hdr, CP_ERR_CAPACITY); return; }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -83,6 +70,44 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep(RowsArgs a) {
         __syncthreads();
     }
     if (tid == 0) a.hdr->n_chunks = s_carry;
+}
+
+// k_rows_prep2 (all blocks): per-hit cos/sin (angles in fp64, R#13) and the per-token row table
+// (source / destination row offsets + plan code) so the copy kernels resolve a token with one load
+__global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    const int nh = *a.count;
+    const int half = a.d / 2;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    if (a.dir == 0) {
+        const int64_t npairs = (int64_t)nh * half;
+        for (int64_t q = gt; q < npairs; q += nt) {
+            const int hh = (int)(q / half), i = (int)(q % half);
+            const int delta = a.l_delta[hh];
+            if (delta == 0) continue;
+            const double th = pow(a.theta, -2.0 * (double)i / (double)a.d);
+            double sn, cs;
+            sincos((double)delta * th, &sn, &cs);
+            a.hit_cs[q] = make_float2((float)cs, (float)sn);
+        }
+    }
+    const int64_t rowE = (int64_t)a.H * a.d;
+    const int64_t ntok = (int64_t)a.hdr->n_chunks * CP_GATHER_CHUNK;
+    for (int64_t q = gt; q < ntok; q += nt) {
+        const int c = (int)(q / CP_GATHER_CHUNK), i = (int)(q % CP_GATHER_CHUNK);
+        const int hh = a.chunk_hit[c];
+        const int t = a.chunk_t0[c] + i;
+        if (t >= a.l_len[hh]) continue;
+        const int r = a.l_req[hh], k = a.l_dst[hh], slot = a.l_slot[hh];
+        const int pos = k + t;                                              // position in the request
+        const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
+        const int blk = a.block_tables[(int64_t)r * a.max_blocks + (pos >> 4)];
+        const long long pool_row = ((long long)page * CP_BLOCK + (t & 15)) * rowE;
+        const long long paged_row = ((long long)blk * CP_BLOCK + (pos & 15)) * rowE;
+        const long long code = a.dir == 0 ? (long long)a.plan[a.req_off[r] + pos] : (long long)CP_PLAN_REUSED;
+        a.row_src[q] = a.dir == 0 ? pool_row : paged_row;
+        a.row_dst[q] = (a.dir == 0 ? paged_row : pool_row) | (code << 62);
+    }
 }
 
 template <typename T> struct Vec;
@@ -149,17 +174,13 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
         const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
         const int len = a.l_len[hh];
         const int ntok = min(CP_GATHER_CHUNK, len - t0);
-        const int r = a.l_req[hh], k = a.l_dst[hh], slot = a.l_slot[hh];
         const int delta = a.dir == 0 ? a.l_delta[hh] : 0;
         if (tid < ntok) {
-            const int t = t0 + tid;
-            const int q = k + t;                                           // position in the request
-            const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
-            const int blk = a.block_tables[(int64_t)r * a.max_blocks + (q >> 4)];
-            const int64_t pool_row = ((int64_t)page * CP_BLOCK + (t & 15)) * rowE;
-            const int64_t paged_row = ((int64_t)blk * CP_BLOCK + (q & 15)) * rowE;
-            if (a.dir == 0) { s_src[tid] = pool_row; s_dst[tid] = paged_row; s_code[tid] = a.plan[a.req_off[r] + q]; }
-            else { s_src[tid] = paged_row; s_dst[tid] = pool_row; s_code[tid] = CP_PLAN_REUSED; }
+            const int64_t q = (int64_t)c * CP_GATHER_CHUNK + tid;
+            const long long dw = a.row_dst[q];
+            s_src[tid] = a.row_src[q];
+            s_dst[tid] = dw & ((1LL << 62) - 1);
+            s_code[tid] = (int)((unsigned long long)dw >> 62);
         }
         float2 csr[VEC];
         if (delta != 0) {
@@ -239,6 +260,199 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     }
 }
 
+
+// ============================================================================================
+// TMA bulk-copy variant (cp.async.bulk + mbarrier), the default when a stage fits shared memory.
+//   warp 0      : producer -- resolves TOK token rows of the next unit (pool page / block table /
+//                 plan code) and bulk-loads the K and V rows (2 KiB each for the 8B shape) into an
+//                 NST-stage shared-memory ring, completing an mbarrier transaction count
+//   warps 1..4  : consumers -- wait for the stage, rotate the K rows in shared memory (fp32 math,
+//                 cos/sin in registers), fence.proxy.async, named barrier
+//   warp 1 lane0: storer -- bulk-stores every row of the stage to its destination (zero rows come
+//                 from a shared zero row), commit_group, wait_group.read -> frees the stage
+// No data passes through registers except the K rows being rotated.
+// ============================================================================================
+constexpr int kTmaTok = 8;                 // tokens per stage
+constexpr int kTmaCons = 4;                // consumer warps
+constexpr int kPend = 3;                   // bulk-store groups kept in flight by the storer
+constexpr int kTmaThreads = 32 * (1 + kTmaCons);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" :: "n"(32 * kTmaCons) : "memory"); }
+
+struct TmaStageMeta {
+    int64_t dst[kTmaTok];
+    int code[kTmaTok];
+    int ntok, hit, layer, delta;
+};
+
+template <typename T, bool GPTJ>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst) {
+    constexpr int VEC = Vec<T>::N;
+    extern __shared__ __align__(128) unsigned char smx[];
+    const int rowE = a.H * a.d;
+    const int rowB = rowE * (int)sizeof(T);
+    const int stageB = kTmaTok * 2 * rowB;
+    unsigned char* ring = smx;                                            // nst * stageB
+    unsigned char* zrow = smx + (size_t)nst * stageB;                     // rowB zeros
+    TmaStageMeta* meta = (TmaStageMeta*)(zrow + rowB);                    // nst
+    uint64_t* full = (uint64_t*)(meta + nst);                             // nst
+    uint64_t* empty = full + nst;                                         // nst
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (cp_err_set(a.hdr)) return;
+    const int nchunks = a.hdr->n_chunks;
+    const int64_t items = (int64_t)nchunks * a.L;
+    const int64_t pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
+    for (int i = tid; i < rowB / 16; i += blockDim.x) reinterpret_cast<uint4*>(zrow)[i] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async_smem();
+    __syncthreads();
+    const bool zero_rec = (a.flags & CP_ZERO_RECOMPUTE) != 0;
+    const int half = a.d / 2;
+    const int hv = half / VEC;
+    const int tpr = rowE / (2 * VEC);
+
+    if (warp == 0) {
+        // ---------------- producer: one coalesced row-table load per item, then the stages
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            const int c = (int)(item / a.L), l = (int)(item % a.L);
+            const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
+            const int ntok_item = min(CP_GATHER_CHUNK, a.l_len[hh] - t0);
+            const int delta = a.dir == 0 ? a.l_delta[hh] : 0;
+            const char* srcK = a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l];
+            const char* srcV = a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l];
+            long long my_src = 0, my_dst = 0;
+            if (lane < ntok_item) { my_src = a.row_src[(int64_t)c * CP_GATHER_CHUNK + lane]; my_dst = a.row_dst[(int64_t)c * CP_GATHER_CHUNK + lane]; }
+            for (int u0 = 0; u0 < ntok_item; u0 += kTmaTok, ++it) {
+                const int s = it % nst;
+                if (it >= nst) mbar_wait(&empty[s], ((it / nst) - 1) & 1);
+                const int nt = min(kTmaTok, ntok_item - u0);
+                TmaStageMeta& m = meta[s];
+                // lanes u0 .. u0+nt-1 own this stage's tokens
+                const int g = lane - u0;
+                const bool mine = g >= 0 && g < nt;
+                const int code = mine ? (int)((unsigned long long)my_dst >> 62) : -1;
+                if (mine) { m.dst[g] = my_dst & ((1LL << 62) - 1); m.code[g] = code; }
+                if (lane == 0) { m.ntok = nt; m.hit = hh; m.layer = l; m.delta = delta; }
+                const bool load = mine && !(code == CP_PLAN_RECOMPUTE && zero_rec);
+                const unsigned nload = __popc(__ballot_sync(0xffffffffu, load));
+                __syncwarp();
+                if (lane == 0) mbar_expect_tx(&full[s], nload * 2u * (uint32_t)rowB);
+                __syncwarp();
+                if (load) {
+                    unsigned char* st = ring + (size_t)s * stageB;
+                    bulk_g2s(st + (size_t)g * rowB, srcK + my_src * sizeof(T), rowB, &full[s]);
+                    bulk_g2s(st + (size_t)(kTmaTok + g) * rowB, srcV + my_src * sizeof(T), rowB, &full[s]);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers (warps 1..kTmaCons); warp 1 lane 0 also stores
+        const int ct = tid - 32;                               // 0 .. 32*kTmaCons-1
+        const bool storer = ct == 0;
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            const int c = (int)(item / a.L), l = (int)(item % a.L);
+            const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
+            const int ntok_item = min(CP_GATHER_CHUNK, a.l_len[hh] - t0);
+            char* dstK = a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T);
+            char* dstV = a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T);
+            const int delta = a.dir == 0 ? a.l_delta[hh] : 0;
+            for (int u0 = 0; u0 < ntok_item; u0 += kTmaTok, ++it) {
+                const int s = it % nst;
+                mbar_wait(&full[s], (it / nst) & 1);
+                const TmaStageMeta& m = meta[s];
+                const int nt = m.ntok;
+                unsigned char* st = ring + (size_t)s * stageB;
+                if (delta != 0) {
+                    const float2* tab = a.hit_cs + (int64_t)hh * half;
+                    for (int task = ct; task < nt * tpr; task += 32 * kTmaCons) {
+                        const int g = task / tpr, j = task - g * tpr;
+                        if (m.code[g] == CP_PLAN_RECOMPUTE && zero_rec) continue;
+                        int lo, hi, i0;
+                        if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; hi = lo + half; i0 = sub * VEC; }
+                        else { lo = j * 2 * VEC; hi = lo + VEC; i0 = (lo % a.d) / 2; }
+                        T* rowp = reinterpret_cast<T*>(st + (size_t)g * rowB);
+                        uint4* plo = reinterpret_cast<uint4*>(rowp + lo);
+                        uint4* phi = reinterpret_cast<uint4*>(rowp + hi);
+                        float x[VEC], y[VEC];
+                        unpack(*plo, x, T()); unpack(*phi, y, T());
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            if (!GPTJ) {
+                                const float2 cs = __ldg(tab + i0 + e);
+                                const float xo = fmaf(x[e], cs.x, -y[e] * cs.y);
+                                const float yo = fmaf(y[e], cs.x, x[e] * cs.y);
+                                x[e] = xo; y[e] = yo;
+                            } else if ((e & 1) == 0) {
+                                const float2 c0 = __ldg(tab + i0 + e / 2), c1 = __ldg(tab + i0 + VEC / 2 + e / 2);
+                                const float x0 = fmaf(x[e], c0.x, -x[e + 1] * c0.y), x1 = fmaf(x[e + 1], c0.x, x[e] * c0.y);
+                                const float y0 = fmaf(y[e], c1.x, -y[e + 1] * c1.y), y1 = fmaf(y[e + 1], c1.x, y[e] * c1.y);
+                                x[e] = x0; x[e + 1] = x1; y[e] = y0; y[e + 1] = y1;
+                            }
+                        }
+                        *plo = pack(x, T()); *phi = pack(y, T());
+                    }
+                    fence_async_smem();
+                }
+                cons_bar();
+                if (storer) {
+                    for (int g = 0; g < nt; ++g) {
+                        const bool z = m.code[g] == CP_PLAN_RECOMPUTE && zero_rec;
+                        const int64_t d = m.dst[g];
+                        bulk_s2g(dstK + d * sizeof(T), z ? zrow : st + (size_t)g * rowB, rowB);
+                        bulk_s2g(dstV + d * sizeof(T), z ? zrow : st + (size_t)(kTmaTok + g) * rowB, rowB);
+                    }
+                    bulk_commit();
+                    // keep kPend store groups in flight: stage it-kPend has been read -> free it
+                    bulk_wait_read<kPend>();
+                    if (it >= kPend) mbar_arrive(&empty[(it - kPend) % nst]);
+                }
+            }
+        }
+        if (storer) {
+            bulk_wait_all<0>();
+            for (int q = max(0, it - kPend); q < it; ++q) mbar_arrive(&empty[q % nst]);
+        }
+    }
+}
+
 // CP_ZERO_UNCOVERED: zero K and V rows of plan-0 positions (one CTA per (token block of 32, layer))
 template <typename T>
 __global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int32_t R, int64_t total) {
@@ -302,14 +516,41 @@ cp_status launch_rows_c(const RowsArgs& a, int variant, cudaStream_t st) {
     switch (variant) {
         case 1: return go(k_rows<T, G, CR, 2, 4>);
         case 2: return go(k_rows<T, G, CR, 4, 2>);
-        case 3: return go(k_rows<T, G, CR, 8, 1>);
-        default: return go(k_rows<T, G, CR, 3, 2>);      // measured best on B200 (tools/gather_ab.py)
+        case 3: return go(k_rows<T, G, CR, 3, 2>);
+        default: return go(k_rows<T, G, CR, 8, 1>);      // measured best on B200 (tools/gather_ab.py, profiles/r01)
     }
 }
+template <typename T, bool G>
+bool launch_rows_tma(const RowsArgs& a, cudaStream_t st) {
+    const int rowB = a.H * a.d * (int)sizeof(T);
+    const int stageB = kTmaTok * 2 * rowB;
+    if (rowB % 16) return false;
+    const size_t fixed = (size_t)rowB + 0;                         // zero row
+    int nst = 0;
+    for (int n = 8; n >= kPend + 2; --n) {
+        const size_t need = (size_t)n * stageB + fixed + n * (sizeof(TmaStageMeta) + 16) + 256;
+        if (need <= 200 * 1024) { nst = n; break; }
+    }
+    if (!nst) return false;
+    const size_t smem = (size_t)nst * stageB + fixed + nst * (sizeof(TmaStageMeta) + 16) + 256;
+    static bool attr[2][2] = {{false, false}, {false, false}};
+    bool& done = attr[sizeof(T) == 2][G];
+    if (!done) {
+        cudaFuncSetAttribute(k_rows_tma<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        done = true;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rows_tma<T, G>, kTmaThreads, smem);
+    k_rows_tma<T, G><<<sm_count() * std::max(1, occ), kTmaThreads, smem, st>>>(a, nst);
+    return true;
+}
+
 template <typename T, bool G>
 cp_status launch_rows_t(const RowsArgs& a, int variant, cudaStream_t st) {
     constexpr int VEC = Vec<T>::N;
     const int tpr = a.H * a.d / (2 * VEC);
+    if (variant == 4 && launch_rows_tma<T, G>(a, st)) return CP_OK;
+    if (variant == 4) variant = 0;
     return (kRowsThreads % tpr == 0) ? launch_rows_c<T, G, true>(a, variant, st) : launch_rows_c<T, G, false>(a, variant, st);
 }
 
@@ -339,9 +580,12 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim; a.theta = x->cfg.rope_theta;
     a.flags = flags; a.gptj = x->cfg.rope_style == CP_ROPE_GPTJ;
     a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH;
+    a.row_src = x->row_src; a.row_dst = x->row_dst;
     a.hit_cs = x->hit_cs; a.cs_hits = x->CS_HITS;
     if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;
-    k_rows_prep<<<dir == 0 ? 148 : 1, kPrepThreads, 0, st>>>(a);
+    k_rows_prep<<<1, kPrepThreads, 0, st>>>(a);
+    CP_COUNT_LAUNCH();
+    k_rows_prep2<<<sm_count() * 2, kPrepThreads, 0, st>>>(a);
     CP_COUNT_LAUNCH();
     const bool bf16 = x->cfg.dtype == CP_BF16;
     const int var = gather_variant();
@@ -352,7 +596,7 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
 }
 
 extern "C" cp_status cp_set_gather_variant(int32_t v) {
-    if (v < 0 || v > 3) return CP_ERR_INVALID_ARG;
+    if (v < 0 || v > 4) return CP_ERR_INVALID_ARG;
     g_variant = v;
     return CP_OK;
 }

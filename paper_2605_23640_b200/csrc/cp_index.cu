@@ -46,7 +46,7 @@ struct Layout {
     int64_t P; int32_t MP, S; int64_t T; int logT;
     int64_t HS, CH, CS_HITS; int32_t MS; int64_t MAXC, BT; int logBT;
     size_t meta_off[20]; size_t meta_size;
-    size_t scr_off[32]; size_t scr_size;
+    size_t scr_off[40]; size_t scr_size;
 };
 
 bool valid_cfg(const cp_config* c) {
@@ -113,6 +113,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(4 * (size_t)(S + L->MS));                           // 16 removed
     for (int k = 0; k < 5; ++k) sput(4 * (size_t)L->MS);     // 17-21 cp_req cp_slot cp_dst cp_len cp_delta
     sput(4 * (size_t)L->MS);                                 // 22 out_tmp
+    sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 23 row_src
+    sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 24 row_dst
     L->scr_size = o;
 }
 
@@ -838,6 +840,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->cp_req = (int32_t*)(s + L.scr_off[17]); x->cp_slot = (int32_t*)(s + L.scr_off[18]);
     x->cp_dst = (int32_t*)(s + L.scr_off[19]); x->cp_len = (int32_t*)(s + L.scr_off[20]);
     x->cp_delta = (int32_t*)(s + L.scr_off[21]); x->out_tmp = (int32_t*)(s + L.scr_off[22]);
+    x->row_src = (long long*)(s + L.scr_off[23]); x->row_dst = (long long*)(s + L.scr_off[24]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;

@@ -87,6 +87,7 @@ struct cp_index {
     // SCRATCH (gather / copy-in work lists)
     int64_t CH;          // chunk capacity
     int32_t *chunk_hit, *chunk_t0;
+    long long *row_src, *row_dst;   // [CH * CP_GATHER_CHUNK] element offsets; row_dst carries the plan code in bits 62-63
     float2* hit_cs;      // [hits][d/2] cos/sin
     int64_t CS_HITS;     // hits capacity of hit_cs
     // SCRATCH (insert)

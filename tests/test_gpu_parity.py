@@ -220,3 +220,27 @@ def test_score_edge_cases():
             osc, ob = O.score(mats[q].cpu().numpy(), ls[q], rs[q], num, den)
             assert np.array_equal(sc[so[q]:so[q] + m], osc)
             assert np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob), (q, num, den)
+
+
+def test_multidoc_config3_full_size_sampled():
+    """Config 3 at full size (128 readers x ~4K, 512-passage pool, one GPU): all hits, plans and the
+    index bit exact; KV rows sampled (2 requests x 2 layers)."""
+    wl = make_workload(3)
+    case = Case(wl, sample_reqs=2, sample_layers=[0, 31])
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]
+    assert rep.stats["moved_hits"] > 0.8 * rep.stats["hits"]          # heavy re-rotation (system prompt: delta 0)
+
+
+def test_70b_layer_shard_config4_full_size_sampled():
+    """Config 4 at full size on one rank's layer shard (layers 70-79 of 80; 64 readers x 8K)."""
+    wl = make_workload(4)
+    case = Case(wl, layer_range=(70, 80), sample_reqs=2, sample_layers=[0, 9])
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]

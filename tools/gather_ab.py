@@ -21,7 +21,7 @@ def main():
     row = S.shard.num_layers * S.shard.num_heads * S.g.head_dim * 2
     nbytes = (cov - rec) * 2 * row * 2 + rec * 2 * row
     out = {}
-    for v in [0, 1, 2, 3, 0]:
+    for v in [0, 3, 2, 4, 0, 3]:
         cp._lib.lib().cp_set_gather_variant(v)
         for _ in range(3):
             S.idx.gather_rerotate(S.rdb, S.hits, S.dst)

@@ -115,6 +115,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(4 * (size_t)L->MS);                                 // 22 out_tmp
     sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 23 row_src
     sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 24 row_dst
+    sput(4 * (size_t)L->MS);                                 // 25 eq_old
+    sput(sizeof(HEntry) * L->BT);                            // 26 btab2
     L->scr_size = o;
 }
 
@@ -155,6 +157,7 @@ struct InsArgs {
     unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed;
     int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
+    int32_t* eq_old; HEntry* btab2;
 };
 
 // error codes are ordered per span: range -> too short -> capacity -> sensitive (same order as the oracle)
@@ -166,10 +169,15 @@ __global__ void k_ins_validate(InsArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    if (blockIdx.x == 0 && threadIdx.x == 0) { a.hdr->n_cand = 0; a.hdr->n_copy = 0; a.hdr->n_removed = 0; a.hdr->n_new_live = 0; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.hdr->n_cand = 0; a.hdr->n_copy = 0; a.hdr->n_removed = 0; a.hdr->n_new_live = 0;
+        a.hdr->n_cand0 = 0; a.hdr->n_need = 0;
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.S; j += gridDim.x * blockDim.x) a.eq_old[j] = 0;
     // clear the batch prefix table
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.BT; i += (int64_t)gridDim.x * blockDim.x) {
         a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = -1; a.btab[i].len = 0; a.btab[i].full = 0;
+        a.btab2[i].key = CP_EMPTY_KEY; a.btab2[i].slot = -1; a.btab2[i].len = 0; a.btab2[i].full = 0;
     }
     if (cp_err_set(a.hdr)) return;
     for (int s = warp; s < a.S; s += nwarps) {
@@ -237,17 +245,22 @@ __device__ __forceinline__ void push_cand(const InsArgs& a, int hay, int needle,
     else cp_raise(a.hdr, CP_ERR_CAPACITY);
 }
 
-// items [0, S): new span j as haystack (needles: other new spans via btab, live entries via htab)
-// items [S, S + nslots): live slot as haystack (needles: new spans via btab)
-__global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a) {
+// phase 0: items = new spans as haystacks (needles: other new spans via the batch table, live
+//          entries via the pool table)
+// phase 1: items = live slots as haystacks (needles: new spans WITHOUT an equal live entry, via
+//          btab2).  A span equal to a live entry cannot be strictly inside another live entry (the
+//          pool is containment-free), so those spans need no old-haystack scan.
+__global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a, int phase) {
     extern __shared__ uint64_t sm[];
     __shared__ uint64_t wtmp[2 * (kScanThreads / 32)];
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
-    const int64_t items = (int64_t)a.S + a.nslots;
+    if (phase == 1 && a.hdr->n_need == 0) return;
+    const HEntry* bt = phase == 0 ? a.btab : a.btab2;
+    const int64_t items = phase == 0 ? (int64_t)a.S : (int64_t)a.nslots;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const bool is_new = phase == 0;
+        const int id = (int)it;
         int m;
-        bool is_new = it < a.S;
-        int id = is_new ? (int)it : (int)(it - a.S);
         if (is_new) m = a.span_len[id];
         else {
             if (a.slot_state[id] != CP_SLOT_LIVE) continue;
@@ -267,7 +280,7 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a) {
             const bool act = o < nwin;
             const uint64_t W = act ? cp_subhash(sm, o, a.w, Bw) : 0;
             // needles among new spans (batch table)
-            cp_warp_probe<false>(a.btab, (uint32_t)(a.BT - 1), a.logBT, W, act, [&](int owner, const HEntry& e) {
+            cp_warp_probe<false>(bt, (uint32_t)(a.BT - 1), a.logBT, W, act, [&](int owner, const HEntry& e) {
                 const int oo = base + wbase + owner;
                 const int j = e.slot, mj = e.len;
                 if (!(is_new && j == id) && oo + mj <= m && cp_subhash(sm, oo, mj, a.pw[mj]) == e.full)
@@ -285,14 +298,39 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a) {
     }
 }
 
+// after the phase-0 verification: flag spans that equal a live entry, then build btab2 from the rest
+__global__ void k_ins_flag_eq(InsArgs a) {
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    const int nc = min((int64_t)a.hdr->n_cand, a.MAXC);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const Cand cd = a.cand[c];
+        if (cd.ok && cd.hay < 0 && cd.needle >= 0 && a.slot_len[cd.needle] == a.span_len[-1 - cd.hay])
+            a.eq_old[-1 - cd.hay] = 1;
+    }
+}
+__global__ void k_ins_build_btab2(InsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->n_cand0 = min((int64_t)a.hdr->n_cand, a.MAXC);
+    for (int s = warp; s < a.S; s += nwarps) {
+        if (a.eq_old[s]) continue;
+        HEntry v; v.key = a.span_pre[s]; v.full = a.span_full[s]; v.slot = s; v.len = a.span_len[s]; v.pad = 0;
+        cp_warp_insert(a.btab2, (uint32_t)(a.BT - 1), a.logBT, v, false);
+        if (lane == 0) atomicAdd(&a.hdr->n_need, 1);
+    }
+}
+
 // warp per candidate: exact token comparison of needle vs haystack[off, off + len(needle))
-__global__ void k_ins_verify(InsArgs a) {
+__global__ void k_ins_verify(InsArgs a, int from_phase1) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
     const int nc = min((int64_t)a.hdr->n_cand, a.MAXC);
-    for (int c = warp; c < nc; c += nwarps) {
+    const int c0 = from_phase1 ? a.hdr->n_cand0 : 0;
+    for (int c = c0 + warp; c < nc; c += nwarps) {
         const Cand cd = a.cand[c];
         const int nm = cd.needle < 0 ? a.span_len[-1 - cd.needle] : a.slot_len[cd.needle];
         int bad = 0;
@@ -453,7 +491,35 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         __syncthreads();
     };
 
-    int j0 = 0;
+    // ---- parallel prefix: until the first span that must be stored, nothing is stored or removed,
+    //      so every span before it is decided against the initial state (duplicates only refresh
+    //      last_used, which no decision reads).  In steady-state serving this is the whole batch.
+    __shared__ int s_jstar;
+    if (tid == 0) s_jstar = a.S;
+    __syncthreads();
+    for (int j = tid; j < a.S; j += blockDim.x) {
+        bool decided = false;
+        for (int q = soff[j]; q < soff[j + 1] && !decided; ++q) {
+            const int2 rr = rec[q];
+            if (rr.x >= 0 && (sflag[rr.x] & 1) && (rr.y == REL_EQ || rr.y == REL_CONTAINER)) decided = true;
+        }
+        if (!decided) atomicMin(&s_jstar, j);
+    }
+    __syncthreads();
+    const int jstar = s_jstar;
+    for (int j = tid; j < jstar; j += blockDim.x) {
+        int dup = -1, cont = -1, cont_id = 0x7fffffff;
+        for (int q = soff[j]; q < soff[j + 1]; ++q) {
+            const int2 rr = rec[q];
+            if (rr.x < 0 || !(sflag[rr.x] & 1)) continue;
+            if (rr.y == REL_EQ) dup = rr.x;
+            else if (rr.y == REL_CONTAINER) { const int sid = a.slot_id[rr.x]; if (sid < cont_id) { cont_id = sid; cont = rr.x; } }
+        }
+        if (dup >= 0) { a.slot_last[dup] = a.t; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE; }
+        else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
+    }
+    __syncthreads();
+    int j0 = jstar;
     while (true) {
         // ---- thread 0 runs ahead through spans that need no block-wide work
         if (tid == 0) {
@@ -841,6 +907,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->cp_dst = (int32_t*)(s + L.scr_off[19]); x->cp_len = (int32_t*)(s + L.scr_off[20]);
     x->cp_delta = (int32_t*)(s + L.scr_off[21]); x->out_tmp = (int32_t*)(s + L.scr_off[22]);
     x->row_src = (long long*)(s + L.scr_off[23]); x->row_dst = (long long*)(s + L.scr_off[24]);
+    x->eq_old = (int32_t*)(s + L.scr_off[25]); x->btab2 = (HEntry*)(s + L.scr_off[26]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -992,15 +1059,18 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
-    a.out_tmp = x->out_tmp;
+    a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.btab2 = x->btab2;
 
     const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
     k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    const int64_t items = (int64_t)num_spans + x->S;
     const size_t scan_smem = 8 * ((size_t)x->cfg.max_span_len + 1);
-    k_ins_scan<<<(int)std::min<int64_t>(items, 148 * 6), kScanThreads, scan_smem, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_verify<<<148 * 4, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_scan<<<(int)std::min<int64_t>(num_spans, 148 * 6), kScanThreads, scan_smem, st>>>(a, 0); CP_COUNT_LAUNCH();
+    k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 0); CP_COUNT_LAUNCH();
+    k_ins_flag_eq<<<148, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_build_btab2<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
+    k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
     const size_t csm = CommitSmem(x->S, num_spans).total;
     if (csm > 200 * 1024) return CP_ERR_UNSUPPORTED;
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();

@@ -51,7 +51,9 @@ struct DevHeader {                   // first 256 B of META
     int32_t n_removed;               // insert: slots removed this call
     int32_t n_chunks;                // gather/copy: work chunks
     int32_t n_new_live;
-    int32_t pad[46];
+    int32_t n_cand0;                 // insert: candidates of the first scan phase
+    int32_t n_need;                  // insert: spans that need the old-entry haystack scan
+    int32_t pad[44];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 
@@ -99,6 +101,8 @@ struct cp_index {
     Cand* cand;
     int32_t *rel_off, *rel_rec;    // CSR per span of relation records (other << 2 | kind)
     int32_t *new_slot, *removed, *cp_req, *cp_slot, *cp_dst, *cp_len, *cp_delta, *out_tmp;
+    int32_t* eq_old;     // [MS] span has an equal live pool entry
+    HEntry* btab2;       // batch table restricted to spans without an equal live entry
 };
 
 // ---- launch bookkeeping -------------------------------------------------------------------
@@ -251,6 +255,8 @@ __device__ __forceinline__ bool cp_warp_insert(HEntry* tab, uint32_t mask, int l
         const uint32_t p = (p0 + lane) & mask;
         const unsigned long long k = *((volatile unsigned long long*)&tab[p].key);
         unsigned cand = __ballot_sync(0xffffffffu, k == CP_EMPTY_KEY || (allow_tomb && k == CP_TOMB_KEY));
+        // always the FIRST free slot of the probe sequence: linear probing stops at the first EMPTY,
+        // so an entry placed after an EMPTY of its own sequence would be unreachable
         while (cand) {
             const int l = __ffs(cand) - 1;
             int won = 0, was_empty = 0;
@@ -263,7 +269,7 @@ __device__ __forceinline__ bool cp_warp_insert(HEntry* tab, uint32_t mask, int l
             }
             won = __shfl_sync(0xffffffffu, won, l);
             if (won) return __shfl_sync(0xffffffffu, was_empty, l);
-            cand &= cand - 1;
+            cand &= cand - 1;           // lost the race: that slot is taken now, the next free one is first
         }
         p0 = (p0 + 32) & mask;
     }

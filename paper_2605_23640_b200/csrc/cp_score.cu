@@ -12,26 +12,32 @@
 #include "cp_internal.cuh"
 #include <algorithm>
 #include <cstring>
+#include <climits>
 #include <vector>
 
 namespace {
 
-constexpr int kSpansPerLaunch = 256;
+constexpr int kSpansPerLaunch = 900;        // 32-B descriptors: 28.8 KB of kernel parameters
 constexpr int kRowThreads = 256;
 constexpr int kTopkThreads = 1024;
 
-struct SpanDesc {
+struct SpanDesc {                               // 32 B
     const float* A;
-    int32_t n, heads, l, r;
-    int64_t score_off, bits_off, row_begin;
+    int32_t row_begin;                          // first global row of this span within the launch
+    int32_t score_off, bits_off;                // relative to the launch's output bases
+    int32_t n, l;
+    int32_t r_heads;                            // r | (heads << 24)
+    __host__ __device__ int r() const { return r_heads & 0xffffff; }
+    __host__ __device__ int heads() const { return (int)((uint32_t)r_heads >> 24); }
 };
+static_assert(sizeof(SpanDesc) == 32, "SpanDesc must be 32 B");
 
 struct ScoreArgs {
     SpanDesc sp[kSpansPerLaunch];
     int32_t nsp;
-    int64_t total_rows;
+    int32_t total_rows;
     int32_t rho_num, rho_den;
-    long long* scores;
+    long long* scores;                          // launch base (score_off is relative to it)
     uint32_t* bits;
 };
 
@@ -46,42 +52,44 @@ __device__ __forceinline__ float4 ld_nc4(const float4* p) {
     return f;
 }
 
-// warp-strided sum of q(p[0..cnt)) with 128-bit loads on the aligned body
-__device__ __forceinline__ long long warp_qsum(const float* p, int cnt, int lane) {
-    if (cnt <= 0) return 0;
-    long long acc = 0;
-    const int mis = (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
-    const int head = min(cnt, mis ? 4 - mis : 0);
-    if (lane < head) acc += q40(__ldg(p + lane));
-    const int nvec = (cnt - head) >> 2;
-    const float4* v4 = reinterpret_cast<const float4*>(p + head);
-#pragma unroll 4
-    for (int q = lane; q < nvec; q += 32) {
-        const float4 f = ld_nc4(v4 + q);
-        acc += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
-    }
-    const int t0 = head + 4 * nvec;
-    if (t0 + lane < cnt) acc += q40(__ldg(p + t0 + lane));
-    return acc;
-}
-
+// One warp per span row: a single pass over A[i][0..i] with 128-bit loads (4 in flight per lane);
+// columns j < l* add to inter, l* <= j <= i to intra.
 __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t gr = warp; gr < a.total_rows; gr += nwarps) {
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    for (int gr = warp; gr < a.total_rows; gr += nwarps) {
         int lo = 0, hi = a.nsp - 1;
         while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
-        const SpanDesc& s = a.sp[lo];
-        const int i = s.l + (int)(gr - s.row_begin);
+        const SpanDesc s = a.sp[lo];
+        const int i = s.l + (gr - s.row_begin);
         const int l = s.l;
-        long long acc = 0;
-        for (int h = 0; h < s.heads; ++h) {
+        long long inter = 0, intra = 0;
+        const int heads = s.heads();
+        for (int h = 0; h < heads; ++h) {
             const float* row = s.A + ((int64_t)h * s.n + i) * (int64_t)s.n;
             const int cnt = i + 1;                                   // causal: columns 0..i
-            acc += warp_qsum(row, min(l, cnt), lane);                // inter: j < l*
-            acc -= warp_qsum(row + l, cnt - l, lane);                // intra: l* <= j <= i
+            const int mis = (int)((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
+            const int head = min(cnt, mis ? 4 - mis : 0);
+            if (lane < head) { const long long v = q40(__ldg(row + lane)); if (lane < l) inter += v; else intra += v; }
+            const int nvec = (cnt - head) >> 2;
+            const float4* v4 = reinterpret_cast<const float4*>(row + head);
+#pragma unroll 4
+            for (int q = lane; q < nvec; q += 32) {
+                const float4 f = ld_nc4(v4 + q);
+                const int j = head + 4 * q;
+                if (j + 3 < l) inter += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
+                else if (j >= l) intra += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
+                else {
+                    const long long v0 = q40(f.x), v1 = q40(f.y), v2 = q40(f.z), v3 = q40(f.w);
+                    inter += (j < l ? v0 : 0) + (j + 1 < l ? v1 : 0) + (j + 2 < l ? v2 : 0);
+                    intra += (j < l ? 0 : v0) + (j + 1 < l ? 0 : v1) + (j + 2 < l ? 0 : v2) + v3;
+                }
+            }
+            const int t0 = head + 4 * nvec;
+            if (t0 + lane < cnt) { const int j = t0 + lane; const long long v = q40(__ldg(row + j)); if (j < l) inter += v; else intra += v; }
         }
+        long long acc = inter - intra;
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) a.scores[s.score_off + (i - l)] = acc;
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_score_topk(const ScoreArgs a) 
     __shared__ int s_digit, s_rem;
     __shared__ int s_wsum[kTopkThreads / 32 + 1];
     const SpanDesc& s = a.sp[blockIdx.x];
-    const int m = s.r - s.l + 1;
+    const int m = s.r() - s.l + 1;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long* key = (unsigned long long*)smt;
     uint8_t* sel = (uint8_t*)(smt + 8 * (size_t)m);
@@ -192,14 +200,21 @@ extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* a
         ScoreArgs& a = args[0];
         std::memset(&a, 0, sizeof(a));
         a.nsp = std::min(kSpansPerLaunch, num_spans - s0);
+        const int64_t sbase = score_off_h[s0], bbase = bits_off_h[s0];
         int64_t rows = 0;
         for (int q = 0; q < a.nsp; ++q) {
             const int s = s0 + q;
-            a.sp[q] = SpanDesc{attn_h[s], n_h[s], heads_h[s], l_h[s], r_h[s], score_off_h[s], bits_off_h[s], rows};
+            if (heads_h[s] > 255 || n_h[s] >= (1 << 24) || score_off_h[s] - sbase > INT32_MAX ||
+                bits_off_h[s] - bbase > INT32_MAX || rows > INT32_MAX - 65536) return CP_ERR_INVALID_ARG;
+            SpanDesc d;
+            d.A = attn_h[s]; d.row_begin = (int32_t)rows;
+            d.score_off = (int32_t)(score_off_h[s] - sbase); d.bits_off = (int32_t)(bits_off_h[s] - bbase);
+            d.n = n_h[s]; d.l = l_h[s]; d.r_heads = r_h[s] | (heads_h[s] << 24);
+            a.sp[q] = d;
             rows += r_h[s] - l_h[s] + 1;
         }
-        a.total_rows = rows; a.rho_num = rho_num; a.rho_den = rho_den;
-        a.scores = (long long*)out_scores; a.bits = out_bits;
+        a.total_rows = (int32_t)rows; a.rho_num = rho_num; a.rho_den = rho_den;
+        a.scores = (long long*)out_scores + sbase; a.bits = out_bits + bbase;
         const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 8);
         k_score_rows<<<grid, kRowThreads, 0, st>>>(a);
         CP_COUNT_LAUNCH();

@@ -252,8 +252,15 @@ def bench_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only switches: run several ranks on one GPU over gloo (the driver uses NCCL, one GPU per rank)
+    if os.environ.get("BENCH_DEVICE0"):
+        local = 0
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     S = setup_ours(args, rank, world, device)
@@ -303,10 +310,11 @@ def bench_ours(args):
     ms_step = ms_total / K
     gather_ms = float(phase[:, 1].mean())
     if world > 1:
-        t = torch.tensor([ms_step, gather_ms], dtype=torch.float64, device=device)
+        rdev = device if backend == "nccl" else torch.device("cpu")
+        t = torch.tensor([ms_step, gather_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step, gather_ms_max = float(t[0]), float(t[1])
-        tot = torch.tensor([reused_bytes, gather_bytes], dtype=torch.float64, device=device)
+        tot = torch.tensor([reused_bytes, gather_bytes], dtype=torch.float64, device=rdev)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         reused_all, gather_all = float(tot[0]), float(tot[1])
     else:
@@ -392,7 +400,8 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=S.rdb.tokens.device)
+        nccl = dist.get_backend() == "nccl"
+        t = torch.tensor([ms], dtype=torch.float64, device=S.rdb.tokens.device if nccl else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     return {"value": round(reused_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),

@@ -52,8 +52,14 @@ __device__ __forceinline__ float4 ld_nc4(const float4* p) {
     return f;
 }
 
-// One warp per span row: a single pass over A[i][0..i] with 128-bit loads (4 in flight per lane);
-// columns j < l* add to inter, l* <= j <= i to intra.
+// signed fixed-point sum of a float4 at columns j..j+3: + for j < l* (inter), - otherwise (intra)
+__device__ __forceinline__ long long signed4(const float4 f, int j, int l) {
+    const long long v0 = q40(f.x), v1 = q40(f.y), v2 = q40(f.z), v3 = q40(f.w);
+    return (j < l ? v0 : -v0) + (j + 1 < l ? v1 : -v1) + (j + 2 < l ? v2 : -v2) + (j + 3 < l ? v3 : -v3);
+}
+
+// One warp per span row: a single pass over A[i][0..i], 128-bit loads issued four at a time per lane
+// (16 KB in flight per warp-batch) so the row stream is bandwidth- rather than latency-bound.
 __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -61,38 +67,32 @@ __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
     for (int gr = warp; gr < a.total_rows; gr += nwarps) {
         int lo = 0, hi = a.nsp - 1;
         while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
-        const SpanDesc s = a.sp[lo];
-        const int i = s.l + (gr - s.row_begin);
-        const int l = s.l;
-        long long inter = 0, intra = 0;
-        const int heads = s.heads();
+        const float* A = a.sp[lo].A;
+        const int n = a.sp[lo].n, l = a.sp[lo].l, heads = a.sp[lo].heads();
+        const int i = l + (gr - a.sp[lo].row_begin);
+        const int score_off = a.sp[lo].score_off;
+        long long acc = 0;
         for (int h = 0; h < heads; ++h) {
-            const float* row = s.A + ((int64_t)h * s.n + i) * (int64_t)s.n;
+            const float* row = A + ((int64_t)h * n + i) * (int64_t)n;
             const int cnt = i + 1;                                   // causal: columns 0..i
             const int mis = (int)((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
             const int head = min(cnt, mis ? 4 - mis : 0);
-            if (lane < head) { const long long v = q40(__ldg(row + lane)); if (lane < l) inter += v; else intra += v; }
+            if (lane < head) { const long long v = q40(__ldg(row + lane)); acc += lane < l ? v : -v; }
             const int nvec = (cnt - head) >> 2;
             const float4* v4 = reinterpret_cast<const float4*>(row + head);
-#pragma unroll 4
-            for (int q = lane; q < nvec; q += 32) {
-                const float4 f = ld_nc4(v4 + q);
-                const int j = head + 4 * q;
-                if (j + 3 < l) inter += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
-                else if (j >= l) intra += (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w));
-                else {
-                    const long long v0 = q40(f.x), v1 = q40(f.y), v2 = q40(f.z), v3 = q40(f.w);
-                    inter += (j < l ? v0 : 0) + (j + 1 < l ? v1 : 0) + (j + 2 < l ? v2 : 0);
-                    intra += (j < l ? 0 : v0) + (j + 1 < l ? 0 : v1) + (j + 2 < l ? 0 : v2) + v3;
-                }
+            int q = lane;
+            for (; q + 96 < nvec; q += 128) {
+                const float4 f0 = ld_nc4(v4 + q), f1 = ld_nc4(v4 + q + 32), f2 = ld_nc4(v4 + q + 64), f3 = ld_nc4(v4 + q + 96);
+                acc += signed4(f0, head + 4 * q, l) + signed4(f1, head + 4 * (q + 32), l) +
+                       signed4(f2, head + 4 * (q + 64), l) + signed4(f3, head + 4 * (q + 96), l);
             }
+            for (; q < nvec; q += 32) acc += signed4(ld_nc4(v4 + q), head + 4 * q, l);
             const int t0 = head + 4 * nvec;
-            if (t0 + lane < cnt) { const int j = t0 + lane; const long long v = q40(__ldg(row + j)); if (j < l) inter += v; else intra += v; }
+            if (t0 + lane < cnt) { const int j = t0 + lane; const long long v = q40(__ldg(row + j)); acc += j < l ? v : -v; }
         }
-        long long acc = inter - intra;
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.scores[s.score_off + (i - l)] = acc;
+        if (lane == 0) a.scores[score_off + (i - l)] = acc;
     }
 }
 

@@ -188,10 +188,16 @@ def _passage(seed: int, pid: int, lo: int, hi: int) -> np.ndarray:
     return _fill(r, n)
 
 
+_ZIPF_CDF = {}
+
+
 def _zipf(rng: np.random.Generator, n_items: int, s: float, size: int) -> np.ndarray:
-    p = 1.0 / np.power(np.arange(1, n_items + 1, dtype=np.float64), s)
-    p /= p.sum()
-    return rng.choice(n_items, size=size, p=p)
+    key = (n_items, s)
+    if key not in _ZIPF_CDF:
+        p = 1.0 / np.power(np.arange(1, n_items + 1, dtype=np.float64), s)
+        _ZIPF_CDF[key] = np.cumsum(p / p.sum())
+    cdf = _ZIPF_CDF[key]
+    return np.minimum(np.searchsorted(cdf, rng.random(size), side="right"), n_items - 1)
 
 
 # ----------------------------------------------------------------------------

@@ -116,7 +116,9 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 23 row_src
     sput(8 * (size_t)L->CH * CP_GATHER_CHUNK);               // 24 row_dst
     sput(4 * (size_t)L->MS);                                 // 25 eq_old
-    sput(sizeof(HEntry) * L->BT);                            // 26 btab2
+    sput(sizeof(HEntry) * L->BT);                            // 26 dtab
+    sput(4 * (size_t)L->MS);                                 // 27 span_rep
+    sput(sizeof(Rec16) * (size_t)L->MS);                     // 28 precs
     L->scr_size = o;
 }
 
@@ -157,7 +159,7 @@ struct InsArgs {
     unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed;
     int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
-    int32_t* eq_old; HEntry* btab2;
+    int32_t* eq_old; HEntry* dtab; int32_t* span_rep; Rec16* precs;
 };
 
 // error codes are ordered per span: range -> too short -> capacity -> sensitive (same order as the oracle)
@@ -176,8 +178,8 @@ __global__ void k_ins_validate(InsArgs a) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.S; j += gridDim.x * blockDim.x) a.eq_old[j] = 0;
     // clear the batch prefix table
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.BT; i += (int64_t)gridDim.x * blockDim.x) {
-        a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = -1; a.btab[i].len = 0; a.btab[i].full = 0;
-        a.btab2[i].key = CP_EMPTY_KEY; a.btab2[i].slot = -1; a.btab2[i].len = 0; a.btab2[i].full = 0;
+        a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = 0; a.btab[i].len = 0; a.btab[i].full = 0;      // prefix buckets
+        a.dtab[i].key = CP_EMPTY_KEY; a.dtab[i].slot = 0x7fffffff; a.dtab[i].len = 0; a.dtab[i].full = 0;
     }
     if (cp_err_set(a.hdr)) return;
     for (int s = warp; s < a.S; s += nwarps) {
@@ -224,9 +226,92 @@ __global__ void k_ins_hash(InsArgs a) {
             return v;
         };
         const uint64_t pre = fold(a.w), full = fold(m);
-        if (lane == 0) { a.span_pre[s] = pre; a.span_full[s] = full; }
-        HEntry v; v.key = pre; v.full = full; v.slot = s; v.len = m; v.pad = 0;
-        cp_warp_insert(a.btab, (uint32_t)(a.BT - 1), a.logBT, v, false);
+        if (lane == 0) {
+            a.span_pre[s] = pre; a.span_full[s] = full;
+            HEntry* e = cp_find_or_insert(a.dtab, (uint32_t)(a.BT - 1), a.logBT, full);   // batch dedup
+            atomicMin(&e->slot, s);
+        }
+    }
+}
+
+// token fetch helpers (forward)
+__device__ __forceinline__ const int32_t* span_tokens_f(const InsArgs& a, int j) {
+    return a.tokens + a.offsets[a.span_req[j]] + a.span_begin[j];
+}
+
+// warp per span: representative = smallest span with identical tokens (verified); representatives
+// are counted into their prefix bucket
+__global__ void k_ins_rep(InsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    for (int s = warp; s < a.S; s += nwarps) {
+        const HEntry* e = cp_find_unique(a.dtab, (uint32_t)(a.BT - 1), a.logBT, a.span_full[s]);
+        int r = e ? e->slot : s;
+        if (r != s) {
+            bool same = a.span_len[r] == a.span_len[s] && a.span_pre[r] == a.span_pre[s];
+            if (same) {
+                const int32_t* x = span_tokens_f(a, s);
+                const int32_t* y = span_tokens_f(a, r);
+                int bad = 0;
+                for (int t = lane; t < a.span_len[s]; t += 32) bad |= x[t] != y[t];
+                same = !__any_sync(0xffffffffu, bad);
+            }
+            if (!same) r = s;                       // full-hash collision: keep the span on its own
+        }
+        if (lane == 0) {
+            a.span_rep[s] = r;
+            if (r == s) {
+                HEntry* b = cp_find_or_insert(a.btab, (uint32_t)(a.BT - 1), a.logBT, a.span_pre[s]);
+                atomicAdd(&b->len, 1);
+            }
+        }
+    }
+}
+
+// one block: bucket offsets = exclusive scan of the counts over the prefix table
+__global__ void __launch_bounds__(1024) k_ins_bucket_offsets(InsArgs a) {
+    __shared__ int s_w[33];
+    __shared__ int s_carry;
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < a.BT; b0 += 1024) {
+        const int64_t i = b0 + tid;
+        const int v = (i < a.BT && a.btab[i].key != CP_EMPTY_KEY) ? a.btab[i].len : 0;
+        int inc = v;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_w[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            int x = s_w[lane], xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            s_w[lane] = xi - x;
+            if (lane == 31) s_w[32] = xi;
+        }
+        __syncthreads();
+        if (i < a.BT && v > 0) {
+            const int off = s_carry + s_w[wid] + inc - v;
+            a.btab[i].slot = off;
+            a.btab[i].full = (unsigned long long)off;              // fill cursor
+        }
+        __syncthreads();
+        if (tid == 0) s_carry += s_w[32];
+        __syncthreads();
+    }
+}
+
+// thread per representative: scatter into its prefix bucket
+__global__ void k_ins_bucket_fill(InsArgs a) {
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.S; s += gridDim.x * blockDim.x) {
+        if (a.span_rep[s] != s) continue;
+        HEntry* b = const_cast<HEntry*>(cp_find_unique(a.btab, (uint32_t)(a.BT - 1), a.logBT, a.span_pre[s]));
+        const unsigned long long pos = atomicAdd(&b->full, 1ULL);
+        Rec16 r; r.full = a.span_full[s]; r.len = a.span_len[s]; r.id = s;
+        a.precs[pos] = r;
     }
 }
 
@@ -255,14 +340,15 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a, int phase)
     __shared__ uint64_t wtmp[2 * (kScanThreads / 32)];
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
     if (phase == 1 && a.hdr->n_need == 0) return;
-    const HEntry* bt = phase == 0 ? a.btab : a.btab2;
     const int64_t items = phase == 0 ? (int64_t)a.S : (int64_t)a.nslots;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const bool is_new = phase == 0;
         const int id = (int)it;
         int m;
-        if (is_new) m = a.span_len[id];
-        else {
+        if (is_new) {
+            if (a.span_rep[id] != id) continue;               // duplicates inherit their representative's relations
+            m = a.span_len[id];
+        } else {
             if (a.slot_state[id] != CP_SLOT_LIVE) continue;
             m = a.slot_len[id];
         }
@@ -279,11 +365,13 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a, int phase)
             const int o = base + threadIdx.x;
             const bool act = o < nwin;
             const uint64_t W = act ? cp_subhash(sm, o, a.w, Bw) : 0;
-            // needles among new spans (batch table)
-            cp_warp_probe<false>(bt, (uint32_t)(a.BT - 1), a.logBT, W, act, [&](int owner, const HEntry& e) {
+            // needles among the batch's representatives (bucketed prefix table)
+            cp_warp_bucket_probe(a.btab, (uint32_t)(a.BT - 1), a.logBT, a.precs, W, act,
+                                 [&](int owner, unsigned long long full, int mj, int j) {
                 const int oo = base + wbase + owner;
-                const int j = e.slot, mj = e.len;
-                if (!(is_new && j == id) && oo + mj <= m && cp_subhash(sm, oo, mj, a.pw[mj]) == e.full)
+                if (is_new && j == id) return;
+                if (!is_new && a.eq_old[j]) return;           // equal to a live entry: cannot be strictly inside one
+                if (oo + mj <= m && cp_subhash(sm, oo, mj, a.pw[mj]) == full)
                     push_cand(a, is_new ? -1 - id : id, -1 - j, oo);
             });
             // needles among live pool entries (new-span haystacks only)
@@ -308,18 +396,14 @@ __global__ void k_ins_flag_eq(InsArgs a) {
             a.eq_old[-1 - cd.hay] = 1;
     }
 }
-__global__ void k_ins_build_btab2(InsArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+__global__ void k_ins_count_need(InsArgs a) {
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->n_cand0 = min((int64_t)a.hdr->n_cand, a.MAXC);
-    for (int s = warp; s < a.S; s += nwarps) {
-        if (a.eq_old[s]) continue;
-        HEntry v; v.key = a.span_pre[s]; v.full = a.span_full[s]; v.slot = s; v.len = a.span_len[s]; v.pad = 0;
-        cp_warp_insert(a.btab2, (uint32_t)(a.BT - 1), a.logBT, v, false);
-        if (lane == 0) atomicAdd(&a.hdr->n_need, 1);
-    }
+    int need = 0;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.S; s += gridDim.x * blockDim.x)
+        need += (a.span_rep[s] == s && !a.eq_old[s]);
+    for (int o = 16; o; o >>= 1) need += __shfl_xor_sync(0xffffffffu, need, o);
+    if ((threadIdx.x & 31) == 0 && need) atomicAdd(&a.hdr->n_need, need);
 }
 
 // warp per candidate: exact token comparison of needle vs haystack[off, off + len(needle))
@@ -348,10 +432,11 @@ enum { REL_EQ = 0, REL_CONTAINER = 1, REL_CONTAINED = 2 };
 constexpr int kMaxSupersede = 1024;
 
 struct CommitSmem {                  // byte offsets of the dynamic shared-memory carve-up
-    size_t snew, soff, srec, total;
+    size_t snew, srep, soff, srec, total;
     __host__ __device__ CommitSmem(int nslots, int S) {
         snew = ((size_t)nslots + 15) & ~(size_t)15;
-        soff = snew + 4 * (size_t)S;
+        srep = snew + 4 * (size_t)S;
+        soff = srep + 4 * (size_t)S;
         srec = (soff + 4 * ((size_t)S + 1) + 15) & ~(size_t)15;
         total = srec + 8 * (size_t)kCommitRecCap;
     }
@@ -390,6 +475,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     const CommitSmem lay(a.nslots, a.S);
     uint8_t* sflag = smc;
     int32_t* snew = (int32_t*)(smc + lay.snew);
+    int32_t* srep = (int32_t*)(smc + lay.srep);
     int32_t* soff = (int32_t*)(smc + lay.soff);
     int2* srec = (int2*)(smc + lay.srec);
     __shared__ int s_abort, s_nrec, s_j, s_store_slot, s_npg, s_pop_head, s_nrm, s_need;
@@ -421,7 +507,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     // ---- load state
     for (int i = tid; i < a.nslots; i += blockDim.x) sflag[i] = a.slot_state[i] == CP_SLOT_LIVE ? 1 : 0;
-    for (int j = tid; j < a.S; j += blockDim.x) { snew[j] = -1; soff[j] = 0; }
+    for (int j = tid; j < a.S; j += blockDim.x) { snew[j] = -1; soff[j] = 0; srep[j] = a.span_rep[j]; }
     if (tid == 0) {
         soff[a.S] = 0;
         s_live_tokens = a.hdr->live_tokens; s_fifo_head = a.hdr->fifo_head; s_fifo_count = a.hdr->fifo_count;
@@ -499,7 +585,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __syncthreads();
     for (int j = tid; j < a.S; j += blockDim.x) {
         bool decided = false;
-        for (int q = soff[j]; q < soff[j + 1] && !decided; ++q) {
+        const int rj = srep[j];                      // duplicates share their representative's relations
+        for (int q = soff[rj]; q < soff[rj + 1] && !decided; ++q) {
             const int2 rr = rec[q];
             if (rr.x >= 0 && (sflag[rr.x] & 1) && (rr.y == REL_EQ || rr.y == REL_CONTAINER)) decided = true;
         }
@@ -509,7 +596,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     const int jstar = s_jstar;
     for (int j = tid; j < jstar; j += blockDim.x) {
         int dup = -1, cont = -1, cont_id = 0x7fffffff;
-        for (int q = soff[j]; q < soff[j + 1]; ++q) {
+        const int rj = srep[j];
+        for (int q = soff[rj]; q < soff[rj + 1]; ++q) {
             const int2 rr = rec[q];
             if (rr.x < 0 || !(sflag[rr.x] & 1)) continue;
             if (rr.y == REL_EQ) dup = rr.x;
@@ -525,9 +613,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         if (tid == 0) {
             s_j = a.S; s_nrm = 0;
             for (int j = j0; j < a.S; ++j) {
-                const int b = soff[j], e = soff[j + 1];
+                const int rj = srep[j];
+                const int b = soff[rj], e = soff[rj + 1];
                 int dup = -1;
-                for (int q = b; q < e; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
+                if (rj != j && is_live(-1 - rj)) dup = resolve(-1 - rj);      // equal to its stored representative
+                for (int q = b; q < e && dup < 0; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
                 if (dup >= 0) {
                     a.slot_last[dup] = a.t;                      // Duplicate refreshes last_used (R#20)
                     a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
@@ -907,7 +997,8 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->cp_dst = (int32_t*)(s + L.scr_off[19]); x->cp_len = (int32_t*)(s + L.scr_off[20]);
     x->cp_delta = (int32_t*)(s + L.scr_off[21]); x->out_tmp = (int32_t*)(s + L.scr_off[22]);
     x->row_src = (long long*)(s + L.scr_off[23]); x->row_dst = (long long*)(s + L.scr_off[24]);
-    x->eq_old = (int32_t*)(s + L.scr_off[25]); x->btab2 = (HEntry*)(s + L.scr_off[26]);
+    x->eq_old = (int32_t*)(s + L.scr_off[25]); x->dtab = (HEntry*)(s + L.scr_off[26]);
+    x->span_rep = (int32_t*)(s + L.scr_off[27]); x->precs = (Rec16*)(s + L.scr_off[28]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -1059,16 +1150,19 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
-    a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.btab2 = x->btab2;
+    a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
 
     const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
     k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_rep<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_bucket_offsets<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_bucket_fill<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     const size_t scan_smem = 8 * ((size_t)x->cfg.max_span_len + 1);
     k_ins_scan<<<(int)std::min<int64_t>(num_spans, 148 * 6), kScanThreads, scan_smem, st>>>(a, 0); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 0); CP_COUNT_LAUNCH();
     k_ins_flag_eq<<<148, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_build_btab2<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
     const size_t csm = CommitSmem(x->S, num_spans).total;

@@ -57,6 +57,8 @@ struct DevHeader {                   // first 256 B of META
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 
+struct Rec16 { unsigned long long full; int32_t len; int32_t id; };   // bucket record (16 B)
+
 // candidate relation found by the insert scans: needle's tokens occur in haystack at offset
 struct Cand {
     int32_t hay;      // >= 0: pool slot;  < 0: new span (-1 - j)
@@ -102,7 +104,9 @@ struct cp_index {
     int32_t *rel_off, *rel_rec;    // CSR per span of relation records (other << 2 | kind)
     int32_t *new_slot, *removed, *cp_req, *cp_slot, *cp_dst, *cp_len, *cp_delta, *out_tmp;
     int32_t* eq_old;     // [MS] span has an equal live pool entry
-    HEntry* btab2;       // batch table restricted to spans without an equal live entry
+    HEntry* dtab;        // unique table keyed by full hash -> smallest span index (batch dedup)
+    int32_t* span_rep;   // [MS] representative (smallest equal span) of each span
+    Rec16* precs;        // [MS] bucket records of the batch prefix table
 };
 
 // ---- launch bookkeeping -------------------------------------------------------------------
@@ -192,6 +196,54 @@ __device__ void cp_block_prefix_hash(F tok, int n, uint64_t B, uint64_t* sh, uin
     __syncthreads();
 }
 
+
+// ---- unique-key tables (find-or-insert: contention only on the first insert of a key) -----------
+
+__device__ __forceinline__ HEntry* cp_find_or_insert(HEntry* tab, uint32_t mask, int logT, uint64_t key) {
+    uint32_t pos = (uint32_t)((key * 0x9E3779B97F4A7C15ULL) >> (64 - logT));
+    while (true) {
+        const unsigned long long k = *((volatile unsigned long long*)&tab[pos].key);
+        if (k == key) return &tab[pos];
+        if (k == CP_EMPTY_KEY) {
+            const unsigned long long prev = atomicCAS(&tab[pos].key, CP_EMPTY_KEY, (unsigned long long)key);
+            if (prev == CP_EMPTY_KEY || prev == key) return &tab[pos];
+        }
+        pos = (pos + 1) & mask;
+    }
+}
+__device__ __forceinline__ const HEntry* cp_find_unique(const HEntry* tab, uint32_t mask, int logT, uint64_t key) {
+    uint32_t pos = (uint32_t)((key * 0x9E3779B97F4A7C15ULL) >> (64 - logT));
+    while (true) {
+        const unsigned long long k = tab[pos].key;
+        if (k == key) return &tab[pos];
+        if (k == CP_EMPTY_KEY) return nullptr;
+        pos = (pos + 1) & mask;
+    }
+}
+
+// Warp-level probe of a bucketed multi-value table (unique keys -> [offset, count) into `recs`):
+// each lane finds its bucket; small buckets are walked per lane, large ones (hundreds of spans
+// sharing one system-prompt window) by the whole warp, 32 records per step.
+// on_match(owner_lane, full, len, id) is invoked by the lane that loaded the record.
+template <typename F>
+__device__ __forceinline__ void cp_warp_bucket_probe(const HEntry* tab, uint32_t mask, int logT, const Rec16* recs,
+                                                     uint64_t key, bool active, F on_match) {
+    const int lane = threadIdx.x & 31;
+    int off = 0, cnt = 0;
+    if (active) {
+        const HEntry* e = cp_find_unique(tab, mask, logT, key);
+        if (e) { off = e->slot; cnt = e->len; }
+    }
+    if (cnt <= 4) for (int i = 0; i < cnt; ++i) { const Rec16 r = recs[off + i]; on_match(lane, r.full, r.len, r.id); }
+    unsigned pend = __ballot_sync(0xffffffffu, cnt > 4);
+    while (pend) {
+        const int owner = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int o = __shfl_sync(0xffffffffu, off, owner), c = __shfl_sync(0xffffffffu, cnt, owner);
+        for (int b = 0; b < c; b += 32)
+            if (b + lane < c) { const Rec16 r = recs[o + b + lane]; on_match(owner, r.full, r.len, r.id); }
+    }
+}
 
 // ---- hash-table probing ----------------------------------------------------------------------
 __device__ __forceinline__ HEntry cp_ld_entry(const HEntry* p) {

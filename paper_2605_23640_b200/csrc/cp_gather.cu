@@ -33,6 +33,7 @@ struct RowsArgs {
     char* pool_k; char* pool_v; int64_t P;
     const int32_t* slot_pages; int32_t MP;
     int32_t L, H, d; double theta; int32_t flags; int32_t gptj;
+    int32_t LG;                      // layers per work item (small rows: several layers share one row lookup)
     int32_t* chunk_hit; int32_t* chunk_t0; int64_t CH;
     long long* row_src; long long* row_dst;
     float2* hit_cs; int64_t cs_hits;
@@ -153,7 +154,8 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     __shared__ float2 s_cs[256];
     if (cp_err_set(a.hdr)) return;
     const int nchunks = a.hdr->n_chunks;
-    const int64_t items = (int64_t)nchunks * a.L;
+    const int ngroups = (a.L + a.LG - 1) / a.LG;
+    const int64_t items = (int64_t)nchunks * ngroups;
     const int tid = threadIdx.x;
     const int rowE = a.H * a.d;                        // elements per token row
     const int half = a.d / 2;
@@ -170,7 +172,8 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     int lo_t = 0, hi_t = 0, i0_t = 0;
     task_geom(tid % tpr, lo_t, hi_t, i0_t);
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int c = (int)(item / a.L), l = (int)(item % a.L);
+        const int c = (int)(item / ngroups), lg = (int)(item % ngroups);
+        const int l0 = lg * a.LG, nl = min(a.LG, a.L - l0);
         const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
         const int len = a.l_len[hh];
         const int ntok = min(CP_GATHER_CHUNK, len - t0);
@@ -193,25 +196,26 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
             }
         }
         __syncthreads();
-        const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
-        const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
-        T* dstK = (T*)(a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T));
-        T* dstV = (T*)(a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T));
-        const int ntask = ntok * tpr;
+        // task = ((token g * nl) + layer ll) * tpr + column j  -> j = tid % tpr when tpr | block
+        const int ntask = ntok * nl * tpr;
         for (int base = 0; base < ntask; base += kRowsThreads * UNROLL) {
             uint4 klo[UNROLL], khi[UNROLL], vlo[UNROLL], vhi[UNROLL];
-            int gg[UNROLL], code[UNROLL];
+            int gl[UNROLL], code[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
                 const int task = base + u * kRowsThreads + tid;
                 code[u] = -1;
                 if (task < ntask) {
-                    const int g = task / tpr;
+                    const int row = task / tpr;                 // (g, ll) flattened
+                    const int g = row / nl, ll = row - g * nl;
                     int lo = lo_t, hi = hi_t, i0 = i0_t;
-                    if (!creg) task_geom(task - g * tpr, lo, hi, i0);
-                    gg[u] = creg ? g : task;
+                    if (!creg) task_geom(task - row * tpr, lo, hi, i0);
+                    gl[u] = creg ? row : task;
                     code[u] = s_code[g];
                     if (!(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
+                        const int l = l0 + ll;
+                        const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
+                        const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
                         const int64_t so = s_src[g];
                         klo[u] = ld_stream(srcK + so + lo); khi[u] = ld_stream(srcK + so + hi);
                         vlo[u] = ld_stream(srcV + so + lo); vhi[u] = ld_stream(srcV + so + hi);
@@ -221,8 +225,11 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
                 if (code[u] < 0) continue;
-                int lo = lo_t, hi = hi_t, i0 = i0_t, g = gg[u];
-                if (!creg) { g = gg[u] / tpr; task_geom(gg[u] - g * tpr, lo, hi, i0); }
+                int lo = lo_t, hi = hi_t, i0 = i0_t, row = gl[u];
+                if (!creg) { row = gl[u] / tpr; task_geom(gl[u] - row * tpr, lo, hi, i0); }
+                const int g = row / nl, l = l0 + (row - g * nl);
+                T* dstK = (T*)(a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T));
+                T* dstV = (T*)(a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T));
                 const int64_t dof = s_dst[g];
                 T* dk = dstK + dof;
                 T* dv = dstV + dof;
@@ -259,7 +266,6 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
         __syncthreads();
     }
 }
-
 
 // ============================================================================================
 // TMA bulk-copy variant (cp.async.bulk + mbarrier), the default when a stage fits shared memory.
@@ -579,6 +585,11 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     a.pool_k = x->pool_k; a.pool_v = x->pool_v; a.P = x->P; a.slot_pages = x->slot_pages; a.MP = x->MP;
     a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim; a.theta = x->cfg.rope_theta;
     a.flags = flags; a.gptj = x->cfg.rope_style == CP_ROPE_GPTJ;
+    {
+        const int vec = x->cfg.dtype == CP_BF16 ? 8 : 4;
+        const int tpr = x->cfg.num_kv_heads * x->cfg.head_dim / (2 * vec);
+        a.LG = std::max(1, std::min(x->cfg.num_layers, 2048 / std::max(1, CP_GATHER_CHUNK * tpr)));
+    }
     a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH;
     a.row_src = x->row_src; a.row_dst = x->row_dst;
     a.hit_cs = x->hit_cs; a.cs_hits = x->CS_HITS;

@@ -4,7 +4,8 @@
 40 batches x 256 requests of ~1.6K tokens: [system 128] + 9 x ([PII 3-5] [passage 128-192]) from a
 100K-passage Zipf(1.1) corpus.  Per batch (every request is a reader, then a writer):
   cp_match_spans -> cp_gather_rerotate -> cp_score_deviation (rho = 1/4) -> cp_index_insert
-under a 6M-token LRU budget (≈96 GB of this shard's pool).  Reports per-phase device times, the
+under a 1.5M-token LRU budget (the Zipf draws touch ~16K distinct passages = 2.6M tokens, so the
+budget forces steady LRU eviction: 'high churn').  Reports per-phase device times, the
 insert outcome mix and index-level invariants (budget, live counts, no device error).
 Writes gpurun_out/churn.json."""
 import argparse
@@ -28,7 +29,7 @@ def main():
     ap.add_argument("--batches", type=int, default=40)
     ap.add_argument("--per-batch", type=int, default=256)
     ap.add_argument("--corpus", type=int, default=100000)
-    ap.add_argument("--capacity", type=int, default=6_000_000)
+    ap.add_argument("--capacity", type=int, default=1_500_000)
     ap.add_argument("--heads", type=int, default=1)
     args = ap.parse_args()
     g = Geometry(32, 8, 128, "bf16", 500000.0)
@@ -103,6 +104,8 @@ def main():
         "mean_ms": {k: float(np.mean([r[k] for r in rows[1:]])) for k in ("match_ms", "gather_ms", "score_ms", "insert_ms")},
         "match_rate": float(sum(r["covered"] for r in rows) / sum(r["tokens"] for r in rows)),
         "outcomes": {k: int(sum(r[k] for r in rows)) for k in ("stored", "superseded", "duplicate", "dropped")},
+        "removed_by_lru_or_supersede": int(sum(r["stored"] for r in rows) - snap["num_live"]),
+        "mean_gather_GBps": float(np.mean([r["gather_GBps"] for r in rows[1:]])),
         "generator_s": gen_s, "rows": rows,
     }
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -146,7 +146,7 @@ __device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16) {
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <typename T, bool GPTJ, bool CREG, int UNROLL, int MINB>
+template <typename T, bool GPTJ, bool CREG, int UNROLL, int MINB, bool ML>
 __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     constexpr int VEC = Vec<T>::N;
     __shared__ int64_t s_src[CP_GATHER_CHUNK], s_dst[CP_GATHER_CHUNK];
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     __shared__ float2 s_cs[256];
     if (cp_err_set(a.hdr)) return;
     const int nchunks = a.hdr->n_chunks;
-    const int ngroups = (a.L + a.LG - 1) / a.LG;
+    const int ngroups = ML ? (a.L + a.LG - 1) / a.LG : a.L;
     const int64_t items = (int64_t)nchunks * ngroups;
     const int tid = threadIdx.x;
     const int rowE = a.H * a.d;                        // elements per token row
@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     task_geom(tid % tpr, lo_t, hi_t, i0_t);
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int c = (int)(item / ngroups), lg = (int)(item % ngroups);
-        const int l0 = lg * a.LG, nl = min(a.LG, a.L - l0);
+        const int l0 = lg * a.LG;
+        const int nl = ML ? min(a.LG, a.L - l0) : 1;        // compile-time 1 on the single-layer path
         const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
         const int len = a.l_len[hh];
         const int ntok = min(CP_GATHER_CHUNK, len - t0);
@@ -520,10 +521,11 @@ cp_status launch_rows_c(const RowsArgs& a, int variant, cudaStream_t st) {
         return CP_OK;
     };
     switch (variant) {
-        case 1: return go(k_rows<T, G, CR, 2, 4>);
-        case 2: return go(k_rows<T, G, CR, 4, 2>);
-        case 3: return go(k_rows<T, G, CR, 3, 2>);
-        default: return go(k_rows<T, G, CR, 8, 1>);      // measured best on B200 (tools/gather_ab.py, profiles/r01)
+        case 1: return a.LG > 1 ? go(k_rows<T, G, CR, 2, 4, true>) : go(k_rows<T, G, CR, 2, 4, false>);
+        case 2: return a.LG > 1 ? go(k_rows<T, G, CR, 4, 2, true>) : go(k_rows<T, G, CR, 4, 2, false>);
+        case 3: return a.LG > 1 ? go(k_rows<T, G, CR, 3, 2, true>) : go(k_rows<T, G, CR, 3, 2, false>);
+        // measured best on B200 (tools/gather_ab.py, profiles/r01)
+        default: return a.LG > 1 ? go(k_rows<T, G, CR, 8, 1, true>) : go(k_rows<T, G, CR, 8, 1, false>);
     }
 }
 template <typename T, bool G>

@@ -19,7 +19,7 @@ namespace {
 
 constexpr int kSpansPerLaunch = 900;        // 32-B descriptors: 28.8 KB of kernel parameters
 constexpr int kRowThreads = 256;
-constexpr int kTopkThreads = 1024;
+constexpr int kTopkThreads = 256;
 
 struct SpanDesc {                               // 32 B
     const float* A;
@@ -52,14 +52,31 @@ __device__ __forceinline__ float4 ld_nc4(const float4* p) {
     return f;
 }
 
-// signed fixed-point sum of a float4 at columns j..j+3: + for j < l* (inter), - otherwise (intra)
-__device__ __forceinline__ long long signed4(const float4 f, int j, int l) {
-    const long long v0 = q40(f.x), v1 = q40(f.y), v2 = q40(f.z), v3 = q40(f.w);
-    return (j < l ? v0 : -v0) + (j + 1 < l ? v1 : -v1) + (j + 2 < l ? v2 : -v2) + (j + 3 < l ? v3 : -v3);
+__device__ __forceinline__ long long sum4(const float4 f) { return (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w)); }
+
+// warp-strided sum of q(p[0..cnt)): scalar head up to 16-B alignment, then 128-bit loads issued four at a
+// time per lane (branch-free body), scalar tail
+__device__ __forceinline__ long long warp_qsum(const float* p, int cnt, int lane) {
+    if (cnt <= 0) return 0;
+    long long acc = 0;
+    const int mis = (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
+    const int head = min(cnt, mis ? 4 - mis : 0);
+    if (lane < head) acc += q40(__ldg(p + lane));
+    const int nvec = (cnt - head) >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(p + head);
+    int q = lane;
+    for (; q + 96 < nvec; q += 128) {
+        const float4 f0 = ld_nc4(v4 + q), f1 = ld_nc4(v4 + q + 32), f2 = ld_nc4(v4 + q + 64), f3 = ld_nc4(v4 + q + 96);
+        acc += (sum4(f0) + sum4(f1)) + (sum4(f2) + sum4(f3));
+    }
+    for (; q < nvec; q += 32) acc += sum4(ld_nc4(v4 + q));
+    const int t0 = head + 4 * nvec;
+    if (t0 + lane < cnt) acc += q40(__ldg(p + t0 + lane));
+    return acc;
 }
 
-// One warp per span row: a single pass over A[i][0..i], 128-bit loads issued four at a time per lane
-// (16 KB in flight per warp-batch) so the row stream is bandwidth- rather than latency-bound.
+// One warp per span row i: inter = sum over columns [0, l*), intra = sum over [l*, i] (two branch-free
+// streaming passes over the row prefix A[i][0..i]).
 __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -74,21 +91,8 @@ __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
         long long acc = 0;
         for (int h = 0; h < heads; ++h) {
             const float* row = A + ((int64_t)h * n + i) * (int64_t)n;
-            const int cnt = i + 1;                                   // causal: columns 0..i
-            const int mis = (int)((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
-            const int head = min(cnt, mis ? 4 - mis : 0);
-            if (lane < head) { const long long v = q40(__ldg(row + lane)); acc += lane < l ? v : -v; }
-            const int nvec = (cnt - head) >> 2;
-            const float4* v4 = reinterpret_cast<const float4*>(row + head);
-            int q = lane;
-            for (; q + 96 < nvec; q += 128) {
-                const float4 f0 = ld_nc4(v4 + q), f1 = ld_nc4(v4 + q + 32), f2 = ld_nc4(v4 + q + 64), f3 = ld_nc4(v4 + q + 96);
-                acc += signed4(f0, head + 4 * q, l) + signed4(f1, head + 4 * (q + 32), l) +
-                       signed4(f2, head + 4 * (q + 64), l) + signed4(f3, head + 4 * (q + 96), l);
-            }
-            for (; q < nvec; q += 32) acc += signed4(ld_nc4(v4 + q), head + 4 * q, l);
-            const int t0 = head + 4 * nvec;
-            if (t0 + lane < cnt) { const int j = t0 + lane; const long long v = q40(__ldg(row + j)); acc += j < l ? v : -v; }
+            acc += warp_qsum(row, l, lane);                  // inter: j < l* (always < i + 1 here)
+            acc -= warp_qsum(row + l, i + 1 - l, lane);      // intra: l* <= j <= i
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -117,11 +121,25 @@ __global__ void __launch_bounds__(kTopkThreads) k_score_topk(const ScoreArgs a) 
         }
         return;
     }
-    for (int i = tid; i < m; i += blockDim.x) key[i] = (unsigned long long)a.scores[s.score_off + i] ^ (1ULL << 63);
+    __shared__ unsigned long long s_or[kTopkThreads / 32], s_and[kTopkThreads / 32];
+    unsigned long long vor = 0, vand = ~0ULL;
+    for (int i = tid; i < m; i += blockDim.x) {
+        const unsigned long long kx = (unsigned long long)a.scores[s.score_off + i] ^ (1ULL << 63);
+        key[i] = kx; vor |= kx; vand &= kx;
+    }
+    for (int o = 16; o; o >>= 1) { vor |= __shfl_xor_sync(0xffffffffu, vor, o); vand &= __shfl_xor_sync(0xffffffffu, vand, o); }
+    if (lane == 0) { s_or[wid] = vor; s_and[wid] = vand; }
     unsigned long long prefix = 0, pmask = 0;
     if (tid == 0) s_rem = (int)kk;
     __syncthreads();
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    vor = 0; vand = ~0ULL;
+    for (int w = 0; w < kTopkThreads / 32; ++w) { vor |= s_or[w]; vand &= s_and[w]; }
+    // bytes on which every key agrees need no radix pass: fold them into the prefix directly
+    const unsigned long long diff = vor ^ vand;                          // bits that differ somewhere
+    const int top = diff ? 63 - __clzll(diff) : -1;
+    const int start = top < 0 ? -8 : (top / 8) * 8;
+    if (start < 56) { pmask = ~0ULL << (start + 8); prefix = vand & pmask; }
+    for (int shift = start; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
         __syncthreads();
         for (int i = tid; i < m; i += blockDim.x)

@@ -49,6 +49,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(workload: str):
+    """DRAM read+write bytes per launch of the gather from the committed ncu capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
+            t = json.load(f)[workload]
+        return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), int(t["algorithmic_bytes"])
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -320,6 +330,9 @@ def bench_ours(args):
     else:
         gather_ms_max, reused_all, gather_all = gather_ms, float(reused_bytes), float(gather_bytes)
     peak, peak_src = peaks()
+    traffic, traffic_alg = ncu_traffic(S.wl.name) if world == 1 else (None, None)
+    if traffic_alg is not None and traffic_alg != gather_bytes:
+        traffic = None                              # the capture was of a different workload
     value = reused_all / (ms_step * 1e-3) / 1e9
     achieved = gather_bytes / (gather_ms * 1e-3) / 1e9          # this rank's gather kernel
     # ---- e2e through the public API with host buffers
@@ -352,7 +365,8 @@ def bench_ours(args):
                                       else "score (N3) serialized before match on the same stream")},
             "roofline": {"kernel": "k_rows (cp_gather_rerotate: prep + rows)", "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "traffic_source": "profiles/r01/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
                          "algorithmic_bytes_per_launch": gather_bytes,
                          "bytes_rule": "reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + recompute tokens x 2 (K,V) x L*H*d*e (zero writes)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,

@@ -244,3 +244,104 @@ def test_70b_layer_shard_config4_full_size_sampled():
     case.insert(wb, rep, sparse_kv=True)
     case.match_and_gather(rb, rep)
     assert rep.ok, rep.notes[:10]
+
+
+def _one(tokens, mask=None, spans=(), wid=0):
+    t = np.asarray(tokens, np.int32)
+    m = np.zeros(len(t), np.uint8) if mask is None else np.asarray(mask, np.uint8)
+    return Batch(tokens=t, offsets=np.array([0, len(t)], np.int64), mask=m, writer_ids=np.array([wid], np.int64),
+                 span_req=np.zeros(len(spans), np.int32), span_begin=np.array([s[0] for s in spans], np.int32),
+                 span_len=np.array([s[1] for s in spans], np.int32))
+
+
+def test_degenerate_masks_and_sizes():
+    """All-sensitive writer (nothing insertable), zero-span insert, a max_span_len span, an all-masked
+    reader (no hit may cover a masked token), a reader shorter than the window, a reader with no hits."""
+    from synth.gen import Workload
+    g = Geometry(2, 2, 64, "bf16", 500000.0)
+    rng = np.random.default_rng(12)
+    long_seg = rng.integers(1000, 90000, 1024).astype(np.int32)               # = max_span_len
+    rounds = [
+        (_one(rng.integers(1000, 90000, 300), mask=np.ones(300), wid=0),         # all sensitive, no spans
+         _one(long_seg, wid=100)),
+        (_one(long_seg, spans=[(0, 1024)], wid=1), _one(long_seg, mask=np.ones(1024), wid=101)),
+        (_one(rng.integers(1000, 90000, 50), wid=2), _one(long_seg[:100], wid=102)),
+        (_one(np.concatenate([long_seg[:10], long_seg]), spans=[(10, 1024)], wid=3),   # duplicate at another origin
+         pack_batches([_one(np.concatenate([rng.integers(1000, 90000, 37), long_seg]), wid=103),
+                       _one(rng.integers(1000, 90000, 700), wid=104)])),
+    ]
+    wl = Workload("degenerate", g, rounds, pool_capacity_tokens=5000, max_span_len=1024)
+    res = run_round_parity(Case(wl), score=False)
+    _assert(res)
+    assert res["hits"] == 1                      # only round 3's first reader reuses the 1024-token entry
+
+
+def test_zero_uncovered_flag_and_match_error():
+    import paper_2605_23640_b200 as cp
+    case = Case(make_workload(1))
+    wb, rb = case.wl.rounds[0]
+    rep = ParityReport()
+    case.insert(wb, rep)
+    db = case._dev_batch(rb)
+    hits = case.dev.match_spans(db, 50)
+    dst = case.dst_kv(rb)
+    case.dev.gather_rerotate(db, hits, dst, zero_recompute=True, zero_uncovered=True)
+    plan = hits.plan.cpu().numpy()[:rb.total_tokens]
+    bt = dst.block_tables.cpu().numpy()
+    q = np.nonzero(plan == 0)[0]
+    assert len(q) > 0
+    blk = torch.from_numpy(bt[0, q // 16].astype(np.int64)).cuda()
+    slot = torch.from_numpy((q % 16).astype(np.int64)).cuda()
+    for l in range(case.g.num_layers):
+        assert float(dst.k[l][blk, slot].abs().max()) == 0.0 and float(dst.v[l][blk, slot].abs().max()) == 0.0
+    assert case.dev.last_error() == 0
+    # a request longer than max_req_tokens raises the sticky device error; later calls no-op
+    case = Case(make_workload(2, scale=0.05), sample_reqs=1, sample_layers=[0])
+    long = np.arange(1000, 1000 + case.cfg.max_req_tokens + 5, dtype=np.int32)
+    bad = cp.DeviceBatch.from_numpy(long, np.array([0, len(long)], np.int64), None)
+    bad.max_req_len = case.cfg.max_req_tokens
+    case.dev.match_spans(bad, 51, use_mask=False)
+    assert case.dev.last_error() == cp._lib.CP_ERR_INVALID_ARG
+    assert case.dev.last_error() == 0            # cleared by the read
+
+
+def test_churn_config5_full_batches_invariants():
+    """Config 5 at its full batch size (256 requests x ~1.6K tokens, 100K-passage corpus) for a few
+    batches on one head shard with a budget that forces LRU eviction; device-only invariants (the
+    oracle cannot replay this size): budget, no device error, every stored entry is unmasked in its
+    writer and its tokens equal the writer's span, no entry strictly contains another."""
+    import paper_2605_23640_b200 as cp
+    from synth.gen import churn_workload
+    g = Geometry(32, 8, 128, "bf16", 500000.0)
+    wl = churn_workload(batches=4, per_batch=256, corpus=100000, capacity_tokens=400_000, geometry=g)
+    case = Case(wl, head_range=(0, 1), sample_reqs=1, sample_layers=[0])
+    for bi, (wb, rb) in enumerate(wl.rounds):
+        db = case._dev_batch(rb)
+        hits = case.dev.match_spans(db, 2 * bi + 1)
+        nb = [(int(n) + 15) // 16 for n in wb.lens]
+        bt = torch.zeros((wb.num_reqs, max(nb)), dtype=torch.int32)
+        o = 0
+        for r, k in enumerate(nb):
+            bt[r, :k] = torch.arange(o, o + k); o += k
+        kv = cp.PagedKV.allocate(32, o, 1, 128, torch.bfloat16, bt, "cuda", zero=True)
+        sp = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda() for a in (wb.span_req, wb.span_begin, wb.span_len)]
+        ids, oc = case.dev.insert(db, kv, *sp, None, None, 2 * bi + 2)
+        assert case.dev.last_error() == 0
+        del kv
+    snap = case.dev.snapshot()
+    assert snap["live_tokens"] <= 400_000 and snap["error"] == 0
+    assert snap["next_id"] > snap["num_live"]           # evictions happened
+    seqs = {}
+    for wb, _ in wl.rounds:
+        for s in range(len(wb.span_len)):
+            r, b0, m = int(wb.span_req[s]), int(wb.span_begin[s]), int(wb.span_len[s])
+            assert not wb.req_mask(r)[b0:b0 + m].any()
+            seqs.setdefault(m, set()).add(wb.req_tokens(r)[b0:b0 + m].tobytes())
+    strs = []
+    for e in snap["entries"]:
+        assert e["tokens"].tobytes() in seqs[e["len"]]   # privacy: stored tokens are an unmasked writer span
+        strs.append("," + ",".join(map(str, e["tokens"].tolist())) + ",")
+    for i in range(0, len(strs), 97):                     # containment-freedom (sampled pairs)
+        for j in range(len(strs)):
+            if i != j:
+                assert strs[i] not in strs[j]

@@ -518,3 +518,73 @@ void orc_rerotate_rows(const float* xin, int64_t nrows, int32_t H, int32_t d, in
     for (int64_t r = 0; r < nrows; ++r)
         orc_rerotate_row(xin + r * (int64_t)H * d, H, d, gptj, theta_base, delta, out_bf16, out + r * (int64_t)H * d);
 }
+
+/* ------------------------------------------------------------------------- */
+/* C1 Steps 1-2: summed-area table + optimal substring per coarse segment     */
+/* (SPEC annotator.select_reusable S:L169-177)                    */
+/* ------------------------------------------------------------------------- */
+/*
+ * A: fp32 [heads][n][n], causal final-layer attention; values are summed over heads in the
+ * 2^-40 fixed point of R#17, so every sum below is an exact integer (ties resolve identically).
+ * Step 1: T[i][j] = a[i][j] + T[i-1][j] + T[i][j-1] - T[i-1][j-1], 1-based, zero border.
+ * rect(x1,x2,y1,y2) = T[x2][y2] - T[x1-1][y2] - T[x2][y1-1] + T[x1-1][y1-1]
+ * Coarse segments: maximal runs of mask-0 positions [a, b] (1-based).
+ * Step 2: for every substring [l, r] of the segment with r - l + 1 >= min_len,
+ *   diff = IntraAttn(l, r) - InterAttn(l, r) = rect(l, r, l, r) - rect(l, r, 1, l - 1)
+ * choose max diff; ties -> longer, then leftmost; store only if diff > 0.
+ * Outputs (0-based, inclusive) per coarse segment s: out_l[s], out_r[s] (-1 if none), out_diff[s];
+ * returns the number of coarse segments (<= max_segments) or -1 if there are more.
+ */
+int32_t orc_annotate(const float* A, int64_t n, int32_t heads, const uint8_t* mask, int32_t min_len,
+                     int32_t max_segments, int32_t* out_l, int32_t* out_r, int64_t* out_diff) {
+    int64_t* T = (int64_t*)calloc((size_t)(n + 1) * (size_t)(n + 1), sizeof(int64_t));
+#define TT(i, j) T[(int64_t)(i) * (n + 1) + (j)]
+    for (int64_t i = 1; i <= n; ++i)
+        for (int64_t j = 1; j <= n; ++j) {
+            int64_t a = 0;
+            for (int32_t h = 0; h < heads; ++h) a += fixq(A[((int64_t)h * n + (i - 1)) * n + (j - 1)]);
+            TT(i, j) = a + TT(i - 1, j) + TT(i, j - 1) - TT(i - 1, j - 1);
+        }
+#define RECT(x1, x2, y1, y2) (TT(x2, y2) - TT((x1) - 1, y2) - TT(x2, (y1) - 1) + TT((x1) - 1, (y1) - 1))
+    int32_t nseg = 0;
+    int64_t i = 1;
+    while (i <= n) {
+        if (mask[i - 1]) { ++i; continue; }
+        int64_t a = i;
+        while (i <= n && !mask[i - 1]) ++i;
+        int64_t b = i - 1;
+        if (nseg >= max_segments) { free(T); return -1; }
+        int32_t bl = -1, br = -1;
+        int64_t bd = 0;
+        for (int64_t l = a; l <= b; ++l)
+            for (int64_t r = l + min_len - 1; r <= b; ++r) {
+                const int64_t intra = RECT(l, r, l, r);
+                const int64_t inter = l > 1 ? RECT(l, r, 1, l - 1) : 0;
+                const int64_t diff = intra - inter;
+                const int64_t len = r - l + 1, blen = br - bl + 1;
+                if (bl < 0 || diff > bd || (diff == bd && (len > blen || (len == blen && l - 1 < bl)))) {
+                    bd = diff; bl = (int32_t)(l - 1); br = (int32_t)(r - 1);
+                }
+            }
+        if (bl >= 0 && bd <= 0) { bl = -1; br = -1; }
+        out_l[nseg] = bl; out_r[nseg] = br; out_diff[nseg] = bl >= 0 ? bd : 0;
+        ++nseg;
+    }
+#undef RECT
+#undef TT
+    free(T);
+    return nseg;
+}
+
+/* Step 1 alone, for pins: the SAT of the fixed-point matrix (n+1)^2 with zero border. */
+void orc_sat(const float* A, int64_t n, int32_t heads, int64_t* T) {
+    for (int64_t j = 0; j <= n; ++j) T[j] = 0;
+    for (int64_t i = 1; i <= n; ++i) {
+        T[i * (n + 1)] = 0;
+        for (int64_t j = 1; j <= n; ++j) {
+            int64_t a = 0;
+            for (int32_t h = 0; h < heads; ++h) a += fixq(A[((int64_t)h * n + (i - 1)) * n + (j - 1)]);
+            T[i * (n + 1) + j] = a + T[(i - 1) * (n + 1) + j] + T[i * (n + 1) + j - 1] - T[(i - 1) * (n + 1) + j - 1];
+        }
+    }
+}

@@ -61,6 +61,8 @@ def lib():
             "orc_rerotate_row": (None, [vp, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_score": (i32, [vp, i64, i32, i32, i32, i32, i32, vp, vp]),
             "orc_rerotate_rows": (None, [vp, i64, i32, i32, i32, C.c_double, i64, i32, vp]),
+            "orc_annotate": (i32, [vp, i64, i32, vp, i32, i32, vp, vp, vp]),
+            "orc_sat": (None, [vp, i64, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -151,6 +153,31 @@ def score(A, l: int, r: int, rho_num: int = 1, rho_den: int = 4):
     if rc != OK:
         raise ValueError(f"orc_score rc={rc}")
     return sc[:m], bits[:(m + 31) // 32]
+
+
+def sat(A) -> np.ndarray:
+    """C1 Step 1 on the 2^-40 fixed-point matrix: int64 [(n+1), (n+1)] with zero border."""
+    A = _c(A, np.float32)
+    if A.ndim == 2:
+        A = A[None]
+    n = A.shape[1]
+    T = np.zeros((n + 1, n + 1), np.int64)
+    lib().orc_sat(_p(A), n, A.shape[0], _p(T))
+    return T
+
+
+def annotate(A, mask, min_len: int = 128, max_segments: int = 4096):
+    """C1 Steps 1-2: list of (l, r, diff) per coarse segment (l = r = -1 if none)."""
+    A = _c(A, np.float32)
+    if A.ndim == 2:
+        A = A[None]
+    n = A.shape[1]
+    m = _c(mask, np.uint8)
+    ol = np.zeros(max_segments, np.int32); orr = np.zeros(max_segments, np.int32); od = np.zeros(max_segments, np.int64)
+    k = lib().orc_annotate(_p(A), n, A.shape[0], _p(m), min_len, max_segments, _p(ol), _p(orr), _p(od))
+    if k < 0:
+        raise ValueError("too many coarse segments")
+    return [(int(ol[i]), int(orr[i]), int(od[i])) for i in range(k)]
 
 
 def bits_to_bool(bits: np.ndarray, m: int) -> np.ndarray:

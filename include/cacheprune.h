@@ -186,6 +186,28 @@ cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, cons
                              int64_t* out_scores, const int64_t* score_offsets_h,
                              uint32_t* out_bits, const int64_t* bits_word_offsets_h, void* stream);
 
+/* ---- NEXT-1: on-device KV Annotator (C1 Steps 1-2) -------------------------- */
+
+/* Workspace bytes cp_annotate_spans needs for these requests (8 n(n+1) + 8(n+1) + 8 max_segments
+ * per request, 256-B aligned). */
+size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, int32_t max_segments);
+
+/*
+ * For every coarse segment (maximal mask-0 run) of every request, select the substring
+ * [l*, r*] with r*-l*+1 >= min_len maximising IntraAttn - InterAttn (Step 2 P:L635-639)
+ * of the causal final-layer attention attn_h[r] (device fp32 [heads][n][n], heads summed, only
+ * j <= i read), computed exactly in the 2^-40 fixed point of R#17 (Step 1's summed-area sums,
+ * P:L600-613).  Ties: longer, then leftmost; reported only if the difference is > 0.
+ * mask_h[r]: device uint8 [n] (1 = sensitive).  Outputs (device): out_nseg[r] = number of coarse
+ * segments (-1 if more than max_segments); for s < out_nseg[r], at [r * max_segments + s]:
+ * out_l / out_r (0-based inclusive, -1 if the segment yields no reusable span) and out_diff.
+ * workspace: device, >= cp_annotate_workspace(...) bytes, caller-owned.
+ */
+cp_status cp_annotate_spans(int32_t num_reqs, const float* const* attn_h, const int32_t* n_h,
+                            const int32_t* heads_h, const uint8_t* const* mask_h, int32_t min_len,
+                            int32_t max_segments, void* workspace, size_t workspace_bytes,
+                            int32_t* out_nseg, int32_t* out_l, int32_t* out_r, int64_t* out_diff, void* stream);
+
 /* ---- test / diagnostic exports ------------------------------------------------------------- */
 
 /* Prefix hashes of every request: out_h (device u64) gets n_r + 1 values per request starting at

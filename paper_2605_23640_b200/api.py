@@ -272,6 +272,47 @@ def score_deviation(attn: Sequence[torch.Tensor], n: Sequence[int], heads: Seque
     return out_scores, out_bits, so, bo
 
 
+def annotate_spans(attn: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], heads: Sequence[int],
+                   min_len: int = 128, max_segments: int = 64, workspace_bytes: int = 4 << 30, stream=None):
+    """NEXT-1 (cp_annotate_spans): per request, per coarse segment, the reusable span (l, r, diff) of
+    C1 Steps 1-2, or (-1, -1, 0).  Requests are processed in chunks that fit `workspace_bytes`."""
+    lib = L.lib()
+    R = len(attn)
+    ns = [int(a.shape[-1]) for a in attn]
+    out = [None] * R
+    dev = attn[0].device if R else torch.device("cuda")
+    i = 0
+    while i < R:
+        j = i + 1
+        while j < R:
+            arr = (C.c_int32 * (j + 1 - i))(*ns[i:j + 1])
+            if lib.cp_annotate_workspace(j + 1 - i, arr, max_segments) > workspace_bytes:
+                break
+            j += 1
+        k = j - i
+        n_arr = (C.c_int32 * k)(*ns[i:j])
+        need = int(lib.cp_annotate_workspace(k, n_arr, max_segments))
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        nseg = torch.zeros(k, dtype=torch.int32, device=dev)
+        ol = torch.full((k * max_segments,), -1, dtype=torch.int32, device=dev)
+        orr = torch.full((k * max_segments,), -1, dtype=torch.int32, device=dev)
+        od = torch.zeros(k * max_segments, dtype=torch.int64, device=dev)
+        A = (C.c_void_p * k)(*[a.data_ptr() for a in attn[i:j]])
+        M = (C.c_void_p * k)(*[m.data_ptr() for m in masks[i:j]])
+        h_arr = (C.c_int32 * k)(*[int(h) for h in heads[i:j]])
+        L.check(lib.cp_annotate_spans(k, A, n_arr, h_arr, M, min_len, max_segments, _ptr(ws), need, _ptr(nseg),
+                                      _ptr(ol), _ptr(orr), _ptr(od), _stream(stream)), "cp_annotate_spans")
+        nseg_h, ol_h, or_h, od_h = nseg.cpu().numpy(), ol.cpu().numpy(), orr.cpu().numpy(), od.cpu().numpy()
+        for q in range(k):
+            c = int(nseg_h[q])
+            if c < 0:
+                raise L.CacheHitError("cp_annotate_spans: more coarse segments than max_segments")
+            b = q * max_segments
+            out[i + q] = [(int(ol_h[b + s]), int(or_h[b + s]), int(od_h[b + s])) for s in range(c)]
+        i = j
+    return out
+
+
 def hash_prefix(batch: DeviceBatch, hash_seed: int, stream=None) -> torch.Tensor:
     out = torch.zeros(batch.total_tokens + batch.num_reqs, dtype=torch.int64, device=batch.tokens.device)
     rb = batch.c(False)

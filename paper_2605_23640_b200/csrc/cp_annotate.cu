@@ -1,0 +1,263 @@
+// cp_annotate.cu -- NEXT-1: the KV Annotator's C1 Steps 1-2 on the device (§4.2.1).
+//
+// The paper builds a summed-area table of the final-layer attention on the CPU after a GPU->CPU copy
+// (383 ms at 10K tokens) and names GPU SAT construction as future work.  Here the
+// attention never leaves HBM.  Every sum is taken in the 2^-40 fixed point of R#17 (exact int64),
+// so the argmax below -- and its tie-breaks -- are bit-identical to the oracle's.
+//
+// For a substring [l, r] (0-based, inclusive) of a coarse segment, with row prefixes
+// R(i, x) = sum_{j < x} a[i][j] (heads summed) and P(x) = sum_{i < x} R(i, i+1):
+//     IntraAttn - InterAttn = sum_{i=l}^{r} (R(i, i+1) - R(i, l)) - sum_{i=l}^{r} R(i, l)
+//                           = P(r+1) - P(l) - 2 * sum_{i=l}^{r} R(i, l)
+// which is exactly the paper's rectangle-sum form for causal attention.
+//
+//   k_ann_rows : warp per (request, row i): R(i, 0..i+1) into the workspace (the SAT's row pass)
+//   k_ann_segs : CTA per request: P by block scan; coarse segments from the mask
+//   k_ann_best : CTA per (request, segment): thread per start l walks rows i = l..b accumulating
+//                sum R(i, l) (coalesced across l), best (diff desc, length desc, l asc) by a block
+//                reduction; a span is reported only if diff > 0 and length >= min_len
+#include "cp_internal.cuh"
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+constexpr int kAnnReqsPerLaunch = 512;
+constexpr int kBestThreads = 512;
+
+struct AnnReq {
+    const float* A;          // [heads][n][n]
+    const uint8_t* mask;     // [n]
+    long long r_off;         // workspace byte offsets
+    long long p_off;
+    long long s_off;
+    int32_t n, heads;
+    int32_t row_begin;       // first global row of this request within the launch
+    int32_t pad;
+};
+
+struct AnnArgs {
+    AnnReq rq[kAnnReqsPerLaunch];
+    int32_t nreq, total_rows, min_len, max_seg;
+    char* ws;
+    int32_t* out_nseg;       // launch bases
+    int32_t* out_l;
+    int32_t* out_r;
+    long long* out_diff;
+};
+
+__device__ __forceinline__ long long q40(float x) { return __float2ll_rz(x * 1099511627776.0f); }
+
+__device__ __forceinline__ int find_req(const AnnArgs& a, int gr) {
+    int lo = 0, hi = a.nreq - 1;
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.rq[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    for (int gr = warp; gr < a.total_rows; gr += nwarps) {
+        const int q = find_req(a, gr);
+        const AnnReq& rq = a.rq[q];
+        const int n = rq.n, i = gr - rq.row_begin;
+        long long* R = reinterpret_cast<long long*>(a.ws + rq.r_off) + (int64_t)i * (n + 1);
+        long long carry = 0;
+        if (lane == 0) R[0] = 0;
+        for (int base = 0; base <= i; base += 32) {
+            const int x = base + lane;
+            long long v = 0;
+            if (x <= i)
+                for (int h = 0; h < rq.heads; ++h) v += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
+            long long inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+            if (x <= i) R[x + 1] = carry + inc;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_ann_segs(const AnnArgs a) {
+    __shared__ long long s_w[33];
+    __shared__ int s_wi[33];
+    __shared__ long long s_carry;
+    __shared__ int s_cnt;
+    const AnnReq& rq = a.rq[blockIdx.x];
+    const int n = rq.n;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    long long* P = reinterpret_cast<long long*>(a.ws + rq.p_off);
+    int2* seg = reinterpret_cast<int2*>(a.ws + rq.s_off);
+    if (tid == 0) { s_carry = 0; s_cnt = 0; P[0] = 0; }
+    __syncthreads();
+    // P(x+1) = P(x) + R(x, x+1)   (prefix of row sums)
+    for (int b0 = 0; b0 < n; b0 += 1024) {
+        const int i = b0 + tid;
+        const long long v = i < n ? R[(int64_t)i * (n + 1) + i + 1] : 0;
+        long long inc = v;
+        for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_w[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            long long x = s_w[lane], xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            s_w[lane] = xi - x;
+            if (lane == 31) s_w[32] = xi;
+        }
+        __syncthreads();
+        if (i < n) P[i + 1] = s_carry + s_w[wid] + inc;
+        __syncthreads();
+        if (tid == 0) s_carry += s_w[32];
+        __syncthreads();
+    }
+    // coarse segments: maximal mask-0 runs, in order
+    for (int b0 = 0; b0 < n; b0 += 1024) {
+        const int i = b0 + tid;
+        const bool start = i < n && !rq.mask[i] && (i == 0 || rq.mask[i - 1]);
+        int inc = start;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_wi[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            int x = s_wi[lane], xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            s_wi[lane] = xi - x;
+            if (lane == 31) s_wi[32] = xi;
+        }
+        __syncthreads();
+        if (start) {
+            const int k = s_cnt + s_wi[wid] + inc - 1;
+            int e = i;
+            while (e + 1 < n && !rq.mask[e + 1]) ++e;
+            if (k < a.max_seg) seg[k] = make_int2(i, e);
+        }
+        __syncthreads();
+        if (tid == 0) s_cnt += s_wi[32];
+        __syncthreads();
+    }
+    if (tid == 0) a.out_nseg[blockIdx.x] = s_cnt <= a.max_seg ? s_cnt : -1;
+}
+
+struct Best { long long d; int len; int l; };
+__device__ __forceinline__ bool better(const Best& x, const Best& y) {      // diff desc, length desc, l asc
+    if (x.len < 0) return false;
+    if (y.len < 0) return true;
+    if (x.d != y.d) return x.d > y.d;
+    if (x.len != y.len) return x.len > y.len;
+    return x.l < y.l;
+}
+
+__global__ void __launch_bounds__(kBestThreads) k_ann_best(const AnnArgs a) {
+    __shared__ long long s_d[kBestThreads / 32];
+    __shared__ int s_len[kBestThreads / 32], s_l[kBestThreads / 32];
+    const int q = blockIdx.x / a.max_seg, s = blockIdx.x % a.max_seg;
+    const AnnReq& rq = a.rq[q];
+    const int nseg = a.out_nseg[q];
+    if (nseg < 0 || s >= nseg) return;
+    const int2 sg = reinterpret_cast<const int2*>(a.ws + rq.s_off)[s];
+    const int n = rq.n, sa = sg.x, sb = sg.y;
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    const long long* P = reinterpret_cast<const long long*>(a.ws + rq.p_off);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int lmax = sb - a.min_len + 1;                                   // last admissible start
+    Best best{0, -1, 0};
+    for (int l0 = sa + (tid & ~31); l0 <= lmax; l0 += kBestThreads) {
+        const int l = l0 + lane;                                           // warp covers starts l0..l0+31
+        const bool act = l <= lmax;
+        const long long Pl = act ? P[l] : 0;
+        long long acc = 0;
+        Best mine{0, -1, 0};
+        for (int i = l0; i <= sb; ++i) {                                   // warp-uniform row loop, coalesced in l
+            if (act && i >= l) {
+                acc += R[(int64_t)i * (n + 1) + l];
+                if (i >= l + a.min_len - 1) {
+                    const Best c{P[i + 1] - Pl - 2 * acc, i - l + 1, l};
+                    if (better(c, mine)) mine = c;
+                }
+            }
+        }
+        if (better(mine, best)) best = mine;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const Best y{__shfl_xor_sync(0xffffffffu, best.d, o), __shfl_xor_sync(0xffffffffu, best.len, o),
+                     __shfl_xor_sync(0xffffffffu, best.l, o)};
+        if (better(y, best)) best = y;
+    }
+    if (lane == 0) { s_d[wid] = best.d; s_len[wid] = best.len; s_l[wid] = best.l; }
+    __syncthreads();
+    if (tid == 0) {
+        Best b{0, -1, 0};
+        for (int w = 0; w < kBestThreads / 32; ++w) { const Best y{s_d[w], s_len[w], s_l[w]}; if (better(y, b)) b = y; }
+        const int o = q * a.max_seg + s;
+        const bool ok = b.len > 0 && b.d > 0;
+        a.out_l[o] = ok ? b.l : -1;
+        a.out_r[o] = ok ? b.l + b.len - 1 : -1;
+        a.out_diff[o] = ok ? b.d : 0;
+    }
+}
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+}  // namespace
+
+extern "C" size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, int32_t max_segments) {
+    if (num_reqs <= 0 || !n_h || max_segments <= 0) return 0;
+    size_t tot = 0;
+    for (int r = 0; r < num_reqs; ++r) {
+        const size_t n = (size_t)std::max(n_h[r], 0);
+        tot += align256(8 * n * (n + 1)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments);
+    }
+    return tot;
+}
+
+extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* attn_h, const int32_t* n_h,
+                                       const int32_t* heads_h, const uint8_t* const* mask_h, int32_t min_len,
+                                       int32_t max_segments, void* workspace, size_t workspace_bytes,
+                                       int32_t* out_nseg, int32_t* out_l, int32_t* out_r, int64_t* out_diff,
+                                       void* stream) {
+    if (num_reqs < 0 || min_len < 1 || max_segments < 1) return CP_ERR_INVALID_ARG;
+    if (num_reqs == 0) return CP_OK;
+    if (!attn_h || !n_h || !heads_h || !mask_h || !workspace || !out_nseg || !out_l || !out_r || !out_diff)
+        return CP_ERR_INVALID_ARG;
+    if (workspace_bytes < cp_annotate_workspace(num_reqs, n_h, max_segments)) return CP_ERR_CAPACITY;
+    for (int r = 0; r < num_reqs; ++r)
+        if (!attn_h[r] || !mask_h[r] || n_h[r] < 1 || heads_h[r] < 1 || n_h[r] > (1 << 20)) return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<AnnArgs> hold(1);
+    size_t off = 0;
+    for (int r0 = 0; r0 < num_reqs; r0 += kAnnReqsPerLaunch) {
+        AnnArgs& a = hold[0];
+        std::memset(&a, 0, sizeof(a));
+        a.nreq = std::min(kAnnReqsPerLaunch, num_reqs - r0);
+        long long rows = 0;
+        for (int q = 0; q < a.nreq; ++q) {
+            const int r = r0 + q;
+            const size_t n = (size_t)n_h[r];
+            AnnReq& d = a.rq[q];
+            d.A = attn_h[r]; d.mask = mask_h[r]; d.n = n_h[r]; d.heads = heads_h[r];
+            d.r_off = (long long)off; off += align256(8 * n * (n + 1));
+            d.p_off = (long long)off; off += align256(8 * (n + 1));
+            d.s_off = (long long)off; off += align256(8 * (size_t)max_segments);
+            d.row_begin = (int32_t)rows;
+            rows += n_h[r];
+        }
+        if (rows > INT32_MAX) return CP_ERR_INVALID_ARG;
+        a.total_rows = (int32_t)rows; a.min_len = min_len; a.max_seg = max_segments;
+        a.ws = (char*)workspace;
+        a.out_nseg = out_nseg + r0;
+        a.out_l = out_l + (int64_t)r0 * max_segments;
+        a.out_r = out_r + (int64_t)r0 * max_segments;
+        a.out_diff = (long long*)out_diff + (int64_t)r0 * max_segments;
+        k_ann_rows<<<(int)std::min<long long>((rows + 7) / 8, 148 * 16), 256, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_ann_segs<<<a.nreq, 1024, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_ann_best<<<a.nreq * max_segments, kBestThreads, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    }
+    return CP_OK;
+}

@@ -15,7 +15,7 @@ def declared_functions():
         if fn.endswith(".h"):
             src = open(os.path.join(ROOT, "include", fn)).read()
             src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-            for m in re.finditer(r"\b(?:cp_status|int64_t|int32_t|uint64_t|const char\*)\s+(cp_\w+)\s*\(", src):
+            for m in re.finditer(r"\b(?:cp_status|int64_t|int32_t|uint64_t|size_t|const char\*)\s+(cp_\w+)\s*\(", src):
                 names.add(m.group(1))
     return names
 
@@ -26,7 +26,8 @@ def test_library_exports_every_declared_symbol():
     from paper_2605_23640_b200 import _lib as L
     lib = L.lib()
     names = declared_functions()
-    assert {"cp_index_insert", "cp_match_spans", "cp_gather_rerotate", "cp_score_deviation"} <= names
+    assert {"cp_index_insert", "cp_match_spans", "cp_gather_rerotate", "cp_score_deviation",
+            "cp_annotate_spans", "cp_annotate_workspace"} <= names
     for n in sorted(names):
         assert hasattr(lib, n), n
         assert n in L.EXPORTS, f"binding does not declare {n}"

@@ -13,33 +13,38 @@
 //
 //   k_ann_rows : warp per (request, row i): R(i, 0..i+1) into the workspace (the SAT's row pass)
 //   k_ann_segs : CTA per request: P by block scan; coarse segments from the mask
-//   k_ann_best : CTA per (request, segment): thread per start l walks rows i = l..b accumulating
-//                sum R(i, l) (coalesced across l), best (diff desc, length desc, l asc) by a block
-//                reduction; a span is reported only if diff > 0 and length >= min_len
+//   k_ann_best : CTA per (request, segment, chunk of 256 starts): thread per start l walks rows
+//                i = l..b (8 independent loads per step) accumulating sum R(i, l) (coalesced across l),
+//                chunk best (diff desc, length desc, l asc) by a block reduction
+//   k_ann_final: per segment, best over its chunks; reported only if diff > 0
 #include "cp_internal.cuh"
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <vector>
 
 namespace {
 
 constexpr int kAnnReqsPerLaunch = 512;
-constexpr int kBestThreads = 512;
+constexpr int kBestThreads = 256;           // one start l per thread; a CTA covers 256 starts
+constexpr int kRowUnroll = 8;
 
 struct AnnReq {
     const float* A;          // [heads][n][n]
     const uint8_t* mask;     // [n]
     long long r_off;         // workspace byte offsets
     long long p_off;
-    long long s_off;
+    long long s_off;         // segments, then the per-(segment, chunk) partial bests
     int32_t n, heads;
     int32_t row_begin;       // first global row of this request within the launch
     int32_t pad;
 };
 
+struct PartialBest { long long d; int32_t len; int32_t l; };
+
 struct AnnArgs {
     AnnReq rq[kAnnReqsPerLaunch];
-    int32_t nreq, total_rows, min_len, max_seg;
+    int32_t nreq, total_rows, min_len, max_seg, nchunk;
     char* ws;
     int32_t* out_nseg;       // launch bases
     int32_t* out_l;
@@ -150,36 +155,57 @@ __device__ __forceinline__ bool better(const Best& x, const Best& y) {      // d
     return x.l < y.l;
 }
 
+// CTA per (request, segment, chunk of 256 starts l): thread per l walks rows i = l..b (unrolled, the row
+// loads of one step issued together) accumulating sum R(i, l); P(i+1) comes from shared memory.
 __global__ void __launch_bounds__(kBestThreads) k_ann_best(const AnnArgs a) {
     __shared__ long long s_d[kBestThreads / 32];
     __shared__ int s_len[kBestThreads / 32], s_l[kBestThreads / 32];
-    const int q = blockIdx.x / a.max_seg, s = blockIdx.x % a.max_seg;
+    extern __shared__ long long sP[];                                       // P(sa .. sb+1)
+    const int per_req = a.max_seg * a.nchunk;
+    const int q = blockIdx.x / per_req, rem = blockIdx.x % per_req;
+    const int s = rem / a.nchunk, ch = rem % a.nchunk;
     const AnnReq& rq = a.rq[q];
     const int nseg = a.out_nseg[q];
     if (nseg < 0 || s >= nseg) return;
     const int2 sg = reinterpret_cast<const int2*>(a.ws + rq.s_off)[s];
+    PartialBest* part = reinterpret_cast<PartialBest*>(a.ws + rq.s_off + 8 * (size_t)a.max_seg);
     const int n = rq.n, sa = sg.x, sb = sg.y;
+    const int lmax = sb - a.min_len + 1;                                   // last admissible start
+    const int l_lo = sa + ch * kBestThreads;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (l_lo > lmax) return;                                                // no admissible start in this chunk
     const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
     const long long* P = reinterpret_cast<const long long*>(a.ws + rq.p_off);
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int lmax = sb - a.min_len + 1;                                   // last admissible start
+    for (int x = l_lo + tid; x <= sb + 1; x += kBestThreads) sP[x - l_lo] = P[x];
+    __syncthreads();
+    const int l = l_lo + tid;
+    const bool act = l <= lmax;
     Best best{0, -1, 0};
-    for (int l0 = sa + (tid & ~31); l0 <= lmax; l0 += kBestThreads) {
-        const int l = l0 + lane;                                           // warp covers starts l0..l0+31
-        const bool act = l <= lmax;
-        const long long Pl = act ? P[l] : 0;
+    if (act) {
+        const long long Pl = sP[l - l_lo];
         long long acc = 0;
-        Best mine{0, -1, 0};
-        for (int i = l0; i <= sb; ++i) {                                   // warp-uniform row loop, coalesced in l
-            if (act && i >= l) {
-                acc += R[(int64_t)i * (n + 1) + l];
-                if (i >= l + a.min_len - 1) {
-                    const Best c{P[i + 1] - Pl - 2 * acc, i - l + 1, l};
-                    if (better(c, mine)) mine = c;
+        const int rmin = l + a.min_len - 1;
+        int i = l;
+        for (; i + kRowUnroll - 1 <= sb; i += kRowUnroll) {
+            long long v[kRowUnroll];
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) {
+                acc += v[u];
+                if (i + u >= rmin) {
+                    const Best c{sP[i + u + 1 - l_lo] - Pl - 2 * acc, i + u - l + 1, l};
+                    if (better(c, best)) best = c;
                 }
             }
         }
-        if (better(mine, best)) best = mine;
+        for (; i <= sb; ++i) {
+            acc += __ldg(R + (int64_t)i * (n + 1) + l);
+            if (i >= rmin) {
+                const Best c{sP[i + 1 - l_lo] - Pl - 2 * acc, i - l + 1, l};
+                if (better(c, best)) best = c;
+            }
+        }
     }
     for (int o = 16; o; o >>= 1) {
         const Best y{__shfl_xor_sync(0xffffffffu, best.d, o), __shfl_xor_sync(0xffffffffu, best.len, o),
@@ -191,12 +217,32 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best(const AnnArgs a) {
     if (tid == 0) {
         Best b{0, -1, 0};
         for (int w = 0; w < kBestThreads / 32; ++w) { const Best y{s_d[w], s_len[w], s_l[w]}; if (better(y, b)) b = y; }
-        const int o = q * a.max_seg + s;
-        const bool ok = b.len > 0 && b.d > 0;
-        a.out_l[o] = ok ? b.l : -1;
-        a.out_r[o] = ok ? b.l + b.len - 1 : -1;
-        a.out_diff[o] = ok ? b.d : 0;
+        PartialBest pb; pb.d = b.d; pb.len = b.len; pb.l = b.l;
+        part[s * a.nchunk + ch] = pb;
     }
+}
+
+// thread per (request, segment): best over the chunks' partial bests
+__global__ void k_ann_final(const AnnArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.nreq * a.max_seg) return;
+    const int q = t / a.max_seg, s = t % a.max_seg;
+    const int nseg = a.out_nseg[q];
+    if (nseg < 0 || s >= nseg) return;
+    const AnnReq& rq = a.rq[q];
+    const int2 sg = reinterpret_cast<const int2*>(a.ws + rq.s_off)[s];
+    const PartialBest* part = reinterpret_cast<const PartialBest*>(a.ws + rq.s_off + 8 * (size_t)a.max_seg);
+    const int lmax = sg.y - a.min_len + 1;
+    Best b{0, -1, 0};
+    for (int ch = 0; ch < a.nchunk && sg.x + ch * kBestThreads <= lmax; ++ch) {
+        const PartialBest pb = part[s * a.nchunk + ch];
+        const Best y{pb.d, pb.len, pb.l};
+        if (better(y, b)) b = y;
+    }
+    const bool ok = b.len > 0 && b.d > 0;
+    a.out_l[t] = ok ? b.l : -1;
+    a.out_r[t] = ok ? b.l + b.len - 1 : -1;
+    a.out_diff[t] = ok ? b.d : 0;
 }
 
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -208,7 +254,8 @@ extern "C" size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, in
     size_t tot = 0;
     for (int r = 0; r < num_reqs; ++r) {
         const size_t n = (size_t)std::max(n_h[r], 0);
-        tot += align256(8 * n * (n + 1)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments);
+        const size_t nch = (n + kBestThreads - 1) / kBestThreads;
+        tot += align256(8 * n * (n + 1)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * nch);
     }
     return tot;
 }
@@ -233,6 +280,7 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
         std::memset(&a, 0, sizeof(a));
         a.nreq = std::min(kAnnReqsPerLaunch, num_reqs - r0);
         long long rows = 0;
+        int64_t nmax = 1;
         for (int q = 0; q < a.nreq; ++q) {
             const int r = r0 + q;
             const size_t n = (size_t)n_h[r];
@@ -240,12 +288,15 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
             d.A = attn_h[r]; d.mask = mask_h[r]; d.n = n_h[r]; d.heads = heads_h[r];
             d.r_off = (long long)off; off += align256(8 * n * (n + 1));
             d.p_off = (long long)off; off += align256(8 * (n + 1));
-            d.s_off = (long long)off; off += align256(8 * (size_t)max_segments);
+            d.s_off = (long long)off;
+            off += align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * ((n + kBestThreads - 1) / kBestThreads));
+            nmax = std::max<int64_t>(nmax, (int64_t)n);
             d.row_begin = (int32_t)rows;
             rows += n_h[r];
         }
         if (rows > INT32_MAX) return CP_ERR_INVALID_ARG;
         a.total_rows = (int32_t)rows; a.min_len = min_len; a.max_seg = max_segments;
+        a.nchunk = (int32_t)((nmax + kBestThreads - 1) / kBestThreads);
         a.ws = (char*)workspace;
         a.out_nseg = out_nseg + r0;
         a.out_l = out_l + (int64_t)r0 * max_segments;
@@ -255,7 +306,15 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
         CP_COUNT_LAUNCH();
         k_ann_segs<<<a.nreq, 1024, 0, st>>>(a);
         CP_COUNT_LAUNCH();
-        k_ann_best<<<a.nreq * max_segments, kBestThreads, 0, st>>>(a);
+        const size_t psmem = 8 * ((size_t)nmax + 2);
+        if (psmem > 200 * 1024) return CP_ERR_UNSUPPORTED;
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(k_ann_best, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); attr = true; }
+        const long long nblk = (long long)a.nreq * max_segments * a.nchunk;
+        if (nblk > INT32_MAX) return CP_ERR_INVALID_ARG;
+        k_ann_best<<<(int)nblk, kBestThreads, psmem, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_ann_final<<<(a.nreq * max_segments + 255) / 256, 256, 0, st>>>(a);
         CP_COUNT_LAUNCH();
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }

@@ -38,14 +38,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4])
     ap.add_argument("--by", default="layer", choices=["layer", "head"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
-    ap.add_argument("--overlap", type=int, default=1, help="1: run N3 on a side stream concurrently with N1+N2")
+    ap.add_argument("--overlap", type=int, default=0, help="1: run N3 on a side stream concurrently with N1+N2")
+    ap.add_argument("--shard-world", type=int, default=0,
+                    help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
+    ap.add_argument("--shard-rank", type=int, default=0)
     return ap.parse_args()
 
 
@@ -125,8 +128,13 @@ def setup_ours(args, rank, world, device):
     S = Setup()
     wl = make_workload(args.config, scale=args.scale)
     g = wl.geometry
-    sh = make_shard(rank, world, g.num_layers, g.num_kv_heads, args.by)
-    S.shard, S.owner = sh, score_owner(world, g.num_layers, args.by)
+    sim_world = getattr(args, "shard_world", 0)
+    if sim_world and world == 1:                      # one simulated rank of an N-GPU layout
+        sh = make_shard(args.shard_rank, sim_world, g.num_layers, g.num_kv_heads, args.by)
+        S.shard, S.owner = sh, (0 if score_owner(sim_world, g.num_layers, args.by) == args.shard_rank else -1)
+    else:
+        sh = make_shard(rank, world, g.num_layers, g.num_kv_heads, args.by)
+        S.shard, S.owner = sh, score_owner(world, g.num_layers, args.by)
     wb, rb = wl.rounds[0]
     S.wl, S.wb, S.rb, S.g = wl, wb, rb, g
     w = g.window_len
@@ -164,7 +172,7 @@ def setup_ours(args, rank, world, device):
         db = cp.DeviceBatch.from_numpy(sub.tokens, sub.offsets, sub.mask, device)
         spans = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device)
                  for a in (sub.span_req, sub.span_begin, sub.span_len)]
-        bits, boff = score_spans(sub, device, torch, cp, attention_torch)
+        bits, boff = score_spans(sub, device, torch, cp, attention_torch)   # N3 output as the insert's input
         S.t += 1
         torch.cuda.synchronize()
         e0 = time.perf_counter()
@@ -351,7 +359,9 @@ def bench_ours(args):
             "config": {"workload": S.wl.name + f" (BASELINE configs[{args.config - 1}])",
                        "kv_shape": f"{S.g.num_layers} layers x {S.g.num_kv_heads} KV heads x {d}, {S.g.dtype}",
                        "requests": S.rb.num_reqs, "request_tokens": S.rb.total_tokens,
-                       "index_entries": len(S.wb.span_len), "parallelism": f"{args.by}-sharded x{world}",
+                       "index_entries": len(S.wb.span_len),
+                       "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
+                                       if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "shard_layers": L, "shard_heads": H, "rho": "1/4", "window_len": S.g.window_len,
                        "l2": "inputs larger than L2 (pool + destination caches ~100 GB), no flush needed"},
             "matched_tokens_per_s": round(cov / (ms_step * 1e-3), 1),

@@ -197,17 +197,43 @@ def setup_ours(args, rank, world, device):
     for tsr in S.dst.k + S.dst.v:
         tsr.normal_(0.0, 1.0, generator=gen)
     S.hits = cp.Hits(rb.total_tokens // w + rb.num_reqs + 1, rb.num_reqs, rb.total_tokens, device)
-    S.spans = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device)
-               for a in (rb.span_req, rb.span_begin, rb.span_len)]
     S.is_owner = rank == S.owner
+    if args.config == 2:
+        # MSMARCO pairs: the readers' own segments go back into the pool (Duplicates of the writers')
+        ib = rb
+        S.ins_db, S.ins_kv = S.rdb, S.dst
+    else:
+        # strict-masking corpora: a reader's coarse segment is its whole system+passages run, so the
+        # insert half of the step re-inserts a batch of passage writers (their spans, scored by N3 on
+        # their own final-layer attention); in steady state these are Duplicates and the index -- and
+        # with it the heavy re-rotation of the readers' hits -- stays as configured.
+        ib = wb.subset(range(0, min(64, wb.num_reqs)))
+        S.ins_db = cp.DeviceBatch.from_numpy(ib.tokens, ib.offsets, ib.mask, device)
+        nbi = [(int(n) + 15) // 16 for n in ib.lens]
+        bti = torch.zeros((ib.num_reqs, max(nbi)), dtype=torch.int32)
+        o = 1                                                         # block 0: shared dummy for masked blocks
+        for r in range(ib.num_reqs):
+            for s_ in range(len(ib.span_req)):
+                if int(ib.span_req[s_]) != r:
+                    continue
+                a0, a1 = int(ib.span_begin[s_]) // 16, (int(ib.span_begin[s_]) + int(ib.span_len[s_]) + 15) // 16
+                for blk in range(a0, a1):
+                    if bti[r, blk] == 0:
+                        bti[r, blk] = o; o += 1
+        S.ins_kv = cp.PagedKV.allocate(L, o, H, d, tdt, bti, device, zero=False)
+        for tsr in S.ins_kv.k + S.ins_kv.v:
+            tsr.normal_(0.0, 1.0, generator=gen)
+    S.ib = ib
+    S.spans = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device)
+               for a in (ib.span_req, ib.span_begin, ib.span_len)]
     S.attn = {}
     if S.is_owner:
-        for r in sorted(set(int(x) for x in rb.span_req)):
-            S.attn[r] = attention_torch(int(rb.lens[r]), rb.segments[r], 0.01, seed=r, device=device)
-    ms = [int(m) for m in rb.span_len]
-    S.score_args = ([S.attn.get(int(r)) for r in rb.span_req], [int(rb.lens[int(r)]) for r in rb.span_req],
-                    [1] * len(ms), [int(b) for b in rb.span_begin],
-                    [int(b) + int(m) - 1 for b, m in zip(rb.span_begin, rb.span_len)])
+        for r in sorted(set(int(x) for x in ib.span_req)):
+            S.attn[r] = attention_torch(int(ib.lens[r]), ib.segments[r], 0.01, seed=r, device=device)
+    ms = [int(m) for m in ib.span_len]
+    S.score_args = ([S.attn.get(int(r)) for r in ib.span_req], [int(ib.lens[int(r)]) for r in ib.span_req],
+                    [1] * len(ms), [int(b) for b in ib.span_begin],
+                    [int(b) + int(m) - 1 for b, m in zip(ib.span_begin, ib.span_len)])
     so, bo = [0], [0]
     for m in ms:
         so.append(so[-1] + m); bo.append(bo[-1] + (m + 31) // 32)
@@ -257,7 +283,7 @@ def run_step(S, torch, cp, world, events=None):
     if ev: ev[2].record()
     main.wait_event(S.ev_score_done)
     if ev: ev[3].record()
-    S.idx.insert(S.rdb, S.dst, *S.spans, S.bits, S.bits_off, S.t)                  # N4
+    S.idx.insert(S.ins_db, S.ins_kv, *S.spans, S.bits, S.bits_off, S.t)            # N4
     if ev: ev[4].record()
     S.ev_insert_done.record()
 
@@ -359,7 +385,7 @@ def bench_ours(args):
             "config": {"workload": S.wl.name + f" (BASELINE configs[{args.config - 1}])",
                        "kv_shape": f"{S.g.num_layers} layers x {S.g.num_kv_heads} KV heads x {d}, {S.g.dtype}",
                        "requests": S.rb.num_reqs, "request_tokens": S.rb.total_tokens,
-                       "index_entries": len(S.wb.span_len),
+                       "index_entries": len(S.wb.span_len), "insert_batch_spans": len(S.ib.span_len),
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "shard_layers": L, "shard_heads": H, "rho": "1/4", "window_len": S.g.window_len,

@@ -422,15 +422,16 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
     """Same step through the public API with the per-step inputs in pinned HOST memory: H2D of the
     reader batch (tokens, offsets, mask, spans) each step, D2H of the result (hits, plan, stats,
     insert outcomes).  KV pool / paged caches / attention are device-resident state."""
-    rb = S.rb
-    host = {"tokens": torch.from_numpy(rb.tokens.copy()).pin_memory(),
-            "offsets": torch.from_numpy(rb.offsets.copy()).pin_memory(),
-            "mask": torch.from_numpy(rb.mask.copy()).pin_memory(),
-            "sr": torch.from_numpy(np.ascontiguousarray(rb.span_req, np.int32)).pin_memory(),
-            "sb": torch.from_numpy(np.ascontiguousarray(rb.span_begin, np.int32)).pin_memory(),
-            "sl": torch.from_numpy(np.ascontiguousarray(rb.span_len, np.int32)).pin_memory()}
+    rb, ib = S.rb, S.ib
+    pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+    host = {"tokens": pin(rb.tokens, np.int32), "offsets": pin(rb.offsets, np.int64), "mask": pin(rb.mask, np.uint8),
+            "sr": pin(ib.span_req, np.int32), "sb": pin(ib.span_begin, np.int32), "sl": pin(ib.span_len, np.int32)}
     dev = {"tokens": S.rdb.tokens, "offsets": S.rdb.offsets, "mask": S.rdb.mask,
            "sr": S.spans[0], "sb": S.spans[1], "sl": S.spans[2]}
+    if S.ins_db is not S.rdb:                     # configs 3/4: the insert batch is a separate writer batch
+        host.update({"itokens": pin(ib.tokens, np.int32), "ioffsets": pin(ib.offsets, np.int64),
+                     "imask": pin(ib.mask, np.uint8)})
+        dev.update({"itokens": S.ins_db.tokens, "ioffsets": S.ins_db.offsets, "imask": S.ins_db.mask})
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     outs = [S.hits.num_hits, S.hits.req_hit_offsets, S.hits.hit_req, S.hits.hit_entry, S.hits.hit_dst,
             S.hits.hit_len, S.hits.hit_delta, S.hits.plan, S.hits.req_covered, S.hits.req_recompute,

@@ -160,6 +160,7 @@ struct InsArgs {
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed;
     int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
     int32_t* eq_old; HEntry* dtab; int32_t* span_rep; Rec16* precs;
+    int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
 };
 
 // error codes are ordered per span: range -> too short -> capacity -> sensitive (same order as the oracle)
@@ -432,13 +433,15 @@ enum { REL_EQ = 0, REL_CONTAINER = 1, REL_CONTAINED = 2 };
 constexpr int kMaxSupersede = 1024;
 
 struct CommitSmem {                  // byte offsets of the dynamic shared-memory carve-up
-    size_t snew, srep, soff, srec, total;
-    __host__ __device__ CommitSmem(int nslots, int S) {
+    size_t snew, srep, soff, srec, ckey, cslot, total;
+    __host__ __device__ CommitSmem(int nslots, int S, int K = 0) {
         snew = ((size_t)nslots + 15) & ~(size_t)15;
         srep = snew + 4 * (size_t)S;
         soff = srep + 4 * (size_t)S;
         srec = (soff + 4 * ((size_t)S + 1) + 15) & ~(size_t)15;
-        total = srec + 8 * (size_t)kCommitRecCap;
+        ckey = srec + 8 * (size_t)kCommitRecCap;            // LRU candidates: (last_used - min) << 32 | id
+        cslot = ckey + 8 * (size_t)K;
+        total = cslot + 4 * (size_t)K;
     }
 };
 
@@ -472,8 +475,10 @@ __device__ int block_excl_scan(int32_t* v, int n, int32_t* wsum) {
 __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     extern __shared__ __align__(16) unsigned char smc[];
     const int tid = threadIdx.x;
-    const CommitSmem lay(a.nslots, a.S);
+    const CommitSmem lay(a.nslots, a.S, a.candK);
     uint8_t* sflag = smc;
+    unsigned long long* ckey = (unsigned long long*)(smc + lay.ckey);
+    int32_t* cslot = (int32_t*)(smc + lay.cslot);
     int32_t* snew = (int32_t*)(smc + lay.snew);
     int32_t* srep = (int32_t*)(smc + lay.srep);
     int32_t* soff = (int32_t*)(smc + lay.soff);
@@ -607,6 +612,87 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
     }
     __syncthreads();
+    // ---- LRU candidates (R#21): the K smallest live (last_used, id) keys, sorted, in shared
+    //      memory.  Within this call keys only grow (a Duplicate refresh sets last_used = t >= all old
+    //      values when time is monotone) and new entries sort after every old one, so evictions pop
+    //      this list, skipping entries removed or refreshed since; the block-wide arg-min remains the
+    //      fallback (list exhausted, non-monotone time, K = 0).
+    __shared__ unsigned long long s_minl, s_maxl;
+    __shared__ int s_cn, s_cp, s_heap, s_hist[256], s_digit, s_rem2, s_victim;
+    if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_cn = 0; s_cp = 0; s_heap = 0; }
+    __syncthreads();
+    if (a.candK > 0) {
+        unsigned long long mn = ~0ULL, mx = 0;
+        for (int sl = tid; sl < a.nslots; sl += blockDim.x)
+            if (sflag[sl] & 1) { const unsigned long long lu = a.slot_last[sl]; mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx; }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, mn, o), b2 = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a2 < mn ? a2 : mn; mx = b2 > mx ? b2 : mx;
+        }
+        if ((tid & 31) == 0) { atomicMin(&s_minl, mn); atomicMax(&s_maxl, mx); }
+        __syncthreads();
+        const bool ok = s_maxl >= s_minl && (s_maxl - s_minl) < (1ULL << 32) && a.t >= s_maxl;
+        if (ok) {
+            const unsigned long long minl = s_minl;
+            auto keyof = [&](int sl) -> unsigned long long {
+                return ((a.slot_last[sl] - minl) << 32) | (unsigned long long)(uint32_t)a.slot_id[sl];
+            };
+            // radix-select the K-th smallest key (8-bit digits, MSB first)
+            unsigned long long prefix = 0, pmask = 0;
+            if (tid == 0) s_rem2 = a.candK;
+            __syncthreads();
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0;
+                __syncthreads();
+                for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
+                    if (!(sflag[sl] & 1)) continue;
+                    const unsigned long long k = keyof(sl);
+                    if ((k & pmask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    int cum = 0, rem = s_rem2, dg = 255;
+                    for (int b = 0; b < 256; ++b) {
+                        if (cum + s_hist[b] >= rem) { dg = b; rem -= cum; break; }
+                        cum += s_hist[b];
+                    }
+                    s_digit = dg; s_rem2 = rem;
+                }
+                __syncthreads();
+                prefix |= (unsigned long long)s_digit << shift;
+                pmask |= 0xFFULL << shift;
+                __syncthreads();
+            }
+            const unsigned long long T = prefix;                   // K-th smallest (or the max if fewer live)
+            for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
+                if (!(sflag[sl] & 1)) continue;
+                const unsigned long long k = keyof(sl);
+                if (k <= T) { const int p = atomicAdd(&s_cn, 1); if (p < a.candK) { ckey[p] = k; cslot[p] = sl; } }
+            }
+            __syncthreads();
+            const int cn = min(s_cn, a.candK);
+            for (int p = cn + tid; p < a.candK; p += blockDim.x) { ckey[p] = ~0ULL; cslot[p] = -1; }
+            __syncthreads();
+            // bitonic sort of the K candidates by key (keys are unique)
+            for (int kk = 2; kk <= a.candK; kk <<= 1)
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                    for (int i2 = tid; i2 < a.candK; i2 += blockDim.x) {
+                        const int ix = i2 ^ jj;
+                        if (ix > i2) {
+                            const bool up = (i2 & kk) == 0;
+                            const unsigned long long x = ckey[i2], y = ckey[ix];
+                            if ((x > y) == up) {
+                                ckey[i2] = y; ckey[ix] = x;
+                                const int t2 = cslot[i2]; cslot[i2] = cslot[ix]; cslot[ix] = t2;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            if (tid == 0) { s_cn = cn; s_heap = 1; }
+        }
+        __syncthreads();
+    }
     int j0 = jstar;
     while (true) {
         // ---- thread 0 runs ahead through spans that need no block-wide work
@@ -681,6 +767,28 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         __syncthreads();
         // ---- LRU eviction: victim = min (last_used, id) among live entries (R#21)
         while (s_need) {
+            if (tid == 0) {
+                s_victim = -1;
+                if (s_heap) {
+                    while (s_cp < s_cn) {
+                        const int sl = cslot[s_cp];
+                        const unsigned long long k = ckey[s_cp];
+                        ++s_cp;
+                        // still live and not refreshed by a Duplicate in this call
+                        if ((sflag[sl] & 1) && a.slot_last[sl] == (k >> 32) + s_minl && !(sflag[sl] & 2)) { s_victim = sl; break; }
+                    }
+                }
+                if (s_victim >= 0) {
+                    s_rm[0] = s_victim; s_rm_base[0] = 0; s_rm_base[1] = (a.slot_len[s_victim] + CP_BLOCK - 1) / CP_BLOCK;
+                }
+            }
+            __syncthreads();
+            if (s_victim >= 0) {
+                remove_slots(1);
+                if (tid == 0) s_need = s_live_tokens > a.capacity;
+                __syncthreads();
+                continue;
+            }
             unsigned long long best_last = ~0ULL; int best_id = 0x7fffffff, best_slot = -1;
             for (int s = tid; s < a.nslots; s += blockDim.x) {
                 if (!(sflag[s] & 1)) continue;
@@ -1165,7 +1273,11 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
-    const size_t csm = CommitSmem(x->S, num_spans).total;
+    int candK = 4096;
+    while (candK >= 256 && CommitSmem(x->S, num_spans, candK).total > 200 * 1024) candK >>= 1;
+    if (candK < 256) candK = 0;
+    a.candK = candK;
+    const size_t csm = CommitSmem(x->S, num_spans, candK).total;
     if (csm > 200 * 1024) return CP_ERR_UNSUPPORTED;
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();

@@ -431,6 +431,8 @@ __global__ void k_ins_verify(InsArgs a, int from_phase1) {
 
 enum { REL_EQ = 0, REL_CONTAINER = 1, REL_CONTAINED = 2 };
 constexpr int kMaxSupersede = 1024;
+constexpr int kStackCache = 2048;          // free-slot stack entries cached in shared memory
+constexpr int kFifoCache = 4096;           // free-page FIFO head entries cached in shared memory
 
 struct CommitSmem {                  // byte offsets of the dynamic shared-memory carve-up
     size_t snew, srep, soff, srec, ckey, cslot, total;
@@ -483,11 +485,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     int32_t* srep = (int32_t*)(smc + lay.srep);
     int32_t* soff = (int32_t*)(smc + lay.soff);
     int2* srec = (int2*)(smc + lay.srec);
-    __shared__ int s_abort, s_nrec, s_j, s_store_slot, s_npg, s_pop_head, s_nrm, s_need;
+    __shared__ int s_abort, s_nrec;
     __shared__ long long s_live_tokens;
     __shared__ int s_fifo_head, s_fifo_count, s_next_id, s_free_top, s_num_live, s_nremoved;
     __shared__ int s_rm[kMaxSupersede];
-    __shared__ int s_rm_base[kMaxSupersede + 1];
     __shared__ unsigned long long s_red_key[kCommitThreads / 32];
     __shared__ int s_red_slot[kCommitThreads / 32];
     __shared__ int32_t s_wsum[kCommitThreads / 32 + 1];
@@ -558,29 +559,6 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     auto resolve = [&](int code) -> int { return code >= 0 ? code : snew[-1 - code]; };
     auto is_live = [&](int code) -> bool { const int s = resolve(code); return s >= 0 && (sflag[s] & 1); };
 
-    // remove s_rm[0..n): pages go to the FIFO tail in order (all threads)
-    auto remove_slots = [&](int n) {
-        __syncthreads();
-        const int total = s_rm_base[n];
-        for (int q = tid; q < total; q += blockDim.x) {
-            int lo = 0, hi = n - 1;                 // find r with s_rm_base[r] <= q < s_rm_base[r+1]
-            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rm_base[mid] <= q) lo = mid; else hi = mid - 1; }
-            const int slot = s_rm[lo];
-            a.fifo[(s_fifo_head + s_fifo_count + q) % a.P] = a.slot_pages[(int64_t)slot * a.MP + (q - s_rm_base[lo])];
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int r = 0; r < n; ++r) {
-                const int slot = s_rm[r];
-                a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
-                sflag[slot] = 0;
-                s_live_tokens -= a.slot_len[slot];
-                s_num_live -= 1;
-            }
-            s_fifo_count += total;
-        }
-        __syncthreads();
-    };
 
     // ---- parallel prefix: until the first span that must be stored, nothing is stored or removed,
     //      so every span before it is decided against the initial state (duplicates only refresh
@@ -618,7 +596,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     //      this list, skipping entries removed or refreshed since; the block-wide arg-min remains the
     //      fallback (list exhausted, non-monotone time, K = 0).
     __shared__ unsigned long long s_minl, s_maxl;
-    __shared__ int s_cn, s_cp, s_heap, s_hist[256], s_digit, s_rem2, s_victim;
+    __shared__ int s_cn, s_cp, s_heap, s_hist[256], s_digit, s_rem2;
     if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_cn = 0; s_cp = 0; s_heap = 0; }
     __syncthreads();
     if (a.candK > 0) {
@@ -693,39 +671,85 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         }
         __syncthreads();
     }
+    // ---- sequential part.  Thread 0 applies spans in order -- duplicates, drops, supersedes, stores
+    //      and candidate-list evictions -- without block barriers (free-slot stack top and the free-page
+    //      FIFO head are cached in shared memory).  Only an arg-min eviction (candidate list exhausted)
+    //      brings the whole block in.
+    __shared__ int s_stack_cache[kStackCache];
+    __shared__ int s_fifo_cache[kFifoCache];
+    __shared__ int s_sc_n, s_fc_n, s_fifo_head0, s_resume, s_argmin;
+    if (tid == 0) {
+        s_sc_n = min(s_free_top, kStackCache);
+        s_fc_n = min(s_fifo_count, kFifoCache);
+        s_fifo_head0 = s_fifo_head;
+    }
+    __syncthreads();
+    for (int k = tid; k < s_sc_n; k += blockDim.x) s_stack_cache[k] = a.slot_stack[s_free_top - 1 - k];
+    for (int k = tid; k < s_fc_n; k += blockDim.x) s_fifo_cache[k] = a.fifo[(s_fifo_head0 + k) % a.P];
+    __syncthreads();
+    const int free_top0 = s_free_top;
+    auto pop_slot = [&]() -> int {
+        const int k = free_top0 - s_free_top;                  // pops so far
+        const int slot = k < s_sc_n ? s_stack_cache[k] : a.slot_stack[s_free_top - 1];
+        --s_free_top;
+        return slot;
+    };
+    auto fifo_at = [&](int pos) -> int {                      // pos: absolute FIFO position
+        const int off = (int)(((int64_t)pos - s_fifo_head0 + a.P) % a.P);
+        return off < s_fc_n ? s_fifo_cache[off] : a.fifo[pos];
+    };
+    auto remove_serial = [&](int slot) {                      // pages to the FIFO tail (R#22)
+        const int npg = (a.slot_len[slot] + CP_BLOCK - 1) / CP_BLOCK;
+        const int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
+        for (int i = 0; i < npg; ++i) a.fifo[(int)(((int64_t)s_fifo_head + s_fifo_count + i) % a.P)] = pl[i];
+        s_fifo_count += npg;
+        a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
+        sflag[slot] = 0;
+        s_live_tokens -= a.slot_len[slot];
+        s_num_live -= 1;
+    };
+    auto pop_candidate = [&]() -> int {
+        if (!s_heap) return -1;
+        while (s_cp < s_cn) {
+            const int sl = cslot[s_cp];
+            const unsigned long long k = ckey[s_cp];
+            ++s_cp;
+            if ((sflag[sl] & 1) && !(sflag[sl] & 2) && a.slot_last[sl] == (k >> 32) + s_minl) return sl;
+        }
+        return -1;
+    };
     int j0 = jstar;
     while (true) {
-        // ---- thread 0 runs ahead through spans that need no block-wide work
         if (tid == 0) {
-            s_j = a.S; s_nrm = 0;
-            for (int j = j0; j < a.S; ++j) {
+            s_resume = a.S; s_argmin = 0;
+            for (int j = j0; j < a.S && !s_argmin; ++j) {
                 const int rj = srep[j];
                 const int b = soff[rj], e = soff[rj + 1];
                 int dup = -1;
                 if (rj != j && is_live(-1 - rj)) dup = resolve(-1 - rj);      // equal to its stored representative
                 for (int q = b; q < e && dup < 0; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
                 if (dup >= 0) {
-                    a.slot_last[dup] = a.t;                      // Duplicate refreshes last_used (R#20)
+                    a.slot_last[dup] = a.t;                                    // Duplicate refreshes last_used (R#20)
                     a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
                     continue;
                 }
                 int cont = -1, cont_id = 0x7fffffff;
                 for (int q = b; q < e; ++q)
                     if (rec[q].y == REL_CONTAINER && is_live(rec[q].x)) {
-                        const int s = resolve(rec[q].x);
-                        const int sid = a.slot_id[s];
-                        if (sid < cont_id) { cont_id = sid; cont = s; }
+                        const int sx = resolve(rec[q].x);
+                        const int sid = a.slot_id[sx];
+                        if (sid < cont_id) { cont_id = sid; cont = sx; }
                     }
                 if (cont >= 0) { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; continue; }
-                // store; first the live entries it strictly contains, ascending id
+                // supersede: the live entries it strictly contains, ascending id
                 int n = 0;
                 for (int q = b; q < e; ++q)
                     if (rec[q].y == REL_CONTAINED && is_live(rec[q].x)) {
-                        const int s = resolve(rec[q].x);
+                        const int sx = resolve(rec[q].x);
                         bool seen = false;
-                        for (int z = 0; z < n; ++z) seen |= (s_rm[z] == s);
+                        for (int z = 0; z < n; ++z) seen |= (s_rm[z] == sx);
                         if (!seen) {
-                            if (n < kMaxSupersede) s_rm[n++] = s;
+                            if (n < kMaxSupersede) s_rm[n++] = sx;
                             else cp_raise(a.hdr, CP_ERR_CAPACITY);
                         }
                     }
@@ -733,68 +757,39 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     for (int y = x; y > 0 && a.slot_id[s_rm[y]] < a.slot_id[s_rm[y - 1]]; --y) {
                         const int tmp = s_rm[y]; s_rm[y] = s_rm[y - 1]; s_rm[y - 1] = tmp;
                     }
-                s_rm_base[0] = 0;
-                for (int x = 0; x < n; ++x) s_rm_base[x + 1] = s_rm_base[x] + (a.slot_len[s_rm[x]] + CP_BLOCK - 1) / CP_BLOCK;
-                s_nrm = n;
-                s_j = j;
-                break;
+                for (int x = 0; x < n; ++x) remove_serial(s_rm[x]);
+                // store span j: id = next id, pages from the FIFO head (R#22)
+                const int m = a.span_len[j];
+                const int slot = pop_slot();
+                const int id = s_next_id++;
+                const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
+                if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
+                int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
+                for (int i = 0; i < npg; ++i) pl[i] = fifo_at((int)(((int64_t)s_fifo_head + i) % a.P));
+                s_fifo_head = (int)((s_fifo_head + npg) % a.P); s_fifo_count -= npg;
+                s_live_tokens += m; s_num_live += 1;
+                sflag[slot] = 3; snew[j] = slot;
+                a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_origin[slot] = a.span_begin[j];
+                a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j]; a.slot_last[slot] = a.t;
+                a.out_tmp[j] = slot; a.out_oc[j] = n > 0 ? CP_SUPERSEDED : CP_STORED;
+                // LRU eviction: victim = min (last_used, id) among live entries (R#21)
+                while (s_live_tokens > a.capacity) {
+                    const int v = pop_candidate();
+                    if (v < 0) { s_argmin = 1; s_resume = j + 1; break; }
+                    remove_serial(v);
+                }
             }
         }
         __syncthreads();
-        const int j = s_j;
-        if (j >= a.S) break;
-        const int nrm = s_nrm;
-        if (nrm > 0) remove_slots(nrm);
-        // ---- store span j: id = next id, pages from the FIFO head (R#22)
-        if (tid == 0) {
-            const int m = a.span_len[j];
-            const int slot = a.slot_stack[--s_free_top];
-            const int id = s_next_id++;
-            const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
-            if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
-            s_store_slot = slot; s_npg = npg; s_pop_head = s_fifo_head;
-            s_fifo_head = (int)((s_fifo_head + npg) % a.P); s_fifo_count -= npg;
-            s_live_tokens += m; s_num_live += 1;
-            sflag[slot] = 3; snew[j] = slot;
-            a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_origin[slot] = a.span_begin[j];
-            a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j]; a.slot_last[slot] = a.t;
-            a.out_tmp[j] = slot; a.out_oc[j] = nrm > 0 ? CP_SUPERSEDED : CP_STORED;
-            s_need = s_live_tokens > a.capacity;
-        }
-        __syncthreads();
-        for (int i = tid; i < s_npg; i += blockDim.x)
-            a.slot_pages[(int64_t)s_store_slot * a.MP + i] = a.fifo[(s_pop_head + i) % a.P];
-        __syncthreads();
-        // ---- LRU eviction: victim = min (last_used, id) among live entries (R#21)
-        while (s_need) {
-            if (tid == 0) {
-                s_victim = -1;
-                if (s_heap) {
-                    while (s_cp < s_cn) {
-                        const int sl = cslot[s_cp];
-                        const unsigned long long k = ckey[s_cp];
-                        ++s_cp;
-                        // still live and not refreshed by a Duplicate in this call
-                        if ((sflag[sl] & 1) && a.slot_last[sl] == (k >> 32) + s_minl && !(sflag[sl] & 2)) { s_victim = sl; break; }
-                    }
-                }
-                if (s_victim >= 0) {
-                    s_rm[0] = s_victim; s_rm_base[0] = 0; s_rm_base[1] = (a.slot_len[s_victim] + CP_BLOCK - 1) / CP_BLOCK;
-                }
-            }
-            __syncthreads();
-            if (s_victim >= 0) {
-                remove_slots(1);
-                if (tid == 0) s_need = s_live_tokens > a.capacity;
-                __syncthreads();
-                continue;
-            }
+        if (!s_argmin) break;
+        // block-wide arg-min evictions until the budget holds, then continue after span s_resume - 1
+        while (s_live_tokens > a.capacity) {
             unsigned long long best_last = ~0ULL; int best_id = 0x7fffffff, best_slot = -1;
-            for (int s = tid; s < a.nslots; s += blockDim.x) {
-                if (!(sflag[s] & 1)) continue;
-                const unsigned long long lu = a.slot_last[s];
-                const int sid = a.slot_id[s];
-                if (lu < best_last || (lu == best_last && sid < best_id)) { best_last = lu; best_id = sid; best_slot = s; }
+            for (int sx = tid; sx < a.nslots; sx += blockDim.x) {
+                if (!(sflag[sx] & 1)) continue;
+                const unsigned long long lu = a.slot_last[sx];
+                const int sid = a.slot_id[sx];
+                if (lu < best_last || (lu == best_last && sid < best_id)) { best_last = lu; best_id = sid; best_slot = sx; }
             }
             for (int off = 16; off; off >>= 1) {
                 const unsigned long long ol = __shfl_xor_sync(0xffffffffu, best_last, off);
@@ -810,13 +805,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     if (s_red_slot[w] < 0) continue;
                     if (s_red_key[w] < bl || (s_red_key[w] == bl && s_wsum[w] < bi)) { bl = s_red_key[w]; bi = s_wsum[w]; bs = s_red_slot[w]; }
                 }
-                s_rm[0] = bs; s_rm_base[0] = 0; s_rm_base[1] = (a.slot_len[bs] + CP_BLOCK - 1) / CP_BLOCK;
+                remove_serial(bs);
             }
-            remove_slots(1);
-            if (tid == 0) s_need = s_live_tokens > a.capacity;
             __syncthreads();
         }
-        j0 = j + 1;
+        j0 = s_resume;
     }
     __syncthreads();
     // ---- write back; removed slots return to the free stack; list the new entries to publish
@@ -1274,11 +1267,11 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
     int candK = 4096;
-    while (candK >= 256 && CommitSmem(x->S, num_spans, candK).total > 200 * 1024) candK >>= 1;
+    while (candK >= 256 && CommitSmem(x->S, num_spans, candK).total > 180 * 1024) candK >>= 1;
     if (candK < 256) candK = 0;
     a.candK = candK;
     const size_t csm = CommitSmem(x->S, num_spans, candK).total;
-    if (csm > 200 * 1024) return CP_ERR_UNSUPPORTED;
+    if (csm > 180 * 1024) return CP_ERR_UNSUPPORTED;     // + ~35 KB static shared memory <= 227 KB
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();

@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if (rr.y == REL_EQ) dup = rr.x;
             else if (rr.y == REL_CONTAINER) { const int sid = a.slot_id[rr.x]; if (sid < cont_id) { cont_id = sid; cont = rr.x; } }
         }
-        if (dup >= 0) { a.slot_last[dup] = a.t; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE; }
+        if (dup >= 0) { a.slot_last[dup] = a.t; sflag[dup] |= 4; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE; }
         else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
     }
     __syncthreads();
@@ -597,9 +597,17 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     //      fallback (list exhausted, non-monotone time, K = 0).
     __shared__ unsigned long long s_minl, s_maxl;
     __shared__ int s_cn, s_cp, s_heap, s_hist[256], s_digit, s_rem2;
-    if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_cn = 0; s_cp = 0; s_heap = 0; }
+    __shared__ long long s_pending;
+    if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_cn = 0; s_cp = 0; s_heap = 0; s_pending = 0; }
     __syncthreads();
-    if (a.candK > 0) {
+    {   // upper bound of the tokens this call can still store: if it fits the budget, no eviction happens
+        long long pend = 0;
+        for (int j = jstar + tid; j < a.S; j += blockDim.x) pend += a.span_len[j];
+        for (int o = 16; o; o >>= 1) pend += __shfl_xor_sync(0xffffffffu, pend, o);
+        if ((tid & 31) == 0 && pend) atomicAdd((unsigned long long*)&s_pending, (unsigned long long)pend);
+    }
+    __syncthreads();
+    if (a.candK > 0 && s_live_tokens + s_pending > a.capacity) {
         unsigned long long mn = ~0ULL, mx = 0;
         for (int sl = tid; sl < a.nslots; sl += blockDim.x)
             if (sflag[sl] & 1) { const unsigned long long lu = a.slot_last[sl]; mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx; }
@@ -699,13 +707,21 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         return off < s_fc_n ? s_fifo_cache[off] : a.fifo[pos];
     };
     auto remove_serial = [&](int slot) {                      // pages to the FIFO tail (R#22)
-        const int npg = (a.slot_len[slot] + CP_BLOCK - 1) / CP_BLOCK;
+        const int len = a.slot_len[slot];
+        const int npg = (len + CP_BLOCK - 1) / CP_BLOCK;
         const int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
-        for (int i = 0; i < npg; ++i) a.fifo[(int)(((int64_t)s_fifo_head + s_fifo_count + i) % a.P)] = pl[i];
+        for (int i0 = 0; i0 < npg; i0 += 16) {                // 16 independent loads, then the stores
+            int v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = (i0 + u < npg) ? __ldcg(pl + i0 + u) : 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (i0 + u < npg) a.fifo[(int)(((int64_t)s_fifo_head + s_fifo_count + i0 + u) % a.P)] = v[u];
+        }
         s_fifo_count += npg;
         a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
         sflag[slot] = 0;
-        s_live_tokens -= a.slot_len[slot];
+        s_live_tokens -= len;
         s_num_live -= 1;
     };
     auto pop_candidate = [&]() -> int {
@@ -713,8 +729,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         while (s_cp < s_cn) {
             const int sl = cslot[s_cp];
             const unsigned long long k = ckey[s_cp];
+            if ((k >> 32) + s_minl >= a.t) return -1;             // t-group: ordered by id with refreshed/new ones
             ++s_cp;
-            if ((sflag[sl] & 1) && !(sflag[sl] & 2) && a.slot_last[sl] == (k >> 32) + s_minl) return sl;
+            if ((sflag[sl] & 1) && !(sflag[sl] & 6)) return sl;    // live, not stored or refreshed in this call
         }
         return -1;
     };
@@ -730,6 +747,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 for (int q = b; q < e && dup < 0; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
                 if (dup >= 0) {
                     a.slot_last[dup] = a.t;                                    // Duplicate refreshes last_used (R#20)
+                    sflag[dup] |= 4;
                     a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
                     continue;
                 }
@@ -1111,7 +1129,9 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     if (cudaGetLastError() != cudaSuccess) { delete x; return CP_ERR_CUDA; }
     if (cudaStreamSynchronize(st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
     // opt-in shared memory for the large kernels
-    cudaFuncSetAttribute(k_ins_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (cudaFuncSetAttribute(k_ins_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024) != cudaSuccess) {
+        delete x; return CP_ERR_CUDA;
+    }
     cudaFuncSetAttribute(k_ins_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hash_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     *out = x;

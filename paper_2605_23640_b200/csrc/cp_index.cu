@@ -702,9 +702,13 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         --s_free_top;
         return slot;
     };
-    auto fifo_at = [&](int pos) -> int {                      // pos: absolute FIFO position
-        const int off = (int)(((int64_t)pos - s_fifo_head0 + a.P) % a.P);
-        return off < s_fc_n ? s_fifo_cache[off] : a.fifo[pos];
+    const int P32 = (int)a.P;                                  // page count (< 2^31)
+    auto wrap = [&](int v) -> int { return v >= P32 ? v - P32 : v; };   // positions wrap at most once
+    long long popped = 0;                                      // pages popped by this call (thread 0)
+    auto fifo_at = [&](int pos) -> int {                      // pos: absolute FIFO position in [0, P)
+        const int off = pos >= s_fifo_head0 ? pos - s_fifo_head0 : pos + P32 - s_fifo_head0;
+        // the cached head window is valid until the FIFO could have wrapped around onto it
+        return (off < s_fc_n && popped < (long long)P32 - s_fc_n) ? s_fifo_cache[off] : a.fifo[pos];
     };
     auto remove_serial = [&](int slot) {                      // pages to the FIFO tail (R#22)
         const int len = a.slot_len[slot];
@@ -714,9 +718,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             int v[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) v[u] = (i0 + u < npg) ? __ldcg(pl + i0 + u) : 0;
+            int pos = wrap(wrap(s_fifo_head + s_fifo_count) + i0);       // FIFO tail + i0
 #pragma unroll
             for (int u = 0; u < 16; ++u)
-                if (i0 + u < npg) a.fifo[(int)(((int64_t)s_fifo_head + s_fifo_count + i0 + u) % a.P)] = v[u];
+                if (i0 + u < npg) { a.fifo[pos] = v[u]; pos = wrap(pos + 1); }
         }
         s_fifo_count += npg;
         a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
@@ -783,8 +788,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
                 if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
                 int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
-                for (int i = 0; i < npg; ++i) pl[i] = fifo_at((int)(((int64_t)s_fifo_head + i) % a.P));
-                s_fifo_head = (int)((s_fifo_head + npg) % a.P); s_fifo_count -= npg;
+                for (int i = 0, pos = s_fifo_head; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
+                popped += npg;
+                s_fifo_head = wrap(s_fifo_head + npg); s_fifo_count -= npg;
                 s_live_tokens += m; s_num_live += 1;
                 sflag[slot] = 3; snew[j] = slot;
                 a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_origin[slot] = a.span_begin[j];

@@ -320,6 +320,7 @@ def bench_ours(args):
     cov = int(S.hits.req_covered.sum().item())
     rec = int(S.hits.req_recompute.sum().item())
     nh = int(S.hits.num_hits.item())
+    S.covered = cov
     reused = cov - rec
     reused_bytes = reused * 2 * row * 2                 # K + V, read + write
     zero_bytes = rec * 2 * row                          # K + V zero placeholders (writes)
@@ -450,6 +451,12 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
+    if S.idx.last_error():
+        raise RuntimeError(f"device error during e2e steps: {S.idx.last_error()}")
+    # the e2e steps must do the same work as the device-timed ones
+    cov = int(S.hits.req_covered.sum().item())
+    if cov != S.covered:
+        raise RuntimeError(f"e2e steps covered {cov} tokens, device-timed steps {S.covered}")
     if world > 1:
         nccl = dist.get_backend() == "nccl"
         t = torch.tensor([ms], dtype=torch.float64, device=S.rdb.tokens.device if nccl else "cpu")

@@ -246,6 +246,10 @@ uint64_t cp_index_hash_base(const cp_index* idx);
 /* Select the gather kernel's (unroll, min-blocks) variant 0-3 (A/B measurement; default 0). */
 cp_status cp_set_gather_variant(int32_t variant);
 
+/* Diagnostic: contiguous copy of `bytes` (multiple of 16) with the gather's 128-bit streaming load /
+ * store instructions, ctas_per_sm x 256-thread CTAs per SM (roofline reference for the gather). */
+cp_status cp_copy_diag(const void* src, void* dst, int64_t bytes, int32_t ctas_per_sm, void* stream);
+
 /* Number of kernels this library launched since load (evidence for gpu_launches). */
 uint64_t cp_kernel_launch_count(void);
 

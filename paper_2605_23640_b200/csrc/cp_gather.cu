@@ -640,3 +640,26 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
     }
     return CP_OK;
 }
+
+// ---- diagnostic: contiguous streaming copy with the gather's load/store instructions -----------------
+// (the roofline check for the copy-shaped gather: what LDG.128.nc / STG.128.cs reach on this part)
+namespace {
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_copy_diag(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * UNROLL;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * UNROLL + threadIdx.x; base < n16; base += stride) {
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) { const int64_t i = base + (int64_t)u * blockDim.x; if (i < n16) v[u] = ld_stream(src + i); }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) { const int64_t i = base + (int64_t)u * blockDim.x; if (i < n16) st_stream(dst + i, v[u]); }
+    }
+}
+}  // namespace
+
+extern "C" cp_status cp_copy_diag(const void* src, void* dst, int64_t bytes, int32_t ctas_per_sm, void* stream) {
+    if (!src || !dst || bytes <= 0 || (bytes & 15) || ctas_per_sm < 1) return CP_ERR_INVALID_ARG;
+    k_copy_diag<8><<<sm_count() * ctas_per_sm, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, bytes / 16);
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}

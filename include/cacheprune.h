@@ -52,7 +52,10 @@ typedef enum {
 
 enum { CP_FP32 = 0, CP_BF16 = 1 };                 /* KV storage dtype                          */
 enum { CP_ROPE_NEOX = 0, CP_ROPE_GPTJ = 1 };       /* pairs (i, i+d/2) | (2i, 2i+1)  (R#12)      */
-enum { CP_MATCH_NO_TOUCH = 1 };                    /* cp_match_spans flags                       */
+enum { CP_MATCH_NO_TOUCH = 1,                     /* cp_match_spans flags                       */
+       CP_MATCH_FIXED_CHUNK = 2,                  /* NEXT-3 baseline policies (R#28-29)          */
+       CP_MATCH_PREFIX_ONLY = 4 };
+enum { CP_POLICY_FIXED_CHUNK = 1, CP_POLICY_PREFIX_ONLY = 2 };   /* cp_policy_spans              */
 enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2 }; /* cp_gather_rerotate flags (R#14)         */
 enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
 enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
@@ -155,6 +158,20 @@ typedef struct {
  * range) is a verified candidate; hits are assembled greedily left to right, longest first, then
  * smaller id (R#7).  Accepted hits touch last_used[e] = max(last_used[e], logical_time) unless
  * CP_MATCH_NO_TOUCH.  Device error: a request longer than cfg.max_req_tokens, or max_hits exceeded.
+ *
+ * Baseline policies (NEXT-3, Fig. 4, §5.7), at most one
+ * of the two flags:
+ *   CP_MATCH_FIXED_CHUNK -- FixedChunk(w): only the chunk-aligned windows k = c*w (k + w <= n) are
+ *     probed and only entries of length w are accepted; a chunk is covered iff an equal live
+ *     length-w entry exists and the chunk has no mask-1 token (Fig. 4-b).  Position-independent
+ *     (delta = k - origin may be nonzero).  The chunk store is filled by cp_policy_spans (R#28).
+ *   CP_MATCH_PREFIX_ONLY -- PrefixOnly: only entries stored at origin 0 whose first w tokens equal
+ *     the request's first w tokens; the covered prefix is the longest common prefix with such an
+ *     entry, ending where tokens diverge, at the first mask-1 token, or at the entry's end (Fig. 4-a);
+ *     covered only if >= w tokens (R#29).  One hit at dst 0, delta 0, hit_len = that prefix (may be
+ *     shorter than the entry), longest first then smaller id.  More origin-0 candidates than
+ *     min(max_req_len, cfg.max_req_tokens) for one request: device error CP_ERR_CAPACITY.
+ * Both flags set: CP_ERR_INVALID_ARG.
  */
 cp_status cp_match_spans(cp_index* idx, const cp_batch* readers_h, uint64_t logical_time,
                          int32_t flags, const cp_hits* out_h, void* stream);
@@ -185,6 +202,22 @@ cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, cons
                              int32_t rho_num, int32_t rho_den, int32_t mode, int32_t max_m,
                              int64_t* out_scores, const int64_t* score_offsets_h,
                              uint32_t* out_bits, const int64_t* bits_word_offsets_h, void* stream);
+
+/*
+ * NEXT-3: the spans a baseline policy stores for a writer batch (R#28-29), in
+ * (request, position) order:
+ *   CP_POLICY_FIXED_CHUNK -- every chunk [c*chunk_len, (c+1)*chunk_len) inside the request that has
+ *     no mask-1 token ("full-chunk hashes of prior requests' chunks, invalidating
+ *     sensitive-containing chunks");
+ *   CP_POLICY_PREFIX_ONLY -- [0, min(first mask-1 position, n, max_len)) if at least chunk_len long.
+ * writers_h: batch with mask (required).  Outputs (device, caller-owned, room for max_spans):
+ * span_req / span_begin / span_len, and count_d[0] = number of spans the policy yields (may exceed
+ * max_spans; only the first max_spans are written).  If count_h is non-NULL the call synchronizes
+ * the stream, stores the count there and returns CP_ERR_CAPACITY when it exceeds max_spans.
+ */
+cp_status cp_policy_spans(const cp_batch* writers_h, int32_t policy, int32_t chunk_len, int32_t max_len,
+                          int32_t max_spans, int32_t* span_req, int32_t* span_begin, int32_t* span_len,
+                          int32_t* count_d, int32_t* count_h, void* stream);
 
 /* ---- NEXT-1: on-device KV Annotator (C1 Steps 1-2) -------------------------- */
 

@@ -20,7 +20,10 @@
  *   - match: the plain definition -- every (k, e) with request[k..k+m_e) equal
  *     to entry e's tokens ("appears as a contiguous substring"),
  *     found by naive substring search; then greedy left-to-right assembly
- *     (R#7), plan codes, LRU touch;
+ *     (R#7), plan codes, LRU touch; the NEXT-3 baseline policies
+ *     FixedChunk (aligned windows, length-w entries) and PrefixOnly (longest
+ *     common prefix with an origin-0 entry) restrict the same naive search
+ *     (Fig. 4; R#28-29);
  *   - RoPE re-rotation of one K row by delta in fp64, one rounding (R#11-13);
  *   - recompute score inter(i) - intra(i) in 2^-40 fixed point and top
  *     ceil(rho*m) selection (R#15-19).
@@ -332,21 +335,60 @@ static int cand_cmp(const void* a, const void* b) {       /* (k asc, m desc, id 
  * (max(last_used, t)) after all requests (the index is a snapshot for the call).
  * Returns the number of hits, or -1 if max_hits would overflow.
  */
+/* flags: bit 0 no LRU touch; bit 1 FixedChunk; bit 2 PrefixOnly (NEXT-3). */
+#define ORC_MATCH_NO_TOUCH 1
+#define ORC_MATCH_FIXED_CHUNK 2
+#define ORC_MATCH_PREFIX_ONLY 4
+
 int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, const uint8_t* mask,
-                  int32_t num_reqs, uint64_t t, int32_t no_touch, int32_t max_hits,
+                  int32_t num_reqs, uint64_t t, int32_t flags, int32_t max_hits,
                   int32_t* req_hit_offsets, int32_t* hit_req, int32_t* hit_entry, int32_t* hit_dst,
                   int32_t* hit_len, int32_t* hit_delta, uint8_t* plan,
                   int32_t* req_covered, int32_t* req_recompute, int32_t* req_candidates) {
+    const int fixed = (flags & ORC_MATCH_FIXED_CHUNK) != 0, prefix = (flags & ORC_MATCH_PREFIX_ONLY) != 0;
+    if (fixed && prefix) return -2;
     int32_t nh = 0;
     req_hit_offsets[0] = 0;
     for (int32_t r = 0; r < num_reqs; ++r) {
         const int32_t* q = tokens + offsets[r];
         int64_t n = offsets[r + 1] - offsets[r];
         const uint8_t* mk = mask ? mask + offsets[r] : NULL;
+        uint8_t* pl = plan + offsets[r];
+        memset(pl, 0, (size_t)n);
+        int32_t cov = 0, rec = 0, cands = 0;
+        if (prefix) {
+            /* PrefixOnly (Fig. 4-a): the covered prefix ends where the tokens
+             * diverge or at the first mask-1 token.  Stored prefixes are the entries at origin 0 whose
+             * first w tokens equal the request's (R#29). */
+            int32_t best = -1, bl = 0;
+            for (int32_t i = 0; n >= x->w && i < x->n_e; ++i) {
+                orc_entry* e = &x->e[i];
+                if (!e->live) continue;
+                int64_t j = 0;
+                while (j < x->w && q[j] == e->tokens[j]) ++j;
+                if (j < x->w) continue;
+                cands++;
+                if (e->origin_pos != 0) continue;
+                int32_t l = 0;
+                while (l < e->len && l < n && q[l] == e->tokens[l] && (!mk || mk[l] == 0)) ++l;
+                if (l < x->w) continue;
+                if (l > bl || (l == bl && e->id < best)) { bl = l; best = e->id; }
+            }
+            if (best >= 0) {
+                if (nh >= max_hits) return -1;
+                orc_entry* e = &x->e[best];
+                hit_req[nh] = r; hit_entry[nh] = e->id; hit_dst[nh] = 0; hit_len[nh] = bl; hit_delta[nh] = 0;
+                nh++;
+                for (int32_t z = 0; z < bl; ++z) { pl[z] = e->recompute[z] ? 2 : 1; cov++; rec += e->recompute[z]; }
+            }
+            req_hit_offsets[r + 1] = nh;
+            req_covered[r] = cov; req_recompute[r] = rec; req_candidates[r] = cands;
+            continue;
+        }
         int64_t nc = 0, cap = 16;
         orc_cand* V = (orc_cand*)malloc(sizeof(orc_cand) * (size_t)cap);
-        int32_t cands = 0;
-        for (int64_t k = 0; k + x->w <= n; ++k) {
+        /* FixedChunk (Fig. 4-b): only chunk-aligned windows, only length-w entries (R#28) */
+        for (int64_t k = 0; k + x->w <= n; k += fixed ? x->w : 1) {
             for (int32_t i = 0; i < x->n_e; ++i) {
                 orc_entry* e = &x->e[i];
                 if (!e->live) continue;
@@ -354,6 +396,7 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
                 while (j < x->w && q[k + j] == e->tokens[j]) ++j;
                 if (j < x->w) continue;
                 cands++;
+                if (fixed && e->len != x->w) continue;
                 if (k + e->len > n) continue;
                 while (j < e->len && q[k + j] == e->tokens[j]) ++j;
                 if (j < e->len) continue;
@@ -367,10 +410,7 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
             }
         }
         qsort(V, (size_t)nc, sizeof(orc_cand), cand_cmp);
-        uint8_t* pl = plan + offsets[r];
-        memset(pl, 0, (size_t)n);
         int64_t cursor = 0;
-        int32_t cov = 0, rec = 0;
         for (int64_t c = 0; c < nc; ++c) {
             if (V[c].k < cursor) continue;
             if (nh >= max_hits) { free(V); return -1; }
@@ -388,7 +428,7 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
         req_covered[r] = cov; req_recompute[r] = rec; req_candidates[r] = cands;
         free(V);
     }
-    if (!no_touch)
+    if (!(flags & ORC_MATCH_NO_TOUCH))
         for (int32_t h = 0; h < nh; ++h) {
             orc_entry* e = &x->e[hit_entry[h]];
             if (e->last_used < t) e->last_used = t;

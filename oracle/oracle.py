@@ -199,6 +199,30 @@ def pack_bits(flags_per_span):
     return (np.concatenate(words) if words else np.zeros(0, np.uint32)), np.array(offs, np.int64)
 
 
+# --- NEXT-3 baseline stores (R#28-29) ------------------------
+def policy_spans(batch, policy: str, chunk_len: int, max_len: int):
+    """Spans a baseline policy stores for a writer batch, in (request, position) order.
+    fixed_chunk: every chunk [c*L, (c+1)*L) of the request with no mask-1 token (Fig. 4-b).
+    prefix_only: [0, min(first mask-1 position, n, max_len)) if at least L long (Fig. 4-a)."""
+    req, beg, ln = [], [], []
+    for r in range(batch.num_reqs):
+        a, b = int(batch.offsets[r]), int(batch.offsets[r + 1])
+        m = [int(x) for x in batch.mask[a:b]]
+        n = b - a
+        if policy == "fixed_chunk":
+            for c in range(n // chunk_len):
+                if not any(m[c * chunk_len:(c + 1) * chunk_len]):
+                    req.append(r); beg.append(c * chunk_len); ln.append(chunk_len)
+        elif policy == "prefix_only":
+            first = m.index(1) if 1 in m else n
+            p = min(first, n, max_len)
+            if p >= chunk_len:
+                req.append(r); beg.append(0); ln.append(p)
+        else:
+            raise ValueError(policy)
+    return np.array(req, np.int32), np.array(beg, np.int32), np.array(ln, np.int32)
+
+
 # --- index ---------------------------------------------------------------------------
 @dataclass
 class MatchResult:
@@ -241,7 +265,9 @@ class OracleIndex:
         return rc, out_id[:S], out_oc[:S]
 
     def match(self, batch, t: int = 0, no_touch: bool = False, use_mask: bool = True,
-              max_hits: Optional[int] = None) -> MatchResult:
+              max_hits: Optional[int] = None, policy: Optional[str] = None) -> MatchResult:
+        """policy None: CrossUserSelective (the method); "fixed_chunk" / "prefix_only": NEXT-3
+        baselines (R#28-29)."""
         R, T = batch.num_reqs, batch.total_tokens
         tok, off = _c(batch.tokens, np.int32), _c(batch.offsets, np.int64)
         msk = _c(batch.mask, np.uint8) if use_mask else None
@@ -251,7 +277,8 @@ class OracleIndex:
         hr, he, hd, hl, hdl = o(mh), o(mh), o(mh), o(mh), o(mh)
         plan = o(T, np.uint8)
         cov, rec, cand = o(R), o(R), o(R)
-        nh = lib().orc_match(self.h, _p(tok), _p(off), _p(msk), R, t, int(no_touch), mh, _p(rho),
+        flags = int(no_touch) | {None: 0, "fixed_chunk": 2, "prefix_only": 4}[policy]
+        nh = lib().orc_match(self.h, _p(tok), _p(off), _p(msk), R, t, flags, mh, _p(rho),
                              _p(hr), _p(he), _p(hd), _p(hl), _p(hdl), _p(plan), _p(cov), _p(rec), _p(cand))
         if nh < 0:
             raise RuntimeError("oracle match: hit buffer overflow")

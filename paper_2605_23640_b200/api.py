@@ -191,13 +191,16 @@ class KVIndex:
         return out_id[:S], out_oc[:S]
 
     def match_spans(self, readers: DeviceBatch, t: int = 0, no_touch: bool = False, use_mask: bool = True,
-                    hits: Optional[Hits] = None, stream=None) -> Hits:
+                    hits: Optional[Hits] = None, stream=None, policy: Optional[str] = None) -> Hits:
+        """policy None: the method (cross-user selective); "fixed_chunk" / "prefix_only": the NEXT-3
+        baseline policies (CP_MATCH_FIXED_CHUNK / CP_MATCH_PREFIX_ONLY)."""
+        flags = (L.CP_MATCH_NO_TOUCH if no_touch else 0) | {
+            None: 0, "fixed_chunk": L.CP_MATCH_FIXED_CHUNK, "prefix_only": L.CP_MATCH_PREFIX_ONLY}[policy]
         if hits is None:
             hits = Hits(readers.total_tokens // self.cfg.window_len + readers.num_reqs + 1, readers.num_reqs,
                         readers.total_tokens, self.device)
         rb, hc = readers.c(use_mask), hits.c()
-        rc = L.lib().cp_match_spans(self.h, C.byref(rb), int(t), L.CP_MATCH_NO_TOUCH if no_touch else 0,
-                                    C.byref(hc), _stream(stream))
+        rc = L.lib().cp_match_spans(self.h, C.byref(rb), int(t), flags, C.byref(hc), _stream(stream))
         L.check(rc, "cp_match_spans")
         return hits
 
@@ -318,6 +321,23 @@ def hash_prefix(batch: DeviceBatch, hash_seed: int, stream=None) -> torch.Tensor
     rb = batch.c(False)
     L.check(L.lib().cp_hash_prefix(C.byref(rb), int(hash_seed), _ptr(out), _stream(stream)), "cp_hash_prefix")
     return out
+
+
+def policy_spans(batch: DeviceBatch, policy: str, chunk_len: int, max_len: int = 1 << 30, stream=None):
+    """NEXT-3: the spans a baseline policy stores for a writer batch (cp_policy_spans); returns
+    (span_req, span_begin, span_len) device int32 tensors.  Synchronizes (the count sizes them)."""
+    code = {"fixed_chunk": L.CP_POLICY_FIXED_CHUNK, "prefix_only": L.CP_POLICY_PREFIX_ONLY}[policy]
+    dev = batch.tokens.device
+    cap = batch.total_tokens // max(chunk_len, 1) + 1 if policy == "fixed_chunk" else batch.num_reqs + 1
+    out = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(3)]
+    cnt_d = torch.zeros(1, dtype=torch.int32, device=dev)
+    cnt_h = C.c_int32(0)
+    rb = batch.c(True)
+    L.check(L.lib().cp_policy_spans(C.byref(rb), code, int(chunk_len), int(min(max_len, 2**31 - 1)), cap,
+                                    _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(cnt_d), C.byref(cnt_h),
+                                    _stream(stream)), "cp_policy_spans")
+    n = int(cnt_h.value)
+    return tuple(o[:n] for o in out)
 
 
 def kernel_launch_count() -> int:

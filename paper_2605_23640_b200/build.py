@@ -5,7 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRCS = ["cp_index.cu", "cp_match.cu", "cp_gather.cu", "cp_score.cu", "cp_annotate.cu"]
+SRCS = ["cp_index.cu", "cp_match.cu", "cp_gather.cu", "cp_score.cu", "cp_annotate.cu", "cp_policy.cu"]
 OUT = os.path.join(HERE, "libcacheprune.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -13,6 +13,10 @@
 //   5. hits -> sparse per-request scratch, LRU touch (atomicMax), plan codes + stats
 //   6. the last CTA to finish (ticket) scans the per-request hit counts and compacts the hits
 //      into the caller's dense arrays -- no extra launch, no host round trip.
+// NEXT-3 baseline policies (R#28-29) reuse the same CTA: FixedChunk probes only the chunk-aligned
+// windows and accepts only length-w entries (steps 3-4 unchanged); PrefixOnly probes window 0,
+// collects the origin-0 entries and replaces steps 3-4 by a warp-per-candidate longest common
+// prefix (ballot over 32 tokens per step) and a warp max over (prefix length, -id).
 #include "cp_internal.cuh"
 #include <algorithm>
 #include <cstring>
@@ -24,7 +28,7 @@ constexpr int kNT = 512;
 struct MatchArgs {
     DevHeader* hdr;
     const int32_t* tokens; const int64_t* offsets; const uint8_t* mask; int32_t R;
-    unsigned long long t; int32_t no_touch;
+    unsigned long long t; int32_t no_touch; int32_t policy;   // 0 selective, 1 FixedChunk, 2 PrefixOnly
     int32_t w; uint64_t B; uint64_t Bw; const unsigned long long* pw;
     const HEntry* htab; int logT; int64_t T;
     const int32_t* slot_id; const int32_t* slot_len; const int32_t* slot_origin;
@@ -82,17 +86,27 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         for (int k = tid; k < nw; k += kNT) vslot[k] = -1;
         __syncthreads();
         // ---- 2. rolling windows -> prefix filter -> O(1) full-hash pre-check (warp-level probing)
+        // windows examined: every k (the method), k = c*w (FixedChunk), k = 0 (PrefixOnly)
+        const int kstep = a.policy == 1 ? a.w : 1;
+        const int nwin = a.policy == 0 ? nw : a.policy == 1 ? n / a.w : (nw > 0 ? 1 : 0);
         int my_cands = 0;
         const int wbase = tid & ~31;
-        for (int base = 0; base < nw; base += kNT) {
-            const int k = base + tid;
-            const bool act = k < nw;
-            const uint64_t W = act ? cp_subhash(h, k, a.w, a.Bw) : 0;
+        for (int base = 0; base < nwin; base += kNT) {
+            const int c = base + tid;
+            const bool act = c < nwin;
+            const uint64_t W = act ? cp_subhash(h, c * kstep, a.w, a.Bw) : 0;
             cp_warp_probe<true>(a.htab, (uint32_t)(a.T - 1), a.logT, W, act, [&](int owner, const HEntry& e) {
                 ++my_cands;
-                const int kk = base + wbase + owner;
+                const int kk = (base + wbase + owner) * kstep;
                 const int m = e.len;
-                if (kk + m <= n && cp_subhash(h, kk, m, __ldg(a.pw + m)) == e.full) {
+                if (a.policy == 2) {
+                    // PrefixOnly: stored prefixes are the entries at origin 0 (R#29)
+                    if (__ldg(a.slot_origin + e.slot) == 0) {
+                        const int i = atomicAdd(&s_nc, 1);
+                        if (i < a.nmax) clist[i] = e.slot;
+                    }
+                } else if ((a.policy == 0 || m == a.w) && kk + m <= n &&
+                           cp_subhash(h, kk, m, __ldg(a.pw + m)) == e.full) {
                     // containment-free pool: at most one true match starts at kk (first writer wins)
                     if (atomicCAS(&vslot[kk], -1, e.slot) == -1) clist[atomicAdd(&s_nc, 1)] = kk;
                 }
@@ -102,9 +116,57 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         for (int o = 16; o; o >>= 1) my_cands += __shfl_xor_sync(0xffffffffu, my_cands, o);
         if (lane == 0 && my_cands) atomicAdd(&s_cands, my_cands);
         __syncthreads();
+        const uint8_t* mk = a.mask ? a.mask + off : nullptr;
+        if (a.policy == 2) {
+            // ---- 3'. PrefixOnly: longest common prefix with each origin-0 candidate, one warp each
+            if (tid == 0 && s_nc > a.nmax) cp_raise(a.hdr, CP_ERR_CAPACITY);
+            const int nc = min(s_nc, a.nmax);
+            for (int c = wid; c < nc; c += kNT / 32) {
+                const int slot = clist[c];
+                const int lim = min(__ldg(a.slot_len + slot), n);
+                const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+                int l = lim;
+                for (int i0 = 0; i0 < lim; i0 += 32) {
+                    const int i = i0 + lane;
+                    bool stop = true;
+                    if (i < lim) {
+                        const int32_t et = __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15));
+                        stop = et != tok[i] || (mk && mk[i]);
+                    }
+                    const unsigned b = __ballot_sync(0xffffffffu, stop);
+                    if (b) { l = i0 + __ffs(b) - 1; break; }
+                }
+                if (lane == 0) vslot[c] = l;
+            }
+            __syncthreads();
+            // ---- 4'. the longest prefix, then the smaller id; covered only if >= w (R#29)
+            if (wid == 0) {
+                unsigned long long best = 0;
+                for (int c = lane; c < nc; c += 32) {
+                    const int l = vslot[c];
+                    if (l < a.w) continue;
+                    const unsigned long long key = ((unsigned long long)l << 32) |
+                                                   (unsigned)(0x7fffffff - __ldg(a.slot_id + clist[c]));
+                    best = key > best ? key : best;
+                }
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+                    best = y > best ? y : best;
+                }
+                if (best) {
+                    for (int c = lane; c < nc; c += 32) {
+                        const int l = vslot[c];
+                        if (l >= a.w && (unsigned)(0x7fffffff - __ldg(a.slot_id + clist[c])) == (unsigned)(best & 0xffffffffu)) {
+                            hk[0] = 0; hs[0] = clist[c]; hm[0] = l;
+                        }
+                    }
+                }
+                if (lane == 0) s_nh = best ? 1 : 0;
+            }
+            __syncthreads();
+        } else {
         // ---- 3. exact verification, one warp per candidate
         const int nc = s_nc;
-        const uint8_t* mk = a.mask ? a.mask + off : nullptr;
         for (int c = wid; c < nc; c += kNT / 32) {
             const int k = clist[c];
             const int slot = vslot[k];
@@ -138,6 +200,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             if (lane == 0) s_nh = nh;
         }
         __syncthreads();
+        }   // policy != PrefixOnly
         nh = s_nh;
         // ---- 5. sparse hits + LRU touch
         const int64_t base = off / a.w + r;
@@ -235,6 +298,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
 extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, int32_t flags, const cp_hits* o,
                                     void* stream) {
     if (!x || !b || !o) return CP_ERR_INVALID_ARG;
+    if ((flags & CP_MATCH_FIXED_CHUNK) && (flags & CP_MATCH_PREFIX_ONLY)) return CP_ERR_INVALID_ARG;
     if (b->num_reqs < 0 || b->num_reqs > x->cfg.max_batch_reqs || b->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
     if (!o->num_hits || !o->req_hit_offsets || !o->hit_req || !o->hit_entry || !o->hit_slot || !o->hit_dst ||
         !o->hit_len || !o->hit_delta || !o->plan || !o->req_covered || !o->req_recompute || !o->req_candidates)
@@ -252,6 +316,7 @@ extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, 
     std::memset(&a, 0, sizeof(a));
     a.hdr = x->hdr; a.tokens = b->tokens; a.offsets = b->offsets; a.mask = b->mask; a.R = b->num_reqs;
     a.t = t; a.no_touch = (flags & CP_MATCH_NO_TOUCH) ? 1 : 0;
+    a.policy = (flags & CP_MATCH_FIXED_CHUNK) ? 1 : (flags & CP_MATCH_PREFIX_ONLY) ? 2 : 0;
     a.w = x->cfg.window_len; a.B = x->B; a.Bw = x->Bw; a.pw = x->pw;
     a.htab = x->htab; a.logT = x->logT; a.T = x->T;
     a.slot_id = x->slot_id; a.slot_len = x->slot_len; a.slot_origin = x->slot_origin; a.slot_full = x->slot_full;

@@ -87,7 +87,7 @@ class Case:
 
     def __init__(self, wl: Workload, device="cuda", seed: int = 0, rho=(1, 4), layer_range=None,
                  head_range=None, sample_reqs: Optional[int] = None, sample_layers: Optional[Sequence[int]] = None,
-                 use_reader_mask: bool = True, hash_seed: int = 42):
+                 use_reader_mask: bool = True, hash_seed: int = 42, policy: Optional[str] = None):
         import torch
         import paper_2605_23640_b200 as cp
         self.torch, self.cp = torch, cp
@@ -100,8 +100,11 @@ class Case:
         self.rho = rho
         self.sample_reqs, self.sample_layers = sample_reqs, sample_layers
         self.use_reader_mask = use_reader_mask
+        self.policy = policy                 # None: the method; "fixed_chunk" / "prefix_only": NEXT-3 baselines
         lens = [int(b.lens.max()) for wb, rb in wl.rounds for b in (wb, rb) if b is not None]
         spans = [len(wb.span_len) for wb, rb in wl.rounds if wb is not None]
+        if policy is not None:
+            spans += [wb.total_tokens // g.window_len + wb.num_reqs for wb, rb in wl.rounds if wb is not None]
         reqs = [b.num_reqs for wb, rb in wl.rounds for b in (wb, rb) if b is not None]
         toks = [b.total_tokens for wb, rb in wl.rounds for b in (wb, rb) if b is not None]
         w = g.window_len
@@ -149,8 +152,27 @@ class Case:
         return kv
 
     # ------------------------------------------------------------------ steps
+    def policy_spans(self, wb: Batch, rep: ParityReport):
+        """NEXT-3: each side derives the baseline store's spans on its own; they must agree exactly.
+        Returns the writer batch with the oracle's spans (for the oracle and the payload) and the
+        device's span tensors (for the device insert)."""
+        import dataclasses
+        db = self._dev_batch(wb)
+        d_sr, d_sb, d_sl = self.cp.policy_spans(db, self.policy, self.g.window_len, self.wl.max_span_len)
+        o_sr, o_sb, o_sl = O.policy_spans(wb, self.policy, self.g.window_len, self.wl.max_span_len)
+        for name, d, o in (("req", d_sr, o_sr), ("begin", d_sb, o_sb), ("len", d_sl, o_sl)):
+            if not np.array_equal(d.cpu().numpy(), o):
+                rep.fail(f"policy_spans({self.policy}): span_{name} differs")
+        rep.stats["policy_spans"] = rep.stats.get("policy_spans", 0) + len(o_sr)
+        return dataclasses.replace(wb, span_req=o_sr, span_begin=o_sb, span_len=o_sl), (d_sr, d_sb, d_sl)
+
     def insert(self, wb: Batch, rep: ParityReport, bits_flags=None, sparse_kv=False):
         torch = self.torch
+        dev_spans = None
+        if self.policy is not None:
+            wb, dev_spans = self.policy_spans(wb, rep)
+            if not rep.ok:
+                return
         self.t += 1
         t = self.t
         if bits_flags is None:
@@ -161,7 +183,8 @@ class Case:
         sp = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(self.device)
         dwords = torch.from_numpy(words.view(np.int32).copy() if len(words) else np.zeros(1, np.int32)).to(self.device)
         doffs = torch.from_numpy(offs.astype(np.int64)).to(self.device)
-        ids, oc = self.dev.insert(db, kv, sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len), dwords, doffs, t)
+        dsp = dev_spans if dev_spans is not None else (sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len))
+        ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t)
         err = self.dev.last_error()
         rc, oids, ooc = self.orc.insert(wb, words, offs, t)
         if err != rc:
@@ -210,7 +233,7 @@ class Case:
         self.t += 1
         t = self.t
         db = self._dev_batch(rb, with_mask=self.use_reader_mask)
-        hits = self.dev.match_spans(db, t, no_touch=no_touch, use_mask=self.use_reader_mask)
+        hits = self.dev.match_spans(db, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy)
         dst = self.dst_kv(rb) if check_kv else None
         if check_kv:
             self.dev.gather_rerotate(db, hits, dst, zero_recompute=True)
@@ -218,7 +241,7 @@ class Case:
         if err:
             rep.fail(f"match t={t}: device error {err}")
             return
-        res = self.orc.match(rb, t, no_touch=no_touch, use_mask=self.use_reader_mask)
+        res = self.orc.match(rb, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy)
         h = hits.to_host()
         if h["num_hits"] != res.num_hits:
             rep.fail(f"match t={t}: num_hits {h['num_hits']} != {res.num_hits}")
@@ -241,6 +264,9 @@ class Case:
         rep.stats["tokens"] = rep.stats.get("tokens", 0) + rb.total_tokens
         rep.stats["hits"] = rep.stats.get("hits", 0) + res.num_hits
         rep.stats["moved_hits"] = rep.stats.get("moved_hits", 0) + int(np.sum(res.hit_delta != 0))
+        if self.policy == "prefix_only":          # hits shorter than their entry (partial prefixes)
+            rep.stats["partial_hits"] = rep.stats.get("partial_hits", 0) + sum(
+                int(res.hit_len[i]) < self.orc.entry(int(res.hit_entry[i]))["len"] for i in range(res.num_hits))
         if check_kv:
             self.compare_kv(rb, res, dst, rep)
         self.compare_index(rep, f"after match t={t}", tokens=False)

@@ -119,6 +119,7 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(sizeof(HEntry) * L->BT);                            // 26 dtab
     sput(4 * (size_t)L->MS);                                 // 27 span_rep
     sput(sizeof(Rec16) * (size_t)L->MS);                     // 28 precs
+    sput(4 * (size_t)(S + L->MS));                           // 29 rm_pos (FIFO tail position per removal)
     L->scr_size = o;
 }
 
@@ -157,10 +158,11 @@ struct InsArgs {
     int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; int logT; int64_t T; const unsigned long long* pw;
     // scratch
     unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
-    Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed;
+    Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed; int32_t* rm_pos;
     int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
     int32_t* eq_old; HEntry* dtab; int32_t* span_rep; Rec16* precs;
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
+    int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
 
 // error codes are ordered per span: range -> too short -> capacity -> sensitive (same order as the oracle)
@@ -435,15 +437,20 @@ constexpr int kStackCache = 2048;          // free-slot stack entries cached in 
 constexpr int kFifoCache = 4096;           // free-page FIFO head entries cached in shared memory
 
 struct CommitSmem {                  // byte offsets of the dynamic shared-memory carve-up
-    size_t snew, srep, soff, srec, ckey, cslot, total;
-    __host__ __device__ CommitSmem(int nslots, int S, int K = 0) {
+    size_t snew, srep, soff, seq, slen, sfpos, ckey, cslot, clen, srec, fixed, total;
+    __host__ __device__ CommitSmem(int nslots, int S, int K, int rec_cap) {
         snew = ((size_t)nslots + 15) & ~(size_t)15;
         srep = snew + 4 * (size_t)S;
         soff = srep + 4 * (size_t)S;
-        srec = (soff + 4 * ((size_t)S + 1) + 15) & ~(size_t)15;
-        ckey = srec + 8 * (size_t)kCommitRecCap;            // LRU candidates: (last_used - min) << 32 | id
+        seq = soff + 4 * ((size_t)S + 1);                   // per group: last entry known equal to it
+        slen = seq + 4 * (size_t)S;                         // span lengths
+        sfpos = slen + 4 * (size_t)S;                       // deferred stores: FIFO position of their pages
+        ckey = (sfpos + 4 * (size_t)S + 15) & ~(size_t)15;   // LRU candidates: (last_used - min) << 32 | id
         cslot = ckey + 8 * (size_t)K;
-        total = cslot + 4 * (size_t)K;
+        clen = cslot + 4 * (size_t)K;
+        srec = (clen + 4 * (size_t)K + 15) & ~(size_t)15;  // relation records (rec_cap of them)
+        fixed = srec;
+        total = srec + 8 * (size_t)rec_cap;
     }
 };
 
@@ -472,18 +479,34 @@ __device__ int block_excl_scan(int32_t* v, int n, int32_t* wsum) {
     return total;
 }
 
+#ifdef CP_COMMIT_PROF
+// diagnostic build only: [0..5] phase timestamps, [6..11] cycles per path, [12..15] counts
+__device__ unsigned long long g_commit_prof[16];
+#define PROF_T(i) do { if (tid == 0) g_commit_prof[i] += clock64() - t_phase; if (tid == 0) t_phase = clock64(); } while (0)
+#define PROF_ACC(i, c) do { g_commit_prof[i] += clock64() - (c); } while (0)
+#define PROF_CNT(i, n) do { g_commit_prof[i] += (n); } while (0)
+#else
+#define PROF_T(i) do {} while (0)
+#define PROF_ACC(i, c) do {} while (0)
+#define PROF_CNT(i, n) do {} while (0)
+#endif
+
 // One CTA applies the spans in input order (exact sequential semantics of R#20-22).
 // sflag bit 0: live; bit 1: stored by this call.
 __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     extern __shared__ __align__(16) unsigned char smc[];
     const int tid = threadIdx.x;
-    const CommitSmem lay(a.nslots, a.S, a.candK);
+    const CommitSmem lay(a.nslots, a.S, a.candK, a.rec_cap);
     uint8_t* sflag = smc;
     unsigned long long* ckey = (unsigned long long*)(smc + lay.ckey);
     int32_t* cslot = (int32_t*)(smc + lay.cslot);
     int32_t* snew = (int32_t*)(smc + lay.snew);
     int32_t* srep = (int32_t*)(smc + lay.srep);
     int32_t* soff = (int32_t*)(smc + lay.soff);
+    int32_t* seq = (int32_t*)(smc + lay.seq);
+    int32_t* slen = (int32_t*)(smc + lay.slen);
+    int32_t* sfpos = (int32_t*)(smc + lay.sfpos);
+    int32_t* clen = (int32_t*)(smc + lay.clen);
     int2* srec = (int2*)(smc + lay.srec);
     __shared__ int s_abort, s_nrec;
     __shared__ long long s_live_tokens;
@@ -492,6 +515,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __shared__ unsigned long long s_red_key[kCommitThreads / 32];
     __shared__ int s_red_slot[kCommitThreads / 32];
     __shared__ int32_t s_wsum[kCommitThreads / 32 + 1];
+#ifdef CP_COMMIT_PROF
+    long long t_phase = clock64();
+#endif
 
     if (tid == 0) {
         s_abort = 0;
@@ -513,7 +539,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     // ---- load state
     for (int i = tid; i < a.nslots; i += blockDim.x) sflag[i] = a.slot_state[i] == CP_SLOT_LIVE ? 1 : 0;
-    for (int j = tid; j < a.S; j += blockDim.x) { snew[j] = -1; soff[j] = 0; srep[j] = a.span_rep[j]; }
+    for (int j = tid; j < a.S; j += blockDim.x) {
+        snew[j] = -1; soff[j] = 0; srep[j] = a.span_rep[j]; seq[j] = -1; slen[j] = a.span_len[j]; sfpos[j] = -1;
+    }
     if (tid == 0) {
         soff[a.S] = 0;
         s_live_tokens = a.hdr->live_tokens; s_fifo_head = a.hdr->fifo_head; s_fifo_count = a.hdr->fifo_count;
@@ -523,7 +551,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __syncthreads();
     // ---- relation CSR over new spans: (other, kind) records per span
     const int nc = a.hdr->n_cand;
-    auto len_of = [&](int code) { return code < 0 ? a.span_len[-1 - code] : a.slot_len[code]; };
+    auto len_of = [&](int code) { return code < 0 ? slen[-1 - code] : a.slot_len[code]; };
     for (int c = tid; c < nc; c += blockDim.x) {
         const Cand cd = a.cand[c];
         if (!cd.ok) continue;
@@ -551,10 +579,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     for (int j = tid; j <= a.S; j += blockDim.x) soff[j] = a.rel_off[j];
     if (tid == 0) s_nrec = nrec;
     __syncthreads();
-    const bool rec_in_smem = s_nrec <= kCommitRecCap;
+    const bool rec_in_smem = s_nrec <= a.rec_cap;
     if (rec_in_smem) for (int i = tid; i < s_nrec; i += blockDim.x) srec[i] = a.rel_rec[i];
     __syncthreads();
     const int2* rec = rec_in_smem ? srec : a.rel_rec;
+    PROF_T(0);
 
     auto resolve = [&](int code) -> int { return code >= 0 ? code : snew[-1 - code]; };
     auto is_live = [&](int code) -> bool { const int s = resolve(code); return s >= 0 && (sflag[s] & 1); };
@@ -586,10 +615,13 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if (rr.y == REL_EQ) dup = rr.x;
             else if (rr.y == REL_CONTAINER) { const int sid = a.slot_id[rr.x]; if (sid < cont_id) { cont_id = sid; cont = rr.x; } }
         }
-        if (dup >= 0) { a.slot_last[dup] = a.t; sflag[dup] |= 4; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE; }
-        else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
+        if (dup >= 0) {
+            a.slot_last[dup] = a.t; sflag[dup] |= 4; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
+            seq[rj] = dup;                        // the one live entry with this content (benign equal-value race)
+        } else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
     }
     __syncthreads();
+    PROF_T(1);
     // ---- LRU candidates (R#21): the K smallest live (last_used, id) keys, sorted, in shared
     //      memory.  Within this call keys only grow (a Duplicate refresh sets last_used = t >= all old
     //      values when time is monotone) and new entries sort after every old one, so evictions pop
@@ -602,7 +634,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __syncthreads();
     {   // upper bound of the tokens this call can still store: if it fits the budget, no eviction happens
         long long pend = 0;
-        for (int j = jstar + tid; j < a.S; j += blockDim.x) pend += a.span_len[j];
+        for (int j = jstar + tid; j < a.S; j += blockDim.x) pend += slen[j];
         for (int o = 16; o; o >>= 1) pend += __shfl_xor_sync(0xffffffffu, pend, o);
         if ((tid & 31) == 0 && pend) atomicAdd((unsigned long long*)&s_pending, (unsigned long long)pend);
     }
@@ -653,11 +685,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
                 if (!(sflag[sl] & 1)) continue;
                 const unsigned long long k = keyof(sl);
-                if (k <= T) { const int p = atomicAdd(&s_cn, 1); if (p < a.candK) { ckey[p] = k; cslot[p] = sl; } }
+                if (k <= T) { const int p = atomicAdd(&s_cn, 1); if (p < a.candK) { ckey[p] = k; cslot[p] = sl; clen[p] = a.slot_len[sl]; } }
             }
             __syncthreads();
             const int cn = min(s_cn, a.candK);
-            for (int p = cn + tid; p < a.candK; p += blockDim.x) { ckey[p] = ~0ULL; cslot[p] = -1; }
+            for (int p = cn + tid; p < a.candK; p += blockDim.x) { ckey[p] = ~0ULL; cslot[p] = -1; clen[p] = 0; }
             __syncthreads();
             // bitonic sort of the K candidates by key (keys are unique)
             for (int kk = 2; kk <= a.candK; kk <<= 1)
@@ -670,6 +702,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                             if ((x > y) == up) {
                                 ckey[i2] = y; ckey[ix] = x;
                                 const int t2 = cslot[i2]; cslot[i2] = cslot[ix]; cslot[ix] = t2;
+                                const int l2 = clen[i2]; clen[i2] = clen[ix]; clen[ix] = l2;
                             }
                         }
                     }
@@ -679,19 +712,30 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         }
         __syncthreads();
     }
-    // ---- sequential part.  Thread 0 applies spans in order -- duplicates, drops, supersedes, stores
-    //      and candidate-list evictions -- without block barriers (free-slot stack top and the free-page
-    //      FIFO head are cached in shared memory).  Only an arg-min eviction (candidate list exhausted)
-    //      brings the whole block in.
+    // ---- sequential part (warp 0).  Spans are applied in input order, 32 at a time: a Duplicate or a
+    //      Dropped span changes no liveness, so every span up to the first one that must be stored is
+    //      decided by its own lane against the same state; lane 0 then stores that span (supersedes,
+    //      LRU evictions from the candidate list) and the next window starts after it.  Free-slot
+    //      stack and free-page FIFO heads are cached in shared memory.  Page traffic is deferred:
+    //      stores only record their FIFO position and removals their tail position; the block fills
+    //      page lists and appends removed pages in parallel at the end.  That is exact while pops
+    //      read only the FIFO's initial region and appends do not wrap onto it, and while no entry
+    //      stored in this call is removed again; otherwise lane 0 materialises everything so far and
+    //      continues immediately (flush).  Only an arg-min eviction (candidate list exhausted) brings
+    //      the whole block in.
     __shared__ int s_stack_cache[kStackCache];
     __shared__ int s_fifo_cache[kFifoCache];
     __shared__ int s_sc_n, s_fc_n, s_fifo_head0, s_resume, s_argmin;
+    __shared__ int s_defer, s_count0, s_ndef_rm;
+    __shared__ long long s_appended;
     if (tid == 0) {
         s_sc_n = min(s_free_top, kStackCache);
         s_fc_n = min(s_fifo_count, kFifoCache);
         s_fifo_head0 = s_fifo_head;
+        s_defer = 1; s_count0 = s_fifo_count; s_ndef_rm = 0; s_appended = 0;
     }
     __syncthreads();
+    PROF_T(2);
     for (int k = tid; k < s_sc_n; k += blockDim.x) s_stack_cache[k] = a.slot_stack[s_free_top - 1 - k];
     for (int k = tid; k < s_fc_n; k += blockDim.x) s_fifo_cache[k] = a.fifo[(s_fifo_head0 + k) % a.P];
     __syncthreads();
@@ -710,18 +754,41 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         // the cached head window is valid until the FIFO could have wrapped around onto it
         return (off < s_fc_n && popped < (long long)P32 - s_fc_n) ? s_fifo_cache[off] : a.fifo[pos];
     };
-    auto remove_serial = [&](int slot) {                      // pages to the FIFO tail (R#22)
-        const int len = a.slot_len[slot];
+    auto flush_deferred = [&]() {                              // thread 0: deferred page traffic, in order
+        for (int r = 0; r < s_ndef_rm; ++r) {                  // appends land beyond the initial region
+            const int sl = a.removed[r] & 0x7fffffff;
+            const int npg = (a.slot_len[sl] + CP_BLOCK - 1) / CP_BLOCK;
+            const int32_t* pl = a.slot_pages + (int64_t)sl * a.MP;
+            for (int i = 0, pos = a.rm_pos[r]; i < npg; ++i, pos = wrap(pos + 1)) a.fifo[pos] = pl[i];
+        }
+        for (int j = 0; j < a.S; ++j) {                        // pops read the initial region
+            if (sfpos[j] < 0) continue;
+            const int npg = (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
+            int32_t* pl = a.slot_pages + (int64_t)snew[j] * a.MP;
+            for (int i = 0, pos = sfpos[j]; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
+            sfpos[j] = -1;
+        }
+        s_defer = 0;
+    };
+    auto remove_serial = [&](int slot, int len) {             // pages to the FIFO tail (R#22)
         const int npg = (len + CP_BLOCK - 1) / CP_BLOCK;
-        const int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
-        for (int i0 = 0; i0 < npg; i0 += 16) {                // 16 independent loads, then the stores
-            int v[16];
+        if (s_defer && ((sflag[slot] & 2) || (long long)s_count0 + s_appended + npg > (long long)P32)) flush_deferred();
+        const int tail = wrap(s_fifo_head + s_fifo_count);
+        if (s_defer) {
+            a.rm_pos[s_nremoved] = tail;
+            s_appended += npg;
+            s_ndef_rm = s_nremoved + 1;
+        } else {
+            const int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
+            for (int i0 = 0; i0 < npg; i0 += 16) {            // 16 independent loads, then the stores
+                int v[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = (i0 + u < npg) ? __ldcg(pl + i0 + u) : 0;
-            int pos = wrap(wrap(s_fifo_head + s_fifo_count) + i0);       // FIFO tail + i0
+                for (int u = 0; u < 16; ++u) v[u] = (i0 + u < npg) ? __ldcg(pl + i0 + u) : 0;
+                int pos = wrap(tail + i0);
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-                if (i0 + u < npg) { a.fifo[pos] = v[u]; pos = wrap(pos + 1); }
+                for (int u = 0; u < 16; ++u)
+                    if (i0 + u < npg) { a.fifo[pos] = v[u]; pos = wrap(pos + 1); }
+            }
         }
         s_fifo_count += npg;
         a.removed[s_nremoved++] = slot | ((sflag[slot] & 2) ? (int)0x80000000 : 0);
@@ -729,12 +796,13 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         s_live_tokens -= len;
         s_num_live -= 1;
     };
-    auto pop_candidate = [&]() -> int {
+    auto pop_candidate = [&](int& len) -> int {
         if (!s_heap) return -1;
         while (s_cp < s_cn) {
             const int sl = cslot[s_cp];
             const unsigned long long k = ckey[s_cp];
             if ((k >> 32) + s_minl >= a.t) return -1;             // t-group: ordered by id with refreshed/new ones
+            len = clen[s_cp];
             ++s_cp;
             if ((sflag[sl] & 1) && !(sflag[sl] & 6)) return sl;    // live, not stored or refreshed in this call
         }
@@ -742,70 +810,107 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     };
     int j0 = jstar;
     while (true) {
-        if (tid == 0) {
-            s_resume = a.S; s_argmin = 0;
-            for (int j = j0; j < a.S && !s_argmin; ++j) {
-                const int rj = srep[j];
-                const int b = soff[rj], e = soff[rj + 1];
-                int dup = -1;
-                if (rj != j && is_live(-1 - rj)) dup = resolve(-1 - rj);      // equal to its stored representative
-                for (int q = b; q < e && dup < 0; ++q) if (rec[q].y == REL_EQ && is_live(rec[q].x)) { dup = resolve(rec[q].x); break; }
-                if (dup >= 0) {
-                    a.slot_last[dup] = a.t;                                    // Duplicate refreshes last_used (R#20)
-                    sflag[dup] |= 4;
-                    a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
-                    continue;
-                }
-                int cont = -1, cont_id = 0x7fffffff;
-                for (int q = b; q < e; ++q)
-                    if (rec[q].y == REL_CONTAINER && is_live(rec[q].x)) {
-                        const int sx = resolve(rec[q].x);
-                        const int sid = a.slot_id[sx];
-                        if (sid < cont_id) { cont_id = sid; cont = sx; }
+        if (tid < 32) {
+            if (tid == 0) { s_resume = a.S; s_argmin = 0; }
+            __syncwarp();
+            int j = j0;
+            while (j < a.S) {
+                // ---- each lane decides span j + lane against the state at the window start
+                const int jj = j + tid;
+                int kind = 3, target = -1, rjj = 0;                // 0 Duplicate, 1 Dropped, 2 store, 3 none
+                if (jj < a.S) {
+                    rjj = srep[jj];
+                    const int b = soff[rjj], e = soff[rjj + 1];
+                    const int known = seq[rjj];                    // the pool holds at most one live entry per content
+                    if (known >= 0 && (sflag[known] & 1)) target = known;
+                    else {
+                        if (rjj != jj && is_live(-1 - rjj)) target = resolve(-1 - rjj);   // its stored representative
+                        for (int q = b; q < e && target < 0; ++q)
+                            if (rec[q].y == REL_EQ && is_live(rec[q].x)) target = resolve(rec[q].x);
                     }
-                if (cont >= 0) { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; continue; }
-                // supersede: the live entries it strictly contains, ascending id
-                int n = 0;
-                for (int q = b; q < e; ++q)
-                    if (rec[q].y == REL_CONTAINED && is_live(rec[q].x)) {
-                        const int sx = resolve(rec[q].x);
-                        bool seen = false;
-                        for (int z = 0; z < n; ++z) seen |= (s_rm[z] == sx);
-                        if (!seen) {
-                            if (n < kMaxSupersede) s_rm[n++] = sx;
-                            else cp_raise(a.hdr, CP_ERR_CAPACITY);
+                    if (target >= 0) kind = 0;
+                    else {
+                        int cont_id = 0x7fffffff;
+                        for (int q = b; q < e; ++q)
+                            if (rec[q].y == REL_CONTAINER && is_live(rec[q].x)) {
+                                const int sx = resolve(rec[q].x);
+                                const int sid = a.slot_id[sx];
+                                if (sid < cont_id) { cont_id = sid; target = sx; }
+                            }
+                        kind = target >= 0 ? 1 : 2;
+                    }
+                }
+                const unsigned need = __ballot_sync(0xffffffffu, kind == 2);
+                const int f = need ? __ffs(need) - 1 : 32;
+                if (tid < f && kind == 0) {                        // Duplicate refreshes last_used (R#20)
+                    seq[rjj] = target;
+                    a.slot_last[target] = a.t;
+                    sflag[target] |= 4;                            // same value from every lane that writes it
+                    a.out_tmp[jj] = target; a.out_oc[jj] = CP_DUPLICATE;
+                } else if (tid < f && kind == 1) {
+                    a.out_tmp[jj] = target; a.out_oc[jj] = CP_DROPPED_CONTAINED;
+                }
+                __syncwarp();
+                if (f == 32) { j += 32; continue; }
+                const int js = j + f;                              // the first span that must be stored
+                if (tid == 0) {
+                    const int rj = srep[js];
+                    const int b = soff[rj], e = soff[rj + 1];
+                    // supersede: the live entries it strictly contains, ascending id
+                    int n = 0;
+                    for (int q = b; q < e; ++q)
+                        if (rec[q].y == REL_CONTAINED && is_live(rec[q].x)) {
+                            const int sx = resolve(rec[q].x);
+                            bool seen = false;
+                            for (int z = 0; z < n; ++z) seen |= (s_rm[z] == sx);
+                            if (!seen) {
+                                if (n < kMaxSupersede) s_rm[n++] = sx;
+                                else cp_raise(a.hdr, CP_ERR_CAPACITY);
+                            }
                         }
+                    for (int x = 1; x < n; ++x)      // insertion sort by id
+                        for (int y = x; y > 0 && a.slot_id[s_rm[y]] < a.slot_id[s_rm[y - 1]]; --y) {
+                            const int tmp = s_rm[y]; s_rm[y] = s_rm[y - 1]; s_rm[y - 1] = tmp;
+                        }
+                    for (int x = 0; x < n; ++x) remove_serial(s_rm[x], a.slot_len[s_rm[x]]);
+                    // store span js: id = next id, pages from the FIFO head (R#22)
+                    const int m = slen[js];
+                    const int slot = pop_slot();
+                    const int id = s_next_id++;
+                    const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
+                    if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
+                    if (s_defer && popped + npg > (long long)s_count0) flush_deferred();
+                    if (s_defer) sfpos[js] = s_fifo_head;
+                    else {
+                        int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
+                        for (int i = 0, pos = s_fifo_head; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
                     }
-                for (int x = 1; x < n; ++x)      // insertion sort by id
-                    for (int y = x; y > 0 && a.slot_id[s_rm[y]] < a.slot_id[s_rm[y - 1]]; --y) {
-                        const int tmp = s_rm[y]; s_rm[y] = s_rm[y - 1]; s_rm[y - 1] = tmp;
+                    popped += npg;
+                    s_fifo_head = wrap(s_fifo_head + npg); s_fifo_count -= npg;
+                    s_live_tokens += m; s_num_live += 1;
+                    sflag[slot] = 3; snew[js] = slot; seq[rj] = slot;
+                    // id / len / last_used are read by later decisions; origin and hashes are written by
+                    // the parallel write-back (no global loads on this path)
+                    a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_last[slot] = a.t;
+                    a.out_tmp[js] = slot; a.out_oc[js] = n > 0 ? CP_SUPERSEDED : CP_STORED;
+                    PROF_CNT(13, 1);
+                    // LRU eviction: victim = min (last_used, id) among live entries (R#21)
+                    while (s_live_tokens > a.capacity) {
+                        int vlen = 0;
+                        const int v = pop_candidate(vlen);
+                        if (v < 0) { s_argmin = 1; s_resume = js + 1; break; }
+                        remove_serial(v, vlen);
+                        PROF_CNT(14, 1);
                     }
-                for (int x = 0; x < n; ++x) remove_serial(s_rm[x]);
-                // store span j: id = next id, pages from the FIFO head (R#22)
-                const int m = a.span_len[j];
-                const int slot = pop_slot();
-                const int id = s_next_id++;
-                const int npg = (m + CP_BLOCK - 1) / CP_BLOCK;
-                if (s_fifo_count < npg) cp_raise(a.hdr, CP_ERR_CAPACITY);
-                int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
-                for (int i = 0, pos = s_fifo_head; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
-                popped += npg;
-                s_fifo_head = wrap(s_fifo_head + npg); s_fifo_count -= npg;
-                s_live_tokens += m; s_num_live += 1;
-                sflag[slot] = 3; snew[j] = slot;
-                a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_origin[slot] = a.span_begin[j];
-                a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j]; a.slot_last[slot] = a.t;
-                a.out_tmp[j] = slot; a.out_oc[j] = n > 0 ? CP_SUPERSEDED : CP_STORED;
-                // LRU eviction: victim = min (last_used, id) among live entries (R#21)
-                while (s_live_tokens > a.capacity) {
-                    const int v = pop_candidate();
-                    if (v < 0) { s_argmin = 1; s_resume = j + 1; break; }
-                    remove_serial(v);
                 }
+                __syncwarp();
+                if (s_argmin) break;
+                j = js + 1;
             }
         }
         __syncthreads();
         if (!s_argmin) break;
+        PROF_CNT(15, tid == 0 ? 1 : 0);
         // block-wide arg-min evictions until the budget holds, then continue after span s_resume - 1
         while (s_live_tokens > a.capacity) {
             unsigned long long best_last = ~0ULL; int best_id = 0x7fffffff, best_slot = -1;
@@ -829,31 +934,59 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     if (s_red_slot[w] < 0) continue;
                     if (s_red_key[w] < bl || (s_red_key[w] == bl && s_wsum[w] < bi)) { bl = s_red_key[w]; bi = s_wsum[w]; bs = s_red_slot[w]; }
                 }
-                remove_serial(bs);
+                remove_serial(bs, a.slot_len[bs]);
             }
             __syncthreads();
         }
         j0 = s_resume;
     }
     __syncthreads();
-    // ---- write back; removed slots return to the free stack; list the new entries to publish
-    if (tid == 0) {
-        for (int r = 0; r < s_nremoved; ++r) a.slot_stack[s_free_top++] = a.removed[r] & 0x7fffffff;
-        int nl = 0;
-        for (int j = 0; j < a.S; ++j) {
-            const int slot = snew[j];
-            if (slot >= 0 && (sflag[slot] & 1)) {
-                a.cp_req[nl] = a.span_req[j]; a.cp_slot[nl] = slot; a.cp_dst[nl] = a.span_begin[j];
-                a.cp_len[nl] = a.span_len[j]; a.cp_delta[nl] = j;       // cp_delta carries the span index
-                ++nl;
-            }
+    // ---- deferred page traffic, block-parallel (warp per removal / per stored span): appended pages
+    //      go beyond the FIFO's initial region, page lists are read from inside it -- disjoint
+    if (s_defer) {
+        const int cw = tid >> 5, cl = tid & 31, nw = kCommitThreads / 32;
+        for (int r = cw; r < s_ndef_rm; r += nw) {
+            const int sl = a.removed[r] & 0x7fffffff;
+            const int npg = (a.slot_len[sl] + CP_BLOCK - 1) / CP_BLOCK;
+            const int32_t* pl = a.slot_pages + (int64_t)sl * a.MP;
+            for (int i = cl; i < npg; i += 32) a.fifo[wrap(a.rm_pos[r] + i)] = pl[i];
         }
-        a.hdr->n_copy = nl; a.hdr->n_new_live = nl; a.hdr->n_removed = s_nremoved;
+        for (int j = cw; j < a.S; j += nw) {
+            if (sfpos[j] < 0) continue;
+            const int npg = (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
+            int32_t* pl = a.slot_pages + (int64_t)snew[j] * a.MP;
+            for (int i = cl; i < npg; i += 32) pl[i] = a.fifo[wrap(sfpos[j] + i)];
+        }
+    }
+    __syncthreads();
+    PROF_T(3);
+    // ---- write back (block-parallel): removed slots return to the free stack; the new live entries
+    //      get their origin / hashes and are listed, in span order, for publishing and copy-in
+    const int nrm = s_nremoved, top0 = s_free_top;
+    for (int r = tid; r < nrm; r += blockDim.x) a.slot_stack[top0 + r] = a.removed[r] & 0x7fffffff;
+    for (int j = tid; j < a.S; j += blockDim.x) {           // soff is free now: new-live flags
+        const int slot = snew[j];
+        soff[j] = (slot >= 0 && (sflag[slot] & 1)) ? 1 : 0;
+    }
+    __syncthreads();
+    const int nl = block_excl_scan<kCommitThreads>(soff, a.S, s_wsum);
+    for (int j = tid; j < a.S; j += blockDim.x) {
+        const int slot = snew[j];
+        if (slot < 0 || !(sflag[slot] & 1)) continue;
+        const int q = soff[j];
+        a.slot_origin[slot] = a.span_begin[j]; a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j];
+        a.cp_req[q] = a.span_req[j]; a.cp_slot[q] = slot; a.cp_dst[q] = a.span_begin[j];
+        a.cp_len[q] = slen[j]; a.cp_delta[q] = j;            // cp_delta carries the span index
+    }
+    if (tid == 0) {
+        a.hdr->n_copy = nl; a.hdr->n_new_live = nl; a.hdr->n_removed = nrm;
         a.hdr->live_tokens = s_live_tokens; a.hdr->fifo_head = s_fifo_head; a.hdr->fifo_count = s_fifo_count;
-        a.hdr->next_id = s_next_id; a.hdr->slot_free_top = s_free_top; a.hdr->num_live = s_num_live;
+        a.hdr->next_id = s_next_id; a.hdr->slot_free_top = top0 + nrm; a.hdr->num_live = s_num_live;
     }
     __syncthreads();
     for (int i = tid; i < a.nslots; i += blockDim.x) a.slot_state[i] = (sflag[i] & 1) ? CP_SLOT_LIVE : CP_SLOT_FREE;
+    __syncthreads();
+    PROF_T(4);
 }
 
 // map the committed slot of each span to its entry id (parallel)
@@ -1124,6 +1257,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->row_src = (long long*)(s + L.scr_off[23]); x->row_dst = (long long*)(s + L.scr_off[24]);
     x->eq_old = (int32_t*)(s + L.scr_off[25]); x->dtab = (HEntry*)(s + L.scr_off[26]);
     x->span_rep = (int32_t*)(s + L.scr_off[27]); x->precs = (Rec16*)(s + L.scr_off[28]);
+    x->rm_pos = (int32_t*)(s + L.scr_off[29]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -1275,7 +1409,7 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     a.pw = x->pw;
     a.span_pre = x->span_pre; a.span_full = x->span_full; a.btab = x->btab; a.logBT = x->logBT; a.BT = x->BT;
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
-    a.new_slot = x->new_slot; a.removed = x->removed;
+    a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
 
@@ -1292,11 +1426,15 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
+    // shared memory: flags + per-span arrays, then the LRU candidate list (4096 halved to fit), then
+    // as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)
     int candK = 4096;
-    while (candK >= 256 && CommitSmem(x->S, num_spans, candK).total > 180 * 1024) candK >>= 1;
+    while (candK >= 256 && CommitSmem(x->S, num_spans, candK, 0).fixed > 180 * 1024) candK >>= 1;
     if (candK < 256) candK = 0;
     a.candK = candK;
-    const size_t csm = CommitSmem(x->S, num_spans, candK).total;
+    const size_t fixed = CommitSmem(x->S, num_spans, candK, 0).fixed;
+    a.rec_cap = fixed >= 180 * 1024 ? 0 : (int)std::min<size_t>(kCommitRecCap, (180 * 1024 - fixed) / 8);
+    const size_t csm = CommitSmem(x->S, num_spans, candK, a.rec_cap).total;
     if (csm > 180 * 1024) return CP_ERR_UNSUPPORTED;     // + ~35 KB static shared memory <= 227 KB
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -1312,3 +1450,10 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
 }
 
 }  // extern "C"
+
+#ifdef CP_COMMIT_PROF
+extern "C" cp_status cp_commit_prof_read(unsigned long long* out_h) {
+    if (cudaMemcpyFromSymbol(out_h, g_commit_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return CP_ERR_CUDA;
+    return CP_OK;
+}
+#endif

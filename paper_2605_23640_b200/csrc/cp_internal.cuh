@@ -102,7 +102,7 @@ struct cp_index {
     HEntry* btab;
     Cand* cand;
     int32_t *rel_off, *rel_rec;    // CSR per span of relation records (other << 2 | kind)
-    int32_t *new_slot, *removed, *cp_req, *cp_slot, *cp_dst, *cp_len, *cp_delta, *out_tmp;
+    int32_t *new_slot, *removed, *rm_pos, *cp_req, *cp_slot, *cp_dst, *cp_len, *cp_delta, *out_tmp;
     int32_t* eq_old;     // [MS] span has an equal live pool entry
     HEntry* dtab;        // unique table keyed by full hash -> smallest span index (batch dedup)
     int32_t* span_rep;   // [MS] representative (smallest equal span) of each span

@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
-    ap.add_argument("--overlap", type=int, default=0, help="1: run N3 on a side stream concurrently with N1+N2")
+    ap.add_argument("--overlap", type=int, default=1, help="1 (default): run N3 on a side stream concurrently with N1+N2; 0: serialize")
     ap.add_argument("--shard-world", type=int, default=0,
                     help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
     ap.add_argument("--shard-rank", type=int, default=0)

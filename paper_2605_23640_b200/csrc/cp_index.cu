@@ -417,14 +417,23 @@ __global__ void k_ins_verify(InsArgs a, int from_phase1) {
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
     const int nc = min((int64_t)a.hdr->n_cand, a.MAXC);
     const int c0 = from_phase1 ? a.hdr->n_cand0 : 0;
+    constexpr int U = 8;                      // tokens per lane in flight (256 per warp step)
     for (int c = c0 + warp; c < nc; c += nwarps) {
         const Cand cd = a.cand[c];
         const int nm = cd.needle < 0 ? a.span_len[-1 - cd.needle] : a.slot_len[cd.needle];
+        const int32_t* xs = cd.needle < 0 ? span_tokens(a, -1 - cd.needle) : nullptr;
+        const int32_t* ys = cd.hay < 0 ? span_tokens(a, -1 - cd.hay) + cd.off : nullptr;
         int bad = 0;
-        for (int t = lane; t < nm; t += 32) {
-            const int32_t x = cd.needle < 0 ? span_tokens(a, -1 - cd.needle)[t] : slot_token(a, cd.needle, t);
-            const int32_t y = cd.hay < 0 ? span_tokens(a, -1 - cd.hay)[cd.off + t] : slot_token(a, cd.hay, cd.off + t);
-            bad |= (x != y);
+        for (int t0 = 0; t0 < nm && !__any_sync(0xffffffffu, bad); t0 += 32 * U) {
+            int32_t x[U], y[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + 32 * u + lane;
+                x[u] = t < nm ? (xs ? xs[t] : slot_token(a, cd.needle, t)) : 0;
+                y[u] = t < nm ? (ys ? ys[t] : slot_token(a, cd.hay, cd.off + t)) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) bad |= (x[u] != y[u]);
         }
         bad = __any_sync(0xffffffffu, bad);
         if (lane == 0) a.cand[c].ok = !bad;

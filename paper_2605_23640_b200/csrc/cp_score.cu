@@ -52,31 +52,44 @@ __device__ __forceinline__ float4 ld_nc4(const float4* p) {
     return f;
 }
 
-__device__ __forceinline__ long long sum4(const float4 f) { return (q40(f.x) + q40(f.y)) + (q40(f.z) + q40(f.w)); }
+constexpr int kRowBatch = 4;                   // 16-B loads in flight per lane (2 KiB per warp); 8 measured
+                                               // slower (tools/score_rows_ab.cu: issue-bound on predicated tails)
 
-// warp-strided sum of q(p[0..cnt)): scalar head up to 16-B alignment, then 128-bit loads issued four at a
-// time per lane (branch-free body), scalar tail
-__device__ __forceinline__ long long warp_qsum(const float* p, int cnt, int lane) {
-    if (cnt <= 0) return 0;
-    long long acc = 0;
+// One streaming pass over the row prefix A[i][0..i]: returns this lane's share of
+//   inter - intra = sum_{j<l*} q(A[i][j]) - sum_{l*<=j<=i} q(A[i][j])
+// accumulated as 2 * sum_{j<l*} q - sum_{j<=i} q (the same integers, regrouped exactly; the row sum
+// is read, never assumed to be 1 -- R#27).  Scalar head up to 16-B alignment, then batches of
+// kRowBatch predicated 128-bit loads per lane issued before any arithmetic, scalar tail.
+__device__ __forceinline__ long long warp_row_score(const float* p, int cnt, int l, int lane) {
+    long long all = 0, inter = 0;
     const int mis = (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
     const int head = min(cnt, mis ? 4 - mis : 0);
-    if (lane < head) acc += q40(__ldg(p + lane));
+    if (lane < head) { const long long x = q40(__ldg(p + lane)); all += x; if (lane < l) inter += x; }
     const int nvec = (cnt - head) >> 2;
     const float4* v4 = reinterpret_cast<const float4*>(p + head);
-    int q = lane;
-    for (; q + 96 < nvec; q += 128) {
-        const float4 f0 = ld_nc4(v4 + q), f1 = ld_nc4(v4 + q + 32), f2 = ld_nc4(v4 + q + 64), f3 = ld_nc4(v4 + q + 96);
-        acc += (sum4(f0) + sum4(f1)) + (sum4(f2) + sum4(f3));
+    for (int q0 = 0; q0 < nvec; q0 += 32 * kRowBatch) {
+        float4 f[kRowBatch];
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            const int q = q0 + u * 32 + lane;
+            f[u] = q < nvec ? ld_nc4(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            const int j0 = head + 4 * (q0 + u * 32 + lane);     // column of f[u].x
+            const long long x0 = q40(f[u].x), x1 = q40(f[u].y), x2 = q40(f[u].z), x3 = q40(f[u].w);
+            const long long s = (x0 + x1) + (x2 + x3);
+            all += s;
+            if (j0 + 3 < l) inter += s;
+            else if (j0 < l) inter += x0 + (j0 + 1 < l ? x1 : 0) + (j0 + 2 < l ? x2 : 0);
+        }
     }
-    for (; q < nvec; q += 32) acc += sum4(ld_nc4(v4 + q));
-    const int t0 = head + 4 * nvec;
-    if (t0 + lane < cnt) acc += q40(__ldg(p + t0 + lane));
-    return acc;
+    const int t = head + 4 * nvec + lane;
+    if (t < cnt) { const long long x = q40(__ldg(p + t)); all += x; if (t < l) inter += x; }
+    return 2 * inter - all;
 }
 
-// One warp per span row i: inter = sum over columns [0, l*), intra = sum over [l*, i] (two branch-free
-// streaming passes over the row prefix A[i][0..i]).
+// One warp per span row i (all heads), a single pass over A_h[i][0..i].
 __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -89,11 +102,8 @@ __global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
         const int i = l + (gr - a.sp[lo].row_begin);
         const int score_off = a.sp[lo].score_off;
         long long acc = 0;
-        for (int h = 0; h < heads; ++h) {
-            const float* row = A + ((int64_t)h * n + i) * (int64_t)n;
-            acc += warp_qsum(row, l, lane);                  // inter: j < l* (always < i + 1 here)
-            acc -= warp_qsum(row + l, i + 1 - l, lane);      // intra: l* <= j <= i
-        }
+        for (int h = 0; h < heads; ++h)
+            acc += warp_row_score(A + ((int64_t)h * n + i) * (int64_t)n, i + 1, l, lane);
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) a.scores[score_off + (i - l)] = acc;
@@ -145,13 +155,23 @@ __global__ void __launch_bounds__(kTopkThreads) k_score_topk(const ScoreArgs a) 
         for (int i = tid; i < m; i += blockDim.x)
             if ((key[i] & pmask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 255], 1);
         __syncthreads();
-        if (tid == 0) {
-            int cum = 0, rem = s_rem, dg = 0;
-            for (int b = 255; b >= 0; --b) {
-                if (cum + hist[b] >= rem) { dg = b; rem -= cum; break; }
-                cum += hist[b];
+        if (wid == 0) {                 // warp-parallel: lane owns bins [8 lane, 8 lane + 8)
+            int c[8], tot = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { c[k] = hist[8 * lane + k]; tot += c[k]; }
+            int incl = tot;             // keys in bins >= 8 lane
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(0xffffffffu, incl, o); if (lane + o < 32) incl += y; }
+            const int rem = s_rem, excl = incl - tot;
+            __syncwarp();
+            if (excl < rem && rem <= incl) {          // exactly one lane holds the k-th largest digit
+                int cum = excl;
+#pragma unroll
+                for (int k = 7; k >= 0; --k) {
+                    if (cum + c[k] >= rem) { s_digit = 8 * lane + k; s_rem = rem - cum; break; }
+                    cum += c[k];
+                }
             }
-            s_digit = dg; s_rem = rem;
         }
         __syncthreads();
         prefix |= (unsigned long long)s_digit << shift;
@@ -233,7 +253,7 @@ extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* a
         }
         a.total_rows = (int32_t)rows; a.rho_num = rho_num; a.rho_den = rho_den;
         a.scores = (long long*)out_scores + sbase; a.bits = out_bits + bbase;
-        const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 8);
+        const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 4);   // 4 CTAs/SM: best in score_rows_ab
         k_score_rows<<<grid, kRowThreads, 0, st>>>(a);
         CP_COUNT_LAUNCH();
         k_score_topk<<<a.nsp, kTopkThreads, smem, st>>>(a);

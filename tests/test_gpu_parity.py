@@ -222,6 +222,25 @@ def test_score_edge_cases():
             assert np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob), (q, num, den)
 
 
+def test_score_multihead_long_misaligned_rows():
+    """Rows longer than one load batch (> 8 x 32 x 4 floats), odd n (rows not 16-B aligned), l* not
+    a multiple of 4, several heads, non-row-stochastic attention (R#27), several spans per launch."""
+    import paper_2605_23640_b200 as cp
+    rng = np.random.default_rng(7)
+    mats, ns, hs, ls, rs = [], [], [], [], []
+    for n, h, l, r in [(2051, 2, 777, 2050), (4099, 1, 1234, 4098), (1027, 3, 1, 1026), (1536, 1, 161, 1535),
+                       (4099, 1, 4097, 4098)]:
+        A = np.tril(rng.uniform(0, 1.5, (h, n, n))).astype(np.float32)    # row sums != 1
+        mats.append(torch.from_numpy(A).cuda()); ns.append(n); hs.append(h); ls.append(l); rs.append(r)
+    sc, bits, so, bo = cp.score_deviation(mats, ns, hs, ls, rs, 1, 4)
+    sc, bits = sc.cpu().numpy(), bits.cpu().numpy().view(np.uint32)
+    for q in range(len(ns)):
+        m = rs[q] - ls[q] + 1
+        osc, ob = O.score(mats[q].cpu().numpy(), ls[q], rs[q], 1, 4)
+        assert np.array_equal(sc[so[q]:so[q] + m], osc), q
+        assert np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob), q
+
+
 def test_multidoc_config3_full_size_sampled():
     """Config 3 at full size (128 readers x ~4K, 512-passage pool, one GPU): all hits, plans and the
     index bit exact; KV rows sampled (2 requests x 2 layers)."""

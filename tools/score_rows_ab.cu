@@ -1,0 +1,117 @@
+// score_rows_ab.cu -- A/B microbenchmark of the N3 row-sum inner loop (not part of the library).
+// 256 requests x causal fp32 [n x n] attention (n = 1536), span rows [l, n) with l = 160: the
+// config-2 shape of k_score_rows.  Variants: q(x) via F2I.S64 or via integer decode of the fp32
+// bits; loads in flight per lane.  Prints GB/s of algorithmic bytes (row prefixes read).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/score_ab tools/score_rows_ab.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ long long q40_cvt(float x) { return __float2ll_rz(x * 1099511627776.0f); }
+// trunc(x * 2^40) from the bits: |x| < 2^23 finite; denormals give 0 (as x*2^40 < 1 for them)
+__device__ __forceinline__ long long q40_int(float x) {
+    const uint32_t u = __float_as_uint(x);
+    const int E = (u >> 23) & 255;
+    const long long mant = (long long)((u & 0x7FFFFFu) | 0x800000u);
+    const int sh = E - 110;
+    long long q = sh >= 0 ? (mant << sh) : (sh > -24 ? (mant >> -sh) : 0);
+    q = E ? q : 0;
+    return (u >> 31) ? -q : q;
+}
+
+__device__ __forceinline__ float4 ld_nc4(const float4* p) {
+    float4 f;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "l"(p));
+    return f;
+}
+
+template <int B, bool INT>
+__global__ void __launch_bounds__(256) k_rows(const float* A, int n, int l, int reqs, long long* out) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    const int rows_per = n - l, total = rows_per * reqs;
+    for (int gr = warp; gr < total; gr += nwarps) {
+        const int req = gr / rows_per, i = l + gr % rows_per;
+        const float* p = A + ((int64_t)req * n + i) * n;
+        const int cnt = i + 1, nvec = cnt >> 2;
+        const float4* v4 = reinterpret_cast<const float4*>(p);
+        long long all = 0, inter = 0;
+        for (int q0 = 0; q0 < nvec; q0 += 32 * B) {
+            float4 f[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int q = q0 + u * 32 + lane;
+                f[u] = q < nvec ? ld_nc4(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int j0 = 4 * (q0 + u * 32 + lane);
+                long long x0, x1, x2, x3;
+                if (INT) { x0 = q40_int(f[u].x); x1 = q40_int(f[u].y); x2 = q40_int(f[u].z); x3 = q40_int(f[u].w); }
+                else { x0 = q40_cvt(f[u].x); x1 = q40_cvt(f[u].y); x2 = q40_cvt(f[u].z); x3 = q40_cvt(f[u].w); }
+                const long long s = (x0 + x1) + (x2 + x3);
+                all += s;
+                if (j0 + 3 < l) inter += s;
+                else if (j0 < l) inter += x0 + (j0 + 1 < l ? x1 : 0) + (j0 + 2 < l ? x2 : 0);
+            }
+        }
+        const int t = 4 * nvec + lane;
+        if (t < cnt) { const long long x = INT ? q40_int(p[t]) : q40_cvt(p[t]); all += x; if (t < l) inter += x; }
+        long long acc = 2 * inter - all;
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[gr] = acc;
+    }
+}
+
+__global__ void fill(float* A, int64_t N) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)(k * 2654435761u) ^ (uint32_t)(k >> 17);
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        A[k] = (h >> 8) * (1.0f / 16777216.0f) * 0.01f;
+    }
+}
+
+template <int B, bool INT>
+void run(const char* name, const float* A, int n, int l, int reqs, long long* out, long long* ref, int blocks_per_sm) {
+    const int grid = 148 * blocks_per_sm;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int w = 0; w < 3; ++w) k_rows<B, INT><<<grid, 256>>>(A, n, l, reqs, out);
+    cudaEventRecord(e0);
+    const int it = 10;
+    for (int w = 0; w < it; ++w) k_rows<B, INT><<<grid, 256>>>(A, n, l, reqs, out);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= it;
+    double bytes = 0;
+    for (int i = l; i < n; ++i) bytes += 4.0 * ((i + 1) & ~3) ;
+    bytes *= reqs;
+    int bad = 0;
+    if (ref) {
+        static long long h1[1 << 20], h2[1 << 20];
+        const int tot = (n - l) * reqs;
+        cudaMemcpy(h1, out, 8 * (size_t)tot, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h2, ref, 8 * (size_t)tot, cudaMemcpyDeviceToHost);
+        for (int k = 0; k < tot; ++k) bad += h1[k] != h2[k];
+    }
+    printf("%-22s blocks/SM %d  %.3f ms  %.0f GB/s  mismatches %d\n", name, blocks_per_sm, ms, bytes / ms / 1e6, bad);
+}
+
+int main() {
+    const int n = 1536, l = 160, reqs = 256;
+    const int64_t N = (int64_t)reqs * n * n;
+    float* A; long long *out, *ref;
+    cudaMalloc(&A, N * 4); cudaMalloc(&out, 8ll * reqs * n); cudaMalloc(&ref, 8ll * reqs * n);
+    fill<<<148 * 8, 256>>>(A, N);
+    k_rows<8, false><<<148 * 8, 256>>>(A, n, l, reqs, ref);
+    cudaDeviceSynchronize();
+    for (int bps : {4, 6, 8}) {
+        run<4, false>("cvt B4", A, n, l, reqs, out, ref, bps);
+        run<8, false>("cvt B8", A, n, l, reqs, out, ref, bps);
+        run<4, true>("int B4", A, n, l, reqs, out, ref, bps);
+        run<8, true>("int B8", A, n, l, reqs, out, ref, bps);
+        run<12, true>("int B12", A, n, l, reqs, out, ref, bps);
+    }
+    printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

@@ -47,7 +47,7 @@ typedef enum {
     CP_ERR_SPAN_TOO_SHORT = -3,  /* an insert span is shorter than window_len    */
     CP_ERR_CAPACITY = -4,        /* span longer than the budget / max_span_len, buffers full  */
     CP_ERR_CUDA = -5,            /* a CUDA runtime call failed                                  */
-    CP_ERR_UNSUPPORTED = -6      /* configuration or mode not built (e.g. CP_SCORE_KVDEV)      */
+    CP_ERR_UNSUPPORTED = -6      /* configuration or mode not built                           */
 } cp_status;
 
 enum { CP_FP32 = 0, CP_BF16 = 1 };                 /* KV storage dtype                          */
@@ -195,13 +195,41 @@ cp_status cp_gather_rerotate(cp_index* idx, const cp_batch* readers_h, const cp_
  * out_scores (device int64) receives m_s scores from score_offsets_h[s]; out_bits (device uint32)
  * receives ceil(m_s/32) words from bits_word_offsets_h[s]: the first ceil(rho_num*m/rho_den) tokens in
  * (score desc, index asc) order get bit 1 (R#15-16).  max_m bounds m_s (<= 16384).
- * mode CP_SCORE_KVDEV (CacheBlend deviation) returns CP_ERR_UNSUPPORTED in this build.
+ * mode CP_SCORE_KVDEV takes KV caches, not attention: it returns CP_ERR_UNSUPPORTED here; the
+ * CacheBlend selector is cp_score_kv_deviation below.
  */
 cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, const int32_t* n_h,
                              const int32_t* heads_h, const int32_t* span_l_h, const int32_t* span_r_h,
                              int32_t rho_num, int32_t rho_den, int32_t mode, int32_t max_m,
                              int64_t* out_scores, const int64_t* score_offsets_h,
                              uint32_t* out_bits, const int64_t* bits_word_offsets_h, void* stream);
+
+/*
+ * NEXT-4: CacheBlend's recompute selector, the KV-deviation variant the paper contrasts with its own
+ * score ("compares the first-layer KV of a chunk in its original context with that
+ * from a full recomputation in the new context, then recomputes the top 15% of tokens with the
+ * largest deviation").  The paper gives no norm; R#30 fixes it.  For span s (request
+ * span_req_h[s], positions [span_l_h[s], span_r_h[s]] inclusive) and token q in it:
+ *   dev(q) = sum_{h < H, c < d} |q24(Kr[q][h][c]) - q24(Kf[q][h][c])| + |q24(Vr[q][h][c]) - q24(Vf[q][h][c])|
+ * with q24(x) = trunc(x * 2^24) in int64 (exact and order independent, so GPU == oracle bit for bit).
+ *   reused_{k,v}: ONE layer (the first) of the request's paged cache holding the reused KV (the
+ *                 cp_gather_rerotate output: re-rotated to the new positions, so the comparison is
+ *                 position-consistent), vLLM NHD [blocks][16][H][d] in `dtype`;
+ *   fresh_{k,v}:  the same layer from a full recomputation in the new context, same layout;
+ *   *_block_tables: int32 [num_reqs][*_max_blocks] block ids (may differ between the two caches).
+ * Outputs as cp_score_deviation: out_scores[score_offsets_h[s] + i] = dev(span_l + i) (int64);
+ * bits from bits_word_offsets_h[s]: the first ceil(rho_num*m/rho_den) tokens in (dev desc, index asc)
+ * order get bit 1 (R#15-16; CacheBlend's 15% = 3/20).  Requirements: H*d*elem_bytes a multiple of
+ * 16 bytes, |x| * 2^24 * 2 * H * d < 2^63 (|x| < 2^12 for H*d = 1024), max_m <= 16384.
+ */
+cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* span_req_h, const int32_t* span_l_h,
+                                const int32_t* span_r_h, const void* reused_k, const void* reused_v,
+                                const int32_t* reused_block_tables, int32_t reused_max_blocks,
+                                const void* fresh_k, const void* fresh_v, const int32_t* fresh_block_tables,
+                                int32_t fresh_max_blocks, int32_t num_kv_heads, int32_t head_dim, int32_t dtype,
+                                int32_t rho_num, int32_t rho_den, int32_t max_m, int64_t* out_scores,
+                                const int64_t* score_offsets_h, uint32_t* out_bits,
+                                const int64_t* bits_word_offsets_h, void* stream);
 
 /*
  * NEXT-3: the spans a baseline policy stores for a writer batch (R#28-29), in

@@ -552,6 +552,41 @@ int32_t orc_score(const float* A, int64_t n, int32_t heads, int32_t l, int32_t r
     return ORC_OK;
 }
 
+/*
+ * NEXT-4: CacheBlend's KV-deviation selector ("compares the first-layer KV of a chunk in its
+ * original context with that from a full recomputation in the new context, then recomputes the top
+ * 15% of tokens with the largest deviation").  The paper names no norm; reading R#30 takes the L1
+ * distance over K and V in the 2^-24 fixed point q24(x) = trunc(x * 2^24):
+ *   dev(t) = sum_{c < width} |q24(Kr[t][c]) - q24(Kf[t][c])| + |q24(Vr[t][c]) - q24(Vf[t][c])|
+ * Rows are dense fp32 [m][width] (width = H * d; bf16 values widen to fp32 exactly).  Kr/Vr: the
+ * reused (re-rotated) first-layer KV; Kf/Vf: the freshly recomputed one.  Selection as orc_score:
+ * the first ceil(rho_num * m / rho_den) tokens of (dev desc, t asc) get bit 1.
+ */
+static int64_t fixq24(float x) { return (int64_t)((double)x * 16777216.0); }
+static int64_t absdiff(int64_t a, int64_t b) { return a > b ? a - b : b - a; }
+
+int32_t orc_kv_deviation(const float* Kr, const float* Vr, const float* Kf, const float* Vf, int64_t m,
+                         int32_t width, int32_t rho_num, int32_t rho_den, int64_t* dev, uint32_t* bits) {
+    if (m < 1 || width < 1 || rho_den <= 0 || rho_num < 0 || rho_num > rho_den) return ORC_ERR_INVALID_ARG;
+    orc_sc* v = (orc_sc*)malloc(sizeof(orc_sc) * (size_t)m);
+    for (int64_t t = 0; t < m; ++t) {
+        int64_t s = 0;
+        for (int32_t c = 0; c < width; ++c) {
+            const int64_t o = t * width + c;
+            s += absdiff(fixq24(Kr[o]), fixq24(Kf[o]));
+            s += absdiff(fixq24(Vr[o]), fixq24(Vf[o]));
+        }
+        dev[t] = s;
+        v[t].s = s; v[t].i = (int32_t)t;
+    }
+    qsort(v, (size_t)m, sizeof(orc_sc), sc_cmp);
+    int64_t k = ((int64_t)rho_num * m + rho_den - 1) / rho_den;
+    for (int64_t w = 0; w < (m + 31) / 32; ++w) bits[w] = 0;
+    for (int64_t c = 0; c < k; ++c) bits[v[c].i / 32] |= 1u << (v[c].i % 32);
+    free(v);
+    return ORC_OK;
+}
+
 /* Re-rotate `nrows` consecutive rows (plain loop over orc_rerotate_row). */
 void orc_rerotate_rows(const float* xin, int64_t nrows, int32_t H, int32_t d, int32_t gptj, double theta_base,
                        int64_t delta, int32_t out_bf16, float* out) {

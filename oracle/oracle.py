@@ -60,6 +60,7 @@ def lib():
             "orc_fifo_get": (None, [vp, vp]),
             "orc_rerotate_row": (None, [vp, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_score": (i32, [vp, i64, i32, i32, i32, i32, i32, vp, vp]),
+            "orc_kv_deviation": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp, vp]),
             "orc_rerotate_rows": (None, [vp, i64, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_annotate": (i32, [vp, i64, i32, vp, i32, i32, vp, vp, vp]),
             "orc_sat": (None, [vp, i64, i32, vp]),
@@ -153,6 +154,19 @@ def score(A, l: int, r: int, rho_num: int = 1, rho_den: int = 4):
     if rc != OK:
         raise ValueError(f"orc_score rc={rc}")
     return sc[:m], bits[:(m + 31) // 32]
+
+
+def kv_deviation(Kr, Vr, Kf, Vf, rho_num: int = 3, rho_den: int = 20):
+    """NEXT-4 (CacheBlend selector; R#30): rows [m, width] (any float dtype that widens to fp32
+    exactly).  Returns (dev int64 [m], bits uint32 [ceil(m/32)])."""
+    Kr, Vr, Kf, Vf = (_c(np.asarray(x, np.float32).reshape(np.shape(x)[0], -1), np.float32) for x in (Kr, Vr, Kf, Vf))
+    m, width = Kr.shape
+    dev = np.zeros(max(m, 1), np.int64)
+    bits = np.zeros(max((m + 31) // 32, 1), np.uint32)
+    rc = lib().orc_kv_deviation(_p(Kr), _p(Vr), _p(Kf), _p(Vf), m, width, rho_num, rho_den, _p(dev), _p(bits))
+    if rc != OK:
+        raise ValueError(f"orc_kv_deviation rc={rc}")
+    return dev[:m], bits[:(m + 31) // 32]
 
 
 def sat(A) -> np.ndarray:

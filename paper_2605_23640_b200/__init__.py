@@ -5,5 +5,5 @@ thin Python binding (api.py) plus the build helper (build.py).  It never
 imports oracle/ and has no CPU fallback.
 """
 from .api import (DeviceBatch, Hits, IndexConfig, KVIndex, PagedKV, annotate_spans, hash_prefix, policy_spans,  # noqa: F401
-                  kernel_launch_count, score_deviation)
+                  kernel_launch_count, score_deviation, score_kv_deviation)
 from . import _lib  # noqa: F401

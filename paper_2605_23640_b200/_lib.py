@@ -69,6 +69,8 @@ EXPORTS = {
     "cp_gather_rerotate": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), C.POINTER(CpPagedKV), i32, vp]),
     "cp_score_deviation": (i32, [i32, C.POINTER(vp), P_i32, P_i32, P_i32, P_i32, i32, i32, i32, i32,
                                  vp, P_i64, vp, P_i64, vp]),
+    "cp_score_kv_deviation": (i32, [i32, P_i32, P_i32, P_i32, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32,
+                                    i32, i32, i32, vp, P_i64, vp, P_i64, vp]),
     "cp_hash_prefix": (i32, [C.POINTER(CpBatch), u64, vp, vp]),
     "cp_policy_spans": (i32, [C.POINTER(CpBatch), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "cp_index_snapshot": (i32, [vp, C.POINTER(CpSnapshot), vp]),

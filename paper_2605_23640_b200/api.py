@@ -275,6 +275,42 @@ def score_deviation(attn: Sequence[torch.Tensor], n: Sequence[int], heads: Seque
     return out_scores, out_bits, so, bo
 
 
+def score_kv_deviation(span_req: Sequence[int], span_l: Sequence[int], span_r: Sequence[int],
+                       reused_k: torch.Tensor, reused_v: torch.Tensor, reused_block_tables: torch.Tensor,
+                       fresh_k: torch.Tensor, fresh_v: torch.Tensor, fresh_block_tables: torch.Tensor,
+                       rho_num: int = 3, rho_den: int = 20, out_scores=None, out_bits=None, stream=None):
+    """NEXT-4, CacheBlend's selector (cp_score_kv_deviation; R#30): per span token the L1 KV
+    deviation between one layer of the reused cache and of a fresh recomputation ([blocks, 16, H, d]
+    each), top ceil(rho*m) marked (default 15% = 3/20).  Returns (dev, bits, score_offsets,
+    bits_word_offsets) like score_deviation."""
+    S = len(span_l)
+    ms = [int(r) - int(l) + 1 for l, r in zip(span_l, span_r)]
+    so, bo = [0], [0]
+    for m in ms:
+        so.append(so[-1] + m)
+        bo.append(bo[-1] + (m + 31) // 32)
+    dev = reused_k.device
+    if out_scores is None:
+        out_scores = torch.zeros(max(so[-1], 1), dtype=torch.int64, device=dev)
+    if out_bits is None:
+        out_bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=dev)
+    for t in (reused_k, reused_v, fresh_k, fresh_v):
+        if not t.is_contiguous() or t.shape[1:] != reused_k.shape[1:] or t.dtype != reused_k.dtype:
+            raise ValueError("caches must be contiguous [blocks, 16, H, d] of one dtype")
+    H, d = int(reused_k.shape[2]), int(reused_k.shape[3])
+    arr32 = lambda xs: (C.c_int32 * max(S, 1))(*[int(x) for x in xs])
+    arr64 = lambda xs: (C.c_int64 * max(len(xs), 1))(*[int(x) for x in xs])
+    rbt, fbt = reused_block_tables.contiguous(), fresh_block_tables.contiguous()
+    rc = L.lib().cp_score_kv_deviation(S, arr32(span_req), arr32(span_l), arr32(span_r), _ptr(reused_k),
+                                       _ptr(reused_v), _ptr(rbt), int(rbt.shape[1]), _ptr(fresh_k), _ptr(fresh_v),
+                                       _ptr(fbt), int(fbt.shape[1]), H, d,
+                                       L.CP_BF16 if reused_k.dtype == torch.bfloat16 else L.CP_FP32,
+                                       rho_num, rho_den, max(ms) if ms else 1, _ptr(out_scores),
+                                       arr64(so[:-1] or [0]), _ptr(out_bits), arr64(bo[:-1] or [0]), _stream(stream))
+    L.check(rc, "cp_score_kv_deviation")
+    return out_scores, out_bits, so, bo
+
+
 def annotate_spans(attn: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], heads: Sequence[int],
                    min_len: int = 128, max_segments: int = 64, workspace_bytes: int = 4 << 30, stream=None):
     """NEXT-1 (cp_annotate_spans): per request, per coarse segment, the reusable span (l, r, diff) of

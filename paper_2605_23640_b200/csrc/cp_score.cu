@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <climits>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -208,6 +209,127 @@ __global__ void __launch_bounds__(kTopkThreads) k_score_topk(const ScoreArgs a) 
     }
 }
 
+// ---------------------------------------------------------------------------------------------------
+// NEXT-4: CacheBlend KV deviation (R#30).  One warp per span token: the token's K and V
+// rows (H*d elements each) of the reused and the fresh first-layer caches, 16-B loads (4 tensors x
+// kDevBatch vectors per lane in flight), dev = sum |q24(reused) - q24(fresh)| in exact int64.
+// The scores then go through the same k_score_topk as N3.
+struct KvDevArgs {
+    const uint4* rk; const uint4* rv; const int32_t* rbt;
+    const uint4* fk; const uint4* fv; const int32_t* fbt;
+    int32_t rmaxb, fmaxb;
+    int32_t vec_per_row;                        // 16-B vectors per token row (H * d * elem / 16)
+};
+constexpr int kDevBatch = 4;
+
+__device__ __forceinline__ long long q24(float x) { return __float2ll_rz(x * 16777216.0f); }
+__device__ __forceinline__ long long absll(long long x) { return x < 0 ? -x : x; }
+__device__ __forceinline__ long long vdev(const uint4 a, const uint4 b, std::true_type) {      // 8 x bf16
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+    long long s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        s += absll(q24(__uint_as_float(wa[k] << 16)) - q24(__uint_as_float(wb[k] << 16)));
+        s += absll(q24(__uint_as_float(wa[k] & 0xffff0000u)) - q24(__uint_as_float(wb[k] & 0xffff0000u)));
+    }
+    return s;
+}
+__device__ __forceinline__ long long vdev(const uint4 a, const uint4 b, std::false_type) {     // 4 x fp32
+    return absll(q24(__uint_as_float(a.x)) - q24(__uint_as_float(b.x))) + absll(q24(__uint_as_float(a.y)) - q24(__uint_as_float(b.y))) +
+           absll(q24(__uint_as_float(a.z)) - q24(__uint_as_float(b.z))) + absll(q24(__uint_as_float(a.w)) - q24(__uint_as_float(b.w)));
+}
+__device__ __forceinline__ uint4 ld_nc_u4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kRowThreads) k_kvdev_rows(const ScoreArgs a, const KvDevArgs k) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    const int V = k.vec_per_row;
+    for (int gr = warp; gr < a.total_rows; gr += nwarps) {
+        int lo = 0, hi = a.nsp - 1;
+        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
+        const int req = a.sp[lo].n, l = a.sp[lo].l;
+        const int i = l + (gr - a.sp[lo].row_begin);
+        const int64_t ro = ((int64_t)k.rbt[(int64_t)req * k.rmaxb + (i >> 4)] * 16 + (i & 15)) * V;
+        const int64_t fo = ((int64_t)k.fbt[(int64_t)req * k.fmaxb + (i >> 4)] * 16 + (i & 15)) * V;
+        long long acc = 0;
+        for (int v0 = 0; v0 < V; v0 += 32 * kDevBatch) {
+            uint4 x[kDevBatch][4];
+#pragma unroll
+            for (int u = 0; u < kDevBatch; ++u) {
+                const int v = v0 + 32 * u + lane;
+                const bool ok = v < V;
+                const uint4 z = make_uint4(0, 0, 0, 0);
+                x[u][0] = ok ? ld_nc_u4(k.rk + ro + v) : z;
+                x[u][1] = ok ? ld_nc_u4(k.fk + fo + v) : z;
+                x[u][2] = ok ? ld_nc_u4(k.rv + ro + v) : z;
+                x[u][3] = ok ? ld_nc_u4(k.fv + fo + v) : z;
+            }
+#pragma unroll
+            for (int u = 0; u < kDevBatch; ++u)
+                acc += vdev(x[u][0], x[u][1], std::integral_constant<bool, BF16>()) +
+                       vdev(x[u][2], x[u][3], std::integral_constant<bool, BF16>());
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.scores[a.sp[lo].score_off + (i - l)] = acc;
+    }
+}
+
+}  // namespace
+
+namespace {
+
+cp_status topk_smem(int32_t max_m, size_t* smem) {
+    *smem = 9 * (size_t)max_m + 16;
+    static size_t attr = 0;
+    if (*smem > attr) {
+        if (cudaFuncSetAttribute(k_score_topk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(*smem, 48 * 1024)) != cudaSuccess)
+            return CP_ERR_CUDA;
+        attr = *smem;
+    }
+    return CP_OK;
+}
+
+// Offsets of one launch (<= kSpansPerLaunch spans) must fit the 32-bit descriptor fields.
+bool launch_fits(int s0, int nsp, const int32_t* l_h, const int32_t* r_h, const int64_t* score_off_h,
+                 const int64_t* bits_off_h) {
+    int64_t rows = 0;
+    for (int s = s0; s < s0 + nsp; ++s) {
+        if (score_off_h[s] - score_off_h[s0] > INT32_MAX || bits_off_h[s] - bits_off_h[s0] > INT32_MAX) return false;
+        rows += r_h[s] - l_h[s] + 1;
+    }
+    return rows <= INT32_MAX - 65536;
+}
+
+// Build the descriptors of spans [s0, s0 + nsp) (A / n / heads per span as given) into `a`.
+void fill_args(ScoreArgs& a, int s0, int nsp, const float* const* A_h, const int32_t* n_h, const int32_t* heads_h,
+               const int32_t* l_h, const int32_t* r_h, int32_t rho_num, int32_t rho_den, int64_t* out_scores,
+               const int64_t* score_off_h, uint32_t* out_bits, const int64_t* bits_off_h) {
+    std::memset(&a, 0, sizeof(a));
+    a.nsp = nsp;
+    const int64_t sbase = score_off_h[s0], bbase = bits_off_h[s0];
+    int64_t rows = 0;
+    for (int q = 0; q < nsp; ++q) {
+        const int s = s0 + q;
+        SpanDesc d;
+        d.A = A_h ? A_h[s] : nullptr; d.row_begin = (int32_t)rows;
+        d.score_off = (int32_t)(score_off_h[s] - sbase); d.bits_off = (int32_t)(bits_off_h[s] - bbase);
+        d.n = n_h[s]; d.l = l_h[s]; d.r_heads = r_h[s] | ((heads_h ? heads_h[s] : 1) << 24);
+        a.sp[q] = d;
+        rows += r_h[s] - l_h[s] + 1;
+    }
+    a.total_rows = (int32_t)rows; a.rho_num = rho_num; a.rho_den = rho_den;
+    a.scores = (long long*)out_scores + sbase; a.bits = out_bits + bbase;
+}
+
 }  // namespace
 
 extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* attn_h, const int32_t* n_h,
@@ -215,46 +337,75 @@ extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* a
                                         int32_t rho_num, int32_t rho_den, int32_t mode, int32_t max_m,
                                         int64_t* out_scores, const int64_t* score_off_h, uint32_t* out_bits,
                                         const int64_t* bits_off_h, void* stream) {
-    if (mode == CP_SCORE_KVDEV) return CP_ERR_UNSUPPORTED;
+    if (mode == CP_SCORE_KVDEV) return CP_ERR_UNSUPPORTED;            // KV caches, not attention: cp_score_kv_deviation
     if (mode != CP_SCORE_INTER_INTRA) return CP_ERR_INVALID_ARG;
     if (num_spans < 0 || rho_den <= 0 || rho_num < 0 || rho_num > rho_den || max_m < 1 || max_m > 16384) return CP_ERR_INVALID_ARG;
     if (num_spans == 0) return CP_OK;
     if (!attn_h || !n_h || !heads_h || !l_h || !r_h || !out_scores || !score_off_h || !out_bits || !bits_off_h)
         return CP_ERR_INVALID_ARG;
-    for (int s = 0; s < num_spans; ++s) {
-        if (!attn_h[s] || n_h[s] < 1 || heads_h[s] < 1 || l_h[s] < 0 || r_h[s] < l_h[s] || r_h[s] >= n_h[s]) return CP_ERR_INVALID_ARG;
-        if (r_h[s] - l_h[s] + 1 > max_m) return CP_ERR_INVALID_ARG;
+    for (int s = 0; s < num_spans; ++s) {          // every check before any launch: no side effects on error
+        if (!attn_h[s] || n_h[s] < 1 || n_h[s] >= (1 << 24) || heads_h[s] < 1 || heads_h[s] > 255 || l_h[s] < 0 ||
+            r_h[s] < l_h[s] || r_h[s] >= n_h[s] || r_h[s] - l_h[s] + 1 > max_m) return CP_ERR_INVALID_ARG;
     }
+    for (int s0 = 0; s0 < num_spans; s0 += kSpansPerLaunch)
+        if (!launch_fits(s0, std::min(kSpansPerLaunch, num_spans - s0), l_h, r_h, score_off_h, bits_off_h))
+            return CP_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t smem = 9 * (size_t)max_m + 16;
-    static size_t attr = 0;
-    if (smem > attr) {
-        if (cudaFuncSetAttribute(k_score_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 * 1024)) != cudaSuccess)
-            return CP_ERR_CUDA;
-        attr = smem;
-    }
+    size_t smem;
+    if (topk_smem(max_m, &smem) != CP_OK) return CP_ERR_CUDA;
     std::vector<ScoreArgs> args(1);
     for (int s0 = 0; s0 < num_spans; s0 += kSpansPerLaunch) {
         ScoreArgs& a = args[0];
-        std::memset(&a, 0, sizeof(a));
-        a.nsp = std::min(kSpansPerLaunch, num_spans - s0);
-        const int64_t sbase = score_off_h[s0], bbase = bits_off_h[s0];
-        int64_t rows = 0;
-        for (int q = 0; q < a.nsp; ++q) {
-            const int s = s0 + q;
-            if (heads_h[s] > 255 || n_h[s] >= (1 << 24) || score_off_h[s] - sbase > INT32_MAX ||
-                bits_off_h[s] - bbase > INT32_MAX || rows > INT32_MAX - 65536) return CP_ERR_INVALID_ARG;
-            SpanDesc d;
-            d.A = attn_h[s]; d.row_begin = (int32_t)rows;
-            d.score_off = (int32_t)(score_off_h[s] - sbase); d.bits_off = (int32_t)(bits_off_h[s] - bbase);
-            d.n = n_h[s]; d.l = l_h[s]; d.r_heads = r_h[s] | (heads_h[s] << 24);
-            a.sp[q] = d;
-            rows += r_h[s] - l_h[s] + 1;
-        }
-        a.total_rows = (int32_t)rows; a.rho_num = rho_num; a.rho_den = rho_den;
-        a.scores = (long long*)out_scores + sbase; a.bits = out_bits + bbase;
-        const int grid = (int)std::min<int64_t>((rows + 7) / 8, 148 * 4);   // 4 CTAs/SM: best in score_rows_ab
+        fill_args(a, s0, std::min(kSpansPerLaunch, num_spans - s0), attn_h, n_h, heads_h, l_h, r_h, rho_num, rho_den,
+                  out_scores, score_off_h, out_bits, bits_off_h);
+        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, 148 * 4);   // 4 CTAs/SM: best in score_rows_ab
         k_score_rows<<<grid, kRowThreads, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_score_topk<<<a.nsp, kTopkThreads, smem, st>>>(a);
+        CP_COUNT_LAUNCH();
+        if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    }
+    return CP_OK;
+}
+
+extern "C" cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* req_h, const int32_t* l_h,
+                                           const int32_t* r_h, const void* reused_k, const void* reused_v,
+                                           const int32_t* reused_bt, int32_t reused_maxb, const void* fresh_k,
+                                           const void* fresh_v, const int32_t* fresh_bt, int32_t fresh_maxb,
+                                           int32_t H, int32_t d, int32_t dtype, int32_t rho_num, int32_t rho_den,
+                                           int32_t max_m, int64_t* out_scores, const int64_t* score_off_h,
+                                           uint32_t* out_bits, const int64_t* bits_off_h, void* stream) {
+    if (num_spans < 0 || rho_den <= 0 || rho_num < 0 || rho_num > rho_den || max_m < 1 || max_m > 16384) return CP_ERR_INVALID_ARG;
+    if (num_spans == 0) return CP_OK;
+    if (dtype != CP_BF16 && dtype != CP_FP32) return CP_ERR_INVALID_ARG;
+    const int64_t row_bytes = (int64_t)H * d * (dtype == CP_BF16 ? 2 : 4);
+    if (H < 1 || d < 1 || row_bytes % 16 != 0 || row_bytes / 16 > INT32_MAX) return CP_ERR_INVALID_ARG;
+    if (!req_h || !l_h || !r_h || !reused_k || !reused_v || !reused_bt || !fresh_k || !fresh_v || !fresh_bt ||
+        !out_scores || !score_off_h || !out_bits || !bits_off_h || reused_maxb < 1 || fresh_maxb < 1)
+        return CP_ERR_INVALID_ARG;
+    for (int s = 0; s < num_spans; ++s) {
+        if (req_h[s] < 0 || l_h[s] < 0 || r_h[s] < l_h[s] || r_h[s] - l_h[s] + 1 > max_m) return CP_ERR_INVALID_ARG;
+        if (r_h[s] / 16 >= std::min(reused_maxb, fresh_maxb)) return CP_ERR_INVALID_ARG;   // beyond the block tables
+    }
+    for (int s0 = 0; s0 < num_spans; s0 += kSpansPerLaunch)
+        if (!launch_fits(s0, std::min(kSpansPerLaunch, num_spans - s0), l_h, r_h, score_off_h, bits_off_h))
+            return CP_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t smem;
+    if (topk_smem(max_m, &smem) != CP_OK) return CP_ERR_CUDA;
+    KvDevArgs k;
+    k.rk = (const uint4*)reused_k; k.rv = (const uint4*)reused_v; k.rbt = reused_bt; k.rmaxb = reused_maxb;
+    k.fk = (const uint4*)fresh_k; k.fv = (const uint4*)fresh_v; k.fbt = fresh_bt; k.fmaxb = fresh_maxb;
+    k.vec_per_row = (int32_t)(row_bytes / 16);
+    std::vector<ScoreArgs> args(1);
+    for (int s0 = 0; s0 < num_spans; s0 += kSpansPerLaunch) {
+        ScoreArgs& a = args[0];
+        // SpanDesc.n carries the request index (no attention matrix in this mode)
+        fill_args(a, s0, std::min(kSpansPerLaunch, num_spans - s0), nullptr, req_h, nullptr, l_h, r_h, rho_num,
+                  rho_den, out_scores, score_off_h, out_bits, bits_off_h);
+        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, 148 * 4);
+        if (dtype == CP_BF16) k_kvdev_rows<true><<<grid, kRowThreads, 0, st>>>(a, k);
+        else k_kvdev_rows<false><<<grid, kRowThreads, 0, st>>>(a, k);
         CP_COUNT_LAUNCH();
         k_score_topk<<<a.nsp, kTopkThreads, smem, st>>>(a);
         CP_COUNT_LAUNCH();

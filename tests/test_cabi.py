@@ -53,6 +53,11 @@ def test_host_side_validation_without_gpu():
                                   None, None) == L.CP_ERR_UNSUPPORTED
     assert lib.cp_score_deviation(1, None, None, None, None, None, 5, 4, 0, 1, None, None, None, None,
                                   None) == L.CP_ERR_INVALID_ARG
+    # KV deviation (NEXT-4): bad rho, a row that is not a whole number of 16-B vectors
+    args = lambda rn, H, d: (1, None, None, None, None, None, None, 1, None, None, None, 1, H, d, L.CP_BF16, rn, 20,
+                             16, None, None, None, None, None)
+    assert lib.cp_score_kv_deviation(*args(21, 8, 128)) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_score_kv_deviation(*args(3, 1, 3)) == L.CP_ERR_INVALID_ARG
     assert lib.cp_index_insert(None, None, None, 0, None, None, None, None, None, 0, None, None,
                                None) == L.CP_ERR_INVALID_ARG
     assert lib.cp_status_string(-2) == b"CP_ERR_SENSITIVE_SPAN"

@@ -464,6 +464,40 @@ void orc_fifo_get(const orc_index* x, int32_t* out) {
     for (int32_t i = 0; i < x->fifo_count; ++i) out[i] = x->fifo[(x->fifo_head + i) % x->num_pages];
 }
 
+/*
+ * NEXT-2: zero-copy page linking.  The paper's retriever "link[s] reusable segments without touching
+ * the actual KV"; ordinary prefix reuse shares whole cached blocks.  A link is
+ * possible only where a request block IS a stored page: reading R#31 links request r's block b
+ * (positions [16b, 16b + 16)) to pool page pages(e)[j] iff one hit (e, dst, len, delta) of r has
+ *   delta == 0, dst % 16 == 0, dst <= 16b, 16b + 16 <= dst + len   (then j = (16b - dst) / 16),
+ * and all 16 positions have plan code 1 (reused, no recompute mark).  link[r * max_blocks + b] = page,
+ * every other entry of the first ceil(n_r / 16) blocks = -1 (entries beyond are left as they are).
+ * The hits are the ones orc_match returned for this index state.
+ */
+int32_t orc_link_blocks(const orc_index* x, int32_t num_reqs, const int64_t* offsets, int32_t num_hits,
+                        const int32_t* hit_req, const int32_t* hit_entry, const int32_t* hit_dst,
+                        const int32_t* hit_len, const int32_t* hit_delta, const uint8_t* plan,
+                        int32_t max_blocks, int32_t* link) {
+    for (int32_t r = 0; r < num_reqs; ++r) {
+        const int64_t nb = (offsets[r + 1] - offsets[r] + 15) / 16;
+        if (nb > max_blocks) return ORC_ERR_INVALID_ARG;
+        for (int64_t b = 0; b < nb; ++b) link[(int64_t)r * max_blocks + b] = -1;
+    }
+    for (int32_t h = 0; h < num_hits; ++h) {
+        if (hit_entry[h] < 0 || hit_entry[h] >= x->n_e) return ORC_ERR_INVALID_ARG;
+        if (hit_delta[h] != 0 || hit_dst[h] % 16 != 0) continue;
+        const orc_entry* e = &x->e[hit_entry[h]];
+        const int32_t r = hit_req[h];
+        for (int32_t b = hit_dst[h] / 16; 16 * b + 16 <= hit_dst[h] + hit_len[h]; ++b) {
+            int all_reused = 1;
+            for (int32_t q = 16 * b; q < 16 * b + 16; ++q)
+                if (plan[offsets[r] + q] != 1) all_reused = 0;
+            if (all_reused) link[(int64_t)r * max_blocks + b] = e->pages[(16 * b - hit_dst[h]) / 16];
+        }
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* RoPE re-rotation of one stored K row (R#11-13; the paper never mentions RoPE) */
 /* ------------------------------------------------------------------------- */

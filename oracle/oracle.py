@@ -61,6 +61,7 @@ def lib():
             "orc_rerotate_row": (None, [vp, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_score": (i32, [vp, i64, i32, i32, i32, i32, i32, vp, vp]),
             "orc_kv_deviation": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp, vp]),
+            "orc_link_blocks": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
             "orc_rerotate_rows": (None, [vp, i64, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_annotate": (i32, [vp, i64, i32, vp, i32, i32, vp, vp, vp]),
             "orc_sat": (None, [vp, i64, i32, vp]),
@@ -298,6 +299,20 @@ class OracleIndex:
             raise RuntimeError("oracle match: hit buffer overflow")
         return MatchResult(nh, rho[:R + 1], hr[:nh], he[:nh], hd[:nh], hl[:nh], hdl[:nh], plan[:T],
                            cov[:R], rec[:R], cand[:R])
+
+    def link_blocks(self, batch, res: "MatchResult", max_blocks: Optional[int] = None) -> np.ndarray:
+        """NEXT-2 (R#31): int32 [R, max_blocks] pool page linked to each request block, -1 if none."""
+        R = batch.num_reqs
+        off = _c(batch.offsets, np.int64)
+        mb = max_blocks if max_blocks is not None else int(max((off[r + 1] - off[r] + 15) // 16 for r in range(R)))
+        link = np.full((R, max(mb, 1)), -1, np.int32)
+        rc = lib().orc_link_blocks(self.h, R, _p(off), res.num_hits, _p(_c(res.hit_req, np.int32)),
+                                   _p(_c(res.hit_entry, np.int32)), _p(_c(res.hit_dst, np.int32)),
+                                   _p(_c(res.hit_len, np.int32)), _p(_c(res.hit_delta, np.int32)),
+                                   _p(_c(res.plan, np.uint8)), max(mb, 1), _p(link))
+        if rc != OK:
+            raise ValueError(f"orc_link_blocks rc={rc}")
+        return link[:, :mb]
 
     @property
     def num_ids(self) -> int:

@@ -56,7 +56,8 @@ enum { CP_MATCH_NO_TOUCH = 1,                     /* cp_match_spans flags       
        CP_MATCH_FIXED_CHUNK = 2,                  /* NEXT-3 baseline policies (R#28-29)          */
        CP_MATCH_PREFIX_ONLY = 4 };
 enum { CP_POLICY_FIXED_CHUNK = 1, CP_POLICY_PREFIX_ONLY = 2 };   /* cp_policy_spans              */
-enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2 }; /* cp_gather_rerotate flags (R#14)         */
+enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2,  /* cp_gather_rerotate flags (R#14)            */
+       CP_SKIP_LINKED = 4 };                       /* NEXT-2: leave linkable blocks unwritten (R#31) */
 enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
 enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
 enum { CP_PLAN_UNCOVERED = 0, CP_PLAN_REUSED = 1, CP_PLAN_RECOMPUTE = 2 };              /* plan codes     */
@@ -230,6 +231,24 @@ cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* span_req_h, co
                                 int32_t rho_num, int32_t rho_den, int32_t max_m, int64_t* out_scores,
                                 const int64_t* score_offsets_h, uint32_t* out_bits,
                                 const int64_t* bits_word_offsets_h, void* stream);
+
+/*
+ * NEXT-2: zero-copy page linking (the retriever "link[s] reusable segments without
+ * touching the actual KV"; prefix sharing shares whole cached blocks, L245-252).  A link is possible
+ * only where a request block IS a stored page (R#31): block b of request r (positions
+ * [16b, 16b+16)) links to pool page page_list[e][j] iff one hit (e, dst, len, delta) of r has
+ * delta == 0, dst % 16 == 0, dst <= 16b and 16b + 16 <= dst + len (j = (16b - dst)/16), and all 16
+ * positions have plan code CP_PLAN_REUSED.  Writes link_table[r * max_blocks_per_req + b] = that pool
+ * page, -1 for every other block b < ceil(n_r / 16) (entries beyond are not written).  The page's
+ * rows are the ones cp_gather_rerotate would copy (bit copies: delta 0), so an engine may point its
+ * block table at the pool page (layer l's rows at pool_k + ((l * P + page) * 16) * H * d) instead
+ * of copying; cp_gather_rerotate with CP_SKIP_LINKED then leaves those destination blocks unwritten.
+ * Lifetime: a linked page stays valid until the next cp_index_insert on this index (which may evict
+ * and recycle it).  `hits_h`: the cp_match_spans output for `readers_h` on this index state.
+ * Device error: max_blocks_per_req smaller than a request's block count -> CP_ERR_INVALID_ARG.
+ */
+cp_status cp_link_blocks(cp_index* idx, const cp_batch* readers_h, const cp_hits* hits_h,
+                         int32_t* link_table, int32_t max_blocks_per_req, void* stream);
 
 /*
  * NEXT-3: the spans a baseline policy stores for a writer batch (R#28-29), in

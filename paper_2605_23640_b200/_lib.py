@@ -17,7 +17,7 @@ CP_FP32, CP_BF16 = 0, 1
 CP_ROPE_NEOX, CP_ROPE_GPTJ = 0, 1
 CP_MATCH_NO_TOUCH, CP_MATCH_FIXED_CHUNK, CP_MATCH_PREFIX_ONLY = 1, 2, 4
 CP_POLICY_FIXED_CHUNK, CP_POLICY_PREFIX_ONLY = 1, 2
-CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED = 1, 2
+CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED = 1, 2, 4
 CP_SCORE_INTER_INTRA, CP_SCORE_KVDEV = 0, 1
 CP_STORED, CP_SUPERSEDED, CP_DUPLICATE, CP_DROPPED_CONTAINED = 0, 1, 2, 3
 CP_WS_COUNT = 4
@@ -71,6 +71,7 @@ EXPORTS = {
                                  vp, P_i64, vp, P_i64, vp]),
     "cp_score_kv_deviation": (i32, [i32, P_i32, P_i32, P_i32, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32,
                                     i32, i32, i32, vp, P_i64, vp, P_i64, vp]),
+    "cp_link_blocks": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), vp, i32, vp]),
     "cp_hash_prefix": (i32, [C.POINTER(CpBatch), u64, vp, vp]),
     "cp_policy_spans": (i32, [C.POINTER(CpBatch), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "cp_index_snapshot": (i32, [vp, C.POINTER(CpSnapshot), vp]),

@@ -205,11 +205,24 @@ class KVIndex:
         return hits
 
     def gather_rerotate(self, readers: DeviceBatch, hits: Hits, dst_kv: PagedKV,
-                        zero_recompute: bool = True, zero_uncovered: bool = False, stream=None):
-        flags = (L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0)
+                        zero_recompute: bool = True, zero_uncovered: bool = False, skip_linked: bool = False,
+                        stream=None):
+        flags = ((L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0) |
+                 (L.CP_SKIP_LINKED if skip_linked else 0))
         rb, hc, kv = readers.c(), hits.c(), dst_kv.c()
         L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
                 "cp_gather_rerotate")
+
+    def link_blocks(self, readers: DeviceBatch, hits: Hits, max_blocks: int, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+        """NEXT-2 (cp_link_blocks, R#31): int32 [R, max_blocks] pool page per linkable request block, -1
+        otherwise.  Valid until the next insert on this index."""
+        if out is None:
+            out = torch.full((readers.num_reqs, max_blocks), -1, dtype=torch.int32, device=hits.plan.device)
+        rb, hc = readers.c(), hits.c()
+        L.check(L.lib().cp_link_blocks(self.h, C.byref(rb), C.byref(hc), _ptr(out), int(max_blocks), _stream(stream)),
+                "cp_link_blocks")
+        return out
 
     def last_error(self, stream=None) -> int:
         return int(L.lib().cp_index_last_error(self.h, _stream(stream)))

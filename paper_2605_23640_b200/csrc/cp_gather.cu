@@ -20,6 +20,7 @@ namespace {
 
 constexpr int kRowsThreads = 256;
 constexpr int kPrepThreads = 512;
+constexpr int kCodeLinked = 3;       // row-table code of a token in a linked block (CP_SKIP_LINKED): no load, no store
 
 struct RowsArgs {
     DevHeader* hdr;
@@ -105,7 +106,17 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
         const int blk = a.block_tables[(int64_t)r * a.max_blocks + (pos >> 4)];
         const long long pool_row = ((long long)page * CP_BLOCK + (t & 15)) * rowE;
         const long long paged_row = ((long long)blk * CP_BLOCK + (pos & 15)) * rowE;
-        const long long code = a.dir == 0 ? (long long)a.plan[a.req_off[r] + pos] : (long long)CP_PLAN_REUSED;
+        long long code = a.dir == 0 ? (long long)a.plan[a.req_off[r] + pos] : (long long)CP_PLAN_REUSED;
+        if (a.dir == 0 && (a.flags & CP_SKIP_LINKED) && code == CP_PLAN_REUSED && a.l_delta[hh] == 0 && (k & 15) == 0) {
+            const int b0 = pos & ~15;                                       // >= k: k is page aligned
+            if (b0 + 16 <= k + a.l_len[hh]) {                               // the block lies inside the hit
+                const uint8_t* pl = a.plan + a.req_off[r] + b0;
+                bool all = true;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) all &= pl[i] == CP_PLAN_REUSED;
+                if (all) code = kCodeLinked;                                // R#31: this block IS pool page t>>4
+            }
+        }
         a.row_src[q] = a.dir == 0 ? pool_row : paged_row;
         a.row_dst[q] = (a.dir == 0 ? paged_row : pool_row) | (code << 62);
     }
@@ -212,8 +223,8 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
                     int lo = lo_t, hi = hi_t, i0 = i0_t;
                     if (!creg) task_geom(task - row * tpr, lo, hi, i0);
                     gl[u] = creg ? row : task;
-                    code[u] = s_code[g];
-                    if (!(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
+                    code[u] = s_code[g] == kCodeLinked ? -1 : s_code[g];
+                    if (code[u] >= 0 && !(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
                         const int l = l0 + ll;
                         const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
                         const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
@@ -377,7 +388,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst
                 const int code = mine ? (int)((unsigned long long)my_dst >> 62) : -1;
                 if (mine) { m.dst[g] = my_dst & ((1LL << 62) - 1); m.code[g] = code; }
                 if (lane == 0) { m.ntok = nt; m.hit = hh; m.layer = l; m.delta = delta; }
-                const bool load = mine && !(code == CP_PLAN_RECOMPUTE && zero_rec);
+                const bool load = mine && code != kCodeLinked && !(code == CP_PLAN_RECOMPUTE && zero_rec);
                 const unsigned nload = __popc(__ballot_sync(0xffffffffu, load));
                 __syncwarp();
                 if (lane == 0) mbar_expect_tx(&full[s], nload * 2u * (uint32_t)rowB);
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst
                     const float2* tab = a.hit_cs + (int64_t)hh * half;
                     for (int task = ct; task < nt * tpr; task += 32 * kTmaCons) {
                         const int g = task / tpr, j = task - g * tpr;
-                        if (m.code[g] == CP_PLAN_RECOMPUTE && zero_rec) continue;
+                        if ((m.code[g] == CP_PLAN_RECOMPUTE && zero_rec) || m.code[g] == kCodeLinked) continue;
                         int lo, hi, i0;
                         if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; hi = lo + half; i0 = sub * VEC; }
                         else { lo = j * 2 * VEC; hi = lo + VEC; i0 = (lo % a.d) / 2; }
@@ -441,6 +452,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst
                 cons_bar();
                 if (storer) {
                     for (int g = 0; g < nt; ++g) {
+                        if (m.code[g] == kCodeLinked) continue;
                         const bool z = m.code[g] == CP_PLAN_RECOMPUTE && zero_rec;
                         const int64_t d = m.dst[g];
                         bulk_s2g(dstK + d * sizeof(T), z ? zrow : st + (size_t)g * rowB, rowB);
@@ -639,6 +651,64 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }
     return CP_OK;
+}
+
+// ---- NEXT-2: zero-copy page linking (R#31) ---------------------------------------------------------
+namespace {
+// every block b < ceil(n_r / 16) of every request -> -1; a request with more blocks than the table: error
+__global__ void k_link_clear(DevHeader* hdr, const int64_t* req_off, int32_t R, int32_t* link, int32_t maxb) {
+    if (cp_err_set(hdr)) return;
+    const int64_t n = (int64_t)R * maxb;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(q / maxb), b = (int)(q % maxb);
+        const int64_t nb = (req_off[r + 1] - req_off[r] + 15) >> 4;
+        if (b == 0 && nb > maxb) cp_raise(hdr, CP_ERR_INVALID_ARG);
+        if (b < nb) link[q] = -1;
+    }
+}
+// one warp per hit: lanes take the hit's full pages; a page links iff delta == 0, dst % 16 == 0 and
+// its 16 plan codes are all CP_PLAN_REUSED
+__global__ void k_link_hits(DevHeader* hdr, const int32_t* count, int32_t cap, const int32_t* h_req,
+                            const int32_t* h_slot, const int32_t* h_dst, const int32_t* h_len, const int32_t* h_delta,
+                            const int64_t* req_off, const uint8_t* plan, const int32_t* slot_pages, int32_t MP,
+                            int32_t* link, int32_t maxb) {
+    if (cp_err_set(hdr)) return;
+    const int lane = threadIdx.x & 31;
+    const int nh = min(*count, cap);
+    for (int h = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); h < nh;
+         h += (int)(((int64_t)gridDim.x * blockDim.x) >> 5)) {
+        const int dst = h_dst[h], len = h_len[h];
+        if (h_delta[h] != 0 || (dst & 15) != 0) continue;
+        const int r = h_req[h], slot = h_slot[h];
+        const uint8_t* pl = plan + req_off[r];
+        for (int j = lane; 16 * j + 16 <= len; j += 32) {
+            const int b = (dst >> 4) + j;
+            bool all = true;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) all &= pl[16 * b + i] == CP_PLAN_REUSED;
+            if (all && b < maxb) link[(int64_t)r * maxb + b] = slot_pages[(int64_t)slot * MP + j];
+        }
+    }
+}
+}  // namespace
+
+extern "C" cp_status cp_link_blocks(cp_index* x, const cp_batch* b, const cp_hits* h, int32_t* link,
+                                    int32_t max_blocks, void* stream) {
+    if (!x || !b || !h || !link || max_blocks < 1 || !b->offsets) return CP_ERR_INVALID_ARG;
+    if (!h->num_hits || !h->hit_req || !h->hit_slot || !h->hit_dst || !h->hit_len || !h->hit_delta || !h->plan)
+        return CP_ERR_INVALID_ARG;
+    if (b->num_reqs < 0 || b->num_reqs > x->cfg.max_batch_reqs) return CP_ERR_INVALID_ARG;
+    if (b->num_reqs == 0) return CP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (int64_t)b->num_reqs * max_blocks;
+    k_link_clear<<<(int)std::min<int64_t>((n + 255) / 256, sm_count() * 4), 256, 0, st>>>(x->hdr, b->offsets, b->num_reqs,
+                                                                                          link, max_blocks);
+    CP_COUNT_LAUNCH();
+    k_link_hits<<<sm_count() * 2, 256, 0, st>>>(x->hdr, h->num_hits, h->max_hits, h->hit_req, h->hit_slot, h->hit_dst,
+                                              h->hit_len, h->hit_delta, b->offsets, h->plan, x->slot_pages, x->MP,
+                                              link, max_blocks);
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
 
 // ---- diagnostic: contiguous streaming copy with the gather's load/store instructions -----------------

@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--shard-world", type=int, default=0,
                     help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--rho", default="1/4", help="recompute fraction of N3 (paper: 25%%, P:L1032); 0/1 = no recompute "
+                    "marks (e.g. same-user sessions, P:L719-722)")
+    ap.add_argument("--link", action="store_true",
+                    help="NEXT-2: link page-aligned delta-0 recompute-free blocks (cp_link_blocks) instead of copying")
     return ap.parse_args()
 
 
@@ -240,6 +244,8 @@ def setup_ours(args, rank, world, device):
     S.scores = torch.zeros(max(so[-1], 1), dtype=torch.int64, device=device)
     S.bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=device)
     S.bits_off = torch.tensor(bo[:-1] or [0], dtype=torch.int64, device=device)
+    S.link = bool(getattr(args, "link", False))
+    S.link_tab = torch.full((rb.num_reqs, max(nb)), -1, dtype=torch.int32, device=device)
     S.side = torch.cuda.Stream(device=device)
     S.overlap = bool(getattr(args, "overlap", 0))
     S.ev_score_done = torch.cuda.Event()
@@ -249,12 +255,15 @@ def setup_ours(args, rank, world, device):
     return S
 
 
+RHO = (1, 4)
+
+
 def score_spans(b, device, torch, cp, attention_torch):
     attn = {r: attention_torch(int(b.lens[r]), b.segments[r], 0.01, seed=1000 + r, device=device)
             for r in sorted(set(int(x) for x in b.span_req))}
     args = ([attn[int(r)] for r in b.span_req], [int(b.lens[int(r)]) for r in b.span_req], [1] * len(b.span_req),
             [int(x) for x in b.span_begin], [int(x) + int(m) - 1 for x, m in zip(b.span_begin, b.span_len)])
-    sc, bits, so, bo = cp.score_deviation(*args, 1, 4)
+    sc, bits, so, bo = cp.score_deviation(*args, *RHO)
     return bits, torch.tensor(bo[:-1] or [0], dtype=torch.int64, device=device)
 
 
@@ -271,7 +280,7 @@ def run_step(S, torch, cp, world, events=None):
         with torch.cuda.stream(S.side if S.overlap else main):
             if ev: ev[5].record()
             if S.is_owner:                                                         # N3
-                cp.score_deviation(*S.score_args, 1, 4, out_scores=S.scores, out_bits=S.bits)
+                cp.score_deviation(*S.score_args, *RHO, out_scores=S.scores, out_bits=S.bits)
             if world > 1:
                 broadcast_update(S.bits, S.owner)                                  # C1: index update
             if ev: ev[6].record()
@@ -279,7 +288,9 @@ def run_step(S, torch, cp, world, events=None):
     if ev: ev[0].record()
     S.idx.match_spans(S.rdb, S.t, hits=S.hits)                                     # N1
     if ev: ev[1].record()
-    S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True)               # N2
+    if S.link:                                                                     # NEXT-2
+        S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
+    S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True, skip_linked=S.link)   # N2
     if ev: ev[2].record()
     main.wait_event(S.ev_score_done)
     if ev: ev[3].record()
@@ -322,9 +333,10 @@ def bench_ours(args):
     nh = int(S.hits.num_hits.item())
     S.covered = cov
     reused = cov - rec
+    linked = int((S.link_tab >= 0).sum().item()) * 16 if S.link else 0   # reused without a copy
     reused_bytes = reused * 2 * row * 2                 # K + V, read + write
     zero_bytes = rec * 2 * row                          # K + V zero placeholders (writes)
-    gather_bytes = reused_bytes + zero_bytes
+    gather_bytes = (reused - linked) * 2 * row * 2 + zero_bytes
     # ---- timed region
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
@@ -389,10 +401,11 @@ def bench_ours(args):
                        "index_entries": len(S.wb.span_len), "insert_batch_spans": len(S.ib.span_len),
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
-                       "shard_layers": L, "shard_heads": H, "rho": "1/4", "window_len": S.g.window_len,
+                       "shard_layers": L, "shard_heads": H, "rho": f"{RHO[0]}/{RHO[1]}", "link": bool(args.link), "window_len": S.g.window_len,
                        "l2": "inputs larger than L2 (pool + destination caches ~100 GB), no flush needed"},
             "matched_tokens_per_s": round(cov / (ms_step * 1e-3), 1),
             "covered_tokens": cov, "reused_tokens": reused, "recompute_tokens": rec, "hits": nh,
+            "linked_tokens": linked,
             "match_rate": round(cov / S.rb.total_tokens, 4),
             "value_frac_of_peak": round(value / (peak * world), 4),
             "breakdown_ms": {"match": round(float(phase[:, 0].mean()), 4), "gather": round(gather_ms, 4),
@@ -405,7 +418,7 @@ def bench_ours(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "traffic_source": "profiles/r01/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
                          "algorithmic_bytes_per_launch": gather_bytes,
-                         "bytes_rule": "reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + recompute tokens x 2 (K,V) x L*H*d*e (zero writes)"},
+                         "bytes_rule": "copied reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + recompute tokens x 2 (K,V) x L*H*d*e (zero writes); linked tokens (--link) move no bytes"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
             "setup": {"insert_writers_ms": round(S.setup_insert_ms, 2), "setup_s": round(S.setup_s, 1)},
         }
@@ -507,7 +520,7 @@ def oracle_sample(wl, wb, rb, seconds: float, max_reqs: int = 64, seed: int = 0)
         fl = []
         for s in range(len(one.span_len)):
             b0, m = int(one.span_begin[s]), int(one.span_len[s])
-            _, bits = O.score(attn, b0, b0 + m - 1, 1, 4)
+            _, bits = O.score(attn, b0, b0 + m - 1, *RHO)
             fl.append(O.bits_to_bool(bits, m))
         ww, oo = O.pack_bits(fl)
         idx.insert(one, ww, oo, t=t)
@@ -561,7 +574,9 @@ def bench_reference(args):
 
 
 def main():
+    global RHO
     args = parse()
+    RHO = tuple(int(x) for x in args.rho.split("/"))
     if args.impl == "reference":
         bench_reference(args)
     else:

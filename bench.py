@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
-    ap.add_argument("--overlap", type=int, default=1, help="1 (default): run N3 on a side stream concurrently with N1+N2; 0: serialize")
+    ap.add_argument("--overlap", type=int, default=2, choices=[0, 1, 2],
+                    help="2 (default): N3 beside the insert's read-only half after the gather; 1: N3 beside "
+                         "match + gather; 0: serialized (see run_step)")
     ap.add_argument("--shard-world", type=int, default=0,
                     help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
     ap.add_argument("--shard-rank", type=int, default=0)
@@ -247,8 +249,11 @@ def setup_ours(args, rank, world, device):
     S.link = bool(getattr(args, "link", False))
     S.link_tab = torch.full((rb.num_reqs, max(nb)), -1, dtype=torch.int32, device=device)
     S.side = torch.cuda.Stream(device=device)
-    S.overlap = bool(getattr(args, "overlap", 0))
+    S.overlap = int(getattr(args, "overlap", 2))
     S.ev_score_done = torch.cuda.Event()
+    S.ev_gather_done = torch.cuda.Event()
+    S.ins_out = (torch.full((max(len(ib.span_len), 1),), -1, dtype=torch.int32, device=device),
+                 torch.full((max(len(ib.span_len), 1),), -1, dtype=torch.int32, device=device))
     S.ev_insert_done = torch.cuda.Event()
     S.ev_insert_done.record()
     S.setup_s = time.time() - t0
@@ -268,23 +273,34 @@ def score_spans(b, device, torch, cp, attention_torch):
 
 
 def run_step(S, torch, cp, world, events=None):
-    """One pass of the hot path.  N3 runs on a side stream concurrently with N1 + N2 (it reads only
-    the final-layer attention); the insert waits for both.  The side stream first waits for the
-    previous step's insert (which read the bits N3 is about to overwrite)."""
+    """One pass of the hot path.  Scheduling (--overlap):
+      2 (default): match -> gather on the main stream; then N3 on a side stream concurrently with the
+         insert's read-only half (cp_index_insert_prepare: validation, hashing, dedup, containment
+         scan -- latency-bound kernels that leave HBM idle); the commit waits for both.  The gather
+         runs alone at full bandwidth.
+      1: N3 on a side stream concurrently with match + gather (it then competes with the gather).
+      0: everything serialized on one stream.
+    The side stream first waits for the previous step's insert (which read the bits N3 overwrites)."""
     from paper_2605_23640_b200.shard import broadcast_update
     S.t += 1
     ev = events
     main = torch.cuda.current_stream()
-    if S.is_owner or world > 1:
+    scores = S.is_owner or world > 1
+
+    def score():
+        if ev: ev[5].record()
+        if S.is_owner:                                                             # N3
+            cp.score_deviation(*S.score_args, *RHO, out_scores=S.scores, out_bits=S.bits)
+        if world > 1:
+            broadcast_update(S.bits, S.owner)                                      # C1: index update
+        if ev: ev[6].record()
+        S.ev_score_done.record()
+
+    ins = (S.ins_db, S.ins_kv, *S.spans, S.bits, S.bits_off, S.t)
+    if scores and S.overlap in (0, 1):
         S.side.wait_event(S.ev_insert_done)
-        with torch.cuda.stream(S.side if S.overlap else main):
-            if ev: ev[5].record()
-            if S.is_owner:                                                         # N3
-                cp.score_deviation(*S.score_args, *RHO, out_scores=S.scores, out_bits=S.bits)
-            if world > 1:
-                broadcast_update(S.bits, S.owner)                                  # C1: index update
-            if ev: ev[6].record()
-            S.ev_score_done.record()
+        with torch.cuda.stream(S.side if S.overlap == 1 else main):
+            score()
     if ev: ev[0].record()
     S.idx.match_spans(S.rdb, S.t, hits=S.hits)                                     # N1
     if ev: ev[1].record()
@@ -292,9 +308,22 @@ def run_step(S, torch, cp, world, events=None):
         S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
     S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True, skip_linked=S.link)   # N2
     if ev: ev[2].record()
-    main.wait_event(S.ev_score_done)
-    if ev: ev[3].record()
-    S.idx.insert(S.ins_db, S.ins_kv, *S.spans, S.bits, S.bits_off, S.t)            # N4
+    if S.overlap == 2:
+        if scores:
+            S.ev_gather_done.record()
+            S.side.wait_event(S.ev_gather_done)
+            with torch.cuda.stream(S.side):
+                score()
+        S.idx.insert(*ins, out=S.ins_out, phase="prepare")                         # N4, read-only half
+        if scores:
+            main.wait_event(S.ev_score_done)
+        if ev: ev[3].record()
+        S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
+    else:
+        if scores:
+            main.wait_event(S.ev_score_done)
+        if ev: ev[3].record()
+        S.idx.insert(*ins, out=S.ins_out)                                          # N4
     if ev: ev[4].record()
     S.ev_insert_done.record()
 
@@ -409,10 +438,12 @@ def bench_ours(args):
             "match_rate": round(cov / S.rb.total_tokens, 4),
             "value_frac_of_peak": round(value / (peak * world), 4),
             "breakdown_ms": {"match": round(float(phase[:, 0].mean()), 4), "gather": round(gather_ms, 4),
-                             "wait_score": round(float(phase[:, 2].mean()), 4), "insert": round(float(phase[:, 3].mean()), 4),
+                             ("insert_prepare_and_wait_score" if S.overlap == 2 else "wait_score"): round(float(phase[:, 2].mean()), 4),
+                             ("insert_commit" if S.overlap == 2 else "insert"): round(float(phase[:, 3].mean()), 4),
                              "score_side_stream": round(score_ms, 4),
-                             "note": ("score (N3) on a side stream concurrently with match + gather" if S.overlap
-                                      else "score (N3) serialized before match on the same stream")},
+                             "note": {2: "score (N3) on a side stream after the gather, beside the insert's read-only half",
+                                      1: "score (N3) on a side stream concurrently with match + gather",
+                                      0: "score (N3) serialized before match on the same stream"}[S.overlap]},
             "roofline": {"kernel": "k_rows (cp_gather_rerotate: prep + rows)", "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,

@@ -136,6 +136,29 @@ cp_status cp_index_insert(cp_index* idx, const cp_batch* writers_h, const cp_pag
                           const int64_t* bits_word_offsets, uint64_t logical_time,
                           int32_t* out_entry_id, int32_t* out_outcome, void* stream);
 
+/*
+ * The same insert in two stream-ordered halves, so that its read-only work overlaps other work on the
+ * index.  cp_index_insert_prepare runs validation, hashing, batch dedup and the containment scan /
+ * verification: it reads the index and writes only insert scratch, so it may run on another stream
+ * concurrently with cp_match_spans / cp_gather_rerotate / cp_link_blocks on this index (never with
+ * another insert).  cp_index_insert_commit, called with the SAME arguments, applies the spans (dedup
+ * outcomes, supersede, LRU eviction, table updates, copy-in): it must be stream-ordered after the
+ * prepare and after every gather that reads hits from before it.  recompute_bits are read only by the
+ * commit, so they may be produced concurrently with the prepare.  prepare + commit on one stream is
+ * exactly cp_index_insert.  A commit without a pending prepare, or a second prepare (or a plain insert)
+ * while one is pending, returns CP_ERR_INVALID_ARG with no side effects.
+ */
+cp_status cp_index_insert_prepare(cp_index* idx, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
+                                  int32_t num_spans, const int32_t* span_req, const int32_t* span_begin,
+                                  const int32_t* span_len, const uint32_t* recompute_bits,
+                                  const int64_t* bits_word_offsets, uint64_t logical_time,
+                                  int32_t* out_entry_id, int32_t* out_outcome, void* stream);
+cp_status cp_index_insert_commit(cp_index* idx, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
+                                 int32_t num_spans, const int32_t* span_req, const int32_t* span_begin,
+                                 const int32_t* span_len, const uint32_t* recompute_bits,
+                                 const int64_t* bits_word_offsets, uint64_t logical_time,
+                                 int32_t* out_entry_id, int32_t* out_outcome, void* stream);
+
 /* Outputs of cp_match_spans (all device buffers owned by the caller). */
 typedef struct {
     int32_t  max_hits;              /* capacity; must be >= sum_r floor(n_r / window_len)            */

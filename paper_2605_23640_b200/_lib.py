@@ -65,6 +65,10 @@ EXPORTS = {
     "cp_index_destroy": (i32, [vp]),
     "cp_index_insert": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,
                               vp, vp, vp]),
+    "cp_index_insert_prepare": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,
+                                      vp, vp, vp]),
+    "cp_index_insert_commit": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,
+                                     vp, vp, vp]),
     "cp_match_spans": (i32, [vp, C.POINTER(CpBatch), u64, i32, C.POINTER(CpHits), vp]),
     "cp_gather_rerotate": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), C.POINTER(CpPagedKV), i32, vp]),
     "cp_score_deviation": (i32, [i32, C.POINTER(vp), P_i32, P_i32, P_i32, P_i32, i32, i32, i32, i32,

@@ -179,15 +179,21 @@ class KVIndex:
         return k, v
 
     def insert(self, writers: DeviceBatch, writer_kv: PagedKV, span_req, span_begin, span_len,
-               recompute_bits=None, bits_word_offsets=None, t: int = 0, stream=None):
+               recompute_bits=None, bits_word_offsets=None, t: int = 0, stream=None, phase: Optional[str] = None,
+               out=None):
+        """cp_index_insert; phase "prepare" / "commit" calls the split halves (cp_index_insert_prepare /
+        _commit, same arguments, stream-ordered by the caller).  out: (out_id, out_oc) int32 buffers."""
         S = int(span_req.numel())
-        out_id = torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device)
-        out_oc = torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device)
+        if out is None:
+            out = (torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device),
+                   torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device))
+        out_id, out_oc = out
+        fn = {None: "cp_index_insert", "prepare": "cp_index_insert_prepare", "commit": "cp_index_insert_commit"}[phase]
         wb, kv = writers.c(), writer_kv.c()
-        rc = L.lib().cp_index_insert(self.h, C.byref(wb), C.byref(kv), S, _ptr(span_req), _ptr(span_begin),
-                                     _ptr(span_len), _ptr(recompute_bits), _ptr(bits_word_offsets), int(t),
-                                     _ptr(out_id), _ptr(out_oc), _stream(stream))
-        L.check(rc, "cp_index_insert")
+        rc = getattr(L.lib(), fn)(self.h, C.byref(wb), C.byref(kv), S, _ptr(span_req), _ptr(span_begin),
+                                  _ptr(span_len), _ptr(recompute_bits), _ptr(bits_word_offsets), int(t),
+                                  _ptr(out_id), _ptr(out_oc), _stream(stream))
+        L.check(rc, fn)
         return out_id[:S], out_oc[:S]
 
     def match_spans(self, readers: DeviceBatch, t: int = 0, no_touch: bool = False, use_mask: bool = True,

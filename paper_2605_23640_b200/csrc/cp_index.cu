@@ -1390,10 +1390,15 @@ cp_status cp_hash_prefix(const cp_batch* b, uint64_t hash_seed, uint64_t* out, v
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
 
-cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
-                          const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
-                          const uint32_t* bits, const int64_t* bits_off, uint64_t t,
-                          int32_t* out_id, int32_t* out_oc, void* stream) {
+}  // extern "C"
+
+namespace {
+
+// host-side checks + the kernel argument block shared by the insert phases (no device work)
+cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
+                   const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
+                   const uint32_t* bits, const int64_t* bits_off, uint64_t t, int32_t* out_id, int32_t* out_oc,
+                   InsArgs& a) {
     if (!x || !wb || !kv) return CP_ERR_INVALID_ARG;
     if (num_spans < 0 || num_spans > x->MS) return CP_ERR_INVALID_ARG;
     if (num_spans == 0) return CP_OK;
@@ -1402,8 +1407,6 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     if (wb->num_reqs < 1 || wb->num_reqs > x->cfg.max_batch_reqs || wb->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
     if ((bits == nullptr) != (bits_off == nullptr)) return CP_ERR_INVALID_ARG;
     if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables) return CP_ERR_INVALID_ARG;
-    cudaStream_t st = (cudaStream_t)stream;
-    InsArgs a;
     std::memset(&a, 0, sizeof(a));
     a.hdr = x->hdr; a.tokens = wb->tokens; a.offsets = wb->offsets; a.mask = wb->mask; a.num_reqs = wb->num_reqs;
     a.S = num_spans; a.span_req = span_req; a.span_begin = span_begin; a.span_len = span_len;
@@ -1421,7 +1424,21 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
+    // shared memory of the commit: flags + per-span arrays, then the LRU candidate list (4096 halved to
+    // fit), then as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)
+    int candK = 4096;
+    while (candK >= 256 && CommitSmem(x->S, num_spans, candK, 0).fixed > 180 * 1024) candK >>= 1;
+    if (candK < 256) candK = 0;
+    a.candK = candK;
+    const size_t fixed = CommitSmem(x->S, num_spans, candK, 0).fixed;
+    a.rec_cap = fixed >= 180 * 1024 ? 0 : (int)std::min<size_t>(kCommitRecCap, (180 * 1024 - fixed) / 8);
+    if (CommitSmem(x->S, num_spans, candK, a.rec_cap).total > 180 * 1024) return CP_ERR_UNSUPPORTED;   // + ~35 KB static
+    return CP_OK;
+}
 
+// read-only phases: validation, hashing, batch dedup, containment scan + verification (scratch only)
+cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
+    const int num_spans = a.S;
     const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
     k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -1435,16 +1452,13 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
-    // shared memory: flags + per-span arrays, then the LRU candidate list (4096 halved to fit), then
-    // as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)
-    int candK = 4096;
-    while (candK >= 256 && CommitSmem(x->S, num_spans, candK, 0).fixed > 180 * 1024) candK >>= 1;
-    if (candK < 256) candK = 0;
-    a.candK = candK;
-    const size_t fixed = CommitSmem(x->S, num_spans, candK, 0).fixed;
-    a.rec_cap = fixed >= 180 * 1024 ? 0 : (int)std::min<size_t>(kCommitRecCap, (180 * 1024 - fixed) / 8);
-    const size_t csm = CommitSmem(x->S, num_spans, candK, a.rec_cap).total;
-    if (csm > 180 * 1024) return CP_ERR_UNSUPPORTED;     // + ~35 KB static shared memory <= 227 KB
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}
+
+// mutating phases: sequential apply, table updates, copy-in of the writer KV
+cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp_paged_kv* kv, cudaStream_t st) {
+    const int num_spans = a.S;
+    const size_t csm = CommitSmem(x->S, num_spans, a.candK, a.rec_cap).total;
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -1456,6 +1470,48 @@ cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv
     // copy the writer KV rows of the published entries into their pool pages
     return cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
                           x->MS, wb->offsets, nullptr, kv, 0, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+cp_status cp_index_insert(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
+                          const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
+                          const uint32_t* bits, const int64_t* bits_off, uint64_t t,
+                          int32_t* out_id, int32_t* out_oc, void* stream) {
+    InsArgs a;
+    const cp_status s = ins_args(x, wb, kv, num_spans, span_req, span_begin, span_len, bits, bits_off, t, out_id, out_oc, a);
+    if (s != CP_OK || num_spans == 0) return s;
+    if (x->insert_prepared) return CP_ERR_INVALID_ARG;          // a split insert is in flight
+    const cudaStream_t st = (cudaStream_t)stream;
+    const cp_status p = ins_prepare(x, a, st);
+    return p != CP_OK ? p : ins_commit(x, a, wb, kv, st);
+}
+
+cp_status cp_index_insert_prepare(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
+                                  const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
+                                  const uint32_t* bits, const int64_t* bits_off, uint64_t t,
+                                  int32_t* out_id, int32_t* out_oc, void* stream) {
+    InsArgs a;
+    const cp_status s = ins_args(x, wb, kv, num_spans, span_req, span_begin, span_len, bits, bits_off, t, out_id, out_oc, a);
+    if (s != CP_OK || num_spans == 0) return s;
+    if (x->insert_prepared) return CP_ERR_INVALID_ARG;
+    const cp_status p = ins_prepare(x, a, (cudaStream_t)stream);
+    if (p == CP_OK) x->insert_prepared = 1;
+    return p;
+}
+
+cp_status cp_index_insert_commit(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32_t num_spans,
+                                 const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
+                                 const uint32_t* bits, const int64_t* bits_off, uint64_t t,
+                                 int32_t* out_id, int32_t* out_oc, void* stream) {
+    InsArgs a;
+    const cp_status s = ins_args(x, wb, kv, num_spans, span_req, span_begin, span_len, bits, bits_off, t, out_id, out_oc, a);
+    if (s != CP_OK || num_spans == 0) return s;
+    if (!x->insert_prepared) return CP_ERR_INVALID_ARG;          // commit without prepare
+    x->insert_prepared = 0;
+    return ins_commit(x, a, wb, kv, (cudaStream_t)stream);
 }
 
 }  // extern "C"

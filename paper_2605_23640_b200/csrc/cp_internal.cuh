@@ -71,6 +71,7 @@ struct cp_index {
     cp_config cfg;
     int64_t P;           // physical pages
     int32_t MP;          // max pages per entry
+    int insert_prepared = 0;   // cp_index_insert_prepare issued, commit pending (host-side guard)
     int32_t S;           // slots
     int64_t T;           // prefix-table entries (pow2)
     int32_t logT;

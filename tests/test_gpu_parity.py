@@ -364,3 +364,80 @@ def test_churn_config5_full_batches_invariants():
         for j in range(len(strs)):
             if i != j:
                 assert strs[i] not in strs[j]
+
+
+@pytest.mark.parametrize("cfg", [1, 5])
+def test_split_insert_prepare_concurrent_with_match_and_gather(cfg):
+    """cp_index_insert_prepare on a side stream while cp_match_spans + cp_gather_rerotate of the same
+    index run on the main stream, then cp_index_insert_commit: outcomes, entry ids, the whole index
+    and the hits must equal the oracle's sequential match-then-insert (the prepare reads the index and
+    writes only insert scratch).  Config 5 shape with a small budget: evictions and supersedes."""
+    if cfg == 1:
+        wl = make_workload(1)
+    else:
+        from synth.gen import churn_workload
+        wl = churn_workload(batches=5, per_batch=24, corpus=60, capacity_tokens=9000,
+                            geometry=Geometry(2, 2, 64, "bf16", 500000.0))
+    case = Case(wl, seed=11)
+    rep = ParityReport()
+    rng = np.random.default_rng(cfg)
+    first_wb, _ = wl.rounds[0]
+    case.insert(first_wb, rep)
+    assert rep.ok, rep.notes
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    for k, (wb, rb) in enumerate(wl.rounds[1:]):
+        flags = [rng.random(int(m)) < 0.25 for m in wb.span_len]
+        words, offs = O.pack_bits(flags)
+        kv = case.writer_kv(wb)
+        db = case._dev_batch(wb)
+        sp = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+        spans = (sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len))
+        dwords = torch.from_numpy(words.view(np.int32).copy() if len(words) else np.zeros(1, np.int32)).cuda()
+        doffs = torch.from_numpy(offs.astype(np.int64)).cuda()
+        t_match, t_ins = case.t + 1, case.t + 2
+        case.t += 2
+        rdb = case._dev_batch(rb)
+        dst = case.dst_kv(rb)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            case.dev.insert(db, kv, *spans, dwords, doffs, t_ins, phase="prepare")
+        hits = case.dev.match_spans(rdb, t_match)
+        case.dev.gather_rerotate(rdb, hits, dst)
+        main.wait_stream(side)
+        ids, oc = case.dev.insert(db, kv, *spans, dwords, doffs, t_ins, phase="commit")
+        assert case.dev.last_error() == 0
+        res = case.orc.match(rb, t_match)
+        rc, oids, ooc = case.orc.insert(wb, words, offs, t_ins)
+        assert rc == 0
+        h = hits.to_host()
+        assert h["num_hits"] == res.num_hits
+        for key in ("hit_entry", "hit_dst", "hit_len", "hit_delta"):
+            assert np.array_equal(h[key], getattr(res, key)), key
+        assert np.array_equal(oc.cpu().numpy(), ooc) and np.array_equal(ids.cpu().numpy(), oids)
+        case.compare_index(rep, f"split insert round {k}")
+        assert rep.ok, rep.notes
+
+
+def test_split_insert_misuse_is_rejected_without_side_effects():
+    import paper_2605_23640_b200 as cp
+    case = Case(make_workload(1))
+    wb, _ = case.wl.rounds[0]
+    kv = case.writer_kv(wb)
+    db = case._dev_batch(wb)
+    sp = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+    spans = (sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len))
+    before = case.dev.snapshot()
+    with pytest.raises(cp._lib.CacheHitError):
+        case.dev.insert(db, kv, *spans, t=1, phase="commit")             # commit without prepare
+    case.dev.insert(db, kv, *spans, t=1, phase="prepare")
+    with pytest.raises(cp._lib.CacheHitError):
+        case.dev.insert(db, kv, *spans, t=1, phase="prepare")            # second prepare while pending
+    with pytest.raises(cp._lib.CacheHitError):
+        case.dev.insert(db, kv, *spans, t=1)                             # plain insert while pending
+    after = case.dev.snapshot()
+    assert after["next_id"] == before["next_id"] and after["num_live"] == before["num_live"]
+    case.dev.insert(db, kv, *spans, t=1, phase="commit")
+    assert case.dev.snapshot()["num_live"] > 0

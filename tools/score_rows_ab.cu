@@ -65,6 +65,50 @@ __global__ void __launch_bounds__(256) k_rows(const float* A, int n, int l, int 
     }
 }
 
+// double-buffered: batch k+1 is in flight while batch k is summed
+template <int B>
+__global__ void __launch_bounds__(256) k_rows_db(const float* A, int n, int l, int reqs, long long* out) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    const int rows_per = n - l, total = rows_per * reqs;
+    for (int gr = warp; gr < total; gr += nwarps) {
+        const int req = gr / rows_per, i = l + gr % rows_per;
+        const float* p = A + ((int64_t)req * n + i) * n;
+        const int cnt = i + 1, nvec = cnt >> 2;
+        const float4* v4 = reinterpret_cast<const float4*>(p);
+        long long all = 0, inter = 0;
+        float4 cur[B], nxt[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) { const int q = u * 32 + lane; cur[u] = q < nvec ? ld_nc4(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f); }
+        for (int q0 = 0; q0 < nvec; q0 += 32 * B) {
+            const bool more = q0 + 32 * B < nvec;
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < B; ++u) { const int q = q0 + 32 * B + u * 32 + lane; nxt[u] = q < nvec ? ld_nc4(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f); }
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int j0 = 4 * (q0 + u * 32 + lane);
+                const long long x0 = q40_cvt(cur[u].x), x1 = q40_cvt(cur[u].y), x2 = q40_cvt(cur[u].z), x3 = q40_cvt(cur[u].w);
+                const long long s = (x0 + x1) + (x2 + x3);
+                all += s;
+                if (j0 + 3 < l) inter += s;
+                else if (j0 < l) inter += x0 + (j0 + 1 < l ? x1 : 0) + (j0 + 2 < l ? x2 : 0);
+            }
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < B; ++u) cur[u] = nxt[u];
+            }
+        }
+        const int t = 4 * nvec + lane;
+        if (t < cnt) { const long long x = q40_cvt(p[t]); all += x; if (t < l) inter += x; }
+        long long acc = 2 * inter - all;
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[gr] = acc;
+    }
+}
+
 __global__ void fill(float* A, int64_t N) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
         uint32_t h = (uint32_t)(k * 2654435761u) ^ (uint32_t)(k >> 17);
@@ -73,14 +117,15 @@ __global__ void fill(float* A, int64_t N) {
     }
 }
 
-template <int B, bool INT>
+template <int B, bool INT, bool DB = false>
 void run(const char* name, const float* A, int n, int l, int reqs, long long* out, long long* ref, int blocks_per_sm) {
     const int grid = 148 * blocks_per_sm;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int w = 0; w < 3; ++w) k_rows<B, INT><<<grid, 256>>>(A, n, l, reqs, out);
+    auto go = [&]() { if (DB) k_rows_db<B><<<grid, 256>>>(A, n, l, reqs, out); else k_rows<B, INT><<<grid, 256>>>(A, n, l, reqs, out); };
+    for (int w = 0; w < 3; ++w) go();
     cudaEventRecord(e0);
     const int it = 10;
-    for (int w = 0; w < it; ++w) k_rows<B, INT><<<grid, 256>>>(A, n, l, reqs, out);
+    for (int w = 0; w < it; ++w) go();
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= it;
     double bytes = 0;
@@ -105,12 +150,10 @@ int main() {
     fill<<<148 * 8, 256>>>(A, N);
     k_rows<8, false><<<148 * 8, 256>>>(A, n, l, reqs, ref);
     cudaDeviceSynchronize();
-    for (int bps : {4, 6, 8}) {
+    for (int bps : {2, 3, 4, 6, 8}) {
         run<4, false>("cvt B4", A, n, l, reqs, out, ref, bps);
-        run<8, false>("cvt B8", A, n, l, reqs, out, ref, bps);
-        run<4, true>("int B4", A, n, l, reqs, out, ref, bps);
-        run<8, true>("int B8", A, n, l, reqs, out, ref, bps);
-        run<12, true>("int B12", A, n, l, reqs, out, ref, bps);
+        run<2, false, true>("cvt B2 dbuf", A, n, l, reqs, out, ref, bps);
+        run<4, false, true>("cvt B4 dbuf", A, n, l, reqs, out, ref, bps);
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

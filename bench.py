@@ -35,7 +35,7 @@ METRIC = "reused KV GB/s and % of HBM peak (gather+re-rotate); matched tokens/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4])
@@ -89,7 +89,7 @@ class Clocks:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -352,9 +352,12 @@ def bench_ours(args):
     e = 2 if S.g.dtype == "bf16" else 4
     row = L * H * d * e                                  # one token's K (or V) rows over the shard's layers
     # warm-up (also establishes the per-step algorithmic bytes: the index is steady after warm-up)
+    torch.cuda.synchronize()
+    tw = time.perf_counter()
     for _ in range(args.warmup):
         run_step(S, torch, cp, world)
     torch.cuda.synchronize()
+    S.warm_s_per_step = (time.perf_counter() - tw) / max(1, args.warmup)
     if S.idx.last_error():
         raise RuntimeError("device error during warm-up")
     cov = int(S.hits.req_covered.sum().item())
@@ -370,12 +373,23 @@ def bench_ours(args):
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
     clocks = Clocks(local)
-    l0 = cp.kernel_launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # keep the GPU under load for ~0.3 s while the sampler starts: untimed steps, the same count on
+    # every rank (each step may hold a collective)
+    n_busy = torch.tensor([max(3, int(0.3 / max(S.warm_s_per_step, 1e-4)) + 1)], dtype=torch.int64)
+    if world > 1:
+        nb_dev = n_busy.to(device) if backend == "nccl" else n_busy
+        dist.all_reduce(nb_dev, op=dist.ReduceOp.MAX)
+        n_busy = nb_dev.cpu()
     clocks.start()
-    time.sleep(0.3)
+    for _ in range(int(n_busy.item())):
+        run_step(S, torch, cp, world)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = cp.kernel_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")
     start.record()

@@ -1,0 +1,27 @@
+"""The bench's N > 1 path end to end: two ranks (torchrun, gloo, both on cuda:0 -- this box has one
+GPU) run the layer-sharded step with the N3 owner's bit broadcast, barriers, max-over-ranks timing and
+the e2e leg; rank 0 prints one JSON line.  Catches collective-count mismatches between ranks."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("overlap", [2, 0])
+def test_two_rank_bench_runs_and_reports(overlap):
+    env = dict(os.environ, BENCH_DEVICE0="1", BENCH_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29611 + overlap), "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--scale", "0.1", "--no-cpu-baseline", "--overlap", str(overlap)]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == "layer-sharded x2" and d["gpu_launches"] > 0

@@ -349,6 +349,10 @@ uint64_t cp_index_hash_base(const cp_index* idx);
 /* Select the gather kernel's (unroll, min-blocks) variant 0-3 (A/B measurement; default 0). */
 cp_status cp_set_gather_variant(int32_t variant);
 
+/* Select the N3 row kernel's CTAs per SM (0: 4, 1: 5, 2: 6, 3: 8; register-capped to fit; A/B
+ * measurement; default 0, or the CP_SCORE_VARIANT environment variable). */
+cp_status cp_set_score_variant(int32_t variant);
+
 /* Diagnostic: contiguous copy of `bytes` (multiple of 16) with the gather's 128-bit streaming load /
  * store instructions, ctas_per_sm x 256-thread CTAs per SM (roofline reference for the gather). */
 cp_status cp_copy_diag(const void* src, void* dst, int64_t bytes, int32_t ctas_per_sm, void* stream);

@@ -83,6 +83,7 @@ EXPORTS = {
     "cp_index_hash_base": (u64, [vp]),
     "cp_kernel_launch_count": (u64, []),
     "cp_set_gather_variant": (i32, [i32]),
+    "cp_set_score_variant": (i32, [i32]),
     "cp_copy_diag": (i32, [vp, vp, i64, i32, vp]),
     "cp_annotate_workspace": (C.c_size_t, [i32, P_i32, i32]),
     "cp_annotate_spans": (i32, [i32, C.POINTER(vp), P_i32, P_i32, C.POINTER(vp), i32, i32, vp, C.c_size_t,

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -90,8 +91,10 @@ __device__ __forceinline__ long long warp_row_score(const float* p, int cnt, int
     return 2 * inter - all;
 }
 
-// One warp per span row i (all heads), a single pass over A_h[i][0..i].
-__global__ void __launch_bounds__(kRowThreads) k_score_rows(const ScoreArgs a) {
+// One warp per span row i (all heads), a single pass over A_h[i][0..i].  MINB = CTAs per SM the
+// register budget must allow (variants for A/B measurement: cp_set_score_variant).
+template <int MINB>
+__global__ void __launch_bounds__(kRowThreads, MINB) k_score_rows(const ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
@@ -286,6 +289,33 @@ __global__ void __launch_bounds__(kRowThreads) k_kvdev_rows(const ScoreArgs a, c
 
 namespace {
 
+int sm_count_score() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+int g_score_variant = -1;
+void launch_score_rows(const ScoreArgs& a, cudaStream_t st) {
+    if (g_score_variant < 0) { const char* e = getenv("CP_SCORE_VARIANT"); g_score_variant = e ? atoi(e) : 0; }
+    const int sms = sm_count_score();
+    auto go = [&](auto kern, int per_sm) {
+        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, (int64_t)sms * per_sm);
+        kern<<<grid, kRowThreads, 0, st>>>(a);
+    };
+    switch (g_score_variant) {
+        case 1: go(k_score_rows<5>, 5); break;
+        case 2: go(k_score_rows<6>, 6); break;
+        case 3: go(k_score_rows<8>, 8); break;
+        default: go(k_score_rows<4>, 4); break;           // 4 CTAs/SM: best in tools/score_rows_ab.cu
+    }
+}
+
 cp_status topk_smem(int32_t max_m, size_t* smem) {
     *smem = 9 * (size_t)max_m + 16;
     static size_t attr = 0;
@@ -358,8 +388,7 @@ extern "C" cp_status cp_score_deviation(int32_t num_spans, const float* const* a
         ScoreArgs& a = args[0];
         fill_args(a, s0, std::min(kSpansPerLaunch, num_spans - s0), attn_h, n_h, heads_h, l_h, r_h, rho_num, rho_den,
                   out_scores, score_off_h, out_bits, bits_off_h);
-        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, 148 * 4);   // 4 CTAs/SM: best in score_rows_ab
-        k_score_rows<<<grid, kRowThreads, 0, st>>>(a);
+        launch_score_rows(a, st);
         CP_COUNT_LAUNCH();
         k_score_topk<<<a.nsp, kTopkThreads, smem, st>>>(a);
         CP_COUNT_LAUNCH();
@@ -403,7 +432,7 @@ extern "C" cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* req
         // SpanDesc.n carries the request index (no attention matrix in this mode)
         fill_args(a, s0, std::min(kSpansPerLaunch, num_spans - s0), nullptr, req_h, nullptr, l_h, r_h, rho_num,
                   rho_den, out_scores, score_off_h, out_bits, bits_off_h);
-        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, 148 * 4);
+        const int grid = (int)std::min<int64_t>((a.total_rows + 7) / 8, sm_count_score() * 4);
         if (dtype == CP_BF16) k_kvdev_rows<true><<<grid, kRowThreads, 0, st>>>(a, k);
         else k_kvdev_rows<false><<<grid, kRowThreads, 0, st>>>(a, k);
         CP_COUNT_LAUNCH();
@@ -411,5 +440,11 @@ extern "C" cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* req
         CP_COUNT_LAUNCH();
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }
+    return CP_OK;
+}
+
+extern "C" cp_status cp_set_score_variant(int32_t v) {
+    if (v < 0 || v > 3) return CP_ERR_INVALID_ARG;
+    g_score_variant = v;
     return CP_OK;
 }

@@ -232,6 +232,14 @@ def test_score_multihead_long_misaligned_rows():
                        (4099, 1, 4097, 4098)]:
         A = np.tril(rng.uniform(0, 1.5, (h, n, n))).astype(np.float32)    # row sums != 1
         mats.append(torch.from_numpy(A).cuda()); ns.append(n); hs.append(h); ls.append(l); rs.append(r)
+    for off in (1, 2, 3):                       # base pointer not 16-B aligned (a view into a larger buffer)
+        n, l = 777 + off, 100 + off
+        A = np.tril(rng.uniform(0, 1, (n, n))).astype(np.float32)
+        flat = torch.zeros(n * n + 4, dtype=torch.float32, device="cuda")
+        view = flat[off:off + n * n].view(n, n)
+        view.copy_(torch.from_numpy(A))
+        assert view.data_ptr() % 16 == 4 * off
+        mats.append(view); ns.append(n); hs.append(1); ls.append(l); rs.append(n - 1)
     sc, bits, so, bo = cp.score_deviation(mats, ns, hs, ls, rs, 1, 4)
     sc, bits = sc.cpu().numpy(), bits.cpu().numpy().view(np.uint32)
     for q in range(len(ns)):

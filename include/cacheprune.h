@@ -346,7 +346,9 @@ cp_status cp_index_last_error(cp_index* idx, void* stream);
 /* Hash base B of an index (diagnostic). */
 uint64_t cp_index_hash_base(const cp_index* idx);
 
-/* Select the gather kernel's (unroll, min-blocks) variant 0-3 (A/B measurement; default 0). */
+/* Select the gather kernel variant (A/B measurement; default 0 = unroll 2, 3 CTAs/SM, dynamic item
+ * schedule; 1/2/3/5 static round-robin (unroll, CTAs/SM) = (2,4)/(4,2)/(3,2)/(8,1); 4 TMA bulk copy;
+ * 6/7/8/9 dynamic (3,2)/(2,4)/(4,2)/(8,1)).  Also the CP_GATHER_VARIANT environment variable. */
 cp_status cp_set_gather_variant(int32_t variant);
 
 /* Select the N3 row kernel's CTAs per SM (0: 4, 1: 5, 2: 6, 3: 8; register-capped to fit; A/B

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep(RowsArgs a) {
         if (tid == 0) s_carry += s_scan[kPrepThreads / 32];
         __syncthreads();
     }
-    if (tid == 0) a.hdr->n_chunks = s_carry;
+    if (tid == 0) { a.hdr->n_chunks = s_carry; a.hdr->gather_next = 0; }
 }
 
 // k_rows_prep2 (all blocks): per-hit cos/sin (angles in fp64, R#13) and the per-token row table
@@ -157,12 +157,13 @@ __device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16) {
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <typename T, bool GPTJ, bool CREG, int UNROLL, int MINB, bool ML>
+template <typename T, bool GPTJ, bool CREG, int UNROLL, int MINB, bool ML, bool DYN>
 __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     constexpr int VEC = Vec<T>::N;
     __shared__ int64_t s_src[CP_GATHER_CHUNK], s_dst[CP_GATHER_CHUNK];
     __shared__ int s_code[CP_GATHER_CHUNK];
     __shared__ float2 s_cs[256];
+    __shared__ long long s_item;
     if (cp_err_set(a.hdr)) return;
     const int nchunks = a.hdr->n_chunks;
     const int ngroups = ML ? (a.L + a.LG - 1) / a.LG : a.L;
@@ -182,7 +183,15 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     };
     int lo_t = 0, hi_t = 0, i0_t = 0;
     task_geom(tid % tpr, lo_t, hi_t, i0_t);
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    // DYN: items are taken from a device counter (one atomic per item and CTA), so CTAs that drew
+    // short items (hit tails, zero placeholders) take more -- no static round-robin tail imbalance
+    int64_t item = blockIdx.x;
+    if (DYN) {
+        if (tid == 0) s_item = (long long)atomicAdd(&a.hdr->gather_next, 1ULL);
+        __syncthreads();
+        item = s_item;
+    }
+    while (item < items) {
         const int c = (int)(item / ngroups), lg = (int)(item % ngroups);
         const int l0 = lg * a.LG;
         const int nl = ML ? min(a.LG, a.L - l0) : 1;        // compile-time 1 on the single-layer path
@@ -274,6 +283,13 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
                 st_stream(dk + lo, klo[u]); st_stream(dk + hi, khi[u]);
                 st_stream(dv + lo, vlo[u]); st_stream(dv + hi, vhi[u]);
             }
+        }
+        if (DYN) {
+            if (tid == 0) s_item = (long long)atomicAdd(&a.hdr->gather_next, 1ULL);
+            __syncthreads();
+            item = s_item;
+        } else {
+            item += gridDim.x;
         }
         __syncthreads();
     }
@@ -533,11 +549,19 @@ cp_status launch_rows_c(const RowsArgs& a, int variant, cudaStream_t st) {
         return CP_OK;
     };
     switch (variant) {
-        case 1: return a.LG > 1 ? go(k_rows<T, G, CR, 2, 4, true>) : go(k_rows<T, G, CR, 2, 4, false>);
-        case 2: return a.LG > 1 ? go(k_rows<T, G, CR, 4, 2, true>) : go(k_rows<T, G, CR, 4, 2, false>);
-        case 3: return a.LG > 1 ? go(k_rows<T, G, CR, 3, 2, true>) : go(k_rows<T, G, CR, 3, 2, false>);
-        // measured best on B200 (tools/gather_ab.py, profiles/r01)
-        default: return a.LG > 1 ? go(k_rows<T, G, CR, 8, 1, true>) : go(k_rows<T, G, CR, 8, 1, false>);
+        // static round-robin item schedules (round-1 A/B)
+        case 1: return a.LG > 1 ? go(k_rows<T, G, CR, 2, 4, true, false>) : go(k_rows<T, G, CR, 2, 4, false, false>);
+        case 2: return a.LG > 1 ? go(k_rows<T, G, CR, 4, 2, true, false>) : go(k_rows<T, G, CR, 4, 2, false, false>);
+        case 3: return a.LG > 1 ? go(k_rows<T, G, CR, 3, 2, true, false>) : go(k_rows<T, G, CR, 3, 2, false, false>);
+        case 5: return a.LG > 1 ? go(k_rows<T, G, CR, 8, 1, true, false>) : go(k_rows<T, G, CR, 8, 1, false, false>);
+        // dynamic (device-counter) item schedules
+        case 6: return a.LG > 1 ? go(k_rows<T, G, CR, 3, 2, true, true>) : go(k_rows<T, G, CR, 3, 2, false, true>);
+        case 7: return a.LG > 1 ? go(k_rows<T, G, CR, 2, 4, true, true>) : go(k_rows<T, G, CR, 2, 4, false, true>);
+        case 8: return a.LG > 1 ? go(k_rows<T, G, CR, 4, 2, true, true>) : go(k_rows<T, G, CR, 4, 2, false, true>);
+        case 9: return a.LG > 1 ? go(k_rows<T, G, CR, 8, 1, true, true>) : go(k_rows<T, G, CR, 8, 1, false, true>);
+        // default: unroll 2, 3 CTAs per SM, dynamic -- measured best on B200 for full rows, layer and
+        // head shards and config 3 (tools/gather_ab.py, profiles/r01/gather_variants_ab_dyn.log)
+        default: return a.LG > 1 ? go(k_rows<T, G, CR, 2, 3, true, true>) : go(k_rows<T, G, CR, 2, 3, false, true>);
     }
 }
 template <typename T, bool G>
@@ -621,7 +645,7 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
 }
 
 extern "C" cp_status cp_set_gather_variant(int32_t v) {
-    if (v < 0 || v > 4) return CP_ERR_INVALID_ARG;
+    if (v < 0 || v > 9) return CP_ERR_INVALID_ARG;
     g_variant = v;
     return CP_OK;
 }

@@ -53,7 +53,8 @@ struct DevHeader {                   // first 256 B of META
     int32_t n_new_live;
     int32_t n_cand0;                 // insert: candidates of the first scan phase
     int32_t n_need;                  // insert: spans that need the old-entry haystack scan
-    int32_t pad[44];
+    unsigned long long gather_next;  // gather/copy: next work item (dynamic scheduling), reset by k_rows_prep
+    int32_t pad[42];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 

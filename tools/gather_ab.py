@@ -13,7 +13,14 @@ import paper_2605_23640_b200 as cp  # noqa: E402
 
 
 def main():
-    class A: config = 2; by = "layer"; scale = 1.0
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--by", default="layer")
+    ap.add_argument("--shard-world", type=int, default=0)
+    ap.add_argument("--shard-rank", type=int, default=0)
+    A = ap.parse_args()
+    A.scale = 1.0
     S = bench.setup_ours(A, 0, 1, torch.device("cuda", 0))
     S.idx.match_spans(S.rdb, 1000, hits=S.hits)
     torch.cuda.synchronize()
@@ -21,7 +28,8 @@ def main():
     row = S.shard.num_layers * S.shard.num_heads * S.g.head_dim * 2
     nbytes = (cov - rec) * 2 * row * 2 + rec * 2 * row
     out = {}
-    for v in [0, 3, 2, 4, 0, 3]:
+    variants = [0, 5, 3, 6, 8, 9, 4]
+    for v in variants + variants[:-1]:
         cp._lib.lib().cp_set_gather_variant(v)
         for _ in range(3):
             S.idx.gather_rerotate(S.rdb, S.hits, S.dst)
@@ -34,8 +42,8 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / n
-        out[f"variant{v}"] = {"ms": round(ms, 4), "GBps": round(nbytes / ms / 1e6, 1)}
-        print(v, out[f"variant{v}"], flush=True)
+        out.setdefault(f"variant{v}", []).append({"ms": round(ms, 4), "GBps": round(nbytes / ms / 1e6, 1)})
+        print(v, out[f"variant{v}"][-1], flush=True)
     print(json.dumps(out))
 
 

@@ -41,21 +41,31 @@ def main():
     (rK, rV, rbt), (fK, fV, fbt) = caches
     args = (req, ls, rs, rK, rV, rbt, fK, fV, fbt, 3, 20)
     dev, bits, so, bo = cp.score_kv_deviation(*args)
-    torch.cuda.synchronize()
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        cp.score_kv_deviation(*args, out_scores=dev, out_bits=bits)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    ref = (dev.clone(), bits.clone())
+    variants = {}
+    for var in ("1", "2", "3", "0"):                  # A/B of (loads per lane, CTAs per SM); 0 = default
+        os.environ["CP_KVDEV_VARIANT"] = var
+        for _ in range(2):
+            cp.score_kv_deviation(*args, out_scores=dev, out_bits=bits)
+        torch.cuda.synchronize()
+        reps = 20
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            cp.score_kv_deviation(*args, out_scores=dev, out_bits=bits)
+        e1.record()
+        torch.cuda.synchronize()
+        variants[var] = round(e0.elapsed_time(e1) / reps, 4)
+        assert torch.equal(dev, ref[0]) and torch.equal(bits, ref[1])
+    os.environ.pop("CP_KVDEV_VARIANT")
+    ms = variants["0"]
     tokens = sum(r - l + 1 for l, r in zip(ls, rs))
     nbytes = tokens * 4 * H * d * 2
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     out = {"what": "cp_score_kv_deviation (rows + top-k), config-2 shape, bf16 8x128 first layer, rho 3/20",
            "spans": R, "span_tokens": tokens, "algorithmic_bytes": nbytes, "ms": round(ms, 4),
-           "GBps": round(nbytes / ms / 1e6, 1), "peak_GBps": peak, "frac": round(nbytes / ms / 1e6 / peak, 4)}
+           "GBps": round(nbytes / ms / 1e6, 1), "peak_GBps": peak, "frac": round(nbytes / ms / 1e6 / peak, 4),
+           "variants_ms": variants}
     print(json.dumps(out))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "kvdev_bench.json"), "w") as f:

@@ -237,9 +237,10 @@ def setup_ours(args, rank, world, device):
         for r in sorted(set(int(x) for x in ib.span_req)):
             S.attn[r] = attention_torch(int(ib.lens[r]), ib.segments[r], 0.01, seed=r, device=device)
     ms = [int(m) for m in ib.span_len]
-    S.score_args = ([S.attn.get(int(r)) for r in ib.span_req], [int(ib.lens[int(r)]) for r in ib.span_req],
-                    [1] * len(ms), [int(b) for b in ib.span_begin],
-                    [int(b) + int(m) - 1 for b, m in zip(ib.span_begin, ib.span_len)])
+    S.score_args = ([S.attn.get(int(r)) for r in ib.span_req],                      # marshalled once per call
+                    np.asarray([int(ib.lens[int(r)]) for r in ib.span_req], np.int32), np.ones(len(ms), np.int32),
+                    np.asarray(ib.span_begin, np.int32),
+                    np.asarray([int(b) + int(m) - 1 for b, m in zip(ib.span_begin, ib.span_len)], np.int32))
     so, bo = [0], [0]
     for m in ms:
         so.append(so[-1] + m); bo.append(bo[-1] + (m + 31) // 32)

@@ -10,6 +10,7 @@ import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib as L
@@ -17,6 +18,24 @@ from . import _lib as L
 
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _i32(xs) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(xs, dtype=np.int64).astype(np.int32)).reshape(-1)
+
+
+def _offsets(ms: np.ndarray):
+    """Per-span score offsets and packed-bit word offsets: int64 [S + 1] each (prefix sums)."""
+    so = np.zeros(len(ms) + 1, np.int64)
+    bo = np.zeros(len(ms) + 1, np.int64)
+    np.cumsum(ms, out=so[1:])
+    np.cumsum((ms.astype(np.int64) + 31) // 32, out=bo[1:])
+    return so, bo
+
+
+def _cptr(a: np.ndarray, ctype):
+    """Host array pointer for the C-ABI (the caller keeps `a` alive across the call)."""
+    return a.ctypes.data_as(C.POINTER(ctype))
 
 
 def _stream(stream=None):
@@ -273,25 +292,22 @@ def score_deviation(attn: Sequence[torch.Tensor], n: Sequence[int], heads: Seque
     """Recompute scores + top-rho bits for spans (cp_score_deviation).  Returns (scores, bits,
     score_offsets, bits_word_offsets); scores int64 concatenated, bits uint32 (as int32 storage)."""
     S = len(span_l)
-    ms = [int(r) - int(l) + 1 for l, r in zip(span_l, span_r)]
-    so = [0]
-    bo = [0]
-    for m in ms:
-        so.append(so[-1] + m)
-        bo.append(bo[-1] + (m + 31) // 32)
+    l_, r_ = _i32(span_l), _i32(span_r)
+    ms = r_ - l_ + 1
+    so, bo = _offsets(ms)
     dev = attn[0].device if S else torch.device("cuda")
     if out_scores is None:
-        out_scores = torch.zeros(max(so[-1], 1), dtype=torch.int64, device=dev)
+        out_scores = torch.zeros(max(int(so[-1]), 1), dtype=torch.int64, device=dev)
     if out_bits is None:
-        out_bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=dev)
-    A = (C.c_void_p * max(S, 1))(*[a.data_ptr() for a in attn])
-    arr32 = lambda xs: (C.c_int32 * max(S, 1))(*[int(x) for x in xs])
-    arr64 = lambda xs: (C.c_int64 * max(len(xs), 1))(*[int(x) for x in xs])
-    rc = L.lib().cp_score_deviation(S, A, arr32(n), arr32(heads), arr32(span_l), arr32(span_r), rho_num, rho_den,
-                                    mode, max(ms) if ms else 1, _ptr(out_scores), arr64(so[:-1] or [0]),
-                                    _ptr(out_bits), arr64(bo[:-1] or [0]), _stream(stream))
+        out_bits = torch.zeros(max(int(bo[-1]), 1), dtype=torch.int32, device=dev)
+    A = np.fromiter((a.data_ptr() for a in attn), dtype=np.uint64, count=S) if S else np.zeros(1, np.uint64)
+    n_, h_ = _i32(n), _i32(heads)
+    rc = L.lib().cp_score_deviation(S, _cptr(A, C.c_void_p), _cptr(n_, C.c_int32), _cptr(h_, C.c_int32),
+                                    _cptr(l_, C.c_int32), _cptr(r_, C.c_int32), rho_num, rho_den, mode,
+                                    int(ms.max()) if S else 1, _ptr(out_scores), _cptr(so, C.c_int64),
+                                    _ptr(out_bits), _cptr(bo, C.c_int64), _stream(stream))
     L.check(rc, "cp_score_deviation")
-    return out_scores, out_bits, so, bo
+    return out_scores, out_bits, so.tolist(), bo.tolist()
 
 
 def score_kv_deviation(span_req: Sequence[int], span_l: Sequence[int], span_r: Sequence[int],
@@ -303,31 +319,27 @@ def score_kv_deviation(span_req: Sequence[int], span_l: Sequence[int], span_r: S
     each), top ceil(rho*m) marked (default 15% = 3/20).  Returns (dev, bits, score_offsets,
     bits_word_offsets) like score_deviation."""
     S = len(span_l)
-    ms = [int(r) - int(l) + 1 for l, r in zip(span_l, span_r)]
-    so, bo = [0], [0]
-    for m in ms:
-        so.append(so[-1] + m)
-        bo.append(bo[-1] + (m + 31) // 32)
+    q_, l_, r_ = _i32(span_req), _i32(span_l), _i32(span_r)
+    ms = r_ - l_ + 1
+    so, bo = _offsets(ms)
     dev = reused_k.device
     if out_scores is None:
-        out_scores = torch.zeros(max(so[-1], 1), dtype=torch.int64, device=dev)
+        out_scores = torch.zeros(max(int(so[-1]), 1), dtype=torch.int64, device=dev)
     if out_bits is None:
-        out_bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=dev)
+        out_bits = torch.zeros(max(int(bo[-1]), 1), dtype=torch.int32, device=dev)
     for t in (reused_k, reused_v, fresh_k, fresh_v):
         if not t.is_contiguous() or t.shape[1:] != reused_k.shape[1:] or t.dtype != reused_k.dtype:
             raise ValueError("caches must be contiguous [blocks, 16, H, d] of one dtype")
     H, d = int(reused_k.shape[2]), int(reused_k.shape[3])
-    arr32 = lambda xs: (C.c_int32 * max(S, 1))(*[int(x) for x in xs])
-    arr64 = lambda xs: (C.c_int64 * max(len(xs), 1))(*[int(x) for x in xs])
     rbt, fbt = reused_block_tables.contiguous(), fresh_block_tables.contiguous()
-    rc = L.lib().cp_score_kv_deviation(S, arr32(span_req), arr32(span_l), arr32(span_r), _ptr(reused_k),
-                                       _ptr(reused_v), _ptr(rbt), int(rbt.shape[1]), _ptr(fresh_k), _ptr(fresh_v),
-                                       _ptr(fbt), int(fbt.shape[1]), H, d,
+    rc = L.lib().cp_score_kv_deviation(S, _cptr(q_, C.c_int32), _cptr(l_, C.c_int32), _cptr(r_, C.c_int32),
+                                       _ptr(reused_k), _ptr(reused_v), _ptr(rbt), int(rbt.shape[1]), _ptr(fresh_k),
+                                       _ptr(fresh_v), _ptr(fbt), int(fbt.shape[1]), H, d,
                                        L.CP_BF16 if reused_k.dtype == torch.bfloat16 else L.CP_FP32,
-                                       rho_num, rho_den, max(ms) if ms else 1, _ptr(out_scores),
-                                       arr64(so[:-1] or [0]), _ptr(out_bits), arr64(bo[:-1] or [0]), _stream(stream))
+                                       rho_num, rho_den, int(ms.max()) if S else 1, _ptr(out_scores),
+                                       _cptr(so, C.c_int64), _ptr(out_bits), _cptr(bo, C.c_int64), _stream(stream))
     L.check(rc, "cp_score_kv_deviation")
-    return out_scores, out_bits, so, bo
+    return out_scores, out_bits, so.tolist(), bo.tolist()
 
 
 def annotate_spans(attn: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], heads: Sequence[int],

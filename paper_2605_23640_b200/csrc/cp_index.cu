@@ -594,7 +594,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     const int2* rec = rec_in_smem ? srec : a.rel_rec;
     PROF_T(0);
 
-    auto resolve = [&](int code) -> int { return code >= 0 ? code : snew[-1 - code]; };
+    // a relation names an old slot (code >= 0) or a new span's CONTENT (code < 0: a representative);
+    // that content may have been stored by any span of the same representative, and the pool holds
+    // at most one live entry per content: seq[rep] is the latest slot stored or refreshed for it
+    // (snew[rep] alone misses a duplicate of a Dropped representative that got stored later)
+    auto resolve = [&](int code) -> int { return code >= 0 ? code : seq[srep[-1 - code]]; };
     auto is_live = [&](int code) -> bool { const int s = resolve(code); return s >= 0 && (sflag[s] & 1); };
 
 

@@ -1,0 +1,82 @@
+"""Randomized GPU-vs-oracle stress of the index (a7) and the matcher / gather (a1-a5).
+
+Tiny alphabets make windows collide, segments repeat, contain one another and supersede; a small
+token budget forces LRU eviction every round (candidate-list pops, deferred FIFO traffic and its
+flushes, slot recycling); writers and readers are drawn from a shared pool of token "motifs" so hits
+are frequent and shifted.  Every round the harness compares insert outcomes and entry ids, the whole
+live index (ids, lengths, origins, hashes, digests, last_used, page lists, tokens, recompute bits,
+free-page FIFO), hits, plan codes, stats and the gathered KV rows against the oracle."""
+import numpy as np
+import pytest
+
+pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth.gen import Batch, Geometry, Workload, pack_batches  # noqa: E402
+from tests.harness import Case, ParityReport  # noqa: E402
+
+
+def _request(rng, motifs, alphabet, wid, writer):
+    parts, mask = [], []
+    for _ in range(int(rng.integers(2, 6))):
+        if rng.random() < 0.7:
+            m = motifs[int(rng.integers(len(motifs)))]
+        else:
+            m = rng.integers(0, alphabet, int(rng.integers(3, 40))).astype(np.int32)
+        parts.append(m)
+        mask.append(np.zeros(len(m), np.uint8))
+        if rng.random() < 0.4:                                     # a sensitive run between pieces
+            k = int(rng.integers(1, 4))
+            parts.append(rng.integers(0, alphabet, k).astype(np.int32))
+            mask.append(np.ones(k, np.uint8))
+    toks, msk = np.concatenate(parts), np.concatenate(mask)
+    spans_b, spans_l = [], []
+    if writer:                                                     # spans: maximal mask-free runs >= w, maybe trimmed
+        i, n = 0, len(toks)
+        while i < n:
+            if msk[i]:
+                i += 1
+                continue
+            a = i
+            while i < n and not msk[i]:
+                i += 1
+            if i - a >= 8:
+                b0 = a + int(rng.integers(0, max(1, (i - a - 8) // 3 + 1)))
+                spans_b.append(b0)
+                ln = i - b0 if rng.random() < 0.6 else int(rng.integers(8, i - b0 + 1))
+                spans_l.append(min(ln, 100))                       # <= the smallest budget below
+    return Batch(tokens=toks, offsets=np.array([0, len(toks)], np.int64), mask=msk,
+                 writer_ids=np.array([wid], np.int64), span_req=np.zeros(len(spans_b), np.int32),
+                 span_begin=np.array(spans_b, np.int32), span_len=np.array(spans_l, np.int32))
+
+
+def _workload(seed, dtype):
+    rng = np.random.default_rng(seed)
+    alphabet = int(rng.integers(3, 9))
+    motifs = [rng.integers(0, alphabet, int(rng.integers(8, 60))).astype(np.int32) for _ in range(6)]
+    motifs += [np.concatenate([motifs[0], motifs[1]]), motifs[2][: max(8, len(motifs[2]) // 2)]]
+    rounds, wid = [], 0
+    for _ in range(5):
+        ws = [_request(rng, motifs, alphabet, wid + k, True) for k in range(int(rng.integers(2, 6)))]
+        wid += len(ws)
+        rs = [_request(rng, motifs, alphabet, 10000 + wid + k, False) for k in range(int(rng.integers(1, 5)))]
+        rounds.append((pack_batches(ws), pack_batches(rs)))
+    L, H, d = [(1, 1, 16), (2, 2, 32), (1, 3, 16), (3, 1, 64)][seed % 4]
+    g = Geometry(L, H, d, dtype, 10000.0 if seed % 3 else 500000.0, window_len=8,
+                 rope_style="gptj" if seed % 5 == 0 else "neox")
+    return Workload(f"fuzz{seed}", g, rounds, pool_capacity_tokens=int(rng.integers(120, 400)), max_span_len=256)
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_index_fuzz_rounds(seed):
+    wl = _workload(seed, "fp32" if seed % 2 else "bf16")
+    case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0)
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.insert(wb, rep)
+        assert rep.ok, rep.notes[:6]
+        case.match_and_gather(rb, rep)
+        assert rep.ok, rep.notes[:6]
+        case.match_and_gather(wb, rep, no_touch=True)            # writers re-read their own prompts
+        assert rep.ok, rep.notes[:6]
+    assert rep.stats.get("stored", 0) > 0

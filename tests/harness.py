@@ -190,9 +190,9 @@ class Case:
         if err != rc:
             rep.fail(f"insert t={t}: device status {err} != oracle {rc}")
             return
-        self.calls.append(wb)
         if rc != 0:
-            return
+            return                          # rejected calls store nothing and are not counted by the oracle
+        self.calls.append(wb)
         ids, oc = ids.cpu().numpy(), oc.cpu().numpy()
         if not np.array_equal(oc, ooc):
             rep.fail(f"insert t={t}: outcomes differ at {np.nonzero(oc != ooc)[0][:8]}")

@@ -50,14 +50,15 @@ def _request(rng, motifs, alphabet, wid, writer):
                  span_begin=np.array(spans_b, np.int32), span_len=np.array(spans_l, np.int32))
 
 
-def _workload(seed, dtype):
+def _workload(seed, dtype, heavy=False):
     rng = np.random.default_rng(seed)
     alphabet = int(rng.integers(3, 9))
-    motifs = [rng.integers(0, alphabet, int(rng.integers(8, 60))).astype(np.int32) for _ in range(6)]
+    motifs = [rng.integers(0, alphabet, int(rng.integers(8, 60))).astype(np.int32) for _ in range(3 if heavy else 6)]
     motifs += [np.concatenate([motifs[0], motifs[1]]), motifs[2][: max(8, len(motifs[2]) // 2)]]
     rounds, wid = [], 0
     for _ in range(5):
-        ws = [_request(rng, motifs, alphabet, wid + k, True) for k in range(int(rng.integers(2, 6)))]
+        nw = int(rng.integers(8, 17)) if heavy else int(rng.integers(2, 6))
+        ws = [_request(rng, motifs, alphabet, wid + k, True) for k in range(nw)]
         wid += len(ws)
         rs = [_request(rng, motifs, alphabet, 10000 + wid + k, False) for k in range(int(rng.integers(1, 5)))]
         rounds.append((pack_batches(ws), pack_batches(rs)))
@@ -78,5 +79,21 @@ def test_index_fuzz_rounds(seed):
         case.match_and_gather(rb, rep)
         assert rep.ok, rep.notes[:6]
         case.match_and_gather(wb, rep, no_touch=True)            # writers re-read their own prompts
+        assert rep.ok, rep.notes[:6]
+    assert rep.stats.get("stored", 0) > 0
+
+
+@pytest.mark.parametrize("seed", range(100, 164))
+def test_index_fuzz_heavy_in_batch_repetition(seed):
+    """Few motifs and 8-16 writers per batch: the same content recurs inside one insert call (first
+    Dropped, later Stored after its container is evicted or superseded, ...) -- the batch-dedup /
+    representative paths of the commit."""
+    wl = _workload(seed, "bf16" if seed % 2 else "fp32", heavy=True)
+    case = Case(wl, seed=seed, sample_reqs=None)
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.insert(wb, rep)
+        assert rep.ok, rep.notes[:6]
+        case.match_and_gather(rb, rep)
         assert rep.ok, rep.notes[:6]
     assert rep.stats.get("stored", 0) > 0

@@ -1,0 +1,61 @@
+"""Long randomized GPU-vs-oracle search over the index / matcher / gather (the generators of
+tests/test_gpu_fuzz_index.py), many more seeds than the test suite runs, and the NEXT-3 policies.
+Usage: python tools/fuzz_index.py [first_seed] [count].  Prints failing seeds with their first notes
+and writes gpurun_out/fuzz_index.json."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from tests.harness import Case, ParityReport  # noqa: E402
+from tests.test_gpu_fuzz_index import _workload  # noqa: E402
+
+
+def one(seed):
+    heavy = seed % 2 == 0
+    policy = [None, None, None, "fixed_chunk", "prefix_only"][seed % 5]
+    wl = _workload(seed, "bf16" if (seed // 2) % 2 else "fp32", heavy=heavy)
+    case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0, policy=policy)
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.insert(wb, rep)
+        if not rep.ok:
+            break
+        case.match_and_gather(rb, rep)
+        if not rep.ok:
+            break
+        if seed % 3 == 0:
+            case.match_and_gather(wb, rep, no_touch=True)
+            if not rep.ok:
+                break
+    return rep
+
+
+def main():
+    first = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+    count = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+    fails, stats, t0 = [], {}, time.time()
+    for seed in range(first, first + count):
+        try:
+            rep = one(seed)
+            ok, notes = rep.ok, rep.notes[:4]
+            for k, v in rep.stats.items():
+                if isinstance(v, (int, float)) and k in ("stored", "duplicate", "hits", "moved_hits", "covered"):
+                    stats[k] = stats.get(k, 0) + v
+        except Exception as e:  # noqa: BLE001 -- report and continue
+            ok, notes = False, [repr(e)[:300]]
+        if not ok:
+            fails.append({"seed": seed, "notes": notes})
+            print("FAIL", seed, notes, flush=True)
+    out = {"first_seed": first, "count": count, "failures": fails, "stats": stats, "seconds": round(time.time() - t0, 1)}
+    print(json.dumps(out)[:2000])
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "fuzz_index.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -166,7 +166,10 @@ class Case:
         rep.stats["policy_spans"] = rep.stats.get("policy_spans", 0) + len(o_sr)
         return dataclasses.replace(wb, span_req=o_sr, span_begin=o_sb, span_len=o_sl), (d_sr, d_sb, d_sl)
 
-    def insert(self, wb: Batch, rep: ParityReport, bits_flags=None, sparse_kv=False):
+    def insert(self, wb: Batch, rep: ParityReport, bits_flags=None, sparse_kv=False, concurrent_readers=None):
+        """concurrent_readers: a reader batch matched (NO_TOUCH) and gathered on the main stream while
+        the device insert's read-only half (cp_index_insert_prepare) runs on a side stream; the commit
+        follows both.  The oracle inserts sequentially (the NO_TOUCH match changes no state)."""
         torch = self.torch
         dev_spans = None
         if self.policy is not None:
@@ -184,7 +187,20 @@ class Case:
         dwords = torch.from_numpy(words.view(np.int32).copy() if len(words) else np.zeros(1, np.int32)).to(self.device)
         doffs = torch.from_numpy(offs.astype(np.int64)).to(self.device)
         dsp = dev_spans if dev_spans is not None else (sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len))
-        ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t)
+        if concurrent_readers is None:
+            ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t)
+        else:
+            side, main = torch.cuda.Stream(), torch.cuda.current_stream()
+            ready = torch.cuda.Event()
+            ready.record(main)
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                self.dev.insert(db, kv, *dsp, dwords, doffs, t, phase="prepare")
+            rdb = self._dev_batch(concurrent_readers, with_mask=self.use_reader_mask)
+            hits = self.dev.match_spans(rdb, t, no_touch=True, use_mask=self.use_reader_mask, policy=self.policy)
+            self.dev.gather_rerotate(rdb, hits, self.dst_kv(concurrent_readers), zero_recompute=True)
+            main.wait_stream(side)
+            ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t, phase="commit")
         err = self.dev.last_error()
         rc, oids, ooc = self.orc.insert(wb, words, offs, t)
         if err != rc:
@@ -270,6 +286,22 @@ class Case:
         if check_kv:
             self.compare_kv(rb, res, dst, rep)
         self.compare_index(rep, f"after match t={t}", tokens=False)
+
+    def compare_links(self, rb: Batch, rep: ParityReport):
+        """NEXT-2: link table of a NO_TOUCH match of `rb` vs the oracle's (R#31)."""
+        self.t += 1
+        db = self._dev_batch(rb, with_mask=self.use_reader_mask)
+        hits = self.dev.match_spans(db, self.t, no_touch=True, use_mask=self.use_reader_mask, policy=self.policy)
+        res = self.orc.match(rb, self.t, no_touch=True, use_mask=self.use_reader_mask, policy=self.policy)
+        maxb = max(1, int(max((int(n) + 15) // 16 for n in rb.lens)))
+        got = self.dev.link_blocks(db, hits, maxb).cpu().numpy()
+        if self.dev.last_error():
+            rep.fail(f"link t={self.t}: device error {self.dev.last_error()}")
+            return
+        exp = self.orc.link_blocks(rb, res, maxb)
+        if not np.array_equal(got, exp):
+            rep.fail(f"link t={self.t}: link tables differ at {np.argwhere(got != exp)[:4].tolist()}")
+        rep.stats["linked_blocks"] = rep.stats.get("linked_blocks", 0) + int((exp >= 0).sum())
 
     def _entry_origin(self, eid):
         e = self.orc.entry(int(eid))

@@ -18,15 +18,23 @@ def one(seed):
     heavy = seed % 2 == 0
     policy = [None, None, None, "fixed_chunk", "prefix_only"][seed % 5]
     wl = _workload(seed, "bf16" if (seed // 2) % 2 else "fp32", heavy=heavy)
-    case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0, policy=policy)
+    rho = (0, 4) if seed % 3 == 1 else (1, 4)          # no recompute marks: pages can link (NEXT-2)
+    case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0, policy=policy, rho=rho)
     rep = ParityReport()
+    prev = None
     for wb, rb in wl.rounds:
-        case.insert(wb, rep)
+        case.insert(wb, rep, concurrent_readers=prev if seed % 4 == 1 else None)   # split insert beside match/gather
         if not rep.ok:
             break
         case.match_and_gather(rb, rep)
         if not rep.ok:
             break
+        if seed % 3 == 1:
+            case.compare_links(wb, rep)                    # writers re-reading: delta-0 aligned hits link
+            case.compare_links(rb, rep)
+            if not rep.ok:
+                break
+        prev = rb
         if seed % 3 == 0:
             case.match_and_gather(wb, rep, no_touch=True)
             if not rep.ok:
@@ -43,7 +51,8 @@ def main():
             rep = one(seed)
             ok, notes = rep.ok, rep.notes[:4]
             for k, v in rep.stats.items():
-                if isinstance(v, (int, float)) and k in ("stored", "duplicate", "hits", "moved_hits", "covered"):
+                if isinstance(v, (int, float)) and k in ("stored", "duplicate", "hits", "moved_hits", "covered",
+                                                          "linked_blocks"):
                     stats[k] = stats.get(k, 0) + v
         except Exception as e:  # noqa: BLE001 -- report and continue
             ok, notes = False, [repr(e)[:300]]

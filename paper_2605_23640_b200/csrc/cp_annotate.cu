@@ -302,7 +302,7 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
         a.out_l = out_l + (int64_t)r0 * max_segments;
         a.out_r = out_r + (int64_t)r0 * max_segments;
         a.out_diff = (long long*)out_diff + (int64_t)r0 * max_segments;
-        k_ann_rows<<<(int)std::min<long long>((rows + 7) / 8, 148 * 16), 256, 0, st>>>(a);
+        k_ann_rows<<<(int)std::min<long long>((rows + 7) / 8, (long long)cp_sm_count() * 16), 256, 0, st>>>(a);
         CP_COUNT_LAUNCH();
         k_ann_segs<<<a.nreq, 1024, 0, st>>>(a);
         CP_COUNT_LAUNCH();

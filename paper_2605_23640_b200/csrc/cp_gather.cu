@@ -526,16 +526,7 @@ __global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int
     }
 }
 
-int g_sms = 0;
-int sm_count() {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
-    }
-    return g_sms;
-}
+int sm_count() { return cp_sm_count(); }
 int rows_grid() { return sm_count() * 4; }
 
 // variant = (UNROLL, MINB): selectable with CP_GATHER_VARIANT for A/B measurement

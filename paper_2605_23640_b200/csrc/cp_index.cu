@@ -1450,12 +1450,13 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     k_ins_bucket_offsets<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_bucket_fill<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     const size_t scan_smem = 8 * ((size_t)x->cfg.max_span_len + 1);
-    k_ins_scan<<<(int)std::min<int64_t>(num_spans, 148 * 6), kScanThreads, scan_smem, st>>>(a, 0); CP_COUNT_LAUNCH();
-    k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 0); CP_COUNT_LAUNCH();
-    k_ins_flag_eq<<<148, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    const int sms = cp_sm_count();
+    k_ins_scan<<<(int)std::min<int64_t>(num_spans, sms * 6), kScanThreads, scan_smem, st>>>(a, 0); CP_COUNT_LAUNCH();
+    k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 0); CP_COUNT_LAUNCH();
+    k_ins_flag_eq<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_scan<<<(int)std::min<int64_t>(x->S, 148 * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
-    k_ins_verify<<<148 * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
+    k_ins_scan<<<(int)std::min<int64_t>(x->S, sms * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
+    k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
 

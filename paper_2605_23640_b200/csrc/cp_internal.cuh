@@ -113,6 +113,17 @@ struct cp_index {
 
 // ---- launch bookkeeping -------------------------------------------------------------------
 extern std::atomic<unsigned long long> g_cp_launches;
+// SM count of the current device (grids are sized in multiples of it; 148 on B200)
+inline int cp_sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 #define CP_COUNT_LAUNCH() (g_cp_launches.fetch_add(1, std::memory_order_relaxed))
 #define CP_CUDA_CHECK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return CP_ERR_CUDA; } while (0)
 

@@ -288,16 +288,7 @@ __global__ void __launch_bounds__(kRowThreads, MINB) k_kvdev_rows(const ScoreArg
 
 namespace {
 
-int sm_count_score() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count_score() { return cp_sm_count(); }
 
 int g_score_variant = -1;
 void launch_score_rows(const ScoreArgs& a, cudaStream_t st) {

@@ -27,7 +27,8 @@ namespace {
 
 constexpr int kAnnReqsPerLaunch = 512;
 constexpr int kBestThreads = 256;           // one start l per thread; a CTA covers 256 starts
-constexpr int kRowUnroll = 8;
+constexpr int kRowUnroll = 32;            // k_ann_best: rows of R(i, l) in flight per thread
+constexpr int kRowsBatch = 8;               // k_ann_rows: 32-column chunks whose loads are in flight together
 
 struct AnnReq {
     const float* A;          // [heads][n][n]
@@ -71,16 +72,26 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
         long long* R = reinterpret_cast<long long*>(a.ws + rq.r_off) + (int64_t)i * (n + 1);
         long long carry = 0;
         if (lane == 0) R[0] = 0;
-        for (int base = 0; base <= i; base += 32) {
-            const int x = base + lane;
-            long long v = 0;
-            if (x <= i)
-                for (int h = 0; h < rq.heads; ++h) v += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
-            long long inc = v;
+        // kRowsBatch chunks of 32 columns per step: all their loads are issued before the scans, so a
+        // row costs one memory round trip per 32 * kRowsBatch columns instead of one per 32
+        for (int base = 0; base <= i; base += 32 * kRowsBatch) {
+            long long v[kRowsBatch];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-            if (x <= i) R[x + 1] = carry + inc;
-            carry += __shfl_sync(0xffffffffu, inc, 31);
+            for (int u = 0; u < kRowsBatch; ++u) {
+                const int x = base + u * 32 + lane;
+                v[u] = 0;
+                if (x <= i)
+                    for (int h = 0; h < rq.heads; ++h) v[u] += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
+            }
+#pragma unroll
+            for (int u = 0; u < kRowsBatch; ++u) {
+                const int x = base + u * 32 + lane;
+                long long inc = v[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+                if (x <= i) R[x + 1] = carry + inc;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
         }
     }
 }
@@ -135,9 +146,33 @@ __global__ void __launch_bounds__(1024) k_ann_segs(const AnnArgs a) {
         __syncthreads();
         if (start) {
             const int k = s_cnt + s_wi[wid] + inc - 1;
-            int e = i;
-            while (e + 1 < n && !rq.mask[e + 1]) ++e;
-            if (k < a.max_seg) seg[k] = make_int2(i, e);
+            if (k < a.max_seg) seg[k].x = i;
+        }
+        __syncthreads();
+        if (tid == 0) s_cnt += s_wi[32];
+        __syncthreads();
+    }
+    // segment ends: the k-th mask-0 position followed by a mask-1 one (or the end) closes segment k,
+    // found by the same ordered scan (no per-segment serial walk)
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < n; b0 += 1024) {
+        const int i = b0 + tid;
+        const bool end = i < n && !rq.mask[i] && (i + 1 == n || rq.mask[i + 1]);
+        int inc = end;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_wi[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            int x = s_wi[lane], xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+            s_wi[lane] = xi - x;
+            if (lane == 31) s_wi[32] = xi;
+        }
+        __syncthreads();
+        if (end) {
+            const int k = s_cnt + s_wi[wid] + inc - 1;
+            if (k < a.max_seg) seg[k].y = i;
         }
         __syncthreads();
         if (tid == 0) s_cnt += s_wi[32];

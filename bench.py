@@ -448,6 +448,8 @@ def bench_ours(args):
                        "shard_layers": L, "shard_heads": H, "rho": f"{RHO[0]}/{RHO[1]}", "link": bool(args.link), "window_len": S.g.window_len,
                        "l2": "inputs larger than L2 (pool + destination caches ~100 GB), no flush needed"},
             "matched_tokens_per_s": round(cov / (ms_step * 1e-3), 1),
+            # gather bytes (reused read + write, zero fills) over match + gather time
+            "match_plus_gather_GBps": round(gather_all / ((float(phase[:, 0].mean()) + gather_ms_max) * 1e-3) / 1e9, 1),
             "covered_tokens": cov, "reused_tokens": reused, "recompute_tokens": rec, "hits": nh,
             "linked_tokens": linked,
             "match_rate": round(cov / S.rb.total_tokens, 4),

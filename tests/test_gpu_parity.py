@@ -332,11 +332,31 @@ def test_zero_uncovered_flag_and_match_error():
     assert case.dev.last_error() == 0            # cleared by the read
 
 
+def test_churn_config5_full_size_oracle_parity():
+    """Config 5 at its full batch size (256 requests x ~1.6K tokens per batch, 100K-passage Zipf
+    corpus) on one KV-head shard, 6 batches under a 300K-token budget so that LRU eviction runs from
+    the second insert on: insert outcomes / ids and the whole live index bit exact, hits / plans /
+    stats bit exact, KV rows sampled (2 requests x 2 layers per batch)."""
+    from synth.gen import churn_workload
+    g = Geometry(32, 8, 128, "bf16", 500000.0)
+    wl = churn_workload(batches=6, per_batch=256, corpus=100000, capacity_tokens=300_000, geometry=g)
+    case = Case(wl, head_range=(0, 1), sample_reqs=2, sample_layers=[0, 31])
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.match_and_gather(rb, rep)
+        assert rep.ok, rep.notes[:6]
+        case.insert(wb, rep)
+        assert rep.ok, rep.notes[:6]
+    assert rep.stats["duplicate"] > 0 and rep.stats["hits"] > 0
+    assert case.orc.num_ids > len(case.orc.live_entries())        # entries were evicted
+
+
 def test_churn_config5_full_batches_invariants():
     """Config 5 at its full batch size (256 requests x ~1.6K tokens, 100K-passage corpus) for a few
-    batches on one head shard with a budget that forces LRU eviction; device-only invariants (the
-    oracle cannot replay this size): budget, no device error, every stored entry is unmasked in its
-    writer and its tokens equal the writer's span, no entry strictly contains another."""
+    batches on one head shard with a budget that forces LRU eviction; device-side invariants (the
+    oracle parity of the same shape is test_churn_config5_full_size_oracle_parity): budget, no device
+    error, every stored entry is unmasked in its writer and its tokens equal the writer's span, no
+    entry strictly contains another."""
     import paper_2605_23640_b200 as cp
     from synth.gen import churn_workload
     g = Geometry(32, 8, 128, "bf16", 500000.0)

@@ -28,6 +28,21 @@ def main():
         case.match_and_gather(rb, rep)
         out[name] = dict(ok=rep.ok, notes=rep.notes[:5], secs=time.time() - t0, **rep.stats)
         del case
+    if "--all" in sys.argv:
+        # every request's K/V rows compared (not a sample) at full BASELINE sizes, on a few layers
+        for name, cfg, kw in [("config2_full_all_requests", 2, dict(sample_layers=[0, 13, 31])),
+                              ("config3_full_all_requests", 3, dict(sample_layers=[0, 31])),
+                              ("config4_layer_shard_all_requests", 4, dict(layer_range=(70, 80), sample_layers=[0, 9]))]:
+            t0 = time.time()
+            case = Case(make_workload(cfg), sample_reqs=None, **kw)
+            rep = ParityReport()
+            wb, rb = case.wl.rounds[0]
+            case.insert(wb, rep, sparse_kv=(cfg != 2))
+            case.match_and_gather(rb, rep)
+            out[name] = dict(ok=rep.ok, notes=rep.notes[:5], secs=time.time() - t0, requests_checked=rb.num_reqs,
+                             **rep.stats)
+            print(name, out[name]["ok"], round(out[name]["secs"], 1), flush=True)
+            del case
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "parity_report.json"), "w") as f:
         json.dump(out, f, indent=1, default=float)

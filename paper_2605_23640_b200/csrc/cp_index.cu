@@ -952,6 +952,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             __syncthreads();
         }
         j0 = s_resume;
+        __syncthreads();                 // every thread has read s_resume before thread 0 resets it
     }
     __syncthreads();
     // ---- deferred page traffic, block-parallel (warp per removal / per stored span): appended pages

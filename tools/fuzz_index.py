@@ -22,7 +22,30 @@ def one(seed):
     case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0, policy=policy, rho=rho)
     rep = ParityReport()
     prev = None
+    import dataclasses
+    import numpy as np
+    rng = np.random.default_rng(seed + 7)
     for wb, rb in wl.rounds:
+        if seed % 6 == 5 and rng.random() < 0.5 and len(wb.span_len):
+            # inject one invalid span (covers a masked token, or is shorter than w, or runs past the
+            # request) at a random position: both sides must reject the whole call without side effects
+            kind = int(rng.integers(3))
+            r = int(rng.integers(wb.num_reqs))
+            n = int(wb.lens[r])
+            masked = np.nonzero(wb.req_mask(r))[0]
+            if kind == 0 and len(masked):
+                b0 = max(0, int(masked[0]) - 4); bad = (r, b0, min(n - b0, 12))
+            elif kind == 1:
+                bad = (r, 0, min(n, 5))
+            else:
+                bad = (r, max(0, n - 4), 12)
+            pos = int(rng.integers(len(wb.span_len)))          # replace a span: the call keeps its span count
+            def put(arr, v):
+                arr = np.array(arr, np.int32)
+                arr[pos] = v
+                return arr
+            wb = dataclasses.replace(wb, span_req=put(wb.span_req, bad[0]), span_begin=put(wb.span_begin, bad[1]),
+                                     span_len=put(wb.span_len, bad[2]))
         case.insert(wb, rep, concurrent_readers=prev if seed % 4 == 1 else None)   # split insert beside match/gather
         if not rep.ok:
             break

@@ -1,7 +1,8 @@
 """Long randomized GPU-vs-oracle runs of the NEXT rows' kernels (beyond the test suite's seeds):
   * annotator (cp_annotate_spans, NEXT-1): random causal matrices (1-3 heads, quantized values for
     ties, row-stochastic or not), random masks (including long runs), random min_len;
-  * KV deviation (cp_score_kv_deviation, NEXT-4): random geometries / dtypes / spans / rho.
+  * KV deviation (cp_score_kv_deviation, NEXT-4): random geometries / dtypes / spans / rho;
+  * N3 score + top-k (cp_score_deviation): random spans up to 4000 rows, 1-2 heads, ties, rho 0..1.
 Usage: python tools/fuzz_misc.py [seeds].  Writes gpurun_out/fuzz_misc.json."""
 import json
 import os
@@ -89,11 +90,37 @@ def kvdev_case(seed):
     return True
 
 
+def score_case(seed):
+    rng = np.random.default_rng(seed)
+    mats, ns, hs, ls, rs = [], [], [], [], []
+    big = seed % 10 == 0
+    for _ in range(int(rng.integers(1, 4 if big else 12))):
+        n = int(rng.integers(1, 4000 if big else 600))
+        h = int(rng.integers(1, 3))
+        A = rng.uniform(0, 1, (h, n, n)).astype(np.float32)
+        if rng.random() < 0.5:
+            A = np.floor(A * 8) / 8
+        A = np.tril(A).astype(np.float32)
+        l = int(rng.integers(0, n)); r = int(rng.integers(l, n))
+        mats.append(torch.from_numpy(A).cuda()); ns.append(n); hs.append(h); ls.append(l); rs.append(r)
+    num, den = [(1, 4), (3, 20), (0, 3), (3, 3), (5, 11)][seed % 5]
+    sc, bits, so, bo = cp.score_deviation(mats, ns, hs, ls, rs, num, den)
+    sc, bits = sc.cpu().numpy(), bits.cpu().numpy().view(np.uint32)
+    for q in range(len(ns)):
+        m = rs[q] - ls[q] + 1
+        osc, ob = O.score(mats[q].cpu().numpy(), ls[q], rs[q], num, den)
+        if not (np.array_equal(sc[so[q]:so[q] + m], osc) and np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob)):
+            return False
+    return True
+
+
 def main():
     seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 300
     t0 = time.time()
-    fails = {"annotate": [], "kvdev": []}
+    fails = {"annotate": [], "kvdev": [], "score": []}
     for s in range(seeds):
+        if not score_case(70000 + s):
+            fails["score"].append(70000 + s)
         if not annotate_case(50000 + s):
             fails["annotate"].append(50000 + s)
         if not kvdev_case(60000 + s):

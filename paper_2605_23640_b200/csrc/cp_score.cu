@@ -95,12 +95,17 @@ __device__ __forceinline__ long long warp_row_score(const float* p, int cnt, int
 // register budget must allow (variants for A/B measurement: cp_set_score_variant).
 template <int MINB>
 __global__ void __launch_bounds__(kRowThreads, MINB) k_score_rows(const ScoreArgs a) {
+    // the spans' first rows, staged in shared memory: the per-row binary search then costs shared
+    // loads instead of a chain of dependent kernel-parameter (constant-cache) loads
+    __shared__ int32_t s_rb[kSpansPerLaunch];
+    for (int q = threadIdx.x; q < a.nsp; q += blockDim.x) s_rb[q] = a.sp[q].row_begin;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
     for (int gr = warp; gr < a.total_rows; gr += nwarps) {
         int lo = 0, hi = a.nsp - 1;
-        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
+        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rb[mid] <= gr) lo = mid; else hi = mid - 1; }
         const float* A = a.sp[lo].A;
         const int n = a.sp[lo].n, l = a.sp[lo].l, heads = a.sp[lo].heads();
         const int i = l + (gr - a.sp[lo].row_begin);
@@ -249,13 +254,16 @@ __device__ __forceinline__ uint4 ld_nc_u4(const uint4* p) {
 
 template <bool BF16, int kDevBatch, int MINB>
 __global__ void __launch_bounds__(kRowThreads, MINB) k_kvdev_rows(const ScoreArgs a, const KvDevArgs k) {
+    __shared__ int32_t s_rb[kSpansPerLaunch];          // spans' first rows (see k_score_rows)
+    for (int q = threadIdx.x; q < a.nsp; q += blockDim.x) s_rb[q] = a.sp[q].row_begin;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
     const int V = k.vec_per_row;
     for (int gr = warp; gr < a.total_rows; gr += nwarps) {
         int lo = 0, hi = a.nsp - 1;
-        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.sp[mid].row_begin <= gr) lo = mid; else hi = mid - 1; }
+        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rb[mid] <= gr) lo = mid; else hi = mid - 1; }
         const int req = a.sp[lo].n, l = a.sp[lo].l;
         const int i = l + (gr - a.sp[lo].row_begin);
         const int64_t ro = ((int64_t)k.rbt[(int64_t)req * k.rmaxb + (i >> 4)] * 16 + (i & 15)) * V;

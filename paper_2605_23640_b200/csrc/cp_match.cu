@@ -172,11 +172,25 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             const int slot = vslot[k];
             const int m = __ldg(a.slot_len + slot);
             const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+            // 8 tokens per lane in flight per step (the page-list and token-store loads of a step are
+            // issued before any compare): one round trip per 256 tokens instead of per 32
+            constexpr int U = 8;
             int bad = 0;
-            for (int i = lane; i < m; i += 32) {
-                const int32_t et = __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15));
-                bad |= (et != tok[k + i]);
-                if (mk) bad |= mk[k + i];
+            for (int i0 = 0; i0 < m && !__any_sync(0xffffffffu, bad); i0 += 32 * U) {
+                int32_t et[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + 32 * u + lane;
+                    et[u] = i < m ? __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15)) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + 32 * u + lane;
+                    if (i < m) {
+                        bad |= (et[u] != tok[k + i]);
+                        if (mk) bad |= mk[k + i];
+                    }
+                }
             }
             if (__any_sync(0xffffffffu, bad) && lane == 0) vslot[k] = -1;
         }

@@ -17,7 +17,8 @@ from tests.test_gpu_fuzz_index import _workload  # noqa: E402
 def one(seed):
     heavy = seed % 2 == 0
     policy = [None, None, None, "fixed_chunk", "prefix_only"][seed % 5]
-    wl = _workload(seed, "bf16" if (seed // 2) % 2 else "fp32", heavy=heavy)
+    w = [8, 8, 32, 128][(seed // 7) % 4]                  # window lengths up to the paper's 128
+    wl = _workload(seed, "bf16" if (seed // 2) % 2 else "fp32", heavy=heavy, w=w)
     rho = (0, 4) if seed % 3 == 1 else (1, 4)          # no recompute marks: pages can link (NEXT-2)
     case = Case(wl, seed=seed, sample_reqs=None, use_reader_mask=seed % 7 != 0, policy=policy, rho=rho)
     rep = ParityReport()

@@ -25,6 +25,14 @@ namespace {
 
 constexpr int kNT = 512;
 
+#ifdef CP_MATCH_PROF
+// diagnostic build only: per-phase clock64 cycles of thread 0, summed over CTAs
+__device__ unsigned long long g_match_prof[8];
+#define MPROF(i) do { if (tid == 0) { const long long c_ = clock64(); atomicAdd(&g_match_prof[i], (unsigned long long)(c_ - t_m)); t_m = c_; } } while (0)
+#else
+#define MPROF(i) do {} while (0)
+#endif
+
 struct MatchArgs {
     DevHeader* hdr;
     const int32_t* tokens; const int64_t* offsets; const uint8_t* mask; int32_t R;
@@ -77,6 +85,9 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     if (tid == 0 && !cp_err_set(a.hdr) && n > a.nmax) cp_raise(a.hdr, CP_ERR_INVALID_ARG);
     if (tid == 0) { s_nc = 0; s_cands = 0; s_nh = 0; s_cov = 0; s_rec = 0; }
     int nh = 0;
+#ifdef CP_MATCH_PROF
+    long long t_m = clock64();
+#endif
     if (!skip) {
         // ---- 1. tokens + prefix hashes
         for (int i = tid; i < n; i += kNT) tok[i] = a.tokens[off + i];
@@ -85,6 +96,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         const int nw = n - a.w + 1;                  // number of windows (may be <= 0)
         for (int k = tid; k < nw; k += kNT) vslot[k] = -1;
         __syncthreads();
+        MPROF(0);
         // ---- 2. rolling windows -> prefix filter -> O(1) full-hash pre-check (warp-level probing)
         // windows examined: every k (the method), k = c*w (FixedChunk), k = 0 (PrefixOnly)
         const int kstep = a.policy == 1 ? a.w : 1;
@@ -116,6 +128,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         for (int o = 16; o; o >>= 1) my_cands += __shfl_xor_sync(0xffffffffu, my_cands, o);
         if (lane == 0 && my_cands) atomicAdd(&s_cands, my_cands);
         __syncthreads();
+        MPROF(1);
         const uint8_t* mk = a.mask ? a.mask + off : nullptr;
         if (a.policy == 2) {
             // ---- 3'. PrefixOnly: longest common prefix with each origin-0 candidate, one warp each
@@ -195,6 +208,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             if (__any_sync(0xffffffffu, bad) && lane == 0) vslot[k] = -1;
         }
         __syncthreads();
+        MPROF(2);
         // ---- 4. greedy left-to-right assembly (warp 0)
         if (wid == 0) {
             int cursor = 0;
@@ -248,6 +262,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         for (int o = 16; o; o >>= 1) { cov += __shfl_xor_sync(0xffffffffu, cov, o); rec += __shfl_xor_sync(0xffffffffu, rec, o); }
         if (lane == 0) { atomicAdd(&s_cov, cov); atomicAdd(&s_rec, rec); }
         __syncthreads();
+        MPROF(3);
         if (tid == 0) {
             a.req_cnt[r] = nh;
             a.req_covered[r] = s_cov; a.req_recompute[r] = s_rec; a.req_candidates[r] = s_cands;
@@ -260,10 +275,15 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(&a.hdr->match_done, 1u) == (unsigned)(a.R - 1));
     __syncthreads();
+    MPROF(4);
     if (!s_last) return;
     __threadfence();
     if (cp_err_set(a.hdr)) return;
-    // exclusive scan over R counts in chunks of kNT
+    // exclusive scan over R counts in chunks of kNT; the request table (hit offset, sparse source
+    // offset) is also kept in the dynamic shared memory, free by now, when it fits
+    const bool tab_smem = 8 * ((size_t)a.R + 1) <= MatchSmem(a.nmax, a.w).total;
+    int32_t* s_off = reinterpret_cast<int32_t*>(sm);
+    int32_t* s_src = s_off + (a.R + 1);
     int carry = 0;
     for (int b0 = 0; b0 < a.R; b0 += kNT) {
         const int i = b0 + tid;
@@ -279,10 +299,14 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             if (lane == 31) s_scan[kNT / 32] = xi;
         }
         __syncthreads();
-        if (i < a.R) a.req_hit_offsets[i] = carry + s_scan[wid] + inc - v;
+        if (i < a.R) {
+            a.req_hit_offsets[i] = carry + s_scan[wid] + inc - v;
+            if (tab_smem) { s_off[i] = carry + s_scan[wid] + inc - v; s_src[i] = (int32_t)(a.offsets[i] / a.w + i); }
+        }
         carry += s_scan[kNT / 32];
         __syncthreads();
     }
+    if (tab_smem && tid == 0) s_off[a.R] = carry;
     if (tid == 0) {
         a.req_hit_offsets[a.R] = carry;
         if (carry > a.max_hits) cp_raise(a.hdr, CP_ERR_CAPACITY);
@@ -292,6 +316,21 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     __threadfence_block();
     __syncthreads();
     if (carry > a.max_hits) return;
+    if (tab_smem) {
+        // thread per hit: its request by binary search over the offsets, then one round trip
+        for (int hh = tid; hh < carry; hh += kNT) {
+            int lo = 0, hi = a.R - 1;
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= hh) lo = mid; else hi = mid - 1; }
+            const int64_t src = s_src[lo] + (hh - s_off[lo]);
+            a.hit_req[hh] = lo;
+            a.hit_entry[hh] = *((volatile int32_t*)&a.sp_entry[src]);
+            a.hit_slot[hh] = *((volatile int32_t*)&a.sp_slot[src]);
+            a.hit_dst[hh] = *((volatile int32_t*)&a.sp_dst[src]);
+            a.hit_len[hh] = *((volatile int32_t*)&a.sp_len[src]);
+            a.hit_delta[hh] = *((volatile int32_t*)&a.sp_delta[src]);
+        }
+        return;
+    }
     for (int rr = wid; rr < a.R; rr += kNT / 32) {
         const int cnt = *((volatile int32_t*)&a.req_cnt[rr]);
         const int dst0 = a.req_hit_offsets[rr];
@@ -351,3 +390,10 @@ extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, 
     CP_COUNT_LAUNCH();
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
+
+#ifdef CP_MATCH_PROF
+extern "C" cp_status cp_match_prof_read(unsigned long long* out_h) {
+    if (cudaMemcpyFromSymbol(out_h, g_match_prof, sizeof(unsigned long long) * 8) != cudaSuccess) return CP_ERR_CUDA;
+    return CP_OK;
+}
+#endif

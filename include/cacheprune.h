@@ -77,7 +77,8 @@ typedef struct {
     int64_t  pool_capacity_tokens;  /* LRU budget in tokens (R#21)                              */
     int32_t  max_entries;           /* live-entry slots (>= capacity/window_len + max_spans_per_insert + 1) */
     int32_t  max_span_len;          /* longest storable segment                                          */
-    int32_t  max_req_tokens;        /* longest request accepted by cp_match_spans (<= 10240)             */
+    int32_t  max_req_tokens;        /* longest request accepted by cp_match_spans (<= 2^20); above 10240
+                                       the matcher keeps its per-request arrays in SCRATCH (24 B/token) */
     int32_t  max_batch_reqs;        /* most requests per match / insert call                             */
     int64_t  max_batch_tokens;      /* most tokens per match / insert call                               */
     int32_t  max_spans_per_insert;  /* most spans per insert call                                        */

@@ -120,6 +120,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(4 * (size_t)L->MS);                                 // 27 span_rep
     sput(sizeof(Rec16) * (size_t)L->MS);                     // 28 precs
     sput(4 * (size_t)(S + L->MS));                           // 29 rm_pos (FIFO tail position per removal)
+    // 30 matcher arrays for long requests: request r at 24 * offsets[r] + 64 * r (cp_match.cu)
+    sput(c->max_req_tokens > CP_MATCH_SMEM_TOKENS ? 24 * (size_t)c->max_batch_tokens + 64 * (size_t)c->max_batch_reqs + 64 : 16);
     L->scr_size = o;
 }
 
@@ -1272,6 +1274,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->eq_old = (int32_t*)(s + L.scr_off[25]); x->dtab = (HEntry*)(s + L.scr_off[26]);
     x->span_rep = (int32_t*)(s + L.scr_off[27]); x->precs = (Rec16*)(s + L.scr_off[28]);
     x->rm_pos = (int32_t*)(s + L.scr_off[29]);
+    x->match_g = cfg->max_req_tokens > CP_MATCH_SMEM_TOKENS ? s + L.scr_off[30] : nullptr;
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;

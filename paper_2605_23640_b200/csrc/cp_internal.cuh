@@ -18,7 +18,8 @@
 #define CP_BLOCK 16
 #define CP_MAX_LAYERS 128
 #define CP_GATHER_CHUNK 32          // tokens per gather work item
-#define CP_MAX_MATCH_TOKENS 10240   // per request, limited by shared memory (20 B / token)
+#define CP_MATCH_SMEM_TOKENS 10240  // requests up to this length keep the matcher's arrays in shared memory
+#define CP_MAX_MATCH_TOKENS (1 << 20) // longer ones (cfg.max_req_tokens > CP_MATCH_SMEM_TOKENS) use scratch
 #define CP_NO_ERR_KEY (~0ULL)
 
 // slot states
@@ -72,6 +73,7 @@ struct cp_index {
     cp_config cfg;
     int64_t P;           // physical pages
     int32_t MP;          // max pages per entry
+    char* match_g = nullptr;   // matcher arrays in global scratch (only when max_req_tokens > CP_MATCH_SMEM_TOKENS)
     int insert_prepared = 0;   // cp_index_insert_prepare issued, commit pending (host-side guard)
     int32_t S;           // slots
     int64_t T;           // prefix-table entries (pow2)

@@ -43,6 +43,8 @@ struct MatchArgs {
     const unsigned long long* slot_full; unsigned long long* slot_last;
     const int32_t* slot_pages; int32_t MP; const int32_t* page_tokens; const uint16_t* page_bits;
     int32_t nmax;                      // shared memory is sized for requests of <= nmax tokens
+    char* gscr;                        // long requests: per-request arrays in global scratch (else null)
+    int32_t dyn_smem;                  // dynamic shared memory bytes of this launch
     int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;
     int32_t max_hits; int32_t* num_hits; int32_t* req_hit_offsets;
     int32_t *hit_req, *hit_entry, *hit_slot, *hit_dst, *hit_len, *hit_delta;
@@ -64,23 +66,27 @@ struct MatchSmem {
     }
 };
 
+// G: the per-request arrays (prefix hashes, window slots, tokens, candidates, hits) live in global
+// scratch at 24 * offsets[r] + 64 * r (laid out for the request's own length) instead of shared memory
+template <bool G>
 __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ uint64_t wtmp[2 * (kNT / 32)];
     __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last;
     __shared__ int s_scan[kNT / 32 + 1];
-    const MatchSmem L(a.nmax, a.w);
-    uint64_t* h = (uint64_t*)(sm + L.h);
-    int32_t* vslot = (int32_t*)(sm + L.vslot);
-    int32_t* tok = (int32_t*)(sm + L.tok);
-    int32_t* clist = (int32_t*)(sm + L.clist);
-    int32_t* hk = (int32_t*)(sm + L.hk);
-    int32_t* hs = (int32_t*)(sm + L.hs);
-    int32_t* hm = (int32_t*)(sm + L.hm);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int r = blockIdx.x;
     const int64_t off = a.offsets[r];
     const int n = (int)(a.offsets[r + 1] - off);
+    const MatchSmem L(G ? max(n, 1) : a.nmax, a.w);
+    unsigned char* base = G ? reinterpret_cast<unsigned char*>(a.gscr) + 24 * off + 64 * (int64_t)r : sm;
+    uint64_t* h = (uint64_t*)(base + L.h);
+    int32_t* vslot = (int32_t*)(base + L.vslot);
+    int32_t* tok = (int32_t*)(base + L.tok);
+    int32_t* clist = (int32_t*)(base + L.clist);
+    int32_t* hk = (int32_t*)(base + L.hk);
+    int32_t* hs = (int32_t*)(base + L.hs);
+    int32_t* hm = (int32_t*)(base + L.hm);
     const bool skip = cp_err_set(a.hdr) || n > a.nmax;
     if (tid == 0 && !cp_err_set(a.hdr) && n > a.nmax) cp_raise(a.hdr, CP_ERR_INVALID_ARG);
     if (tid == 0) { s_nc = 0; s_cands = 0; s_nh = 0; s_cov = 0; s_rec = 0; }
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     if (cp_err_set(a.hdr)) return;
     // exclusive scan over R counts in chunks of kNT; the request table (hit offset, sparse source
     // offset) is also kept in the dynamic shared memory, free by now, when it fits
-    const bool tab_smem = 8 * ((size_t)a.R + 1) <= MatchSmem(a.nmax, a.w).total;
+    const bool tab_smem = 8 * ((size_t)a.R + 1) <= (size_t)a.dyn_smem;
     int32_t* s_off = reinterpret_cast<int32_t*>(sm);
     int32_t* s_src = s_off + (a.R + 1);
     int carry = 0;
@@ -381,12 +387,21 @@ extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, 
     a.hit_req = o->hit_req; a.hit_entry = o->hit_entry; a.hit_slot = o->hit_slot; a.hit_dst = o->hit_dst;
     a.hit_len = o->hit_len; a.hit_delta = o->hit_delta; a.plan = o->plan;
     a.req_covered = o->req_covered; a.req_recompute = o->req_recompute; a.req_candidates = o->req_candidates;
-    const size_t smem = MatchSmem(nmax, a.w).total;
     static int attr_set = 0;
-    if (!attr_set) { cudaFuncSetAttribute(k_match, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024); attr_set = 1; }
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_match<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        cudaFuncSetAttribute(k_match<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        attr_set = 1;
+    }
+    const bool global = nmax > CP_MATCH_SMEM_TOKENS;
+    if (global && !x->match_g) return CP_ERR_UNSUPPORTED;
+    // long requests: arrays in scratch; the dynamic shared memory only holds the compaction table
+    const size_t smem = global ? std::min<size_t>(8 * ((size_t)b->num_reqs + 1), 48 * 1024) : MatchSmem(nmax, a.w).total;
     if (smem > 210 * 1024) return CP_ERR_UNSUPPORTED;
+    a.gscr = x->match_g; a.dyn_smem = (int32_t)smem;
     CP_CUDA_CHECK(cudaMemsetAsync(&x->hdr->match_done, 0, 4, st));
-    k_match<<<b->num_reqs, kNT, smem, st>>>(a);
+    if (global) k_match<true><<<b->num_reqs, kNT, smem, st>>>(a);
+    else k_match<false><<<b->num_reqs, kNT, smem, st>>>(a);
     CP_COUNT_LAUNCH();
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }

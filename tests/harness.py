@@ -113,7 +113,7 @@ class Case:
             rope_theta=g.rope_theta, rope_style=g.rope_style, window_len=w, hash_seed=hash_seed,
             pool_capacity_tokens=wl.pool_capacity_tokens,
             max_entries=min(131072, wl.pool_capacity_tokens // w + max(spans + [1]) + 64),
-            max_span_len=wl.max_span_len, max_req_tokens=min(10240, max(lens + [1])),
+            max_span_len=wl.max_span_len, max_req_tokens=max(lens + [1]),
             max_batch_reqs=max(reqs + [1]), max_batch_tokens=max(toks + [1]),
             max_spans_per_insert=max(spans + [1]), layer_offset=self.l0, head_offset=self.h0)
         self.dev = cp.KVIndex(self.cfg, self.device)

@@ -469,3 +469,30 @@ def test_split_insert_misuse_is_rejected_without_side_effects():
     assert after["next_id"] == before["next_id"] and after["num_live"] == before["num_live"]
     case.dev.insert(db, kv, *spans, t=1, phase="commit")
     assert case.dev.snapshot()["num_live"] > 0
+
+
+@pytest.mark.parametrize("n_long", [10241, 30000, 65536])
+def test_requests_longer_than_shared_memory(n_long):
+    """Requests beyond the shared-memory matcher (max_req_tokens > 10240): the per-request arrays
+    live in scratch; hits, plans, stats, the index and sampled KV rows still match the oracle,
+    alongside short requests in the same batch."""
+    g = Geometry(2, 1, 32, "bf16", 500000.0)
+    rng = np.random.default_rng(n_long)
+    base = rng.integers(1000, 50000, n_long).astype(np.int32)
+    spans = [(0, 3000), (5000, 2047), (n_long - 2000, 2000)]
+    w = Batch(tokens=base.copy(), offsets=np.array([0, n_long], np.int64), mask=np.zeros(n_long, np.uint8),
+              writer_ids=np.array([0], np.int64), span_req=np.zeros(len(spans), np.int32),
+              span_begin=np.array([s_[0] for s_ in spans], np.int32), span_len=np.array([s_[1] for s_ in spans], np.int32))
+    shifted = np.concatenate([rng.integers(1000, 50000, 77).astype(np.int32), base])          # every hit moves
+    parts = [Batch(tokens=shifted, offsets=np.array([0, len(shifted)], np.int64), mask=np.zeros(len(shifted), np.uint8),
+                   writer_ids=np.array([1], np.int64)),
+             Batch(tokens=base[5000:7047].copy(), offsets=np.array([0, 2047], np.int64), mask=np.zeros(2047, np.uint8),
+                   writer_ids=np.array([2], np.int64)),
+             Batch(tokens=base[:50].copy(), offsets=np.array([0, 50], np.int64), mask=np.zeros(50, np.uint8),
+                   writer_ids=np.array([3], np.int64))]
+    from synth.gen import Workload
+    wl = Workload("long", g, [(w, pack_batches(parts))], pool_capacity_tokens=100000, max_span_len=4096)
+    case = Case(wl, sample_reqs=2)
+    res = run_round_parity(case, score=False)
+    _assert(res)
+    assert res["hits"] == 4 and res["moved_hits"] == 4

@@ -32,8 +32,8 @@ def main():
     wb = pack_batches(writers)
     cap = int(wb.span_len.sum()) + 1024
     cfg = cp.IndexConfig(num_layers=1, num_kv_heads=1, head_dim=16, dtype="bf16", pool_capacity_tokens=cap,
-                         max_entries=cap // 128 + nseg + 64, max_span_len=512, max_req_tokens=10240,
-                         max_batch_reqs=nseg, max_batch_tokens=max(wb.total_tokens, 10240), max_spans_per_insert=nseg)
+                         max_entries=cap // 128 + nseg + 64, max_span_len=512, max_req_tokens=50000,
+                         max_batch_reqs=nseg, max_batch_tokens=max(wb.total_tokens, 50000), max_spans_per_insert=nseg)
     dev = torch.device("cuda", 0)
     idx = cp.KVIndex(cfg, dev)
     db = cp.DeviceBatch.from_numpy(wb.tokens, wb.offsets, wb.mask, dev)
@@ -50,7 +50,7 @@ def main():
     oidx = O.OracleIndex(128, 42, cap, idx.num_pages)
     oidx.insert(wb, None, None, 1)
     out = {"paper_cpu_ms_at_10k": 8.3, "paper_hw": "2x Xeon Silver 4510 (CPU retriever), P:L1220", "rows": []}
-    for n in [2500, 5000, 7500, 10000]:
+    for n in [2500, 5000, 7500, 10000, 20000, 50000]:        # > 10240: the scratch-array matcher
         # request: segments planted between fresh filler, ~70% covered
         parts, used = [], 0
         while used < n:

@@ -583,9 +583,25 @@ def oracle_sample(wl, wb, rb, seconds: float, max_reqs: int = 64, seed: int = 0)
     return reused_bytes, covered, secs, n
 
 
+def host_cpu():
+    """CPU model and logical core count of this host (report nproc and the model)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
 def cpu_baseline(args, S):
     rb_, cov, secs, n = oracle_sample(S.wl, S.wb, S.rb, args.cpu_seconds)
+    model, nproc = host_cpu()
     return {"value": round(rb_ / secs / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "cpu_model": model, "host_logical_cores": nproc,
             "matched_tokens_per_s": round(cov / secs, 1),
             "sample": f"{n} of {S.rb.num_reqs} reader requests (match + fp64 gather/re-rotation of all "
                       f"{S.g.num_layers} layers + score + insert) against the full 256-writer index, "
@@ -614,6 +630,7 @@ def bench_reference(args):
            "config": {"workload": wl.name + f" (BASELINE configs[{args.config - 1}])", "requests": rb.num_reqs},
            "matched_tokens_per_s": round(tot_cov / tot_s, 1),
            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                            "cpu_model": host_cpu()[0], "host_logical_cores": host_cpu()[1],
                             "sample": f"each step: reader requests of the workload for ~{per:.1f} s "
                                       "(match + fp64 gather/re-rotation + score + insert), single-threaded"},
            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

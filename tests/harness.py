@@ -14,14 +14,13 @@ KV rows are the generator's payload re-rotated by the oracle.
 """
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
 import oracle.oracle as O
-from synth.gen import (Batch, Geometry, Workload, bf16_round_np, fill_paged_kv_torch, make_workload,
+from synth.gen import (Batch, Workload, bf16_round_np, fill_paged_kv_torch, make_workload,
                        payload_np)
 
 SENTINEL = 5.0        # pre-filled into destination caches: outside every payload / rotated value

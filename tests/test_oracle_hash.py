@@ -9,7 +9,6 @@ import os
 import struct
 
 import numpy as np
-import pytest
 
 import oracle.oracle as O
 

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle.oracle as O
-from synth.gen import Batch, pack_batches
+from synth.gen import Batch
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 

@@ -496,3 +496,43 @@ def test_requests_longer_than_shared_memory(n_long):
     res = run_round_parity(case, score=False)
     _assert(res)
     assert res["hits"] == 4 and res["moved_hits"] == 4
+
+
+def test_layer_and_head_shards_concatenate_to_the_full_gather():
+    """SURVEY §4 multi-GPU layer: each shard's index (layer ranges, head ranges) gathers exactly the
+    slice of the one-index gather -- K (moved or not) and V bit for bit -- and the shards' hits,
+    plans and index metadata equal the full index's (they replay the same inserts)."""
+    wl = make_workload(2, scale=0.05)
+    wb, rb = wl.rounds[0]
+
+    def run(**kw):
+        case = Case(wl, seed=5, **kw)
+        rep = ParityReport()
+        case.insert(wb, rep, bits_flags=[np.arange(int(m)) % 4 == 0 for m in wb.span_len])
+        assert rep.ok, rep.notes
+        db = case._dev_batch(rb)
+        hits = case.dev.match_spans(db, 50)
+        dst = case.dst_kv(rb)
+        case.dev.gather_rerotate(db, hits, dst)
+        bt = dst.block_tables.cpu().numpy()
+        rows = []
+        for r in range(rb.num_reqs):
+            q = np.arange(int(rb.lens[r]))
+            blk = torch.from_numpy(bt[r, q // 16].astype(np.int64)).cuda()
+            sl = torch.from_numpy((q % 16).astype(np.int64)).cuda()
+            rows.append((torch.stack([k[blk, sl] for k in dst.k]).cpu(), torch.stack([v[blk, sl] for v in dst.v]).cpu()))
+        h = hits.to_host()
+        return rows, {k: h[k] for k in ("hit_entry", "hit_dst", "hit_len", "hit_delta", "plan")}
+
+    full_rows, full_hits = run()
+    for kw, sel in [(dict(layer_range=(0, 13)), (slice(0, 13), slice(None))),
+                    (dict(layer_range=(13, 32)), (slice(13, 32), slice(None))),
+                    (dict(head_range=(0, 3)), (slice(None), slice(0, 3))),
+                    (dict(head_range=(3, 8)), (slice(None), slice(3, 8)))]:
+        rows, hits = run(**kw)
+        for key in full_hits:
+            assert np.array_equal(hits[key], full_hits[key]), (kw, key)
+        for (fk, fv), (sk, sv) in zip(full_rows, rows):
+            ls, hsl = sel
+            assert torch.equal(sk.view(torch.int16), fk[ls, :, hsl].contiguous().view(torch.int16)), kw
+            assert torch.equal(sv.view(torch.int16), fv[ls, :, hsl].contiguous().view(torch.int16)), kw

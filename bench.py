@@ -45,9 +45,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
-    ap.add_argument("--overlap", type=int, default=2, choices=[0, 1, 2],
-                    help="2 (default): N3 beside the insert's read-only half after the gather; 1: N3 beside "
-                         "match + gather; 0: serialized (see run_step)")
+    ap.add_argument("--overlap", type=int, default=3, choices=[0, 1, 2, 3],
+                    help="3 (default): the insert's read-only half beside match + gather, N3 after the gather "
+                         "on the main stream; 2: N3 beside the insert's read-only half after the gather; "
+                         "1: N3 beside match + gather; 0: serialized (see run_step)")
     ap.add_argument("--shard-world", type=int, default=0,
                     help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
     ap.add_argument("--shard-rank", type=int, default=0)
@@ -250,9 +251,10 @@ def setup_ours(args, rank, world, device):
     S.link = bool(getattr(args, "link", False))
     S.link_tab = torch.full((rb.num_reqs, max(nb)), -1, dtype=torch.int32, device=device)
     S.side = torch.cuda.Stream(device=device)
-    S.overlap = int(getattr(args, "overlap", 2))
+    S.overlap = int(getattr(args, "overlap", 3))
     S.ev_score_done = torch.cuda.Event()
     S.ev_gather_done = torch.cuda.Event()
+    S.ev_prep_done = torch.cuda.Event()
     S.ins_out = (torch.full((max(len(ib.span_len), 1),), -1, dtype=torch.int32, device=device),
                  torch.full((max(len(ib.span_len), 1),), -1, dtype=torch.int32, device=device))
     S.ev_insert_done = torch.cuda.Event()
@@ -275,10 +277,12 @@ def score_spans(b, device, torch, cp, attention_torch):
 
 def run_step(S, torch, cp, world, events=None):
     """One pass of the hot path.  Scheduling (--overlap):
-      2 (default): match -> gather on the main stream; then N3 on a side stream concurrently with the
-         insert's read-only half (cp_index_insert_prepare: validation, hashing, dedup, containment
-         scan -- latency-bound kernels that leave HBM idle); the commit waits for both.  The gather
-         runs alone at full bandwidth.
+      3 (default): the insert's read-only half (cp_index_insert_prepare: validation, hashing, dedup,
+         containment scan -- latency-bound kernels; it needs only the previous commit) on a side
+         stream beside match + gather; on the main stream match -> gather -> N3 (+ the bit broadcast)
+         -> commit after the prepare.  No cross-stream hop on the critical path.
+      2: match -> gather on the main stream; then N3 on a side stream concurrently with the
+         insert's read-only half; the commit waits for both.
       1: N3 on a side stream concurrently with match + gather (it then competes with the gather).
       0: everything serialized on one stream.
     The side stream first waits for the previous step's insert (which read the bits N3 overwrites)."""
@@ -298,6 +302,14 @@ def run_step(S, torch, cp, world, events=None):
         S.ev_score_done.record()
 
     ins = (S.ins_db, S.ins_kv, *S.spans, S.bits, S.bits_off, S.t)
+    if S.overlap == 3:
+        # the insert's read-only half on the side stream, beside match + gather (it needs only the
+        # previous commit); N3 then runs on the main stream right after the gather (no cross-stream
+        # hop on the critical path) and the commit waits for the prepare
+        S.side.wait_event(S.ev_insert_done)
+        with torch.cuda.stream(S.side):
+            S.idx.insert(*ins, out=S.ins_out, phase="prepare")
+            S.ev_prep_done.record()
     if scores and S.overlap in (0, 1):
         S.side.wait_event(S.ev_insert_done)
         with torch.cuda.stream(S.side if S.overlap == 1 else main):
@@ -309,7 +321,13 @@ def run_step(S, torch, cp, world, events=None):
         S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
     S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True, skip_linked=S.link)   # N2
     if ev: ev[2].record()
-    if S.overlap == 2:
+    if S.overlap == 3:
+        if scores:
+            score()                                                                # N3 (+ C1), main stream
+        main.wait_event(S.ev_prep_done)
+        if ev: ev[3].record()
+        S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
+    elif S.overlap == 2:
         if scores:
             S.ev_gather_done.record()
             S.side.wait_event(S.ev_gather_done)
@@ -455,10 +473,11 @@ def bench_ours(args):
             "match_rate": round(cov / S.rb.total_tokens, 4),
             "value_frac_of_peak": round(value / (peak * world), 4),
             "breakdown_ms": {"match": round(float(phase[:, 0].mean()), 4), "gather": round(gather_ms, 4),
-                             ("insert_prepare_and_wait_score" if S.overlap == 2 else "wait_score"): round(float(phase[:, 2].mean()), 4),
-                             ("insert_commit" if S.overlap == 2 else "insert"): round(float(phase[:, 3].mean()), 4),
+                             {2: "insert_prepare_and_wait_score", 3: "score_and_wait_prepare"}.get(S.overlap, "wait_score"): round(float(phase[:, 2].mean()), 4),
+                             ("insert_commit" if S.overlap in (2, 3) else "insert"): round(float(phase[:, 3].mean()), 4),
                              "score_side_stream": round(score_ms, 4),
-                             "note": {2: "score (N3) on a side stream after the gather, beside the insert's read-only half",
+                             "note": {3: "insert's read-only half on a side stream beside match + gather; score (N3) on the main stream after the gather",
+                                      2: "score (N3) on a side stream after the gather, beside the insert's read-only half",
                                       1: "score (N3) on a side stream concurrently with match + gather",
                                       0: "score (N3) serialized before match on the same stream"}[S.overlap]},
             "roofline": {"kernel": "k_rows (cp_gather_rerotate: prep + rows)", "bound": "hbm",

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("overlap", [2, 0])
+@pytest.mark.parametrize("overlap", [3, 2, 0])
 def test_two_rank_bench_runs_and_reports(overlap):
     env = dict(os.environ, BENCH_DEVICE0="1", BENCH_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",

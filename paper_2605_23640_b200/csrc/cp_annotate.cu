@@ -28,7 +28,7 @@ namespace {
 constexpr int kAnnReqsPerLaunch = 512;
 constexpr int kBestThreads = 256;           // one start l per thread; a CTA covers 256 starts
 constexpr int kRowUnroll = 32;            // k_ann_best: rows of R(i, l) in flight per thread
-constexpr int kRowsBatch = 8;               // k_ann_rows: 32-column chunks whose loads are in flight together
+constexpr int kRowsBatch = 2;               // k_ann_rows: 128-column chunks whose loads are in flight together
 
 struct AnnReq {
     const float* A;          // [heads][n][n]
@@ -72,24 +72,31 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
         long long* R = reinterpret_cast<long long*>(a.ws + rq.r_off) + (int64_t)i * (n + 1);
         long long carry = 0;
         if (lane == 0) R[0] = 0;
-        // kRowsBatch chunks of 32 columns per step: all their loads are issued before the scans, so a
-        // row costs one memory round trip per 32 * kRowsBatch columns instead of one per 32
-        for (int base = 0; base <= i; base += 32 * kRowsBatch) {
-            long long v[kRowsBatch];
+        // a lane owns 4 consecutive columns of each 128-column chunk, kRowsBatch chunks per step: all
+        // loads of a step are issued before any scan, and one warp scan serves 128 columns
+        for (int base = 0; base <= i; base += 128 * kRowsBatch) {
+            long long v[kRowsBatch][4];
+#pragma unroll
+            for (int u = 0; u < kRowsBatch; ++u)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int x = base + u * 128 + 4 * lane + e;
+                    v[u][e] = 0;
+                    if (x <= i)
+                        for (int h = 0; h < rq.heads; ++h) v[u][e] += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
+                }
 #pragma unroll
             for (int u = 0; u < kRowsBatch; ++u) {
-                const int x = base + u * 32 + lane;
-                v[u] = 0;
-                if (x <= i)
-                    for (int h = 0; h < rq.heads; ++h) v[u] += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
-            }
-#pragma unroll
-            for (int u = 0; u < kRowsBatch; ++u) {
-                const int x = base + u * 32 + lane;
-                long long inc = v[u];
+                const long long p1 = v[u][0] + v[u][1], p2 = p1 + v[u][2], p3 = p2 + v[u][3];
+                long long inc = p3;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-                if (x <= i) R[x + 1] = carry + inc;
+                const long long ex = carry + inc - p3;                 // sum before this lane's 4 columns
+                const int x0 = base + u * 128 + 4 * lane;
+                if (x0 <= i) R[x0 + 1] = ex + v[u][0];
+                if (x0 + 1 <= i) R[x0 + 2] = ex + p1;
+                if (x0 + 2 <= i) R[x0 + 3] = ex + p2;
+                if (x0 + 3 <= i) R[x0 + 4] = ex + p3;
                 carry += __shfl_sync(0xffffffffu, inc, 31);
             }
         }

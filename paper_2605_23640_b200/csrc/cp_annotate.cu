@@ -21,12 +21,15 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 namespace {
 
 constexpr int kAnnReqsPerLaunch = 512;
-constexpr int kBestThreads = 256;           // one start l per thread; a CTA covers 256 starts
+constexpr int kBestThreads = 256;           // k_ann_best CTA: 8 warps
+constexpr int kStarts = 32;                 // starts l per k_ann_best CTA (one per lane)
+constexpr int kRowWarps = kBestThreads / 32;   // the segment's rows are split across the CTA's warps
 constexpr int kRowUnroll = 32;            // k_ann_best: rows of R(i, l) in flight per thread
 constexpr int kRowsBatch = 2;               // k_ann_rows: 128-column chunks whose loads are in flight together
 
@@ -38,14 +41,14 @@ struct AnnReq {
     long long s_off;         // segments, then the per-(segment, chunk) partial bests
     int32_t n, heads;
     int32_t row_begin;       // first global row of this request within the launch
-    int32_t pad;
+    int32_t nch;             // partial-best stride per segment: ceil(n / kStarts) (the workspace's sizing)
 };
 
 struct PartialBest { long long d; int32_t len; int32_t l; };
 
 struct AnnArgs {
     AnnReq rq[kAnnReqsPerLaunch];
-    int32_t nreq, total_rows, min_len, max_seg, nchunk;
+    int32_t nreq, total_rows, min_len, max_seg, nchunk, cw;   // cw: starts per k_ann_best chunk
     char* ws;
     int32_t* out_nseg;       // launch bases
     int32_t* out_l;
@@ -197,9 +200,9 @@ __device__ __forceinline__ bool better(const Best& x, const Best& y) {      // d
     return x.l < y.l;
 }
 
-// CTA per (request, segment, chunk of 256 starts l): thread per l walks rows i = l..b (unrolled, the row
+// Many-request launches: CTA per (request, segment, chunk of 256 starts l): thread per l walks rows i = l..b (unrolled, the row
 // loads of one step issued together) accumulating sum R(i, l); P(i+1) comes from shared memory.
-__global__ void __launch_bounds__(kBestThreads) k_ann_best(const AnnArgs a) {
+__global__ void __launch_bounds__(kBestThreads) k_ann_best_flat(const AnnArgs a) {
     __shared__ long long s_d[kBestThreads / 32];
     __shared__ int s_len[kBestThreads / 32], s_l[kBestThreads / 32];
     extern __shared__ long long sP[];                                       // P(sa .. sb+1)
@@ -260,7 +263,98 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best(const AnnArgs a) {
         Best b{0, -1, 0};
         for (int w = 0; w < kBestThreads / 32; ++w) { const Best y{s_d[w], s_len[w], s_l[w]}; if (better(y, b)) b = y; }
         PartialBest pb; pb.d = b.d; pb.len = b.len; pb.l = b.l;
-        part[s * a.nchunk + ch] = pb;
+        part[s * rq.nch + ch] = pb;
+    }
+}
+
+// Few-request launches (the flat kernel would fill a fraction of the SMs and its critical path is a
+// whole segment): CTA per (request, segment, chunk of 32 starts l): lane = start, warp w = one of 8 contiguous row
+// ranges of the segment.  Pass 1: each warp sums R(i, l) over its rows i >= l; the per-warp sums are
+// scanned in shared memory, so pass 2 walks each row range from its exact prefix and evaluates
+// P(i+1) - P(l) - 2 * sum_{k=l}^{i} R(k, l) for every admissible end i.  The critical path is one
+// eighth of the segment, at the price of reading R twice.
+__global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a) {
+    __shared__ long long s_sum[kRowWarps][kStarts];
+    __shared__ long long s_d[kRowWarps];
+    __shared__ int s_len[kRowWarps], s_l[kRowWarps];
+    const int per_req = a.max_seg * a.nchunk;
+    const int q = blockIdx.x / per_req, rem = blockIdx.x % per_req;
+    const int s = rem / a.nchunk, ch = rem % a.nchunk;
+    const AnnReq& rq = a.rq[q];
+    const int nseg = a.out_nseg[q];
+    if (nseg < 0 || s >= nseg) return;
+    const int2 sg = reinterpret_cast<const int2*>(a.ws + rq.s_off)[s];
+    PartialBest* part = reinterpret_cast<PartialBest*>(a.ws + rq.s_off + 8 * (size_t)a.max_seg);
+    const int n = rq.n, sa = sg.x, sb = sg.y;
+    const int lmax = sb - a.min_len + 1;                                   // last admissible start
+    const int l_lo = sa + ch * kStarts;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (l_lo > lmax) return;                                                // no admissible start in this chunk
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    const long long* P = reinterpret_cast<const long long*>(a.ws + rq.p_off);
+    const int l = l_lo + lane;
+    const bool act = l <= lmax;
+    const int cs = (sb - l_lo + kRowWarps) / kRowWarps;                    // rows l_lo..sb split in 8
+    const int r0 = max(l_lo + wid * cs, l), r1 = min(sb, l_lo + (wid + 1) * cs - 1);
+    // pass 1: this warp's partial sum of R(i, l)
+    long long part_sum = 0;
+    if (act) {
+        int i = r0;
+        for (; i + kRowUnroll - 1 <= r1; i += kRowUnroll) {
+            long long v[kRowUnroll];
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) part_sum += v[u];
+        }
+        for (; i <= r1; ++i) part_sum += __ldg(R + (int64_t)i * (n + 1) + l);
+    }
+    s_sum[wid][lane] = part_sum;
+    __syncthreads();
+    long long acc = 0;
+    for (int w = 0; w < wid; ++w) acc += s_sum[w][lane];                   // rows before r0 (and >= l)
+    // pass 2: candidates (l, i) for i in this warp's rows
+    Best best{0, -1, 0};
+    if (act && r0 <= r1) {
+        const long long Pl = __ldg(P + l);
+        const int rmin = l + a.min_len - 1;
+        int i = r0;
+        for (; i + kRowUnroll - 1 <= r1; i += kRowUnroll) {
+            long long v[kRowUnroll], pv[kRowUnroll];
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) {
+                v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+                pv[u] = __ldg(P + i + u + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < kRowUnroll; ++u) {
+                acc += v[u];
+                if (i + u >= rmin) {
+                    const Best c{pv[u] - Pl - 2 * acc, i + u - l + 1, l};
+                    if (better(c, best)) best = c;
+                }
+            }
+        }
+        for (; i <= r1; ++i) {
+            acc += __ldg(R + (int64_t)i * (n + 1) + l);
+            if (i >= rmin) {
+                const Best c{__ldg(P + i + 1) - Pl - 2 * acc, i - l + 1, l};
+                if (better(c, best)) best = c;
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const Best y{__shfl_xor_sync(0xffffffffu, best.d, o), __shfl_xor_sync(0xffffffffu, best.len, o),
+                     __shfl_xor_sync(0xffffffffu, best.l, o)};
+        if (better(y, best)) best = y;
+    }
+    if (lane == 0) { s_d[wid] = best.d; s_len[wid] = best.len; s_l[wid] = best.l; }
+    __syncthreads();
+    if (tid == 0) {
+        Best b{0, -1, 0};
+        for (int w = 0; w < kRowWarps; ++w) { const Best y{s_d[w], s_len[w], s_l[w]}; if (better(y, b)) b = y; }
+        PartialBest pb; pb.d = b.d; pb.len = b.len; pb.l = b.l;
+        part[s * rq.nch + ch] = pb;
     }
 }
 
@@ -276,8 +370,8 @@ __global__ void k_ann_final(const AnnArgs a) {
     const PartialBest* part = reinterpret_cast<const PartialBest*>(a.ws + rq.s_off + 8 * (size_t)a.max_seg);
     const int lmax = sg.y - a.min_len + 1;
     Best b{0, -1, 0};
-    for (int ch = 0; ch < a.nchunk && sg.x + ch * kBestThreads <= lmax; ++ch) {
-        const PartialBest pb = part[s * a.nchunk + ch];
+    for (int ch = 0; ch < a.nchunk && sg.x + ch * a.cw <= lmax; ++ch) {
+        const PartialBest pb = part[s * rq.nch + ch];
         const Best y{pb.d, pb.len, pb.l};
         if (better(y, b)) b = y;
     }
@@ -296,7 +390,7 @@ extern "C" size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, in
     size_t tot = 0;
     for (int r = 0; r < num_reqs; ++r) {
         const size_t n = (size_t)std::max(n_h[r], 0);
-        const size_t nch = (n + kBestThreads - 1) / kBestThreads;
+        const size_t nch = (n + kStarts - 1) / kStarts;
         tot += align256(8 * n * (n + 1)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * nch);
     }
     return tot;
@@ -331,14 +425,24 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
             d.r_off = (long long)off; off += align256(8 * n * (n + 1));
             d.p_off = (long long)off; off += align256(8 * (n + 1));
             d.s_off = (long long)off;
-            off += align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * ((n + kBestThreads - 1) / kBestThreads));
+            d.nch = (int32_t)((n_h[r] + kStarts - 1) / kStarts);
+            off += align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * ((n + kStarts - 1) / kStarts));
             nmax = std::max<int64_t>(nmax, (int64_t)n);
             d.row_begin = (int32_t)rows;
             rows += n_h[r];
         }
         if (rows > INT32_MAX) return CP_ERR_INVALID_ARG;
         a.total_rows = (int32_t)rows; a.min_len = min_len; a.max_seg = max_segments;
-        a.nchunk = (int32_t)((nmax + kBestThreads - 1) / kBestThreads);
+        // flat (thread per start, whole segment per thread) when the launch already has a couple of
+        // waves of 256-start chunks and P fits in shared memory; otherwise split the rows across warps
+        const size_t psmem = 8 * ((size_t)nmax + 2);
+        const char* ev = getenv("CP_ANN_VARIANT");            // A/B and parity: 1 = flat, 2 = split, else auto
+        const int var = ev ? atoi(ev) : 0;
+        const bool fits = psmem <= 200 * 1024;
+        const bool flat = fits && (var == 1 || (var != 2 && (long long)a.nreq * ((nmax + kBestThreads - 1) / kBestThreads) >=
+                                                                2LL * cp_sm_count()));
+        a.cw = flat ? kBestThreads : kStarts;
+        a.nchunk = (int32_t)((nmax + a.cw - 1) / a.cw);
         a.ws = (char*)workspace;
         a.out_nseg = out_nseg + r0;
         a.out_l = out_l + (int64_t)r0 * max_segments;
@@ -348,13 +452,15 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
         CP_COUNT_LAUNCH();
         k_ann_segs<<<a.nreq, 1024, 0, st>>>(a);
         CP_COUNT_LAUNCH();
-        const size_t psmem = 8 * ((size_t)nmax + 2);
-        if (psmem > 200 * 1024) return CP_ERR_UNSUPPORTED;
-        static bool attr = false;
-        if (!attr) { cudaFuncSetAttribute(k_ann_best, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); attr = true; }
         const long long nblk = (long long)a.nreq * max_segments * a.nchunk;
         if (nblk > INT32_MAX) return CP_ERR_INVALID_ARG;
-        k_ann_best<<<(int)nblk, kBestThreads, psmem, st>>>(a);
+        if (flat) {
+            static bool attr = false;
+            if (!attr) { cudaFuncSetAttribute(k_ann_best_flat, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); attr = true; }
+            k_ann_best_flat<<<(int)nblk, kBestThreads, psmem, st>>>(a);
+        } else {
+            k_ann_best_split<<<(int)nblk, kBestThreads, 0, st>>>(a);
+        }
         CP_COUNT_LAUNCH();
         k_ann_final<<<(a.nreq * max_segments + 255) / 256, 256, 0, st>>>(a);
         CP_COUNT_LAUNCH();

@@ -18,8 +18,10 @@ def _run(mats, masks, heads, min_len, max_segments=64):
     return cp.annotate_spans(dA, dM, heads, min_len=min_len, max_segments=max_segments)
 
 
+@pytest.mark.parametrize("variant", ["0", "1", "2"])     # auto / flat (thread per start) / split rows
 @pytest.mark.parametrize("seed", range(4))
-def test_random_causal_matrices(seed):
+def test_random_causal_matrices(seed, variant, monkeypatch):
+    monkeypatch.setenv("CP_ANN_VARIANT", variant)
     rng = np.random.default_rng(seed)
     mats, masks, heads, exp = [], [], [], []
     min_len = [1, 3, 8, 17][seed]
@@ -59,3 +61,23 @@ def test_all_masked_and_short():
     I = np.eye(40, dtype=np.float32)
     got = _run([I, I, I], [np.ones(40, np.uint8), np.zeros(40, np.uint8), np.zeros(40, np.uint8)], [1, 1, 1], 50)
     assert got == [[], [(-1, -1, 0)], [(-1, -1, 0)]]
+
+
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_many_segments_beside_long_request(variant, monkeypatch):
+    """A short request with hundreds of coarse segments in the same call as a long one: the partial
+    bests of each request stay inside its own workspace slice (stride ceil(n/32) per segment)."""
+    monkeypatch.setenv("CP_ANN_VARIANT", variant)
+    rng = np.random.default_rng(11)
+    mats, masks, heads, exp = [], [], [], []
+    for n, alt in ((2600, False), (700, True), (1900, False), (650, True)):
+        A = np.tril(rng.uniform(0, 1, (1, n, n))).astype(np.float32)
+        m = np.zeros(n, np.uint8)
+        if alt:
+            m[1::3] = 1                                  # ~n/3 segments of 2 tokens
+        else:
+            m[rng.integers(0, n, 6)] = 1
+        mats.append(A); masks.append(m); heads.append(1)
+        exp.append(O.annotate(A, m, 1))
+    got = _run(mats, masks, heads, 1, max_segments=256)
+    assert got == exp

@@ -33,6 +33,16 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
+def variants(fn):
+    """k_ann_best A/B: CP_ANN_VARIANT 1 = flat (thread per start), 2 = split rows across warps."""
+    t = {}
+    for v, name in (("1", "flat"), ("2", "split")):
+        os.environ["CP_ANN_VARIANT"] = v
+        t[name] = round(timed(fn, reps=3), 3)
+    os.environ.pop("CP_ANN_VARIANT")
+    return t
+
+
 def main():
     out = {"paper": "CPU annotator ~450 ms @10K tokens (transfer <=383 ms, SAT/search <10 ms each), P:L1199-1205",
            "single": [], "batch": None}
@@ -59,7 +69,8 @@ def main():
         cpu_ms = (time.perf_counter() - t0) * 1e3 if exp is not None else None
         row = {"n": n, "gpu_ms": round(ms, 3), "segments": len(res[-1][0]),
                "attention_MB": round(n * (n + 1) / 2 * 4 / 1e6, 1), "oracle_cpu_ms": cpu_ms,
-               "parity": (res[-1][0] == exp) if exp is not None else "not run (oracle O(n^2) memory)"}
+               "parity": (res[-1][0] == exp) if exp is not None else "not run (oracle O(n^2) memory)",
+               "variants_ms": variants(lambda: cp.annotate_spans([A], [M], [1], min_len=128))}
         out["single"].append(row)
         print(row, flush=True)
         del A
@@ -74,6 +85,8 @@ def main():
     spans = sum(1 for r in res[-1] for (l, rr, d) in r if l >= 0)
     out["batch"] = {"requests": wb.num_reqs, "tokens": wb.total_tokens, "gpu_ms": round(ms, 3),
                     "attention_GB": round(tot / 1e9, 3), "reusable_spans": spans,
+                    "variants_ms": variants(lambda: cp.annotate_spans(mats, masks, [1] * len(mats), min_len=128,
+                                                                      workspace_bytes=8 << 30)),
                     "note": "includes host-side result readback per chunk (annotate_spans returns Python lists)"}
     print(out["batch"], flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

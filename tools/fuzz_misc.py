@@ -39,7 +39,9 @@ def annotate_case(seed):
         exp.append(O.annotate(A, m, min_len))
     dA = [torch.from_numpy(np.ascontiguousarray(A)).cuda() for A in mats]
     dM = [torch.from_numpy(m).cuda() for m in masks]
+    os.environ["CP_ANN_VARIANT"] = str(seed % 3)          # auto / flat / split row walk
     got = cp.annotate_spans(dA, dM, heads, min_len=min_len, max_segments=256)
+    os.environ.pop("CP_ANN_VARIANT")
     return got == exp
 
 

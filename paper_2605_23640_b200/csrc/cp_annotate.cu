@@ -12,11 +12,11 @@
 // which is exactly the paper's rectangle-sum form for causal attention.
 //
 //   k_ann_rows : warp per (request, row i): R(i, 0..i+1) into the workspace (the SAT's row pass)
-//   k_ann_segs : CTA per request: P by block scan; coarse segments from the mask
-//   k_ann_best : CTA per (request, segment, chunk of 256 starts): thread per start l walks rows
-//                i = l..b (8 independent loads per step) accumulating sum R(i, l) (coalesced across l),
-//                chunk best (diff desc, length desc, l asc) by a block reduction
-//   k_ann_final: per segment, best over its chunks; reported only if diff > 0
+//   k_ann_segs : CTA per request: P and the coarse segments by one fused block scan
+//   k_ann_best : chunk best (diff desc, length desc, l asc) of sum R(i, l) walks, coalesced across
+//                starts l; flat form (thread per start, 256 starts per CTA) for many-request calls,
+//                split form (32 starts per CTA, the rows cut across 8 warps, two passes) for few
+//   k_ann_final: warp per segment, best over its chunks; reported only if diff > 0
 #include "cp_internal.cuh"
 #include <algorithm>
 #include <climits>
@@ -80,14 +80,22 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
         for (int base = 0; base <= i; base += 128 * kRowsBatch) {
             long long v[kRowsBatch][4];
 #pragma unroll
-            for (int u = 0; u < kRowsBatch; ++u)
+            for (int u = 0; u < kRowsBatch; ++u) {
+                const int x0 = base + u * 128 + 4 * lane;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int x = base + u * 128 + 4 * lane + e;
-                    v[u][e] = 0;
-                    if (x <= i)
-                        for (int h = 0; h < rq.heads; ++h) v[u][e] += q40(__ldg(rq.A + ((int64_t)h * n + i) * n + x));
+                for (int e = 0; e < 4; ++e) v[u][e] = 0;
+                for (int h = 0; h < rq.heads; ++h) {
+                    const float* pa = rq.A + ((int64_t)h * n + i) * n + x0;
+                    if (x0 + 3 <= i && ((uintptr_t)pa & 15) == 0) {        // one 16-B load for the 4 columns
+                        const float4 f = __ldg(reinterpret_cast<const float4*>(pa));
+                        v[u][0] += q40(f.x); v[u][1] += q40(f.y); v[u][2] += q40(f.z); v[u][3] += q40(f.w);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (x0 + e <= i) v[u][e] += q40(__ldg(pa + e));
+                    }
                 }
+            }
 #pragma unroll
             for (int u = 0; u < kRowsBatch; ++u) {
                 const long long p1 = v[u][0] + v[u][1], p2 = p1 + v[u][2], p3 = p2 + v[u][3];
@@ -106,89 +114,56 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
     }
 }
 
+// One ordered block scan per 1024-row step computes all three: P(x+1) = P(x) + R(x, x+1) (prefix of
+// row sums), the coarse segments' starts (maximal mask-0 runs, in order) and their ends (the k-th
+// mask-0 position followed by a mask-1 one, or the end, closes segment k).
 __global__ void __launch_bounds__(1024) k_ann_segs(const AnnArgs a) {
     __shared__ long long s_w[33];
-    __shared__ int s_wi[33];
+    __shared__ int s_ws[33], s_we[33];
     __shared__ long long s_carry;
-    __shared__ int s_cnt;
+    __shared__ int s_cs, s_ce;
     const AnnReq& rq = a.rq[blockIdx.x];
     const int n = rq.n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
     long long* P = reinterpret_cast<long long*>(a.ws + rq.p_off);
     int2* seg = reinterpret_cast<int2*>(a.ws + rq.s_off);
-    if (tid == 0) { s_carry = 0; s_cnt = 0; P[0] = 0; }
-    __syncthreads();
-    // P(x+1) = P(x) + R(x, x+1)   (prefix of row sums)
+    if (tid == 0) { s_carry = 0; s_cs = 0; s_ce = 0; P[0] = 0; }
     for (int b0 = 0; b0 < n; b0 += 1024) {
         const int i = b0 + tid;
         const long long v = i < n ? R[(int64_t)i * (n + 1) + i + 1] : 0;
+        const bool m0 = i < n && !rq.mask[i];
+        const bool start = m0 && (i == 0 || rq.mask[i - 1]);
+        const bool end = m0 && (i + 1 == n || rq.mask[i + 1]);
         long long inc = v;
-        for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-        if (lane == 31) s_w[wid] = inc;
-        __syncthreads();
+        int incs = start, ince = end;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            const int ys = __shfl_up_sync(0xffffffffu, incs, o), ye = __shfl_up_sync(0xffffffffu, ince, o);
+            if (lane >= o) { inc += y; incs += ys; ince += ye; }
+        }
+        if (lane == 31) { s_w[wid] = inc; s_ws[wid] = incs; s_we[wid] = ince; }
+        __syncthreads();                                     // also orders the previous step's carries
         if (wid == 0) {
             long long x = s_w[lane], xi = x;
-            for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
-            s_w[lane] = xi - x;
-            if (lane == 31) s_w[32] = xi;
+            int xs = s_ws[lane], xsi = xs, xe = s_we[lane], xei = xe;
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, xi, o);
+                const int ys = __shfl_up_sync(0xffffffffu, xsi, o), ye = __shfl_up_sync(0xffffffffu, xei, o);
+                if (lane >= o) { xi += y; xsi += ys; xei += ye; }
+            }
+            s_w[lane] = xi - x; s_ws[lane] = xsi - xs; s_we[lane] = xei - xe;
+            if (lane == 31) { s_w[32] = xi; s_ws[32] = xsi; s_we[32] = xei; }
         }
         __syncthreads();
         if (i < n) P[i + 1] = s_carry + s_w[wid] + inc;
+        if (start) { const int k = s_cs + s_ws[wid] + incs - 1; if (k < a.max_seg) seg[k].x = i; }
+        if (end) { const int k = s_ce + s_we[wid] + ince - 1; if (k < a.max_seg) seg[k].y = i; }
         __syncthreads();
-        if (tid == 0) s_carry += s_w[32];
-        __syncthreads();
+        if (tid == 0) { s_carry += s_w[32]; s_cs += s_ws[32]; s_ce += s_we[32]; }
     }
-    // coarse segments: maximal mask-0 runs, in order
-    for (int b0 = 0; b0 < n; b0 += 1024) {
-        const int i = b0 + tid;
-        const bool start = i < n && !rq.mask[i] && (i == 0 || rq.mask[i - 1]);
-        int inc = start;
-        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-        if (lane == 31) s_wi[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            int x = s_wi[lane], xi = x;
-            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
-            s_wi[lane] = xi - x;
-            if (lane == 31) s_wi[32] = xi;
-        }
-        __syncthreads();
-        if (start) {
-            const int k = s_cnt + s_wi[wid] + inc - 1;
-            if (k < a.max_seg) seg[k].x = i;
-        }
-        __syncthreads();
-        if (tid == 0) s_cnt += s_wi[32];
-        __syncthreads();
-    }
-    // segment ends: the k-th mask-0 position followed by a mask-1 one (or the end) closes segment k,
-    // found by the same ordered scan (no per-segment serial walk)
-    if (tid == 0) s_cnt = 0;
     __syncthreads();
-    for (int b0 = 0; b0 < n; b0 += 1024) {
-        const int i = b0 + tid;
-        const bool end = i < n && !rq.mask[i] && (i + 1 == n || rq.mask[i + 1]);
-        int inc = end;
-        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-        if (lane == 31) s_wi[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            int x = s_wi[lane], xi = x;
-            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
-            s_wi[lane] = xi - x;
-            if (lane == 31) s_wi[32] = xi;
-        }
-        __syncthreads();
-        if (end) {
-            const int k = s_cnt + s_wi[wid] + inc - 1;
-            if (k < a.max_seg) seg[k].y = i;
-        }
-        __syncthreads();
-        if (tid == 0) s_cnt += s_wi[32];
-        __syncthreads();
-    }
-    if (tid == 0) a.out_nseg[blockIdx.x] = s_cnt <= a.max_seg ? s_cnt : -1;
+    if (tid == 0) a.out_nseg[blockIdx.x] = s_cs <= a.max_seg ? s_cs : -1;
 }
 
 struct Best { long long d; int len; int l; };
@@ -358,9 +333,9 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a
     }
 }
 
-// thread per (request, segment): best over the chunks' partial bests
+// warp per (request, segment): lanes stride over the chunks' partial bests, then a shuffle reduction
 __global__ void k_ann_final(const AnnArgs a) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (t >= a.nreq * a.max_seg) return;
     const int q = t / a.max_seg, s = t % a.max_seg;
     const int nseg = a.out_nseg[q];
@@ -370,11 +345,17 @@ __global__ void k_ann_final(const AnnArgs a) {
     const PartialBest* part = reinterpret_cast<const PartialBest*>(a.ws + rq.s_off + 8 * (size_t)a.max_seg);
     const int lmax = sg.y - a.min_len + 1;
     Best b{0, -1, 0};
-    for (int ch = 0; ch < a.nchunk && sg.x + ch * a.cw <= lmax; ++ch) {
+    for (int ch = lane; ch < a.nchunk && sg.x + ch * a.cw <= lmax; ch += 32) {
         const PartialBest pb = part[s * rq.nch + ch];
         const Best y{pb.d, pb.len, pb.l};
         if (better(y, b)) b = y;
     }
+    for (int o = 16; o; o >>= 1) {
+        const Best y{__shfl_xor_sync(0xffffffffu, b.d, o), __shfl_xor_sync(0xffffffffu, b.len, o),
+                     __shfl_xor_sync(0xffffffffu, b.l, o)};
+        if (better(y, b)) b = y;
+    }
+    if (lane) return;
     const bool ok = b.len > 0 && b.d > 0;
     a.out_l[t] = ok ? b.l : -1;
     a.out_r[t] = ok ? b.l + b.len - 1 : -1;
@@ -462,7 +443,7 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
             k_ann_best_split<<<(int)nblk, kBestThreads, 0, st>>>(a);
         }
         CP_COUNT_LAUNCH();
-        k_ann_final<<<(a.nreq * max_segments + 255) / 256, 256, 0, st>>>(a);
+        k_ann_final<<<(a.nreq * max_segments + 7) / 8, 256, 0, st>>>(a);
         CP_COUNT_LAUNCH();
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }

@@ -292,7 +292,8 @@ cp_status cp_policy_spans(const cp_batch* writers_h, int32_t policy, int32_t chu
 
 /* ---- NEXT-1: on-device KV Annotator (C1 Steps 1-2) -------------------------- */
 
-/* Workspace bytes cp_annotate_spans needs for these requests: per request 8 n(n+1) (row prefixes)
+/* Workspace bytes cp_annotate_spans needs for these requests: per request 8 (n S + 3) with S = (n+5) & ~3
+ * (row prefixes, rows padded so a lane's four entries are 32-B aligned)
  * + 8(n+1) (P) + 8 max_segments (segments) + 16 max_segments ceil(n/32) (partial bests), each
  * 256-B aligned. */
 size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, int32_t max_segments);

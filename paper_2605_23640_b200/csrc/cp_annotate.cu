@@ -56,6 +56,11 @@ struct AnnArgs {
     long long* out_diff;
 };
 
+// R layout in the workspace: row i at element 3 + i * rstride(n) (rstride a multiple of 4 >= n + 2),
+// so a lane's 4 entries R(i, x0+1 .. x0+4), x0 % 4 == 0, start on a 32-B boundary (two 16-B stores)
+__host__ __device__ __forceinline__ int64_t rstride(int64_t n) { return (n + 5) & ~(int64_t)3; }
+__host__ __device__ __forceinline__ size_t rbytes(int64_t n) { return 8 * (size_t)(n * rstride(n) + 3); }
+
 __device__ __forceinline__ long long q40(float x) { return __float2ll_rz(x * 1099511627776.0f); }
 
 __device__ __forceinline__ int find_req(const AnnArgs& a, int gr) {
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
         const int q = find_req(a, gr);
         const AnnReq& rq = a.rq[q];
         const int n = rq.n, i = gr - rq.row_begin;
-        long long* R = reinterpret_cast<long long*>(a.ws + rq.r_off) + (int64_t)i * (n + 1);
+        long long* R = reinterpret_cast<long long*>(a.ws + rq.r_off) + 3 + (int64_t)i * rstride(n);
         long long carry = 0;
         if (lane == 0) R[0] = 0;
         // a lane owns 4 consecutive columns of each 128-column chunk, kRowsBatch chunks per step: all
@@ -104,10 +109,15 @@ __global__ void __launch_bounds__(256) k_ann_rows(const AnnArgs a) {
                 for (int o = 1; o < 32; o <<= 1) { const long long y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
                 const long long ex = carry + inc - p3;                 // sum before this lane's 4 columns
                 const int x0 = base + u * 128 + 4 * lane;
-                if (x0 <= i) R[x0 + 1] = ex + v[u][0];
-                if (x0 + 1 <= i) R[x0 + 2] = ex + p1;
-                if (x0 + 2 <= i) R[x0 + 3] = ex + p2;
-                if (x0 + 3 <= i) R[x0 + 4] = ex + p3;
+                if (x0 + 3 <= i) {
+                    longlong2* d2 = reinterpret_cast<longlong2*>(R + x0 + 1);
+                    d2[0] = make_longlong2(ex + v[u][0], ex + p1);
+                    d2[1] = make_longlong2(ex + p2, ex + p3);
+                } else {
+                    if (x0 <= i) R[x0 + 1] = ex + v[u][0];
+                    if (x0 + 1 <= i) R[x0 + 2] = ex + p1;
+                    if (x0 + 2 <= i) R[x0 + 3] = ex + p2;
+                }
                 carry += __shfl_sync(0xffffffffu, inc, 31);
             }
         }
@@ -125,13 +135,13 @@ __global__ void __launch_bounds__(1024) k_ann_segs(const AnnArgs a) {
     const AnnReq& rq = a.rq[blockIdx.x];
     const int n = rq.n;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off) + 3;
     long long* P = reinterpret_cast<long long*>(a.ws + rq.p_off);
     int2* seg = reinterpret_cast<int2*>(a.ws + rq.s_off);
     if (tid == 0) { s_carry = 0; s_cs = 0; s_ce = 0; P[0] = 0; }
     for (int b0 = 0; b0 < n; b0 += 1024) {
         const int i = b0 + tid;
-        const long long v = i < n ? R[(int64_t)i * (n + 1) + i + 1] : 0;
+        const long long v = i < n ? R[(int64_t)i * rstride(n) + i + 1] : 0;
         const bool m0 = i < n && !rq.mask[i];
         const bool start = m0 && (i == 0 || rq.mask[i - 1]);
         const bool end = m0 && (i + 1 == n || rq.mask[i + 1]);
@@ -194,7 +204,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_flat(const AnnArgs a)
     const int l_lo = sa + ch * kBestThreads;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (l_lo > lmax) return;                                                // no admissible start in this chunk
-    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off) + 3;
     const long long* P = reinterpret_cast<const long long*>(a.ws + rq.p_off);
     for (int x = l_lo + tid; x <= sb + 1; x += kBestThreads) sP[x - l_lo] = P[x];
     __syncthreads();
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_flat(const AnnArgs a)
         for (; i + kRowUnroll - 1 <= sb; i += kRowUnroll) {
             long long v[kRowUnroll];
 #pragma unroll
-            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * rstride(n) + l);
 #pragma unroll
             for (int u = 0; u < kRowUnroll; ++u) {
                 acc += v[u];
@@ -220,7 +230,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_flat(const AnnArgs a)
             }
         }
         for (; i <= sb; ++i) {
-            acc += __ldg(R + (int64_t)i * (n + 1) + l);
+            acc += __ldg(R + (int64_t)i * rstride(n) + l);
             if (i >= rmin) {
                 const Best c{sP[i + 1 - l_lo] - Pl - 2 * acc, i - l + 1, l};
                 if (better(c, best)) best = c;
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a
     const int l_lo = sa + ch * kStarts;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (l_lo > lmax) return;                                                // no admissible start in this chunk
-    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off);
+    const long long* R = reinterpret_cast<const long long*>(a.ws + rq.r_off) + 3;
     const long long* P = reinterpret_cast<const long long*>(a.ws + rq.p_off);
     const int l = l_lo + lane;
     const bool act = l <= lmax;
@@ -278,11 +288,11 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a
         for (; i + kRowUnroll - 1 <= r1; i += kRowUnroll) {
             long long v[kRowUnroll];
 #pragma unroll
-            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+            for (int u = 0; u < kRowUnroll; ++u) v[u] = __ldg(R + (int64_t)(i + u) * rstride(n) + l);
 #pragma unroll
             for (int u = 0; u < kRowUnroll; ++u) part_sum += v[u];
         }
-        for (; i <= r1; ++i) part_sum += __ldg(R + (int64_t)i * (n + 1) + l);
+        for (; i <= r1; ++i) part_sum += __ldg(R + (int64_t)i * rstride(n) + l);
     }
     s_sum[wid][lane] = part_sum;
     __syncthreads();
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a
             long long v[kRowUnroll], pv[kRowUnroll];
 #pragma unroll
             for (int u = 0; u < kRowUnroll; ++u) {
-                v[u] = __ldg(R + (int64_t)(i + u) * (n + 1) + l);
+                v[u] = __ldg(R + (int64_t)(i + u) * rstride(n) + l);
                 pv[u] = __ldg(P + i + u + 1);
             }
 #pragma unroll
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(kBestThreads) k_ann_best_split(const AnnArgs a
             }
         }
         for (; i <= r1; ++i) {
-            acc += __ldg(R + (int64_t)i * (n + 1) + l);
+            acc += __ldg(R + (int64_t)i * rstride(n) + l);
             if (i >= rmin) {
                 const Best c{__ldg(P + i + 1) - Pl - 2 * acc, i - l + 1, l};
                 if (better(c, best)) best = c;
@@ -372,7 +382,7 @@ extern "C" size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, in
     for (int r = 0; r < num_reqs; ++r) {
         const size_t n = (size_t)std::max(n_h[r], 0);
         const size_t nch = (n + kStarts - 1) / kStarts;
-        tot += align256(8 * n * (n + 1)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * nch);
+        tot += align256(rbytes((int64_t)n)) + align256(8 * (n + 1)) + align256(8 * (size_t)max_segments + 16 * (size_t)max_segments * nch);
     }
     return tot;
 }
@@ -403,7 +413,7 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
             const size_t n = (size_t)n_h[r];
             AnnReq& d = a.rq[q];
             d.A = attn_h[r]; d.mask = mask_h[r]; d.n = n_h[r]; d.heads = heads_h[r];
-            d.r_off = (long long)off; off += align256(8 * n * (n + 1));
+            d.r_off = (long long)off; off += align256(rbytes((int64_t)n));
             d.p_off = (long long)off; off += align256(8 * (n + 1));
             d.s_off = (long long)off;
             d.nch = (int32_t)((n_h[r] + kStarts - 1) / kStarts);

@@ -351,13 +351,13 @@ def annotate_spans(attn: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], 
     ns = [int(a.shape[-1]) for a in attn]
     out = [None] * R
     dev = attn[0].device if R else torch.device("cuda")
+    # the workspace is a sum of per-request (256-B aligned) terms: size each request once, then chunk
+    per = [int(lib.cp_annotate_workspace(1, (C.c_int32 * 1)(n), max_segments)) for n in ns]
     i = 0
     while i < R:
-        j = i + 1
-        while j < R:
-            arr = (C.c_int32 * (j + 1 - i))(*ns[i:j + 1])
-            if lib.cp_annotate_workspace(j + 1 - i, arr, max_segments) > workspace_bytes:
-                break
+        j, tot = i + 1, per[i]
+        while j < R and tot + per[j] <= workspace_bytes:
+            tot += per[j]
             j += 1
         k = j - i
         n_arr = (C.c_int32 * k)(*ns[i:j])

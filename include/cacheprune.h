@@ -127,9 +127,13 @@ typedef struct {
  * eviction by (last_used, id) while live tokens exceed the budget (R#20-22).
  * recompute_bits: packed LSB-first per span starting at word bits_word_offsets[s] (device arrays;
  * NULL = no recompute marks).  out_entry_id[s]: the stored / duplicate / containing entry id.
- * Device errors (no side effects): CP_ERR_INVALID_ARG (range), CP_ERR_SPAN_TOO_SHORT,
- * CP_ERR_CAPACITY (len > budget or > max_span_len), CP_ERR_SENSITIVE_SPAN -- the first failing
- * span in input order decides the code.
+ * Device errors (no side effects): CP_ERR_INVALID_ARG (range, or a span reaching past the writer's
+ * block table), CP_ERR_SPAN_TOO_SHORT, CP_ERR_CAPACITY (len > budget or > max_span_len), CP_ERR_SENSITIVE_SPAN
+ * -- the first failing span in input order decides the code; then, still before any change,
+ * CP_ERR_CAPACITY if one span strictly contains more than 1024 stored or batch segments, or if the
+ * spans' copy-in work list (sum of ceil(len/32)) exceeds max_batch_tokens/32 + max_spans_per_insert + 1
+ * (possible only with overlapping spans).  Config limits (cp_index_workspace / create reject others):
+ * max_span_len <= 25599; window_len >= 3 when max_req_tokens > 10240.
  */
 cp_status cp_index_insert(cp_index* idx, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
                           int32_t num_spans, const int32_t* span_req, const int32_t* span_begin,
@@ -208,6 +212,8 @@ cp_status cp_match_spans(cp_index* idx, const cp_batch* readers_h, uint64_t logi
  * CP_ZERO_RECOMPUTE, plan-2 positions get +0.0 in K and V (zero placeholders); with
  * CP_ZERO_UNCOVERED, plan-0 positions are zeroed too.  `hits` is the struct cp_match_spans wrote
  * (only num_hits, hit_* and plan are read).  readers_h must be the batch that was matched.
+ * Device error: a block table narrower than a covered position (position >> 4 >= max_blocks_per_req)
+ * -> CP_ERR_INVALID_ARG, and no row is written (the copy kernel sees the error word and exits).
  */
 cp_status cp_gather_rerotate(cp_index* idx, const cp_batch* readers_h, const cp_hits* hits_h,
                              const cp_paged_kv* dst_kv_h, int32_t flags, void* stream);
@@ -257,7 +263,7 @@ cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* span_req_h, co
                                 const int64_t* bits_word_offsets_h, void* stream);
 
 /*
- * NEXT-2: zero-copy page linking (PAPER.md L729-730: the retriever "link[s] reusable segments without
+ * NEXT-2: zero-copy page linking (PAPER.md L726: the retriever "link[s] reusable segments without
  * touching the actual KV"; prefix sharing shares whole cached blocks, L245-252).  A link is possible
  * only where a request block IS a stored page (R#31): block b of request r (positions
  * [16b, 16b+16)) links to pool page page_list[e][j] iff one hit (e, dst, len, delta) of r has

@@ -466,7 +466,7 @@ void orc_fifo_get(const orc_index* x, int32_t* out) {
 
 /*
  * NEXT-2: zero-copy page linking.  The paper's retriever "link[s] reusable segments without touching
- * the actual KV" (P:L729-730); ordinary prefix reuse shares whole cached blocks (P:L245-252).  A link is
+ * the actual KV" (P:L726); ordinary prefix reuse shares whole cached blocks (P:L245-252).  A link is
  * possible only where a request block IS a stored page: reading R#31 links request r's block b
  * (positions [16b, 16b + 16)) to pool page pages(e)[j] iff one hit (e, dst, len, delta) of r has
  *   delta == 0, dst % 16 == 0, dst <= 16b, 16b + 16 <= dst + len   (then j = (16b - dst) / 16),

@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
         if (t >= a.l_len[hh]) continue;
         const int r = a.l_req[hh], k = a.l_dst[hh], slot = a.l_slot[hh];
         const int pos = k + t;                                              // position in the request
+        if ((pos >> 4) >= a.max_blocks) { cp_raise(a.hdr, CP_ERR_INVALID_ARG); continue; }   // table too narrow:
+                                                                           // k_rows then writes nothing
         const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
         const int blk = a.block_tables[(int64_t)r * a.max_blocks + (pos >> 4)];
         const long long pool_row = ((long long)page * CP_BLOCK + (t & 15)) * rowE;
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
 }
 
 // ============================================================================================
-// TMA bulk-copy variant (cp.async.bulk + mbarrier), the default when a stage fits shared memory.
+// TMA bulk-copy variant (cp.async.bulk + mbarrier): opt-in only (CP_GATHER_VARIANT=4), not the default.
 //   warp 0      : producer -- resolves TOK token rows of the next unit (pool page / block table /
 //                 plan code) and bulk-loads the K and V rows (2 KiB each for the 8B shape) into an
 //                 NST-stage shared-memory ring, completing an mbarrier transaction count
@@ -507,9 +509,12 @@ __global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int
                 int lo = 0, hi = R - 1;
                 while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.req_off[mid] <= g) lo = mid; else hi = mid - 1; }
                 const int q = (int)(g - a.req_off[lo]);
-                const int blk = a.block_tables[(int64_t)lo * a.max_blocks + (q >> 4)];
-                s_dst[threadIdx.x] = ((int64_t)blk * CP_BLOCK + (q & 15)) * rowE;
-                s_on[threadIdx.x] = 1;
+                if ((q >> 4) >= a.max_blocks) cp_raise(a.hdr, CP_ERR_INVALID_ARG);   // never write another request's blocks
+                else {
+                    const int blk = a.block_tables[(int64_t)lo * a.max_blocks + (q >> 4)];
+                    s_dst[threadIdx.x] = ((int64_t)blk * CP_BLOCK + (q & 15)) * rowE;
+                    s_on[threadIdx.x] = 1;
+                }
             }
         }
         __syncthreads();

@@ -61,8 +61,11 @@ bool valid_cfg(const cp_config* c) {
     if (c->head_dim > 512) return false;
     if (c->pool_capacity_tokens < c->window_len) return false;
     if (c->max_entries < 1 || c->max_entries > 131072) return false;
-    if (c->max_span_len < c->window_len || c->max_span_len > 65535) return false;
+    // k_ins_scan keeps a span's prefix hashes (8 B per token) in <= 200 KB of shared memory
+    if (c->max_span_len < c->window_len || c->max_span_len > 200 * 1024 / 8 - 1) return false;
     if (c->max_req_tokens < 1 || c->max_req_tokens > CP_MAX_MATCH_TOKENS) return false;
+    // long requests keep the matcher arrays in 24 B/token of scratch: 20 n + 12 (n/w + 1) + 8 fits only for w >= 3
+    if (c->max_req_tokens > CP_MATCH_SMEM_TOKENS && c->window_len < 3) return false;
     if (c->max_batch_reqs < 1 || c->max_batch_tokens < 1 || c->max_spans_per_insert < 1) return false;
     if (c->max_spans_per_insert > 16384) return false;
     if (!(c->rope_theta > 0)) return false;
@@ -163,6 +166,8 @@ struct InsArgs {
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed; int32_t* rm_pos;
     int32_t* cp_req; int32_t* cp_slot; int32_t* cp_dst; int32_t* cp_len; int32_t* cp_delta; int32_t* out_tmp;
     int32_t* eq_old; HEntry* dtab; int32_t* span_rep; Rec16* precs;
+    int64_t CH;             // copy-in chunk capacity (scratch)
+    int32_t max_blocks;     // writer block-table width
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
     int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
@@ -197,6 +202,7 @@ __global__ void k_ins_validate(InsArgs a) {
             if (b < 0 || m < 0 || b + m > n) bad = 0;
             else if (m < a.w) bad = 1;
             else if (m > a.capacity || m > a.max_span_len) bad = 2;
+            else if (((b + m - 1) >> 4) >= a.max_blocks) bad = 0;   // writer block table too narrow for the copy-in
         }
         if (bad < 0) {
             const uint8_t* mk = a.mask + a.offsets[r] + b;
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     int32_t* clen = (int32_t*)(smc + lay.clen);
     int2* srec = (int2*)(smc + lay.srec);
     __shared__ int s_abort, s_nrec;
-    __shared__ long long s_live_tokens;
+    __shared__ long long s_live_tokens, s_chunks;
     __shared__ int s_fifo_head, s_fifo_count, s_next_id, s_free_top, s_num_live, s_nremoved;
     __shared__ int s_rm[kMaxSupersede];
     __shared__ unsigned long long s_red_key[kCommitThreads / 32];
@@ -531,7 +537,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
 #endif
 
     if (tid == 0) {
-        s_abort = 0;
+        s_abort = 0; s_chunks = 0;
         if (cp_err_set(a.hdr)) s_abort = 1;
         else if (a.hdr->first_err != CP_NO_ERR_KEY) {
             const unsigned code = (unsigned)(a.hdr->first_err & 0xffffffffu);
@@ -590,6 +596,30 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     for (int j = tid; j <= a.S; j += blockDim.x) soff[j] = a.rel_off[j];
     if (tid == 0) s_nrec = nrec;
     __syncthreads();
+    // ---- capacity checks before any mutation (an insert that fails changes nothing): the supersede
+    //      list of one span (its CONTAINED records bound it) and the copy-in chunk list (stored spans
+    //      may overlap, so their total length can exceed max_batch_tokens)
+    {
+        int bad = 0;
+        long long chunks = 0;
+        for (int j = tid; j < a.S; j += blockDim.x) {
+            chunks += (slen[j] + CP_GATHER_CHUNK - 1) / CP_GATHER_CHUNK;
+            if (srep[j] != j) continue;
+            int ncont = 0;
+            for (int q = soff[j]; q < soff[j + 1]; ++q) ncont += a.rel_rec[q].y == REL_CONTAINED;
+            bad |= ncont > kMaxSupersede;
+        }
+        for (int o = 16; o; o >>= 1) chunks += __shfl_xor_sync(0xffffffffu, chunks, o);
+        if ((tid & 31) == 0 && chunks) atomicAdd((unsigned long long*)&s_chunks, (unsigned long long)chunks);
+        if (bad) s_abort = 1;
+        __syncthreads();
+        if (tid == 0 && (s_abort || s_chunks > a.CH)) { cp_raise(a.hdr, CP_ERR_CAPACITY); s_abort = 1; }
+        __syncthreads();
+        if (s_abort) {
+            for (int j = tid; j < a.S; j += blockDim.x) { a.out_id[j] = -1; a.out_oc[j] = -1; a.out_tmp[j] = -1; }
+            return;
+        }
+    }
     const bool rec_in_smem = s_nrec <= a.rec_cap;
     if (rec_in_smem) for (int i = tid; i < s_nrec; i += blockDim.x) srec[i] = a.rel_rec[i];
     __syncthreads();
@@ -878,10 +908,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                             const int sx = resolve(rec[q].x);
                             bool seen = false;
                             for (int z = 0; z < n; ++z) seen |= (s_rm[z] == sx);
-                            if (!seen) {
-                                if (n < kMaxSupersede) s_rm[n++] = sx;
-                                else cp_raise(a.hdr, CP_ERR_CAPACITY);
-                            }
+                            if (!seen && n < kMaxSupersede) s_rm[n++] = sx;     // n <= CONTAINED records (checked)
                         }
                     for (int x = 1; x < n; ++x)      // insertion sort by id
                         for (int y = x; y > 0 && a.slot_id[s_rm[y]] < a.slot_id[s_rm[y - 1]]; --y) {
@@ -1431,6 +1458,8 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
+    a.CH = x->CH; a.max_blocks = kv->max_blocks_per_req;
+    if (a.max_blocks < 1) return CP_ERR_INVALID_ARG;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
     // shared memory of the commit: flags + per-span arrays, then the LRU candidate list (4096 halved to
     // fit), then as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)

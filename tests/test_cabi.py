@@ -47,6 +47,16 @@ def test_host_side_validation_without_gpu():
     assert lib.cp_index_workspace(C.byref(bad), sizes) == L.CP_ERR_INVALID_ARG
     bad.block_size = 16; bad.head_dim = 100        # (d/2) not a multiple of the 8-wide bf16 vector
     assert lib.cp_index_workspace(C.byref(bad), sizes) == L.CP_ERR_INVALID_ARG
+    bad.head_dim = 128; bad.max_span_len = 25600   # k_ins_scan's 8 B/token prefix array would exceed 200 KB smem
+    assert lib.cp_index_workspace(C.byref(bad), sizes) == L.CP_ERR_INVALID_ARG
+    bad.max_span_len = 25599; bad.max_entries = 4096
+    assert lib.cp_index_workspace(C.byref(bad), sizes) == 0
+    bad.max_span_len = 2048; bad.window_len = 2; bad.max_req_tokens = 20000   # long-request matcher scratch needs w >= 3
+    assert lib.cp_index_workspace(C.byref(bad), sizes) == L.CP_ERR_INVALID_ARG
+    bad.window_len = 3
+    assert lib.cp_index_workspace(C.byref(bad), sizes) == 0
+    bad.window_len = 2; bad.max_req_tokens = 10240                 # shared-memory matcher: any w
+    assert lib.cp_index_workspace(C.byref(bad), sizes) == 0
     # score: KVDEV mode is not built; bad rho rejected -- both before any device call
     assert lib.cp_score_deviation(0, None, None, None, None, None, 1, 4, L.CP_SCORE_KVDEV, 1, None, None, None,
                                   None, None) == L.CP_ERR_UNSUPPORTED

@@ -1,4 +1,4 @@
-"""GPU parity for NEXT-2, zero-copy page linking (PAPER.md L729-730, L245-252; DESIGN.md R#31):
+"""GPU parity for NEXT-2, zero-copy page linking (PAPER.md L726, L245-252; DESIGN.md R#31):
 cp_link_blocks vs the oracle's link table, bit exact; and the data contract behind a link: with
 CP_SKIP_LINKED the gather leaves exactly the linked destination blocks unwritten, every other row
 is bit-identical to the full gather, and the linked pool page holds bit-for-bit the rows the full

@@ -1,4 +1,4 @@
-"""Pins for the oracle's zero-copy page linking (NEXT-2; PAPER.md L729-730 "link reusable segments
+"""Pins for the oracle's zero-copy page linking (NEXT-2; PAPER.md L726 "link reusable segments
 without touching the actual KV", L245-252 prefix sharing; R#31).
 
 Independent routes: closed forms on a fresh index (the FIFO hands out ascending pages, R#22), the

@@ -39,7 +39,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4])
-    ap.add_argument("--by", default="layer", choices=["layer", "head"])
+    ap.add_argument("--by", default="layer", choices=["layer", "head", "balanced"],
+                    help="layer / head: one contiguous rectangle per rank; balanced: the layer layout cut at KV-head "
+                         "granularity with the N3 owner's share reduced by N3's cost (shard.make_layout)")
+    ap.add_argument("--n3-units", type=float, default=-1.0,
+                    help="balanced layout: N3's cost in (layer, head) gather units (default: measured table N3_UNITS)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-all-cores", action="store_true", help="cpu_baseline on one core only")
@@ -53,6 +57,9 @@ def parse():
     ap.add_argument("--shard-world", type=int, default=0,
                     help="run one rank's shard of an N-GPU layout on this GPU (per-GPU work; no collectives)")
     ap.add_argument("--shard-rank", type=int, default=0)
+    ap.add_argument("--dist-ws1", action="store_true",
+                    help="initialise a world-size-1 process group (NCCL unless BENCH_DIST_BACKEND) and run the "
+                         "multi-rank code path on one GPU")
     ap.add_argument("--rho", default="1/4", help="recompute fraction of N3 (paper: 25%%, P:L1032); 0/1 = no recompute "
                     "marks (e.g. same-user sessions, P:L719-722)")
     ap.add_argument("--link", action="store_true",
@@ -130,19 +137,24 @@ class Setup:
 def setup_ours(args, rank, world, device):
     import torch
     import paper_2605_23640_b200 as cp
-    from paper_2605_23640_b200.shard import make_shard, score_owner
+    from paper_2605_23640_b200.shard import make_layout, score_owner
     from synth.gen import attention_torch, make_workload
 
     S = Setup()
     wl = make_workload(args.config, scale=args.scale)
     g = wl.geometry
     sim_world = getattr(args, "shard_world", 0)
+    n3u = args.n3_units if args.n3_units >= 0 else N3_UNITS.get(args.config, 0.0)
+    S.n3_units = n3u
     if sim_world and world == 1:                      # one simulated rank of an N-GPU layout
-        sh = make_shard(args.shard_rank, sim_world, g.num_layers, g.num_kv_heads, args.by)
-        S.shard, S.owner = sh, (0 if score_owner(sim_world, g.num_layers, args.by) == args.shard_rank else -1)
+        rects = make_layout(args.shard_rank, sim_world, g.num_layers, g.num_kv_heads, args.by, n3u)
+        S.owner = 0 if score_owner(sim_world, g.num_layers, args.by) == args.shard_rank else -1
     else:
-        sh = make_shard(rank, world, g.num_layers, g.num_kv_heads, args.by)
-        S.shard, S.owner = sh, score_owner(world, g.num_layers, args.by)
+        rects = make_layout(rank, world, g.num_layers, g.num_kv_heads, args.by, n3u)
+        S.owner = score_owner(world, g.num_layers, args.by)
+    S.rects = rects
+    sh = rects[0]                                     # the base index's rectangle; the others are pool views
+    S.shard = sh
     wb, rb = wl.rounds[0]
     S.wl, S.wb, S.rb, S.g = wl, wb, rb, g
     w = g.window_len
@@ -158,11 +170,24 @@ def setup_ours(args, rank, world, device):
     S.cfg = cfg
     t0 = time.time()
     S.idx = cp.KVIndex(cfg, device)
+    S.views = [S.idx.view(r.num_layers, r.num_heads, r.layer_lo, r.head_lo) for r in rects[1:]]
     tdt = cfg.torch_dtype
     gen = torch.Generator(device=device)
     gen.manual_seed(1234 + rank)
-    H, d, L = sh.num_heads, g.head_dim, sh.num_layers
+    d = g.head_dim
     S.t = 0
+
+    def alloc_kv(nblocks, bt):
+        # one paged cache per rectangle, all on the one block table (the rank's requests' blocks)
+        out = []
+        for r in rects:
+            kv = cp.PagedKV.allocate(r.num_layers, nblocks, r.num_heads, d, tdt, bt, device, zero=False)
+            for tsr in kv.k + kv.v:
+                tsr.normal_(0.0, 1.0, generator=gen)
+            out.append(kv)
+        for kv in out[1:]:
+            kv.block_tables = out[0].block_tables
+        return out
     # ---- populate the pool with the writers, in chunks (untimed setup)
     insert_ms = 0.0
     chunk = 64
@@ -174,9 +199,7 @@ def setup_ours(args, rank, world, device):
         o = 0
         for r, k in enumerate(nb):
             bt[r, :k] = perm[o:o + k]; o += k
-        wkv = cp.PagedKV.allocate(L, sum(nb), H, d, tdt, bt, device, zero=False)
-        for tsr in wkv.k + wkv.v:
-            tsr.normal_(0.0, 1.0, generator=gen)
+        wkvs = alloc_kv(sum(nb), bt)
         db = cp.DeviceBatch.from_numpy(sub.tokens, sub.offsets, sub.mask, device)
         spans = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device)
                  for a in (sub.span_req, sub.span_begin, sub.span_len)]
@@ -184,10 +207,12 @@ def setup_ours(args, rank, world, device):
         S.t += 1
         torch.cuda.synchronize()
         e0 = time.perf_counter()
-        S.idx.insert(db, wkv, *spans, bits, boff, S.t)
+        S.idx.insert(db, wkvs[0], *spans, bits, boff, S.t)
+        for v, kv in zip(S.views, wkvs[1:]):
+            v.copy_in(db, kv, reuse_worklist=True)
         torch.cuda.synchronize()
         insert_ms += (time.perf_counter() - e0) * 1e3
-        del wkv
+        del wkvs
         torch.cuda.empty_cache()
     err = S.idx.last_error()
     if err:
@@ -201,15 +226,14 @@ def setup_ours(args, rank, world, device):
     o = 0
     for r, k in enumerate(nb):
         bt[r, :k] = perm[o:o + k]; o += k
-    S.dst = cp.PagedKV.allocate(L, sum(nb), H, d, tdt, bt, device, zero=False)
-    for tsr in S.dst.k + S.dst.v:
-        tsr.normal_(0.0, 1.0, generator=gen)
+    S.dsts = alloc_kv(sum(nb), bt)
+    S.dst = S.dsts[0]
     S.hits = cp.Hits(rb.total_tokens // w + rb.num_reqs + 1, rb.num_reqs, rb.total_tokens, device)
     S.is_owner = rank == S.owner
     if args.config == 2:
         # MSMARCO pairs: the readers' own segments go back into the pool (Duplicates of the writers')
         ib = rb
-        S.ins_db, S.ins_kv = S.rdb, S.dst
+        S.ins_db, S.ins_kvs = S.rdb, S.dsts
     else:
         # strict-masking corpora: a reader's coarse segment is its whole system+passages run, so the
         # insert half of the step re-inserts a batch of passage writers (their spans, scored by N3 on
@@ -228,9 +252,8 @@ def setup_ours(args, rank, world, device):
                 for blk in range(a0, a1):
                     if bti[r, blk] == 0:
                         bti[r, blk] = o; o += 1
-        S.ins_kv = cp.PagedKV.allocate(L, o, H, d, tdt, bti, device, zero=False)
-        for tsr in S.ins_kv.k + S.ins_kv.v:
-            tsr.normal_(0.0, 1.0, generator=gen)
+        S.ins_kvs = alloc_kv(o, bti)
+    S.ins_kv = S.ins_kvs[0]
     S.ib = ib
     S.spans = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device)
                for a in (ib.span_req, ib.span_begin, ib.span_len)]
@@ -265,6 +288,9 @@ def setup_ours(args, rank, world, device):
 
 
 RHO = (1, 4)
+# N3's cost on the final-layer owner in (layer, KV head) gather units, for the balanced layout: measured
+# N3 time / (gather time / (L*H)) at N=1 (profiles/r02/scaling: config 2: 0.33 ms vs 13.57 ms / 256)
+N3_UNITS = {2: 6.0, 3: 2.0, 4: 2.0}
 
 
 def score_spans(b, device, torch, cp, attention_torch):
@@ -274,6 +300,12 @@ def score_spans(b, device, torch, cp, attention_torch):
             [int(x) for x in b.span_begin], [int(x) + int(m) - 1 for x, m in zip(b.span_begin, b.span_len)])
     sc, bits, so, bo = cp.score_deviation(*args, *RHO)
     return bits, torch.tensor(bo[:-1] or [0], dtype=torch.int64, device=device)
+
+
+def copy_in_views(S):
+    """The other rectangles' share of the insert's copy-in (pool views; the base's list is reused)."""
+    for v, kv in zip(S.views, S.ins_kvs[1:]):
+        v.copy_in(S.ins_db, kv, reuse_worklist=True)
 
 
 def run_step(S, torch, cp, world, events=None):
@@ -291,13 +323,13 @@ def run_step(S, torch, cp, world, events=None):
     S.t += 1
     ev = events
     main = torch.cuda.current_stream()
-    scores = S.is_owner or world > 1
+    scores = S.is_owner or S.use_dist
 
     def score():
         if ev: ev[5].record()
         if S.is_owner:                                                             # N3
             cp.score_deviation(*S.score_args, *RHO, out_scores=S.scores, out_bits=S.bits)
-        if world > 1:
+        if S.use_dist:
             broadcast_update(S.bits, S.owner)                                      # C1: index update
         if ev: ev[6].record()
         S.ev_score_done.record()
@@ -321,6 +353,8 @@ def run_step(S, torch, cp, world, events=None):
     if S.link:                                                                     # NEXT-2
         S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
     S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True, skip_linked=S.link)   # N2
+    for v, dkv in zip(S.views, S.dsts[1:]):                                        # the rank's other rectangles
+        v.gather_rerotate(S.rdb, S.hits, dkv, zero_recompute=True, skip_linked=S.link, reuse_worklist=True)
     if ev: ev[2].record()
     if S.overlap == 3:
         if scores:
@@ -328,6 +362,7 @@ def run_step(S, torch, cp, world, events=None):
         main.wait_event(S.ev_prep_done)
         if ev: ev[3].record()
         S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
+        copy_in_views(S)
     elif S.overlap == 2:
         if scores:
             S.ev_gather_done.record()
@@ -339,11 +374,13 @@ def run_step(S, torch, cp, world, events=None):
             main.wait_event(S.ev_score_done)
         if ev: ev[3].record()
         S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
+        copy_in_views(S)
     else:
         if scores:
             main.wait_event(S.ev_score_done)
         if ev: ev[3].record()
         S.idx.insert(*ins, out=S.ins_out)                                          # N4
+        copy_in_views(S)
     if ev: ev[4].record()
     S.ev_insert_done.record()
 
@@ -360,7 +397,15 @@ def bench_ours(args):
     if os.environ.get("BENCH_DEVICE0"):
         local = 0
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    if world > 1:
+    use_dist = world > 1 or args.dist_ws1
+    if use_dist and world == 1:
+        # --dist-ws1: a world-size-1 process group, so the N > 1 code path (device-tensor NCCL broadcast of
+        # the index update, max-over-ranks all_reduce) runs on a one-GPU box
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    if use_dist:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -368,9 +413,13 @@ def bench_ours(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     S = setup_ours(args, rank, world, device)
-    L, H, d = S.shard.num_layers, S.shard.num_heads, S.g.head_dim
+    S.use_dist = use_dist
+    d = S.g.head_dim
+    L = sum(r.num_layers for r in S.rects)
+    H = S.shard.num_heads
+    units = sum(r.num_layers * r.num_heads for r in S.rects)
     e = 2 if S.g.dtype == "bf16" else 4
-    row = L * H * d * e                                  # one token's K (or V) rows over the shard's layers
+    row = units * d * e                                  # one token's K (or V) rows over the rank's (layer, head) units
     # warm-up (also establishes the per-step algorithmic bytes: the index is steady after warm-up)
     torch.cuda.synchronize()
     tw = time.perf_counter()
@@ -393,20 +442,20 @@ def bench_ours(args):
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(K)]
     clocks = Clocks(local)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     # keep the GPU under load for ~0.3 s while the sampler starts: untimed steps, the same count on
     # every rank (each step may hold a collective)
     n_busy = torch.tensor([max(3, int(0.3 / max(S.warm_s_per_step, 1e-4)) + 1)], dtype=torch.int64)
-    if world > 1:
+    if use_dist:
         nb_dev = n_busy.to(device) if backend == "nccl" else n_busy
         dist.all_reduce(nb_dev, op=dist.ReduceOp.MAX)
         n_busy = nb_dev.cpu()
     clocks.start()
     for _ in range(int(n_busy.item())):
         run_step(S, torch, cp, world)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = cp.kernel_launch_count()
@@ -420,16 +469,16 @@ def bench_ours(args):
     torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     launches = cp.kernel_launch_count() - l0
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ms_total = start.elapsed_time(end)
     phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(K)])
-    score_ms = float(np.mean([evs[k][5].elapsed_time(evs[k][6]) for k in range(K)])) if (S.is_owner or world > 1) else 0.0
+    score_ms = float(np.mean([evs[k][5].elapsed_time(evs[k][6]) for k in range(K)])) if (S.is_owner or S.use_dist) else 0.0
     if S.idx.last_error():
         raise RuntimeError("device error during timed steps")
     ms_step = ms_total / K
     gather_ms = float(phase[:, 1].mean())
-    if world > 1:
+    if use_dist:
         rdev = device if backend == "nccl" else torch.device("cpu")
         t = torch.tensor([ms_step, gather_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -464,7 +513,10 @@ def bench_ours(args):
                        "index_entries": len(S.wb.span_len), "insert_batch_spans": len(S.ib.span_len),
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
-                       "shard_layers": L, "shard_heads": H, "rho": f"{RHO[0]}/{RHO[1]}", "link": bool(args.link), "window_len": S.g.window_len,
+                       "shard_layers": L, "shard_heads": H, "shard_units": units,
+                       **({"dist_backend": dist.get_backend()} if use_dist else {}),
+                       "shard_rects": [[r.layer_lo, r.layer_hi, r.head_lo, r.head_hi] for r in S.rects],
+                       **({"n3_units": S.n3_units} if args.by == "balanced" else {}), "rho": f"{RHO[0]}/{RHO[1]}", "link": bool(args.link), "window_len": S.g.window_len,
                        "l2": "inputs larger than L2 (pool + destination caches ~100 GB), no flush needed"},
             "matched_tokens_per_s": round(cov / (ms_step * 1e-3), 1),
             # gather bytes (reused read + write, zero fills) over match + gather time
@@ -494,7 +546,7 @@ def bench_ours(args):
         if args.out:
             with open(args.out, "w") as f:
                 json.dump(out, f, indent=1)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return out
@@ -538,7 +590,7 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
     cov = int(S.hits.req_covered.sum().item())
     if cov != S.covered:
         raise RuntimeError(f"e2e steps covered {cov} tokens, device-timed steps {S.covered}")
-    if world > 1:
+    if S.use_dist:
         nccl = dist.get_backend() == "nccl"
         t = torch.tensor([ms], dtype=torch.float64, device=S.rdb.tokens.device if nccl else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -57,7 +57,8 @@ enum { CP_MATCH_NO_TOUCH = 1,                     /* cp_match_spans flags       
        CP_MATCH_PREFIX_ONLY = 4 };
 enum { CP_POLICY_FIXED_CHUNK = 1, CP_POLICY_PREFIX_ONLY = 2 };   /* cp_policy_spans              */
 enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2,  /* cp_gather_rerotate flags (R#14)            */
-       CP_SKIP_LINKED = 4 };                       /* NEXT-2: leave linkable blocks unwritten (R#31) */
+       CP_SKIP_LINKED = 4,                         /* NEXT-2: leave linkable blocks unwritten (R#31) */
+       CP_REUSE_WORKLIST = 8 };                    /* pool views: reuse the sibling's work list      */
 enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
 enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
 enum { CP_PLAN_UNCOVERED = 0, CP_PLAN_REUSED = 1, CP_PLAN_RECOMPUTE = 2 };              /* plan codes     */
@@ -117,6 +118,38 @@ typedef struct {
     const int32_t* block_tables;    /* [num_reqs][max_blocks_per_req] block ids                      */
     int32_t        max_blocks_per_req;
 } cp_paged_kv;
+
+/*
+ * Pool views (multi-GPU load balancing).  A rank whose shard of the (layer, KV head)
+ * grid is not one rectangle holds one index for a rectangle (the base) and a view per further
+ * rectangle: the view has its own geometry (num_layers x num_kv_heads at layer_offset / head_offset;
+ * head_dim, dtype, RoPE and every capacity are the base's) and its own pool K/V workspaces (sizes:
+ * cp_index_workspace of the base's config with the view's geometry), and shares the base's META and
+ * SCRATCH -- the entry table, page lists, hash table, hit and copy lists -- so one match and one
+ * insert serve every rectangle of the rank.  Allowed on a view: cp_gather_rerotate (with the base's
+ * cp_match_spans output; every page id is the base's), cp_link_blocks, cp_index_copy_in,
+ * cp_index_snapshot / cp_index_last_error (the base's state).  cp_match_spans and the insert calls on a
+ * view return CP_ERR_INVALID_ARG.  A view must be destroyed before its base; all calls on a base and
+ * its views must be stream-ordered by the caller (they share scratch).
+ */
+cp_status cp_index_create_view(const cp_index* base, int32_t num_layers, int32_t num_kv_heads, int32_t layer_offset,
+                               int32_t head_offset, void* pool_k, void* pool_v, cp_index** out_h);
+
+/* Copy the writer K/V rows of the entries published by the base's most recent cp_index_insert /
+ * cp_index_insert_commit into this view's pool pages (the view's share of that insert's copy-in;
+ * no rotation; flags: 0 or CP_REUSE_WORKLIST).  writers_h / writer_kv_h: the insert's writer batch and the writer paged KV in the
+ * view's geometry.  Must be stream-ordered after that commit and before the base's next insert. */
+cp_status cp_index_copy_in(cp_index* view, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h, int32_t flags,
+                           void* stream);
+
+/* CP_REUSE_WORKLIST (cp_gather_rerotate / cp_index_copy_in flag): the gather's work list -- chunks of
+ * hits, per-token source/destination row INDICES with plan codes, per-hit cos/sin -- does not depend on
+ * the layer / head geometry, so the rectangles of one rank build it once.  With the flag, the call
+ * reuses the list the immediately preceding gather (or insert copy-in) of this index family built,
+ * and launches only the copy kernel.  The library checks on the host that the previous list was built
+ * from the same buffers (hits, batch offsets, plan, block table pointer and width, CP_SKIP_LINKED) and
+ * that no match / insert ran since, else returns CP_ERR_INVALID_ARG; the caller guarantees that those
+ * buffers' CONTENTS did not change in between (so all rectangles must share one block table). */
 
 /*
  * Insert `num_spans` segments (request span_req[s], positions [span_begin[s], +span_len[s])) of

@@ -17,7 +17,7 @@ CP_FP32, CP_BF16 = 0, 1
 CP_ROPE_NEOX, CP_ROPE_GPTJ = 0, 1
 CP_MATCH_NO_TOUCH, CP_MATCH_FIXED_CHUNK, CP_MATCH_PREFIX_ONLY = 1, 2, 4
 CP_POLICY_FIXED_CHUNK, CP_POLICY_PREFIX_ONLY = 1, 2
-CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED = 1, 2, 4
+CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED, CP_REUSE_WORKLIST = 1, 2, 4, 8
 CP_SCORE_INTER_INTRA, CP_SCORE_KVDEV = 0, 1
 CP_STORED, CP_SUPERSEDED, CP_DUPLICATE, CP_DROPPED_CONTAINED = 0, 1, 2, 3
 CP_WS_COUNT = 4
@@ -63,6 +63,8 @@ EXPORTS = {
     "cp_max_pages_per_entry": (i32, [C.POINTER(CpConfig)]),
     "cp_index_create": (i32, [C.POINTER(CpConfig), C.POINTER(vp), vp, C.POINTER(vp)]),
     "cp_index_destroy": (i32, [vp]),
+    "cp_index_create_view": (i32, [vp, i32, i32, i32, i32, vp, vp, C.POINTER(vp)]),
+    "cp_index_copy_in": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp]),
     "cp_index_insert": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,
                               vp, vp, vp]),
     "cp_index_insert_prepare": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,

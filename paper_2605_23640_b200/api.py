@@ -186,6 +186,12 @@ class KVIndex:
         except Exception:
             pass
 
+    def view(self, num_layers: int, num_kv_heads: int, layer_offset: int, head_offset: int,
+             stream=None) -> "KVIndexView":
+        """cp_index_create_view: a further (layer, head) rectangle of this rank served by this index's
+        metadata (one match, one insert) with its own pool."""
+        return KVIndexView(self, num_layers, num_kv_heads, layer_offset, head_offset)
+
     # --- pool views (for tests / diagnostics) ---
     def pool_views(self):
         c = self.cfg
@@ -231,9 +237,9 @@ class KVIndex:
 
     def gather_rerotate(self, readers: DeviceBatch, hits: Hits, dst_kv: PagedKV,
                         zero_recompute: bool = True, zero_uncovered: bool = False, skip_linked: bool = False,
-                        stream=None):
+                        reuse_worklist: bool = False, stream=None):
         flags = ((L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0) |
-                 (L.CP_SKIP_LINKED if skip_linked else 0))
+                 (L.CP_SKIP_LINKED if skip_linked else 0) | (L.CP_REUSE_WORKLIST if reuse_worklist else 0))
         rb, hc, kv = readers.c(), hits.c(), dst_kv.c()
         L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
                 "cp_gather_rerotate")
@@ -284,6 +290,34 @@ class KVIndex:
                 e["recompute"] = arr["recompute"][q * ML:q * ML + ln].astype(bool)
             out["entries"].append(e)
         return out
+
+
+class KVIndexView(KVIndex):
+    """A pool view (cp_index_create_view): own geometry + pool workspaces, the base's metadata."""
+
+    def __init__(self, base: KVIndex, num_layers: int, num_kv_heads: int, layer_offset: int, head_offset: int):
+        import dataclasses
+        self.base, self.device = base, base.device
+        self.cfg = dataclasses.replace(base.cfg, num_layers=num_layers, num_kv_heads=num_kv_heads,
+                                       layer_offset=layer_offset, head_offset=head_offset)
+        self._c = self.cfg.c()
+        lib = L.lib()
+        sizes = (C.c_size_t * L.CP_WS_COUNT)()
+        L.check(lib.cp_index_workspace(C.byref(self._c), sizes), "cp_index_workspace")
+        self.ws_sizes = [int(sizes[0]), int(sizes[1]), 0, 0]
+        self.ws = [torch.empty(max(int(sizes[i]), 256), dtype=torch.uint8, device=self.device) for i in range(2)]
+        h = C.c_void_p()
+        L.check(lib.cp_index_create_view(base.h, num_layers, num_kv_heads, layer_offset, head_offset,
+                                         _ptr(self.ws[0]), _ptr(self.ws[1]), C.byref(h)), "cp_index_create_view")
+        self.h = h
+        self.num_pages, self.max_pages_per_entry, self.B = base.num_pages, base.max_pages_per_entry, base.B
+
+    def copy_in(self, writers: DeviceBatch, writer_kv: PagedKV, reuse_worklist: bool = False, stream=None):
+        """cp_index_copy_in: this view's share of the base's last insert copy-in."""
+        wb, kv = writers.c(), writer_kv.c()
+        flags = L.CP_REUSE_WORKLIST if reuse_worklist else 0
+        L.check(L.lib().cp_index_copy_in(self.h, C.byref(wb), C.byref(kv), flags, _stream(stream)),
+                "cp_index_copy_in")
 
 
 def score_deviation(attn: Sequence[torch.Tensor], n: Sequence[int], heads: Sequence[int], span_l: Sequence[int],

@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
             a.hit_cs[q] = make_float2((float)cs, (float)sn);
         }
     }
-    const int64_t rowE = (int64_t)a.H * a.d;
     const int64_t ntok = (int64_t)a.hdr->n_chunks * CP_GATHER_CHUNK;
     for (int64_t q = gt; q < ntok; q += nt) {
         const int c = (int)(q / CP_GATHER_CHUNK), i = (int)(q % CP_GATHER_CHUNK);
@@ -106,8 +105,10 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
                                                                            // k_rows then writes nothing
         const int page = a.slot_pages[(int64_t)slot * a.MP + (t >> 4)];
         const int blk = a.block_tables[(int64_t)r * a.max_blocks + (pos >> 4)];
-        const long long pool_row = ((long long)page * CP_BLOCK + (t & 15)) * rowE;
-        const long long paged_row = ((long long)blk * CP_BLOCK + (pos & 15)) * rowE;
+        // token-row INDICES (not element offsets): the table is independent of the shard geometry, so
+        // the pool views of one rank reuse it (CP_REUSE_WORKLIST); the copy kernels scale by H*d
+        const long long pool_row = (long long)page * CP_BLOCK + (t & 15);
+        const long long paged_row = (long long)blk * CP_BLOCK + (pos & 15);
         long long code = a.dir == 0 ? (long long)a.plan[a.req_off[r] + pos] : (long long)CP_PLAN_REUSED;
         if (a.dir == 0 && (a.flags & CP_SKIP_LINKED) && code == CP_PLAN_REUSED && a.l_delta[hh] == 0 && (k & 15) == 0) {
             const int b0 = pos & ~15;                                       // >= k: k is page aligned
@@ -204,8 +205,8 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
         if (tid < ntok) {
             const int64_t q = (int64_t)c * CP_GATHER_CHUNK + tid;
             const long long dw = a.row_dst[q];
-            s_src[tid] = a.row_src[q];
-            s_dst[tid] = dw & ((1LL << 62) - 1);
+            s_src[tid] = a.row_src[q] * rowE;
+            s_dst[tid] = (dw & ((1LL << 62) - 1)) * rowE;
             s_code[tid] = (int)((unsigned long long)dw >> 62);
         }
         float2 csr[VEC];
@@ -394,7 +395,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst
             const char* srcK = a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l];
             const char* srcV = a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l];
             long long my_src = 0, my_dst = 0;
-            if (lane < ntok_item) { my_src = a.row_src[(int64_t)c * CP_GATHER_CHUNK + lane]; my_dst = a.row_dst[(int64_t)c * CP_GATHER_CHUNK + lane]; }
+            if (lane < ntok_item) {
+                my_src = a.row_src[(int64_t)c * CP_GATHER_CHUNK + lane] * rowE;
+                const long long dw = a.row_dst[(int64_t)c * CP_GATHER_CHUNK + lane];
+                my_dst = ((dw & ((1LL << 62) - 1)) * rowE) | (dw & ~((1LL << 62) - 1));
+            }
             for (int u0 = 0; u0 < ntok_item; u0 += kTmaTok, ++it) {
                 const int s = it % nst;
                 if (it >= nst) mbar_wait(&empty[s], ((it / nst) - 1) & 1);
@@ -628,10 +633,23 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     a.row_src = x->row_src; a.row_dst = x->row_dst;
     a.hit_cs = x->hit_cs; a.cs_hits = x->CS_HITS;
     if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;
-    k_rows_prep<<<1, kPrepThreads, 0, st>>>(a);
-    CP_COUNT_LAUNCH();
-    k_rows_prep2<<<sm_count() * 2, kPrepThreads, 0, st>>>(a);
-    CP_COUNT_LAUNCH();
+    WorkKey key;
+    key.valid = 1; key.dir = dir; key.cap = list_cap; key.max_blocks = kv->max_blocks_per_req;
+    key.skip_linked = dir == 0 && (flags & CP_SKIP_LINKED) ? 1 : 0;
+    const void* kp[9] = {d_count, l_req, l_slot, l_dst, l_len, l_delta, req_off, plan, kv->block_tables};
+    for (int i = 0; i < 9; ++i) key.p[i] = kp[i];
+    if (flags & CP_REUSE_WORKLIST) {
+        // the previous gather / copy-in of this index family built the same list (only the layer and head
+        // geometry differ): rewind the dynamic item counter and run the copy kernel alone
+        if (!x->wk || !x->wk->same(key)) return CP_ERR_INVALID_ARG;
+        if (cudaMemsetAsync(&x->hdr->gather_next, 0, sizeof(x->hdr->gather_next), st) != cudaSuccess) return CP_ERR_CUDA;
+    } else {
+        k_rows_prep<<<1, kPrepThreads, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        k_rows_prep2<<<sm_count() * 2, kPrepThreads, 0, st>>>(a);
+        CP_COUNT_LAUNCH();
+        if (x->wk) *x->wk = key;
+    }
     const bool bf16 = x->cfg.dtype == CP_BF16;
     const int var = gather_variant();
     if (bf16) { if (a.gptj) launch_rows_t<__nv_bfloat16, true>(a, var, st); else launch_rows_t<__nv_bfloat16, false>(a, var, st); }

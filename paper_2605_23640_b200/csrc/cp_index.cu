@@ -1318,12 +1318,32 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     }
     cudaFuncSetAttribute(k_ins_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hash_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    x->wk = new WorkKey();
+    *out = x;
+    return CP_OK;
+}
+
+cp_status cp_index_create_view(const cp_index* base, int32_t num_layers, int32_t num_kv_heads, int32_t layer_offset,
+                               int32_t head_offset, void* pool_k, void* pool_v, cp_index** out) {
+    if (!base || base->is_view || !pool_k || !pool_v || !out) return CP_ERR_INVALID_ARG;
+    if (((uintptr_t)pool_k & 255) || ((uintptr_t)pool_v & 255)) return CP_ERR_INVALID_ARG;
+    cp_config vc = base->cfg;
+    vc.num_layers = num_layers; vc.num_kv_heads = num_kv_heads; vc.layer_offset = layer_offset; vc.head_offset = head_offset;
+    if (!valid_cfg(&vc)) return CP_ERR_INVALID_ARG;
+    cp_index* x = new cp_index(*base);          // the base's META / SCRATCH pointers, layout and counters
+    x->cfg = vc;
+    x->is_view = 1;
+    x->insert_prepared = 0;
+    cp_index_workspace(&vc, x->ws);
+    x->ws[CP_WS_META] = 0; x->ws[CP_WS_SCRATCH] = 0;   // not owned by the view
+    x->pool_k = (char*)pool_k; x->pool_v = (char*)pool_v;
     *out = x;
     return CP_OK;
 }
 
 cp_status cp_index_destroy(cp_index* x) {
     if (!x) return CP_ERR_INVALID_ARG;
+    if (!x->is_view) delete x->wk;
     delete x;
     return CP_OK;
 }
@@ -1434,7 +1454,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
                    const int32_t* span_req, const int32_t* span_begin, const int32_t* span_len,
                    const uint32_t* bits, const int64_t* bits_off, uint64_t t, int32_t* out_id, int32_t* out_oc,
                    InsArgs& a) {
-    if (!x || !wb || !kv) return CP_ERR_INVALID_ARG;
+    if (!x || !wb || !kv || x->is_view) return CP_ERR_INVALID_ARG;       // a view's metadata is its base's
     if (num_spans < 0 || num_spans > x->MS) return CP_ERR_INVALID_ARG;
     if (num_spans == 0) return CP_OK;
     if (!span_req || !span_begin || !span_len || !out_id || !out_oc) return CP_ERR_INVALID_ARG;
@@ -1476,6 +1496,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
 // read-only phases: validation, hashing, batch dedup, containment scan + verification (scratch only)
 cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     const int num_spans = a.S;
+    cp_invalidate_worklist(x);
     const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
     k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -1496,6 +1517,7 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
 // mutating phases: sequential apply, table updates, copy-in of the writer KV
 cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp_paged_kv* kv, cudaStream_t st) {
     const int num_spans = a.S;
+    cp_invalidate_worklist(x);
     const size_t csm = CommitSmem(x->S, num_spans, a.candK, a.rec_cap).total;
     k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -1550,6 +1572,16 @@ cp_status cp_index_insert_commit(cp_index* x, const cp_batch* wb, const cp_paged
     if (!x->insert_prepared) return CP_ERR_INVALID_ARG;          // commit without prepare
     x->insert_prepared = 0;
     return ins_commit(x, a, wb, kv, (cudaStream_t)stream);
+}
+
+cp_status cp_index_copy_in(cp_index* v, const cp_batch* wb, const cp_paged_kv* kv, int32_t flags, void* stream) {
+    if (!v || !v->is_view || !wb || !kv || !wb->offsets) return CP_ERR_INVALID_ARG;
+    if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables || kv->max_blocks_per_req < 1) return CP_ERR_INVALID_ARG;
+    if (wb->num_reqs < 1 || wb->num_reqs > v->cfg.max_batch_reqs) return CP_ERR_INVALID_ARG;
+    // the base's last commit left its copy-in list (entries published by that call) in the shared
+    // scratch; the copy kernels re-resolve it against this view's geometry and pool
+    return cp_launch_rows(v, 1, &v->hdr->n_copy, v->cp_req, v->cp_slot, v->cp_dst, v->cp_len, nullptr,
+                          v->MS, wb->offsets, nullptr, kv, flags & CP_REUSE_WORKLIST, (cudaStream_t)stream);
 }
 
 }  // extern "C"

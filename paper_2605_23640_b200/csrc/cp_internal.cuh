@@ -69,12 +69,31 @@ struct Cand {
     int32_t ok;       // set by verification
 };
 
+// Host-side identity of the gather / copy-in work list now in SCRATCH (chunk list, row table, cos/sin),
+// shared by an index and its pool views: a view's gather or copy-in may reuse it (CP_REUSE_WORKLIST)
+// instead of rebuilding it, because the row table holds token-row indices, not geometry-dependent offsets.
+struct WorkKey {
+    int valid = 0;
+    int dir = 0;
+    const void* p[9] = {};      // count, req, slot, dst, len, delta, req_off, plan, block_tables
+    int64_t cap = 0;
+    int32_t max_blocks = 0, skip_linked = 0;
+    bool same(const WorkKey& o) const {
+        if (!valid || !o.valid || dir != o.dir || cap != o.cap || max_blocks != o.max_blocks || skip_linked != o.skip_linked)
+            return false;
+        for (int i = 0; i < 9; ++i) if (p[i] != o.p[i]) return false;
+        return true;
+    }
+};
+
 struct cp_index {
     cp_config cfg;
     int64_t P;           // physical pages
     int32_t MP;          // max pages per entry
     char* match_g = nullptr;   // matcher arrays in global scratch (only when max_req_tokens > CP_MATCH_SMEM_TOKENS)
     int insert_prepared = 0;   // cp_index_insert_prepare issued, commit pending (host-side guard)
+    int is_view = 0;           // a pool view (cp_index_create_view): own geometry + pool, the base's META/SCRATCH
+    WorkKey* wk = nullptr;     // owned by the base, shared by its views
     int32_t S;           // slots
     int64_t T;           // prefix-table entries (pow2)
     int32_t logT;
@@ -137,6 +156,7 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
                          const int32_t* l_slot, const int32_t* l_dst, const int32_t* l_len,
                          const int32_t* l_delta, int64_t list_cap, const int64_t* req_off,
                          const uint8_t* plan, const cp_paged_kv* kv, int32_t flags, cudaStream_t st);
+inline void cp_invalidate_worklist(cp_index* x) { if (x && x->wk) x->wk->valid = 0; }
 
 // ---- device helpers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t cp_mulmod(uint64_t a, uint64_t b) {

@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
 
 extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, int32_t flags, const cp_hits* o,
                                     void* stream) {
+    if (x && x->is_view) return CP_ERR_INVALID_ARG;          // views gather with their base's hits
+    cp_invalidate_worklist(x);                               // it rewrites the hits a gather list was built from
     if (!x || !b || !o) return CP_ERR_INVALID_ARG;
     if ((flags & CP_MATCH_FIXED_CHUNK) && (flags & CP_MATCH_PREFIX_ONLY)) return CP_ERR_INVALID_ARG;
     if (b->num_reqs < 0 || b->num_reqs > x->cfg.max_batch_reqs || b->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;

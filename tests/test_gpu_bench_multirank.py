@@ -43,3 +43,41 @@ def test_single_rank_bench_line_has_the_contract_keys():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "sm_mhz" in d["clocks"]
+
+
+def test_world_size_one_nccl_group_runs_the_multirank_path():
+    """--dist-ws1: a world-size-1 NCCL process group, so bench.py's N > 1 branch -- the device-tensor
+    NCCL broadcast of the recompute bits (shard.broadcast_update), the barriers and the max-over-ranks
+    all_reduce -- executes on this one-GPU box (the driver's SCALE run is then not its first execution)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("BENCH_DIST_BACKEND", "RANK", "WORLD_SIZE")}
+    env["MASTER_PORT"] = "29641"
+    cmd = [sys.executable, "bench.py", "--dist-ws1", "--steps", "3", "--warmup", "3", "--scale", "0.1",
+           "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"].get("dist_backend") == "nccl"
+
+
+@pytest.mark.parametrize("rank", [0, 3, 7])
+def test_balanced_layout_rank_runs(rank):
+    """One simulated rank of the 8-GPU balanced layer layout (base index + pool views) runs the step."""
+    cmd = [sys.executable, "bench.py", "--by", "balanced", "--shard-world", "8", "--shard-rank", str(rank),
+           "--steps", "3", "--warmup", "3", "--scale", "0.1", "--no-cpu-baseline", "--no-e2e"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    from paper_2605_23640_b200.shard import balanced_units
+    u0, u1 = balanced_units(8, 32, 8, d["config"]["n3_units"])[rank]
+    assert d["config"]["shard_units"] == u1 - u0 and d["value"] > 0
+
+
+def test_two_rank_balanced_bench_runs():
+    env = dict(os.environ, BENCH_DEVICE0="1", BENCH_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29651", "bench.py", "--gpus", "2", "--by", "balanced",
+           "--steps", "3", "--warmup", "3", "--scale", "0.1", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "balanced-sharded x2"

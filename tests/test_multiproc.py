@@ -44,6 +44,37 @@ def test_shards_partition_layers_and_heads():
         make_shard(2, 2, 32, 8)
 
 
+def test_balanced_layout_partitions_the_unit_grid():
+    """The balanced layout (shard.make_layout 'balanced'): every (layer, head) unit on exactly one rank,
+    each rank's rectangles contiguous in (layer, head) order, at most three per rank, the owner (last
+    rank) holding the whole final layer and about `extra` units fewer than the others."""
+    from paper_2605_23640_b200.shard import balanced_units, make_layout
+    for L, H in [(32, 8), (80, 8), (2, 2), (32, 1)]:
+        for world in [1, 2, 3, 4, 8]:
+            if world > 1 and L * H - H < world - 1:
+                with pytest.raises(ValueError):
+                    make_layout(0, world, L, H, "balanced", 1.0)
+                continue
+            for extra in [0.0, 2.5, 6.0]:
+                seen = []
+                for r in range(world):
+                    rects = make_layout(r, world, L, H, "balanced", extra)
+                    assert 1 <= len(rects) <= 3
+                    units = [l * H + h for s in rects for l in range(s.layer_lo, s.layer_hi)
+                             for h in range(s.head_lo, s.head_hi)]
+                    assert units == list(range(units[0], units[0] + len(units)))
+                    seen += units
+                assert seen == list(range(L * H))
+                own = make_layout(world - 1, world, L, H, "balanced", extra)
+                assert own[-1].layer_hi == L and any(s.layer_lo <= L - 1 < s.layer_hi and s.head_lo == 0
+                                                     and s.head_hi == H for s in own)
+                sizes = [b - a for a, b in balanced_units(world, L, H, extra)]
+                if world > 1 and sizes[-1] > H:
+                    others = sizes[:-1]
+                    assert max(others) - min(others) <= 1
+                    assert abs((sizes[-1] + extra) - sum(others) / len(others)) <= 1.0 + 1e-9
+
+
 def _snapshot_digest(idx):
     h = hashlib.sha256()
     for e in idx.live_entries():

@@ -289,8 +289,8 @@ def setup_ours(args, rank, world, device):
 
 RHO = (1, 4)
 # N3's cost on the final-layer owner in (layer, KV head) gather units, for the balanced layout: measured
-# N3 time / (gather time / (L*H)) at N=1 (profiles/r02/scaling: config 2: 0.33 ms vs 13.57 ms / 256)
-N3_UNITS = {2: 6.0, 3: 2.0, 4: 2.0}
+# N3 time / (gather time / (L*H)) at N=1 (profiles/r02: config 2: 0.24 ms vs 13.58 ms / 256 units)
+N3_UNITS = {2: 4.5, 3: 2.0, 4: 2.0}
 
 
 def score_spans(b, device, torch, cp, attention_torch):

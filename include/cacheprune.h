@@ -393,8 +393,10 @@ uint64_t cp_index_hash_base(const cp_index* idx);
  * 6/7/8/9 dynamic (3,2)/(2,4)/(4,2)/(8,1)).  Also the CP_GATHER_VARIANT environment variable. */
 cp_status cp_set_gather_variant(int32_t variant);
 
-/* Select the N3 row kernel's CTAs per SM (0: 4, 1: 5, 2: 6, 3: 8; register-capped to fit; A/B
- * measurement; default 0, or the CP_SCORE_VARIANT environment variable). */
+/* Select the N3 row kernel (A/B measurement; default 0, or the CP_SCORE_VARIANT environment variable):
+ * 0 one row per 8-lane group (4 rows per warp), 4 CTAs/SM; 5 16-lane groups; 6 8-lane groups with 6
+ * vectors per lane at 3 CTAs/SM; 7 4-lane groups; 4 the round-1 one-warp-per-row kernel at 4 CTAs/SM and
+ * 1 / 2 / 3 the same at 5 / 6 / 8 CTAs/SM.  All give identical results. */
 cp_status cp_set_score_variant(int32_t variant);
 
 /* Diagnostic: contiguous copy of `bytes` (multiple of 16) with the gather's 128-bit streaming load /

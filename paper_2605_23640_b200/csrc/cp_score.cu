@@ -3,7 +3,8 @@
 // table on the CPU after copying the attention matrix off the GPU (L770, 383 ms at 10K tokens,
 // L1201); here the attention never leaves HBM: the row sums are streamed directly.
 //
-//   k_score_rows : one warp per span row i; reads A_h[i][0..i] (fp32, 128-bit loads where aligned),
+//   k_score_rows_grp (default; k_score_rows = one warp per row, variant 4): one 8-lane group per span
+//                  row i, 4 rows per warp; reads A_h[i][0..i] (fp32, 128-bit loads where aligned),
 //                  accumulates q(x) = trunc(x * 2^40) in int64 (R#17: exact and order independent,
 //                  so the GPU and the oracle agree bit for bit) with sign + for j < l*, - for j >= l*.
 //   k_score_topk : one CTA per span; 8-pass MSB radix select of the k-th largest score
@@ -116,6 +117,70 @@ __global__ void __launch_bounds__(kRowThreads, MINB) k_score_rows(const ScoreArg
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) a.scores[score_off + (i - l)] = acc;
+    }
+}
+
+// ---- k_score_rows_grp (default): the row kernel above with a row per SUB-lane group instead of per
+// warp.  ncu of k_score_rows (profiles/r02/n3): ~457 warp instructions per row at 57% issue-active, the
+// per-row setup (span search, pointers, head / tail, reduction) a third of them; with 32/SUB consecutive
+// rows per warp the setup instructions serve 32/SUB rows at once, each row still read with 16-B loads
+// (SUB x 16 B contiguous per instruction and row), and the reduction is log2(SUB) shuffle levels.
+// Consecutive rows have nearly equal lengths, so the groups of a warp stay converged.
+template <int SUB, int U>
+__device__ __forceinline__ long long grp_row_score(const float* p, int cnt, int l, int sl) {
+    long long all = 0, inter = 0;
+    const int mis = (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
+    const int head = min(cnt, mis ? 4 - mis : 0);
+    if (sl < head) { const long long x = q40(__ldg(p + sl)); all += x; if (sl < l) inter += x; }
+    const int nvec = (cnt - head) >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(p + head);
+    for (int q0 = 0; q0 < nvec; q0 += SUB * U) {
+        float4 f[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u * SUB + sl;
+            f[u] = q < nvec ? ld_nc4(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j0 = head + 4 * (q0 + u * SUB + sl);
+            const long long x0 = q40(f[u].x), x1 = q40(f[u].y), x2 = q40(f[u].z), x3 = q40(f[u].w);
+            const long long sm = (x0 + x1) + (x2 + x3);
+            all += sm;
+            if (j0 + 3 < l) inter += sm;
+            else if (j0 < l) inter += x0 + (j0 + 1 < l ? x1 : 0) + (j0 + 2 < l ? x2 : 0);
+        }
+    }
+    const int t = head + 4 * nvec + sl;
+    if (sl < 3 && t < cnt) { const long long x = q40(__ldg(p + t)); all += x; if (t < l) inter += x; }
+    return 2 * inter - all;
+}
+
+template <int SUB, int U, int MINB>
+__global__ void __launch_bounds__(kRowThreads, MINB) k_score_rows_grp(const ScoreArgs a) {
+    __shared__ int32_t s_rb[kSpansPerLaunch];
+    for (int q = threadIdx.x; q < a.nsp; q += blockDim.x) s_rb[q] = a.sp[q].row_begin;
+    __syncthreads();
+    constexpr int R = 32 / SUB;                                  // rows per warp
+    const int lane = threadIdx.x & 31, sg = lane / SUB, sl = lane % SUB;
+    const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    const int ngroups = (a.total_rows + R - 1) / R;
+    for (int g = warp; g < ngroups; g += nwarps) {
+        const int gr = g * R + sg;
+        long long acc = 0;
+        int lo = 0;
+        if (gr < a.total_rows) {
+            int hi = a.nsp - 1;
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rb[mid] <= gr) lo = mid; else hi = mid - 1; }
+            const float* A = a.sp[lo].A;
+            const int n = a.sp[lo].n, l = a.sp[lo].l, heads = a.sp[lo].heads();
+            const int i = l + (gr - s_rb[lo]);
+            for (int h = 0; h < heads; ++h) acc += grp_row_score<SUB, U>(A + ((int64_t)h * n + i) * (int64_t)n, i + 1, l, sl);
+        }
+#pragma unroll
+        for (int o = SUB / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sl == 0 && gr < a.total_rows) a.scores[a.sp[lo].score_off + (gr - s_rb[lo])] = acc;
     }
 }
 
@@ -307,10 +372,20 @@ void launch_score_rows(const ScoreArgs& a, cudaStream_t st) {
         kern<<<grid, kRowThreads, 0, st>>>(a);
     };
     switch (g_score_variant) {
+        // (lanes per row, 16-B vectors per lane in flight, CTAs/SM); tools/score_ab.py, config 2 (ms incl. top-k):
+        // (8,4,4) 0.233-0.236; (16,4,4) 0.251; (8,6,3) 0.245; (4,4,4) 0.279; (8,2,4) 0.305; (8,8,3) 0.282;
+        // round-1 warp per row (variant 4) 0.293
+        case 0: go(k_score_rows_grp<8, 4, 4>, 4); return;         // default: 4 rows per warp
+        case 5: go(k_score_rows_grp<16, 4, 4>, 4); return;
+        case 6: go(k_score_rows_grp<8, 6, 3>, 3); return;
+        case 7: go(k_score_rows_grp<4, 4, 4>, 4); return;
+        default: break;
+    }
+    switch (g_score_variant) {
         case 1: go(k_score_rows<5>, 5); break;
         case 2: go(k_score_rows<6>, 6); break;
         case 3: go(k_score_rows<8>, 8); break;
-        default: go(k_score_rows<4>, 4); break;           // 4 CTAs/SM: best in tools/score_rows_ab.cu
+        default: go(k_score_rows<4>, 4); break;           // variant 4: the round-1 warp-per-row kernel
     }
 }
 
@@ -455,7 +530,7 @@ extern "C" cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* req
 }
 
 extern "C" cp_status cp_set_score_variant(int32_t v) {
-    if (v < 0 || v > 3) return CP_ERR_INVALID_ARG;
+    if (v < 0 || v > 7) return CP_ERR_INVALID_ARG;
     g_score_variant = v;
     return CP_OK;
 }

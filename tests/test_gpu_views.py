@@ -63,10 +63,19 @@ def test_balanced_rank_views_equal_slices_of_the_full_index(rank, world):
     assert ref.last_error() == 0 and base.last_error() == 0
     # pools: each rectangle's pool is the slice of the full pool (same page ids: shared metadata)
     fk, fv = ref.pool_views()
+    snap = ref.snapshot(with_tokens=False)
+    assert [e["pages"].tolist() for e in snap["entries"]] == \
+        [e["pages"].tolist() for e in base.snapshot(with_tokens=False)["entries"]]
+    # the rows the entries hold (t < len; the rest of the pool is uninitialised)
+    pg = np.concatenate([e["pages"][np.arange(e["len"]) // 16] for e in snap["entries"]]).astype(np.int64)
+    sl = np.concatenate([np.arange(e["len"]) % 16 for e in snap["entries"]]).astype(np.int64)
+    pg, sl = torch.from_numpy(pg).cuda(), torch.from_numpy(sl).cuda()
     for ix, r in zip([base] + views, rects):
         k, v = ix.pool_views()
-        assert torch.equal(k.view(torch.int16), fk[r.layer_lo:r.layer_hi, :, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
-        assert torch.equal(v.view(torch.int16), fv[r.layer_lo:r.layer_hi, :, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
+        assert torch.equal(k[:, pg, sl].view(torch.int16),
+                           fk[r.layer_lo:r.layer_hi][:, pg, sl][:, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
+        assert torch.equal(v[:, pg, sl].view(torch.int16),
+                           fv[r.layer_lo:r.layer_hi][:, pg, sl][:, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
     # match once on the base; gather base + views with the reused work list
     rdb = full._dev_batch(rb)
     fh = ref.match_spans(rdb, 50)

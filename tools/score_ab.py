@@ -1,4 +1,4 @@
-"""A/B of the N3 row kernel's occupancy variants (cp_set_score_variant) on the bench's config-2
+"""A/B of the N3 row kernels (cp_set_score_variant: 0 a row per 8-lane group, 4 vectors per lane in flight, 4 CTAs/SM; 5: 16-lane groups; 6: 6 vectors at 3 CTAs/SM; 7: 4-lane groups; 4 the round-1 warp-per-row kernel, 1-3 its occupancy variants) on the bench's config-2
 score call (512 spans of the 256 reader prompts, synthetic final-layer attention), CUDA events.
 Prints ms and GB/s of algorithmic bytes (the row prefixes A[i][0..i] read)."""
 import os
@@ -22,6 +22,7 @@ def main():
     args = ([attn[int(r)] for r in rb.span_req], [int(rb.lens[int(r)]) for r in rb.span_req], [1] * len(rb.span_req),
             [int(b) for b in rb.span_begin], [int(b) + int(m) - 1 for b, m in zip(rb.span_begin, rb.span_len)])
     nbytes = sum(4 * (i + 1) for l, r in zip(args[3], args[4]) for i in range(l, r + 1))
+    L.check(L.lib().cp_set_score_variant(4))             # the register-staged row kernel as the reference
     sc, bits, so, bo = cp.score_deviation(*args, 1, 4)
     ref = (sc.clone(), bits.clone())
     # marshal once (the binding rebuilds 512-entry ctypes arrays per call; time the kernels, not that)
@@ -38,7 +39,7 @@ def main():
     def call():
         L.check(L.lib().cp_score_deviation(S, A, n_, h_, l_, r_, 1, 4, 0, maxm, C.c_void_p(sc.data_ptr()), so_,
                                            C.c_void_p(bits.data_ptr()), bo_, stream))
-    for v in (0, 1, 2, 3):
+    for v in (4, 0, 5, 6, 7):
         L.check(L.lib().cp_set_score_variant(v))
         for _ in range(3):
             call()

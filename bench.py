@@ -39,9 +39,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4])
-    ap.add_argument("--by", default="layer", choices=["layer", "head", "balanced"],
+    ap.add_argument("--by", default="auto", choices=["auto", "layer", "head", "balanced"],
                     help="layer / head: one contiguous rectangle per rank; balanced: the layer layout cut at KV-head "
-                         "granularity with the N3 owner's share reduced by N3's cost (shard.make_layout)")
+                         "granularity with the N3 owner's share reduced by N3's cost (shard.make_layout); "
+                         "auto (default): balanced for config 2 (N3 reads 1.25 GB), layer otherwise")
     ap.add_argument("--n3-units", type=float, default=-1.0,
                     help="balanced layout: N3's cost in (layer, head) gather units (default: measured table N3_UNITS)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -785,6 +786,8 @@ def bench_reference(args):
 def main():
     global RHO
     args = parse()
+    if args.by == "auto":
+        args.by = "balanced" if args.config == 2 else "layer"
     RHO = tuple(int(x) for x in args.rho.split("/"))
     if args.impl == "reference":
         bench_reference(args)

@@ -24,7 +24,7 @@ def test_two_rank_bench_runs_and_reports(overlap):
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["parallelism"] == "layer-sharded x2" and d["gpu_launches"] > 0
+    assert d["config"]["parallelism"] == "balanced-sharded x2" and d["gpu_launches"] > 0   # config 2 default
 
 
 def test_single_rank_bench_line_has_the_contract_keys():

@@ -385,6 +385,11 @@ cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
 /* Synchronizes, returns and clears the sticky device error word (CP_OK if none). */
 cp_status cp_index_last_error(cp_index* idx, void* stream);
 
+/* Insert commits applied so far by the parallel path and by the sequential path, and the OR of the
+ * reasons the sequential one was taken (diagnostic; out_h[3]; synchronizes).  Both give identical results; the parallel one needs a batch whose segments do not
+ * interact (DESIGN.md §6 N4). */
+cp_status cp_index_commit_stats(cp_index* idx, int32_t* out_h, void* stream);
+
 /* Hash base B of an index (diagnostic). */
 uint64_t cp_index_hash_base(const cp_index* idx);
 

@@ -255,6 +255,13 @@ class KVIndex:
                 "cp_link_blocks")
         return out
 
+    def commit_stats(self, stream=None):
+        """(commits applied by the parallel path, by the sequential path, OR of the fallback reasons)
+        -- cp_index_commit_stats."""
+        out = (C.c_int32 * 3)()
+        L.check(L.lib().cp_index_commit_stats(self.h, out, _stream(stream)), "cp_index_commit_stats")
+        return int(out[0]), int(out[1]), int(out[2])
+
     def last_error(self, stream=None) -> int:
         return int(L.lib().cp_index_last_error(self.h, _stream(stream)))
 

@@ -12,6 +12,8 @@
 //   copy-in         cp_launch_rows(dir = 1): writer paged KV -> pool pages (no rotation)
 #include "cp_internal.cuh"
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -125,6 +127,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(4 * (size_t)(S + L->MS));                           // 29 rm_pos (FIFO tail position per removal)
     // 30 matcher arrays for long requests: request r at 24 * offsets[r] + 64 * r (cp_match.cu)
     sput(c->max_req_tokens > CP_MATCH_SMEM_TOKENS ? 24 * (size_t)c->max_batch_tokens + 64 * (size_t)c->max_batch_reqs + 64 : 16);
+    // 31 parallel-apply scratch: 12 int32 + 1 int64 arrays of MS + 1, 4 int32 arrays of S, 4 int32 + 1 int64 of 4097
+    sput(4 * (size_t)(L->MS + 1) * 12 + 8 * (size_t)(L->MS + 1) + 4 * (size_t)S * 4 + 4 * 4097 * 4 + 8 * 4097 + 64);
     L->scr_size = o;
 }
 
@@ -141,7 +145,7 @@ __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, in
         hdr->error = 0; hdr->next_id = 0; hdr->num_live = 0; hdr->fifo_head = 0; hdr->fifo_count = (int32_t)P;
         hdr->slot_free_top = S; hdr->match_done = 0; hdr->table_used = 0; hdr->live_tokens = 0;
         hdr->first_err = CP_NO_ERR_KEY; hdr->rebuild = 0; hdr->n_cand = 0; hdr->n_copy = 0; hdr->n_removed = 0;
-        hdr->n_chunks = 0; hdr->n_new_live = 0;
+        hdr->n_chunks = 0; hdr->n_new_live = 0; hdr->commits_parallel = 0; hdr->commits_serial = 0; hdr->commit_why = 0;
     }
 }
 
@@ -168,6 +172,15 @@ struct InsArgs {
     int32_t* eq_old; HEntry* dtab; int32_t* span_rep; Rec16* precs;
     int64_t CH;             // copy-in chunk capacity (scratch)
     int32_t max_blocks;     // writer block-table width
+    // parallel-apply scratch (k_ins_commit fast path): per span / per store [MS + 1], per slot [nslots],
+    // per filtered LRU candidate [candK + 1]
+    int32_t *f_last, *f_kind, *f_target, *f_supcnt, *f_suptok, *f_suppg, *f_sidx;
+    int32_t *f_sj, *f_pgpref, *f_rmpref, *f_suppgpref, *f_vk;
+    long long* f_netpref;
+    int32_t *f_refs, *f_evpos, *f_maxpos, *f_supby;
+    int32_t *f_vslot, *f_vlen, *f_vcpg, *f_vfc;
+    long long* f_vcum;
+    int32_t force_serial;   // CP_COMMIT_SERIAL=1: skip the parallel apply (A/B measurement, tests)
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
     int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
@@ -495,6 +508,57 @@ __device__ int block_excl_scan(int32_t* v, int n, int32_t* wsum) {
     __syncthreads();
     return total;
 }
+
+// block-wide exclusive scan of 64-bit values (in place); returns the total
+template <int NT>
+__device__ long long block_excl_scan64(long long* v, int n, long long* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c = (n + NT - 1) / NT, c0 = min(n, tid * c), c1 = min(n, c0 + c);
+    long long loc = 0;
+    for (int i = c0; i < c1; ++i) loc += v[i];
+    long long inc = loc;
+    for (int off = 1; off < 32; off <<= 1) { long long y = __shfl_up_sync(0xffffffffu, inc, off); if (lane >= off) inc += y; }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        long long x = lane < NT / 32 ? wsum[lane] : 0, xi = x;
+        for (int off = 1; off < 32; off <<= 1) { long long y = __shfl_up_sync(0xffffffffu, xi, off); if (lane >= off) xi += y; }
+        if (lane < NT / 32) wsum[lane] = xi - x;
+        if (lane == 31) wsum[NT / 32] = xi;
+    }
+    __syncthreads();
+    long long run = wsum[wid] + inc - loc;
+    for (int i = c0; i < c1; ++i) { long long t = v[i]; v[i] = run; run += t; }
+    const long long total = wsum[NT / 32];
+    __syncthreads();
+    return total;
+}
+
+// block-wide inclusive max-scan of v[0..n) (in place)
+template <int NT>
+__device__ void block_incl_maxscan(int32_t* v, int n, int32_t* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c = (n + NT - 1) / NT, c0 = min(n, tid * c), c1 = min(n, c0 + c);
+    int loc = INT_MIN;
+    for (int i = c0; i < c1; ++i) loc = max(loc, v[i]);
+    int inc = loc;
+    for (int off = 1; off < 32; off <<= 1) { int y = __shfl_up_sync(0xffffffffu, inc, off); if (lane >= off) inc = max(inc, y); }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int x = lane < NT / 32 ? wsum[lane] : INT_MIN, xi = x;
+        for (int off = 1; off < 32; off <<= 1) { int y = __shfl_up_sync(0xffffffffu, xi, off); if (lane >= off) xi = max(xi, y); }
+        const int ex = __shfl_up_sync(0xffffffffu, xi, 1);
+        if (lane < NT / 32) wsum[lane] = lane == 0 ? INT_MIN : ex;
+    }
+    __syncthreads();
+    const int lex = __shfl_up_sync(0xffffffffu, inc, 1);
+    int run = max(wsum[wid], lane == 0 ? INT_MIN : lex);
+    for (int i = c0; i < c1; ++i) { run = max(run, v[i]); v[i] = run; }
+    __syncthreads();
+}
+
+constexpr int kFastSup = 8;               // parallel apply: most live segments one stored span supersedes
 
 #ifdef CP_COMMIT_PROF
 // diagnostic build only: [0..5] phase timestamps, [6..11] cycles per path, [12..15] counts
@@ -853,8 +917,224 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         }
         return -1;
     };
+    // ---- parallel apply.  The sequential loop below pays ~2K cycles per stored span (config-5 churn:
+    //      ~430 stores, ~0.5 ms per batch).  When the batch's segments do not interact -- no containment
+    //      between two batch contents, no live segment superseded by one span and referenced by another,
+    //      no LRU victim referenced by a later span, no candidate the eviction pointer passes before the
+    //      span that refreshes or supersedes it, pops inside the FIFO's initial region, at most kFastSup
+    //      supersedes per span -- every decision is the one the initial state gives, and ids, slots, pages,
+    //      removal order and FIFO positions are prefix sums.  The result is then exactly the sequential
+    //      one (R#20-22); otherwise the sequential loop runs, from the untouched state.
+    __shared__ int s_fast, s_ns;
+    __shared__ long long s_s64[kCommitThreads / 32 + 1];
+    __shared__ int s_why;                 // why the parallel apply was not taken (bit mask, diagnostics)
+    const int Sn = a.S, NSl = a.nslots;
+    if (tid == 0) { s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0; }
+    for (int i = tid; i < NSl; i += blockDim.x) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
+    for (int j = tid; j < Sn; j += blockDim.x) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
+    __syncthreads();
+    for (int j = tid; j < Sn; j += blockDim.x) atomicMax(&a.f_last[srep[j]], j);
+    __syncthreads();
+    for (int r = tid; r < Sn; r += blockDim.x) {                 // decision of each content vs the initial pool
+        if (srep[r] != r) continue;
+        int dup = -1, cont = -1, cont_id = INT_MAX, nsup = 0, suptok = 0, suppg = 0;
+        bool bad = false;
+        for (int q = soff[r]; q < soff[r + 1]; ++q) {
+            const int2 rr = rec[q];
+            if (rr.x < 0) { bad = true; break; }                   // relation between two batch contents
+            if (!(sflag[rr.x] & 1)) continue;
+            if (rr.y == REL_EQ) dup = rr.x;
+            else if (rr.y == REL_CONTAINER) { const int sid = a.slot_id[rr.x]; if (sid < cont_id) { cont_id = sid; cont = rr.x; } }
+            else { ++nsup; suptok += a.slot_len[rr.x]; suppg += (a.slot_len[rr.x] + CP_BLOCK - 1) / CP_BLOCK; }
+        }
+        if (bad) { s_fast = 0; atomicOr(&s_why, 2); continue; }
+        const int kind = dup >= 0 ? 0 : cont >= 0 ? 1 : 2;        // 0 Duplicate, 1 Dropped, 2 store
+        if (kind == 2 && nsup > kFastSup) { s_fast = 0; atomicOr(&s_why, 4); }
+        a.f_kind[r] = kind; a.f_target[r] = dup >= 0 ? dup : cont;
+        a.f_supcnt[r] = kind == 2 ? nsup : 0; a.f_suptok[r] = kind == 2 ? suptok : 0; a.f_suppg[r] = kind == 2 ? suppg : 0;
+        a.f_sidx[r] = kind == 2 ? 1 : 0;
+        const int last = a.f_last[r];
+        for (int q = soff[r]; q < soff[r + 1]; ++q) {
+            const int2 rr = rec[q];
+            if (!(sflag[rr.x] & 1)) continue;
+            atomicAdd(&a.f_refs[rr.x], 1);
+            atomicMax(&a.f_maxpos[rr.x], last);                     // referenced up to the content's last span
+            if (rr.y == REL_EQ) atomicMin(&a.f_evpos[rr.x], r);     // refreshed at r
+            if (rr.y == REL_CONTAINED && kind == 2) {
+                atomicMin(&a.f_evpos[rr.x], r);                     // superseded at r
+                if (atomicCAS(&a.f_supby[rr.x], -1, r) != -1) { s_fast = 0; atomicOr(&s_why, 8); }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < NSl; i += blockDim.x) if (a.f_supby[i] >= 0 && a.f_refs[i] > 1) { s_fast = 0; atomicOr(&s_why, 8); }
+    __syncthreads();
+    if (s_fast) {
+        // store order: exclusive scan of the storing contents (a content is stored by its first span)
+        const int ns = block_excl_scan<kCommitThreads>(a.f_sidx, Sn, s_wsum);
+        if (tid == 0) s_ns = ns;
+        for (int r = tid; r < Sn; r += blockDim.x) {
+            if (srep[r] != r || a.f_kind[r] != 2) continue;
+            const int k = a.f_sidx[r], m = slen[r];
+            a.f_sj[k] = r;
+            a.f_pgpref[k] = (m + CP_BLOCK - 1) / CP_BLOCK;
+            a.f_netpref[k] = (long long)m - a.f_suptok[r];
+            a.f_rmpref[k] = a.f_supcnt[r];
+            a.f_suppgpref[k] = a.f_suppg[r];
+        }
+        __syncthreads();
+        const int totpg = block_excl_scan<kCommitThreads>(a.f_pgpref, ns, s_wsum);
+        const int totsup = block_excl_scan<kCommitThreads>(a.f_rmpref, ns, s_wsum);
+        const int totsuppg = block_excl_scan<kCommitThreads>(a.f_suppgpref, ns, s_wsum);
+        const long long totnet = block_excl_scan64<kCommitThreads>(a.f_netpref, ns, s_s64);
+        (void)totpg; (void)totsup; (void)totsuppg; (void)totnet;
+        __syncthreads();
+        // ---- LRU: the victims, in candidate-list order, that the sequential evictions would pop
+        const long long L0 = s_live_tokens;
+        bool evict = false;
+        for (int k = tid; k < ns; k += blockDim.x) evict |= L0 + a.f_netpref[k] + (long long)slen[a.f_sj[k]] - a.f_suptok[a.f_sj[k]] > a.capacity;
+        evict = __syncthreads_or(evict);
+        if (evict && !s_heap) { if (tid == 0) { s_fast = 0; atomicOr(&s_why, 16); } }
+        __syncthreads();
+        if (s_fast && evict) {
+            const int cn = s_cn;
+            // kept = live old entries not refreshed / superseded in this call (the pop test of the loop)
+            for (int q = tid; q < cn; q += blockDim.x) {
+                const int sl = cslot[q];
+                a.f_vfc[q] = (sl >= 0 && (sflag[sl] & 1) && !(sflag[sl] & 4) && a.f_evpos[sl] == INT_MAX) ? 1 : 0;
+            }
+            __syncthreads();
+            for (int q = tid; q < cn; q += blockDim.x) a.f_vlen[q] = a.f_vfc[q];      // keep flags
+            __syncthreads();
+            const int nv = block_excl_scan<kCommitThreads>(a.f_vfc, cn, s_wsum);        // f_vfc[q] = kept before q
+            for (int q = tid; q < cn; q += blockDim.x)
+                if (a.f_vlen[q]) { const int v = a.f_vfc[q]; a.f_vslot[v] = cslot[q]; }
+            __syncthreads();
+            for (int v = tid; v < nv; v += blockDim.x) {
+                const int L = a.slot_len[a.f_vslot[v]];
+                a.f_vcum[v] = L; a.f_vcpg[v] = (L + CP_BLOCK - 1) / CP_BLOCK;
+            }
+            __syncthreads();
+            const long long vtot = block_excl_scan64<kCommitThreads>(a.f_vcum, nv, s_s64);
+            const int vtotpg = block_excl_scan<kCommitThreads>(a.f_vcpg, nv, s_wsum);
+            if (tid == 0) { a.f_vcum[nv] = vtot; a.f_vcpg[nv] = vtotpg; }
+            __syncthreads();
+            // victims needed after store k: smallest v with L0 + net_incl(k) - vcum[v] <= capacity
+            const bool complete = cn >= s_num_live;                 // the list holds every live entry
+            for (int k = tid; k < ns; k += blockDim.x) {
+                const int j = a.f_sj[k];
+                const long long P = L0 + a.f_netpref[k] + (long long)slen[j] - a.f_suptok[j];
+                int lo = 0, hi = nv;
+                if (P - a.f_vcum[nv] > a.capacity) { s_fast = 0; atomicOr(&s_why, 32); lo = nv; }
+                else while (lo < hi) { const int mid = (lo + hi) >> 1; if (P - a.f_vcum[mid] <= a.capacity) hi = mid; else lo = mid + 1; }
+                a.f_vk[k] = lo;
+            }
+            (void)complete;
+            __syncthreads();
+            block_incl_maxscan<kCommitThreads>(a.f_vk, ns, s_wsum);
+            const int Vtot = ns > 0 ? a.f_vk[ns - 1] : 0;
+            // every list entry the pointer reaches (q with f_vfc[q] < Vtot): not in the t-group (the loop
+            // would fall back to the arg-min), a victim not referenced after its pop, a skipped entry
+            // refreshed / superseded before it
+            for (int q = tid; q < cn; q += blockDim.x) {
+                const int fc = a.f_vfc[q];
+                if (fc >= Vtot) continue;
+                if ((ckey[q] >> 32) + s_minl >= a.t) { s_fast = 0; atomicOr(&s_why, 64); continue; }
+                int lo = 0, hi = ns - 1;                              // store whose eviction reaches q
+                while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.f_vk[mid] > fc) hi = mid; else lo = mid + 1; }
+                const int jk = a.f_sj[lo], sl = cslot[q];
+                if (a.f_vlen[q]) { if (a.f_maxpos[sl] > jk) { s_fast = 0; atomicOr(&s_why, 128); } }
+                else if ((sflag[sl] & 1) && !(sflag[sl] & 4) && !(a.f_evpos[sl] < jk)) { s_fast = 0; atomicOr(&s_why, 256); }
+            }
+        } else if (s_fast) {
+            for (int k = tid; k < ns; k += blockDim.x) a.f_vk[k] = 0;
+            if (tid == 0) { a.f_vcum[0] = 0; a.f_vcpg[0] = 0; }
+        }
+        __syncthreads();
+    }
+    if (s_fast) {
+        // every pop reads a page that is free at that point of the sequential order: the initial free
+        // pages, then the pages appended by removals before it (supersedes up to this store, evictions
+        // after the earlier stores)
+        for (int k = tid; k < s_ns; k += blockDim.x) {
+            const int j = a.f_sj[k];
+            const int end = a.f_pgpref[k] + (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
+            const int app = a.f_suppgpref[k] + a.f_suppg[j] + a.f_vcpg[k > 0 ? a.f_vk[k - 1] : 0];
+            if (end > s_count0 + app) { s_fast = 0; atomicOr(&s_why, 512); }
+        }
+        __syncthreads();
+    }
+    if (s_fast) {
+        // ---- apply (nothing above changed the index)
+        const int ns = s_ns;
+        const int tail0 = wrap(s_fifo_head0 + s_count0);
+        for (int j = tid; j < Sn; j += blockDim.x) {
+            const int r = srep[j], kind = a.f_kind[r];
+            if (kind == 0) {
+                const int X = a.f_target[r];
+                a.slot_last[X] = a.t; a.out_tmp[j] = X; a.out_oc[j] = CP_DUPLICATE;
+            } else if (kind == 1) {
+                a.out_tmp[j] = a.f_target[r]; a.out_oc[j] = CP_DROPPED_CONTAINED;
+            }
+        }
+        for (int k = tid; k < ns; k += blockDim.x) {
+            const int j = a.f_sj[k], m = slen[j];
+            const int slot = k < s_sc_n ? s_stack_cache[k] : a.slot_stack[free_top0 - 1 - k];
+            a.slot_id[slot] = s_next_id + k; a.slot_len[slot] = m; a.slot_last[slot] = a.t;
+            snew[j] = slot; sfpos[j] = wrap(s_fifo_head0 + a.f_pgpref[k]);
+            a.out_tmp[j] = slot; a.out_oc[j] = a.f_supcnt[j] > 0 ? CP_SUPERSEDED : CP_STORED;
+            // removals of this store: its supersedes (ascending id), then its LRU victims
+            const int v0 = k > 0 ? a.f_vk[k - 1] : 0, v1 = a.f_vk[k];
+            int base = a.f_rmpref[k] + v0;
+            int pg = a.f_suppgpref[k] + a.f_vcpg[v0];
+            int sup[kFastSup], ns2 = 0;
+            for (int q = soff[j]; q < soff[j + 1]; ++q) {
+                const int2 rr = rec[q];
+                if (rr.y == REL_CONTAINED && (sflag[rr.x] & 1)) sup[ns2++] = rr.x;
+            }
+            for (int x = 1; x < ns2; ++x)
+                for (int y = x; y > 0 && a.slot_id[sup[y]] < a.slot_id[sup[y - 1]]; --y) { const int tt = sup[y]; sup[y] = sup[y - 1]; sup[y - 1] = tt; }
+            for (int x = 0; x < ns2; ++x) {
+                a.removed[base] = sup[x]; a.rm_pos[base] = wrap(tail0 + pg);
+                pg += (a.slot_len[sup[x]] + CP_BLOCK - 1) / CP_BLOCK; ++base;
+            }
+            for (int v = v0; v < v1; ++v) {
+                const int sl = a.f_vslot[v];
+                a.removed[base] = sl; a.rm_pos[base] = wrap(tail0 + pg);
+                pg += (a.slot_len[sl] + CP_BLOCK - 1) / CP_BLOCK; ++base;
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < Sn; j += blockDim.x) {             // later spans of a stored content: Duplicates
+            const int r = srep[j];
+            if (r != j && a.f_kind[r] == 2) { a.out_tmp[j] = snew[r]; a.out_oc[j] = CP_DUPLICATE; }
+        }
+        const int Vtot = ns > 0 ? a.f_vk[ns - 1] : 0;
+        const int nrm = (ns > 0 ? a.f_rmpref[ns - 1] + a.f_supcnt[a.f_sj[ns - 1]] : 0) + Vtot;
+        for (int x = tid; x < nrm; x += blockDim.x) sflag[a.removed[x]] = 0;
+        __syncthreads();
+        for (int j = tid; j < Sn; j += blockDim.x) {
+            if (srep[j] == j && a.f_kind[j] == 0) sflag[a.f_target[j]] |= 4;
+            if (snew[j] >= 0) sflag[snew[j]] = 3;
+        }
+        if (tid == 0) {
+            const int totpg = ns > 0 ? a.f_pgpref[ns - 1] + (slen[a.f_sj[ns - 1]] + CP_BLOCK - 1) / CP_BLOCK : 0;
+            const int rmpg = (ns > 0 ? a.f_suppgpref[ns - 1] + a.f_suppg[a.f_sj[ns - 1]] : 0) + a.f_vcpg[Vtot];
+            const long long lastnet = ns > 0 ? (long long)slen[a.f_sj[ns - 1]] - a.f_suptok[a.f_sj[ns - 1]] : 0;
+            s_live_tokens = s_live_tokens + (ns > 0 ? a.f_netpref[ns - 1] + lastnet : 0) - a.f_vcum[Vtot];
+            s_fifo_head = wrap(s_fifo_head0 + totpg);
+            s_fifo_count = s_count0 - totpg + rmpg;
+            s_next_id += ns; s_free_top = free_top0 - ns; s_num_live += ns - nrm;
+            s_nremoved = nrm; s_ndef_rm = nrm; s_appended = rmpg;
+            atomicAdd(&a.hdr->commits_parallel, 1);
+        }
+        __syncthreads();
+    } else if (tid == 0) {
+        atomicAdd(&a.hdr->commits_serial, 1);
+        atomicOr(&a.hdr->commit_why, s_why);
+    }
     int j0 = jstar;
-    while (true) {
+    while (!s_fast) {
         if (tid < 32) {
             if (tid == 0) { s_resume = a.S; s_argmin = 0; }
             __syncwarp();
@@ -985,7 +1265,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     __syncthreads();
     // ---- deferred page traffic, block-parallel (warp per removal / per stored span): appended pages
-    //      go beyond the FIFO's initial region, page lists are read from inside it -- disjoint
+    //      go beyond the FIFO's initial region; the sequential loop's pops stay inside it, the parallel
+    //      apply's may reach appended pages (written first)
     if (s_defer) {
         const int cw = tid >> 5, cl = tid & 31, nw = kCommitThreads / 32;
         for (int r = cw; r < s_ndef_rm; r += nw) {
@@ -994,6 +1275,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             const int32_t* pl = a.slot_pages + (int64_t)sl * a.MP;
             for (int i = cl; i < npg; i += 32) a.fifo[wrap(a.rm_pos[r] + i)] = pl[i];
         }
+        __syncthreads();                 // pops past the initial region read pages appended above (parallel apply)
         for (int j = cw; j < a.S; j += nw) {
             if (sfpos[j] < 0) continue;
             const int npg = (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
@@ -1302,6 +1584,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->span_rep = (int32_t*)(s + L.scr_off[27]); x->precs = (Rec16*)(s + L.scr_off[28]);
     x->rm_pos = (int32_t*)(s + L.scr_off[29]);
     x->match_g = cfg->max_req_tokens > CP_MATCH_SMEM_TOKENS ? s + L.scr_off[30] : nullptr;
+    x->fscr = s + L.scr_off[31];
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -1349,6 +1632,15 @@ cp_status cp_index_destroy(cp_index* x) {
 }
 
 uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
+
+cp_status cp_index_commit_stats(cp_index* x, int32_t* out_h, void* stream) {
+    if (!x || !out_h) return CP_ERR_INVALID_ARG;
+    CP_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+    DevHeader h;
+    CP_CUDA_CHECK(cudaMemcpy(&h, x->hdr, sizeof(h), cudaMemcpyDeviceToHost));
+    out_h[0] = h.commits_parallel; out_h[1] = h.commits_serial; out_h[2] = h.commit_why;
+    return CP_OK;
+}
 
 uint64_t cp_kernel_launch_count(void) { return g_cp_launches.load(); }
 
@@ -1478,6 +1770,25 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
+    {
+        const size_t M1 = (size_t)x->MS + 1;
+        int32_t* q = (int32_t*)x->fscr;
+        int32_t** per_span[12] = {&a.f_last, &a.f_kind, &a.f_target, &a.f_supcnt, &a.f_suptok, &a.f_suppg, &a.f_sidx,
+                                  &a.f_sj, &a.f_pgpref, &a.f_rmpref, &a.f_suppgpref, &a.f_vk};
+        for (int k = 0; k < 12; ++k) { *per_span[k] = q; q += M1; }
+        a.f_netpref = (long long*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
+        q = (int32_t*)(a.f_netpref + M1);
+        int32_t** per_slot[4] = {&a.f_refs, &a.f_evpos, &a.f_maxpos, &a.f_supby};
+        for (int k = 0; k < 4; ++k) { *per_slot[k] = q; q += x->S; }
+        int32_t** per_cand[4] = {&a.f_vslot, &a.f_vlen, &a.f_vcpg, &a.f_vfc};
+        for (int k = 0; k < 4; ++k) { *per_cand[k] = q; q += 4097; }
+        a.f_vcum = (long long*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
+    }
+    {
+        static int fs = -1;
+        if (fs < 0) { const char* e = getenv("CP_COMMIT_SERIAL"); fs = (e && atoi(e) != 0) ? 1 : 0; }
+        a.force_serial = fs;
+    }
     a.CH = x->CH; a.max_blocks = kv->max_blocks_per_req;
     if (a.max_blocks < 1) return CP_ERR_INVALID_ARG;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;

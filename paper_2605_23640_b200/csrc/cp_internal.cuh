@@ -55,7 +55,10 @@ struct DevHeader {                   // first 256 B of META
     int32_t n_cand0;                 // insert: candidates of the first scan phase
     int32_t n_need;                  // insert: spans that need the old-entry haystack scan
     unsigned long long gather_next;  // gather/copy: next work item (dynamic scheduling), reset by k_rows_prep
-    int32_t pad[42];
+    int32_t commits_parallel;        // insert commits applied by the parallel path (diagnostics)
+    int32_t commits_serial;          // ... and by the sequential path
+    int32_t commit_why;              // OR of the reasons the sequential path was taken (k_ins_commit bits)
+    int32_t pad[39];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 
@@ -129,6 +132,7 @@ struct cp_index {
     int32_t* eq_old;     // [MS] span has an equal live pool entry
     HEntry* dtab;        // unique table keyed by full hash -> smallest span index (batch dedup)
     int32_t* span_rep;   // [MS] representative (smallest equal span) of each span
+    char* fscr;          // parallel-apply scratch of the commit
     Rec16* precs;        // [MS] bucket records of the batch prefix table
 };
 

@@ -114,3 +114,26 @@ def test_index_fuzz_long_windows(seed):
         case.match_and_gather(rb, rep)
         assert rep.ok, rep.notes[:6]
     assert rep.stats.get("stored", 0) > 0
+
+
+_COMMITS = {"parallel": 0, "serial": 0}
+
+
+@pytest.mark.parametrize("seed", list(range(300, 316)))
+def test_index_fuzz_commit_paths(seed):
+    """Both commit paths on the fuzz generators (the parallel apply where the batch's segments do not
+    interact, the sequential loop otherwise), each against the oracle; the last case checks that
+    both paths were taken over the set."""
+    wl = _workload(seed, "bf16", heavy=seed % 2 == 0, w=[4, 8, 32][seed % 3])
+    case = Case(wl, seed=seed, sample_reqs=None)
+    rep = ParityReport()
+    for wb, rb in wl.rounds:
+        case.insert(wb, rep)
+        assert rep.ok, rep.notes[:6]
+        case.match_and_gather(rb, rep)
+        assert rep.ok, rep.notes[:6]
+    par, ser, why = case.dev.commit_stats()
+    _COMMITS["parallel"] += par
+    _COMMITS["serial"] += ser
+    if seed == 315:
+        assert _COMMITS["parallel"] > 0 and _COMMITS["serial"] > 0, _COMMITS

@@ -349,6 +349,8 @@ def test_churn_config5_full_size_oracle_parity():
         assert rep.ok, rep.notes[:6]
     assert rep.stats["duplicate"] > 0 and rep.stats["hits"] > 0
     assert case.orc.num_ids > len(case.orc.live_entries())        # entries were evicted
+    par, ser, why = case.dev.commit_stats()
+    assert par >= 5, (par, ser, why)                    # the churn batches take the parallel commit
 
 
 def test_churn_config5_full_batches_invariants():

@@ -106,7 +106,10 @@ def main():
         "outcomes": {k: int(sum(r[k] for r in rows)) for k in ("stored", "superseded", "duplicate", "dropped")},
         "removed_by_lru_or_supersede": int(sum(r["stored"] for r in rows) - snap["num_live"]),
         "mean_gather_GBps": float(np.mean([r["gather_GBps"] for r in rows[1:]])),
-        "generator_s": gen_s, "rows": rows,
+        "generator_s": gen_s,
+        "commits_parallel_serial_why": list(idx.commit_stats()),
+        "commit_path": os.environ.get("CP_COMMIT_SERIAL", "0") != "0" and "sequential (CP_COMMIT_SERIAL=1)" or "default",
+        "rows": rows,
     }
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "churn.json"), "w") as f:

@@ -36,53 +36,40 @@ struct RowsArgs {
     int32_t L, H, d; double theta; int32_t flags; int32_t gptj;
     int32_t LG;                      // layers per work item (small rows: several layers share one row lookup)
     int32_t* chunk_hit; int32_t* chunk_t0; int64_t CH;
+    int32_t* hit_coff;                                 // [hits] first chunk of each hit (k_rows_prep)
     long long* row_src; long long* row_dst;
     float2* hit_cs; int64_t cs_hits;
 };
 
-// k_rows_prep (one block): chunk list = scan of ceil(len/32) over the hit list
+// k_rows_prep (one block): per-hit first chunk = exclusive scan of ceil(len/32) over the hit list, a
+// thread owning a contiguous run of hits (one block scan; the chunk list itself is written by the
+// whole grid in k_rows_prep2 -- one SM writing ~12K scattered entries took 17-27 us)
 __global__ void __launch_bounds__(kPrepThreads) k_rows_prep(RowsArgs a) {
     __shared__ int s_scan[kPrepThreads / 32 + 1];
-    __shared__ int s_carry;
-    __shared__ int s_start[kPrepThreads], s_v[kPrepThreads];
     if (cp_err_set(a.hdr)) return;
     const int nh = *a.count;
     if (nh > a.list_cap || nh > a.cs_hits) { if (threadIdx.x == 0) cp_raise(a.hdr, CP_ERR_CAPACITY); return; }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_carry = 0;
+    const int c = (nh + kPrepThreads - 1) / kPrepThreads, h0 = min(nh, tid * c), h1 = min(nh, h0 + c);
+    int loc = 0;
+    for (int h = h0; h < h1; ++h) loc += (a.l_len[h] + CP_GATHER_CHUNK - 1) / CP_GATHER_CHUNK;
+    int inc = loc;
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+    if (lane == 31) s_scan[wid] = inc;
     __syncthreads();
-    for (int b0 = 0; b0 < nh; b0 += kPrepThreads) {
-        const int hh = b0 + tid;
-        const int v = hh < nh ? (a.l_len[hh] + CP_GATHER_CHUNK - 1) / CP_GATHER_CHUNK : 0;
-        int inc = v;
-        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-        if (lane == 31) s_scan[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            int x = lane < kPrepThreads / 32 ? s_scan[lane] : 0, xi = x;
-            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
-            if (lane < kPrepThreads / 32) s_scan[lane] = xi - x;
-            if (lane == 31) s_scan[kPrepThreads / 32] = xi;
-        }
-        __syncthreads();
-        const int start = s_carry + s_scan[wid] + inc - v;
-        s_start[tid] = start; s_v[tid] = v;
-        __syncthreads();
-        // warp per hit, lanes over its chunks: coalesced stores (a thread writing its own hit's chunks
-        // -- ~25K scattered stores from one SM for 512 hits -- took 17 us)
-        const int tot = s_carry + s_scan[kPrepThreads / 32];
-        if (tot <= a.CH)
-            for (int j = wid; j < kPrepThreads && b0 + j < nh; j += kPrepThreads / 32) {
-                const int st0 = s_start[j], vj = s_v[j];
-                for (int c = lane; c < vj; c += 32) { a.chunk_hit[st0 + c] = b0 + j; a.chunk_t0[st0 + c] = c * CP_GATHER_CHUNK; }
-            }
-        __syncthreads();
-        if (tid == 0) s_carry += s_scan[kPrepThreads / 32];
-        __syncthreads();
+    if (wid == 0) {
+        int x = lane < kPrepThreads / 32 ? s_scan[lane] : 0, xi = x;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+        if (lane < kPrepThreads / 32) s_scan[lane] = xi - x;
+        if (lane == 31) s_scan[kPrepThreads / 32] = xi;
     }
+    __syncthreads();
+    int run = s_scan[wid] + inc - loc;
+    for (int h = h0; h < h1; ++h) { a.hit_coff[h] = run; run += (a.l_len[h] + CP_GATHER_CHUNK - 1) / CP_GATHER_CHUNK; }
     if (tid == 0) {
-        if (s_carry > a.CH) { cp_raise(a.hdr, CP_ERR_CAPACITY); a.hdr->n_chunks = 0; }
-        else a.hdr->n_chunks = s_carry;
+        const int tot = s_scan[kPrepThreads / 32];
+        if (tot > a.CH) { cp_raise(a.hdr, CP_ERR_CAPACITY); a.hdr->n_chunks = 0; }
+        else a.hdr->n_chunks = tot;
         a.hdr->gather_next = 0;
     }
 }
@@ -107,10 +94,22 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
         }
     }
     const int64_t ntok = (int64_t)a.hdr->n_chunks * CP_GATHER_CHUNK;
-    for (int64_t q = gt; q < ntok; q += nt) {
-        const int c = (int)(q / CP_GATHER_CHUNK), i = (int)(q % CP_GATHER_CHUNK);
-        const int hh = a.chunk_hit[c];
-        const int t = a.chunk_t0[c] + i;
+    const int lane = threadIdx.x & 31;
+    // the 32 lanes of a warp take the 32 tokens of one chunk (nt is a multiple of 32): lane 0 finds the
+    // chunk's hit (largest h with hit_coff[h] <= c) and writes the chunk-list entry the copy kernel reads
+    for (int64_t qb = gt - lane; qb < ntok; qb += nt) {
+        const int c = (int)(qb / CP_GATHER_CHUNK), i = lane;
+        int hh = 0;
+        if (lane == 0) {
+            int lo = 0, hi = nh - 1;
+            while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.hit_coff[mid] <= c) lo = mid; else hi = mid - 1; }
+            hh = lo;
+            a.chunk_hit[c] = hh;
+            a.chunk_t0[c] = (c - a.hit_coff[hh]) * CP_GATHER_CHUNK;
+        }
+        hh = __shfl_sync(0xffffffffu, hh, 0);
+        const int64_t q = qb + lane;
+        const int t = (c - a.hit_coff[hh]) * CP_GATHER_CHUNK + i;
         if (t >= a.l_len[hh]) continue;
         const int r = a.l_req[hh], k = a.l_dst[hh], slot = a.l_slot[hh];
         const int pos = k + t;                                              // position in the request
@@ -642,7 +641,7 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
         const int tpr = x->cfg.num_kv_heads * x->cfg.head_dim / (2 * vec);
         a.LG = std::max(1, std::min(x->cfg.num_layers, 2048 / std::max(1, CP_GATHER_CHUNK * tpr)));
     }
-    a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH;
+    a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH; a.hit_coff = x->hit_coff;
     a.row_src = x->row_src; a.row_dst = x->row_dst;
     a.hit_cs = x->hit_cs; a.cs_hits = x->CS_HITS;
     if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;

@@ -129,6 +129,7 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(c->max_req_tokens > CP_MATCH_SMEM_TOKENS ? 24 * (size_t)c->max_batch_tokens + 64 * (size_t)c->max_batch_reqs + 64 : 16);
     // 31 parallel-apply scratch: 12 int32 + 1 int64 arrays of MS + 1, 4 int32 arrays of S, 4 int32 + 1 int64 of 4097
     sput(4 * (size_t)(L->MS + 1) * 12 + 8 * (size_t)(L->MS + 1) + 4 * (size_t)S * 4 + 4 * 4097 * 4 + 8 * 4097 + 64);
+    sput(4 * (size_t)(std::max<int64_t>(L->HS, L->MS) + 1));                 // 32 hit_coff (gather / copy-in)
     L->scr_size = o;
 }
 
@@ -294,36 +295,32 @@ __global__ void k_ins_rep(InsArgs a) {
     }
 }
 
-// one block: bucket offsets = exclusive scan of the counts over the prefix table
+// one block: bucket offsets = exclusive scan of the counts over the prefix table; a thread owns a
+// contiguous run of BT/1024 buckets (one block scan instead of BT/1024 rounds of them)
 __global__ void __launch_bounds__(1024) k_ins_bucket_offsets(InsArgs a) {
     __shared__ int s_w[33];
-    __shared__ int s_carry;
     if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_carry = 0;
+    const int64_t c = (a.BT + 1023) / 1024;
+    const int64_t c0 = tid * c < a.BT ? tid * c : a.BT, c1 = c0 + c < a.BT ? c0 + c : a.BT;
+    int loc = 0;
+    for (int64_t i = c0; i < c1; ++i) if (a.btab[i].key != CP_EMPTY_KEY) loc += a.btab[i].len;
+    int inc = loc;
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+    if (lane == 31) s_w[wid] = inc;
     __syncthreads();
-    for (int64_t b0 = 0; b0 < a.BT; b0 += 1024) {
-        const int64_t i = b0 + tid;
-        const int v = (i < a.BT && a.btab[i].key != CP_EMPTY_KEY) ? a.btab[i].len : 0;
-        int inc = v;
-        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
-        if (lane == 31) s_w[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            int x = s_w[lane], xi = x;
-            for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
-            s_w[lane] = xi - x;
-            if (lane == 31) s_w[32] = xi;
-        }
-        __syncthreads();
-        if (i < a.BT && v > 0) {
-            const int off = s_carry + s_w[wid] + inc - v;
-            a.btab[i].slot = off;
-            a.btab[i].full = (unsigned long long)off;              // fill cursor
-        }
-        __syncthreads();
-        if (tid == 0) s_carry += s_w[32];
-        __syncthreads();
+    if (wid == 0) {
+        int x = s_w[lane], xi = x;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+        s_w[lane] = xi - x;
+    }
+    __syncthreads();
+    int run = s_w[wid] + inc - loc;
+    for (int64_t i = c0; i < c1; ++i) {
+        if (a.btab[i].key == CP_EMPTY_KEY) continue;
+        const int v = a.btab[i].len;
+        if (v > 0) { a.btab[i].slot = run; a.btab[i].full = (unsigned long long)run; }   // offset, fill cursor
+        run += v;
     }
 }
 
@@ -1446,7 +1443,6 @@ __global__ void k_ins_publish(InsArgs a) {
             }
             a.page_bits[a.slot_pages[(int64_t)slot * a.MP + pg]] = (uint16_t)v;
         }
-        if (lane == 0) sha256_tokens_dev(tau, m, a.slot_digest + (int64_t)slot * 32);
         HEntry v; v.key = a.slot_prefix[slot]; v.full = a.slot_full[slot]; v.slot = slot; v.len = m; v.pad = 0;
         const bool fresh = cp_warp_insert(a.htab, (uint32_t)(a.T - 1), a.logT, v, true);
         if (fresh && lane == 0) atomicAdd(&a.hdr->table_used, 1);
@@ -1454,6 +1450,17 @@ __global__ void k_ins_publish(InsArgs a) {
 }
 
 // rebuild the prefix table when tombstones accumulate (live + tombstones > T/2)
+// SHA-256 digests of the published entries (thread per entry; launched on the index's side stream,
+// concurrently with the table rebuild and the copy-in, which do not read digests)
+__global__ void k_ins_digest(InsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    const int n = a.hdr->n_new_live;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int slot = a.cp_slot[q], j = a.cp_delta[q], m = a.cp_len[q];
+        sha256_tokens_dev(span_tokens(a, j), m, a.slot_digest + (int64_t)slot * 32);
+    }
+}
+
 __global__ void k_rebuild_check(DevHeader* hdr, int64_t T) {
     hdr->rebuild = (hdr->error == 0 && (int64_t)hdr->table_used * 2 > T) ? 1 : 0;
 }
@@ -1585,6 +1592,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->rm_pos = (int32_t*)(s + L.scr_off[29]);
     x->match_g = cfg->max_req_tokens > CP_MATCH_SMEM_TOKENS ? s + L.scr_off[30] : nullptr;
     x->fscr = s + L.scr_off[31];
+    x->hit_coff = (int32_t*)(s + L.scr_off[32]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -1602,6 +1610,11 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     cudaFuncSetAttribute(k_ins_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_hash_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     x->wk = new WorkKey();
+    if (cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        delete x->wk; delete x; return CP_ERR_CUDA;
+    }
     *out = x;
     return CP_OK;
 }
@@ -1626,7 +1639,12 @@ cp_status cp_index_create_view(const cp_index* base, int32_t num_layers, int32_t
 
 cp_status cp_index_destroy(cp_index* x) {
     if (!x) return CP_ERR_INVALID_ARG;
-    if (!x->is_view) delete x->wk;
+    if (!x->is_view) {
+        delete x->wk;
+        if (x->ev_fork) cudaEventDestroy(x->ev_fork);
+        if (x->ev_join) cudaEventDestroy(x->ev_join);
+        if (x->side) cudaStreamDestroy(x->side);
+    }
     delete x;
     return CP_OK;
 }
@@ -1834,13 +1852,20 @@ cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp
     k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_publish<<<std::max(1, std::min(1184, (num_spans + 7) / 8)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    // digests beside the rest of the commit (rebuild, copy-in): fork onto the side stream, join at the end
+    if (cudaEventRecord(x->ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(x->side, x->ev_fork, 0) != cudaSuccess)
+        return CP_ERR_CUDA;
+    k_ins_digest<<<std::max(1, std::min(148, (num_spans + 127) / 128)), 128, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    if (cudaEventRecord(x->ev_join, x->side) != cudaSuccess) return CP_ERR_CUDA;
     k_rebuild_check<<<1, 1, 0, st>>>(x->hdr, x->T); CP_COUNT_LAUNCH();
     k_rebuild_clear<<<256, 256, 0, st>>>(x->hdr, x->htab, x->T); CP_COUNT_LAUNCH();
     k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->slot_full, x->slot_len, x->S); CP_COUNT_LAUNCH();
     if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     // copy the writer KV rows of the published entries into their pool pages
-    return cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
-                          x->MS, wb->offsets, nullptr, kv, 0, st);
+    const cp_status cs = cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
+                                        x->MS, wb->offsets, nullptr, kv, 0, st);
+    if (cudaStreamWaitEvent(st, x->ev_join, 0) != cudaSuccess) return CP_ERR_CUDA;   // digests done
+    return cs;
 }
 
 }  // namespace

@@ -97,6 +97,8 @@ struct cp_index {
     int insert_prepared = 0;   // cp_index_insert_prepare issued, commit pending (host-side guard)
     int is_view = 0;           // a pool view (cp_index_create_view): own geometry + pool, the base's META/SCRATCH
     WorkKey* wk = nullptr;     // owned by the base, shared by its views
+    cudaStream_t side = nullptr;                       // the insert's SHA-256 digests run here, beside the copy-in
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // (owned by the base)
     int32_t S;           // slots
     int64_t T;           // prefix-table entries (pow2)
     int32_t logT;
@@ -116,7 +118,7 @@ struct cp_index {
     int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;
     // SCRATCH (gather / copy-in work lists)
     int64_t CH;          // chunk capacity
-    int32_t *chunk_hit, *chunk_t0;
+    int32_t *chunk_hit, *chunk_t0, *hit_coff;
     long long *row_src, *row_dst;   // [CH * CP_GATHER_CHUNK] element offsets; row_dst carries the plan code in bits 62-63
     float2* hit_cs;      // [hits][d/2] cos/sin
     int64_t CS_HITS;     // hits capacity of hit_cs

@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-all-cores", action="store_true", help="cpu_baseline on one core only")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-3 and config-5 keys of the line")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
     ap.add_argument("--overlap", type=int, default=3, choices=[0, 1, 2, 3],
@@ -504,6 +505,12 @@ def bench_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(args, S)
+        extras = {}
+        if world == 1 and not args.shard_world and not args.no_extra and args.config == 2 and args.scale == 1.0:
+            del S.dst, S.dsts, S.ins_kvs, S.ins_kv, S.idx, S.views, S.attn
+            torch.cuda.empty_cache()
+            extras["config3"] = extra_config3(args, torch, cp, device)
+            extras["config5"] = extra_config5(torch, cp, device)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -540,7 +547,7 @@ def bench_ours(args):
                          "traffic_source": "profiles/r01/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
                          "algorithmic_bytes_per_launch": gather_bytes,
                          "bytes_rule": "copied reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + recompute tokens x 2 (K,V) x L*H*d*e (zero writes); linked tokens (--link) move no bytes"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, **extras,
             "setup": {"insert_writers_ms": round(S.setup_insert_ms, 2), "setup_s": round(S.setup_s, 1)},
         }
         print(json.dumps(out), flush=True)
@@ -550,6 +557,151 @@ def bench_ours(args):
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
+    return out
+
+
+def extra_config3(args, torch, cp, device, steps=5, warmup=3):
+    """BASELINE configs[2] on this GPU (multi-document RAG, passages reused at shifted positions: heavy
+    RoPE re-rotation), the same step and schedule as the headline, layer layout x1."""
+    import copy
+    a3 = copy.copy(args)
+    a3.config, a3.by, a3.link, a3.shard_world, a3.scale = 3, "layer", False, 0, 1.0
+    S = setup_ours(a3, 0, 1, device)
+    S.use_dist = False
+    for _ in range(warmup):
+        run_step(S, torch, cp, 1)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(steps):
+        run_step(S, torch, cp, 1, evs[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if S.idx.last_error():
+        raise RuntimeError("device error in the config-3 steps")
+    ms = t0.elapsed_time(t1) / steps
+    ph = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(steps)]).mean(axis=0)
+    h = S.hits.to_host()
+    cov, rec = int(h["req_covered"].sum()), int(h["req_recompute"].sum())
+    moved = int(np.sum(h["hit_delta"] != 0))
+    row = S.shard.num_layers * S.shard.num_heads * S.g.head_dim * (2 if S.g.dtype == "bf16" else 4)
+    reused_b = (cov - rec) * 2 * row * 2
+    gather_b = reused_b + rec * 2 * row
+    out = {"workload": S.wl.name + " (BASELINE configs[2])", "requests": S.rb.num_reqs,
+           "request_tokens": S.rb.total_tokens, "steps": steps, "warmup": warmup, "ms_per_step": round(ms, 4),
+           "value_GBps": round(reused_b / (ms * 1e-3) / 1e9, 1), "gather_GBps": round(gather_b / (ph[1] * 1e-3) / 1e9, 1),
+           "gather_frac_of_peak": round(gather_b / (ph[1] * 1e-3) / 1e9 / peaks()[0], 4),
+           "breakdown_ms": {"match": round(float(ph[0]), 4), "gather": round(float(ph[1]), 4),
+                            "score_and_wait_prepare": round(float(ph[2]), 4), "insert_commit": round(float(ph[3]), 4)},
+           "covered_tokens": cov, "hits": int(h["num_hits"]), "moved_hits": moved,
+           "matched_tokens_per_s": round(cov / (ms * 1e-3), 1)}
+    del S
+    torch.cuda.empty_cache()
+    return out
+
+
+def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000):
+    """BASELINE configs[4] on this GPU = one KV-head shard (1 of 8) of the 8-GPU head-sharded layout:
+    high churn (256 requests x ~1.6K tokens per batch, 100K-passage Zipf(1.1) corpus, 1.5M-token LRU
+    budget).  `prefill` batches are inserted untimed (no recompute marks) until the budget is full and
+    LRU eviction runs every batch; then `timed` batches run the full step -- match, gather, N3 (rho =
+    1/4), insert prepare, insert commit (incl. the copy-in of the stored segments) -- each phase timed
+    with CUDA events on the stream."""
+    from synth.gen import Geometry, attention_torch, churn_workload
+    g = Geometry(32, 8, 128, "bf16", 500000.0)
+    wl = churn_workload(batches=prefill + timed, per_batch=256, corpus=100000, capacity_tokens=capacity, geometry=g)
+    w = g.window_len
+    spans_max = max(len(b.span_len) for b, _ in wl.rounds)
+    toks_max = max(b.total_tokens for b, _ in wl.rounds)
+    cfg = cp.IndexConfig(num_layers=32, num_kv_heads=1, head_dim=128, dtype="bf16", rope_theta=5e5,
+                         pool_capacity_tokens=capacity, max_entries=capacity // w + spans_max + 64, max_span_len=256,
+                         max_req_tokens=int(max(b.lens.max() for b, _ in wl.rounds)), max_batch_reqs=256,
+                         max_batch_tokens=toks_max, max_spans_per_insert=spans_max, head_offset=0)
+    idx = cp.KVIndex(cfg, device)
+    nblk = (toks_max + 16 * 256 + 15) // 16
+    maxb = max(int((n + 15) // 16) for b, _ in wl.rounds for n in b.lens)
+    kv = cp.PagedKV.allocate(32, nblk, 1, 128, torch.bfloat16, torch.zeros((256, maxb), dtype=torch.int32), device,
+                             zero=False)
+    for t_ in kv.k + kv.v:
+        t_.normal_()
+    rows = []
+    row = 32 * 1 * 128 * 2
+    for bi, (wb, rb) in enumerate(wl.rounds):
+        t = bi + 1
+        db = cp.DeviceBatch.from_numpy(rb.tokens, rb.offsets, rb.mask, device)
+        nb = [(int(n) + 15) // 16 for n in rb.lens]
+        bt = torch.zeros((rb.num_reqs, maxb), dtype=torch.int32)
+        o = 0
+        for r, k in enumerate(nb):
+            bt[r, :k] = torch.arange(o, o + k); o += k
+        kv.block_tables = bt.to(device)
+        sp = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(device) for a in (rb.span_req, rb.span_begin, rb.span_len)]
+        if bi < prefill:
+            idx.insert(db, kv, *sp, None, None, t)
+            continue
+        attn = {r: attention_torch(int(rb.lens[r]), rb.segments[r], 0.01, seed=bi * 1000 + r, device=device)
+                for r in sorted(set(int(x) for x in rb.span_req))}
+        sargs = ([attn[int(r)] for r in rb.span_req], [int(rb.lens[int(r)]) for r in rb.span_req],
+                 [1] * len(rb.span_req), [int(x) for x in rb.span_begin],
+                 [int(x) + int(m) - 1 for x, m in zip(rb.span_begin, rb.span_len)])
+        ms_ = np.asarray([int(m) for m in rb.span_len])
+        bo = np.zeros(len(ms_) + 1, np.int64)
+        np.cumsum((ms_ + 31) // 32, out=bo[1:])
+        boff = torch.from_numpy(bo[:-1].copy()).to(device)
+        bits = torch.zeros(max(int(bo[-1]), 1), dtype=torch.int32, device=device)
+        scores = torch.zeros(max(int(ms_.sum()), 1), dtype=torch.int64, device=device)
+        before = idx.snapshot(with_tokens=False)
+        p0 = idx.commit_stats()[0]
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        ev[0].record()
+        hits = idx.match_spans(db, t)
+        ev[1].record()
+        idx.gather_rerotate(db, hits, kv)
+        ev[2].record()
+        cp.score_deviation(*sargs, 1, 4, out_scores=scores, out_bits=bits)
+        ev[3].record()
+        idx.insert(db, kv, *sp, bits, boff, t, phase="prepare")
+        ev[4].record()
+        ids, oc = idx.insert(db, kv, *sp, bits, boff, t, phase="commit")
+        ev[5].record()
+        torch.cuda.synchronize()
+        par_commit = idx.commit_stats()[0] > p0
+        if idx.last_error():
+            raise RuntimeError("device error in the config-5 batches")
+        ph = [ev[i].elapsed_time(ev[i + 1]) for i in range(5)]
+        after = idx.snapshot(with_tokens=False)
+        ocn = oc.cpu().numpy()
+        h = hits.to_host()
+        cov, rec = int(h["req_covered"].sum()), int(h["req_recompute"].sum())
+        stored = int(np.sum((ocn == cp._lib.CP_STORED) | (ocn == cp._lib.CP_SUPERSEDED)))
+        stored_tok = int(np.asarray(rb.span_len)[(ocn == cp._lib.CP_STORED) | (ocn == cp._lib.CP_SUPERSEDED)].sum())
+        evicted = before["num_live"] + stored - after["num_live"]
+        gbytes = (cov - rec) * 2 * row * 2 + rec * 2 * row
+        rows.append({"match_ms": ph[0], "gather_ms": ph[1], "score_ms": ph[2], "insert_prepare_ms": ph[3],
+                     "insert_commit_ms": ph[4], "gather_GBps": gbytes / (ph[1] * 1e-3) / 1e9,
+                     "stored": stored, "stored_tokens": stored_tok, "evicted": int(evicted),
+                     "copy_in_bytes": stored_tok * 2 * row * 2, "covered": cov, "parallel_commit": bool(par_commit)})
+        del attn
+    par, ser, why = idx.commit_stats()
+    mean = {k: round(float(np.mean([r[k] for r in rows])), 4) for k in rows[0] if k.endswith("_ms") or k.endswith("GBps")}
+    cin = float(np.mean([r["copy_in_bytes"] for r in rows]))
+    out = {"workload": "high_churn (BASELINE configs[4]), one KV-head shard (1 of 8) of Llama-3-8B KV",
+           "batches_timed": timed, "prefill_batches": prefill, "capacity_tokens": capacity,
+           "per_batch_mean": mean,
+           "stored_per_batch": round(float(np.mean([r["stored"] for r in rows])), 1),
+           "evicted_per_batch": round(float(np.mean([r["evicted"] for r in rows])), 1),
+           "copy_in_bytes_per_batch": int(cin),
+           "copy_in_rule": "stored tokens x 2 (K,V) x 32 layers x 1 head x 128 x 2 B x 2 (read + write)",
+           "commit_GBps_lower_bound": round(cin / (mean["insert_commit_ms"] * 1e-3) / 1e9, 1),
+           "commit_note": "insert_commit = the commit kernels + the copy-in; copy-in bytes / commit time is a lower "
+                          "bound of the copy-in bandwidth",
+           "commits_parallel_serial_why": [par, ser, why],
+           "timed_batches_parallel_commit": int(sum(r["parallel_commit"] for r in rows)),
+           "match_rate": round(float(np.mean([r["covered"] for r in rows])) / float(np.mean([b.total_tokens for b, _ in wl.rounds[prefill:]])), 4)}
+    del idx, kv
+    torch.cuda.empty_cache()
     return out
 
 

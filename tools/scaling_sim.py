@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(args):
-    out = subprocess.run([sys.executable, "bench.py", "--no-cpu-baseline", "--no-e2e"] + args, cwd=ROOT,
+    out = subprocess.run([sys.executable, "bench.py", "--no-cpu-baseline", "--no-e2e", "--no-extra"] + args, cwd=ROOT,
                          capture_output=True, text=True, timeout=600)
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     return json.loads(line)

@@ -390,6 +390,12 @@ cp_status cp_index_last_error(cp_index* idx, void* stream);
  * interact (DESIGN.md §6 N4). */
 cp_status cp_index_commit_stats(cp_index* idx, int32_t* out_h, void* stream);
 
+/* Matcher work counters accumulated by cp_match_spans since creation (or the last reset), out_h[4]:
+ * windows probed (n - w + 1 per request), prefix-filter candidates c, candidates that passed the
+ * full-hash pre-check, and the tokens their exact verification may compare -- the O(n + c) cost of
+ * P:L696-697.  reset != 0 zeroes them.  Synchronizes. */
+cp_status cp_index_match_work(cp_index* idx, uint64_t* out_h, int32_t reset, void* stream);
+
 /* Hash base B of an index (diagnostic). */
 uint64_t cp_index_hash_base(const cp_index* idx);
 

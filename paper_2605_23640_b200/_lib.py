@@ -84,6 +84,7 @@ EXPORTS = {
     "cp_index_last_error": (i32, [vp, vp]),
     "cp_index_hash_base": (u64, [vp]),
     "cp_index_commit_stats": (i32, [vp, P_i32, vp]),
+    "cp_index_match_work": (i32, [vp, P_u64, i32, vp]),
     "cp_kernel_launch_count": (u64, []),
     "cp_set_gather_variant": (i32, [i32]),
     "cp_set_score_variant": (i32, [i32]),

@@ -262,6 +262,12 @@ class KVIndex:
         L.check(L.lib().cp_index_commit_stats(self.h, out, _stream(stream)), "cp_index_commit_stats")
         return int(out[0]), int(out[1]), int(out[2])
 
+    def match_work(self, reset: bool = False, stream=None):
+        """cp_index_match_work: (windows, candidates, full-hash-passed, tokens to verify) since the last reset."""
+        out = (C.c_uint64 * 4)()
+        L.check(L.lib().cp_index_match_work(self.h, out, int(reset), _stream(stream)), "cp_index_match_work")
+        return tuple(int(x) for x in out)
+
     def last_error(self, stream=None) -> int:
         return int(L.lib().cp_index_last_error(self.h, _stream(stream)))
 

@@ -147,6 +147,7 @@ __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, in
         hdr->slot_free_top = S; hdr->match_done = 0; hdr->table_used = 0; hdr->live_tokens = 0;
         hdr->first_err = CP_NO_ERR_KEY; hdr->rebuild = 0; hdr->n_cand = 0; hdr->n_copy = 0; hdr->n_removed = 0;
         hdr->n_chunks = 0; hdr->n_new_live = 0; hdr->commits_parallel = 0; hdr->commits_serial = 0; hdr->commit_why = 0;
+        for (int i = 0; i < 4; ++i) hdr->match_work[i] = 0;
     }
 }
 
@@ -1650,6 +1651,19 @@ cp_status cp_index_destroy(cp_index* x) {
 }
 
 uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
+
+cp_status cp_index_match_work(cp_index* x, uint64_t* out_h, int32_t reset, void* stream) {
+    if (!x || !out_h) return CP_ERR_INVALID_ARG;
+    CP_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+    unsigned long long w[4];
+    CP_CUDA_CHECK(cudaMemcpy(w, x->hdr->match_work, sizeof(w), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; ++i) out_h[i] = w[i];
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        CP_CUDA_CHECK(cudaMemcpy(x->hdr->match_work, z, sizeof(z), cudaMemcpyHostToDevice));
+    }
+    return CP_OK;
+}
 
 cp_status cp_index_commit_stats(cp_index* x, int32_t* out_h, void* stream) {
     if (!x || !out_h) return CP_ERR_INVALID_ARG;

@@ -58,7 +58,9 @@ struct DevHeader {                   // first 256 B of META
     int32_t commits_parallel;        // insert commits applied by the parallel path (diagnostics)
     int32_t commits_serial;          // ... and by the sequential path
     int32_t commit_why;              // OR of the reasons the sequential path was taken (k_ins_commit bits)
-    int32_t pad[39];
+    int32_t pad0;
+    unsigned long long match_work[4];   // matcher work counters (cp_index_match_work)
+    int32_t pad[30];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 

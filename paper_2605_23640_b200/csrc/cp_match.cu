@@ -72,7 +72,7 @@ template <bool G>
 __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ uint64_t wtmp[2 * (kNT / 32)];
-    __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last;
+    __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last, s_vtok;
     __shared__ int s_scan[kNT / 32 + 1];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int r = blockIdx.x;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     int32_t* hm = (int32_t*)(base + L.hm);
     const bool skip = cp_err_set(a.hdr) || n > a.nmax;
     if (tid == 0 && !cp_err_set(a.hdr) && n > a.nmax) cp_raise(a.hdr, CP_ERR_INVALID_ARG);
-    if (tid == 0) { s_nc = 0; s_cands = 0; s_nh = 0; s_cov = 0; s_rec = 0; }
+    if (tid == 0) { s_nc = 0; s_cands = 0; s_nh = 0; s_cov = 0; s_rec = 0; s_vtok = 0; }
     int nh = 0;
 #ifdef CP_MATCH_PROF
     long long t_m = clock64();
@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             const int slot = vslot[k];
             const int m = __ldg(a.slot_len + slot);
             const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+            if (lane == 0) atomicAdd(&s_vtok, m);                 // work counter: tokens a verification may compare
             // 8 tokens per lane in flight per step (the page-list and token-store loads of a step are
             // issued before any compare): one round trip per 256 tokens instead of per 32
             constexpr int U = 8;
@@ -272,6 +273,13 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         if (tid == 0) {
             a.req_cnt[r] = nh;
             a.req_covered[r] = s_cov; a.req_recompute[r] = s_rec; a.req_candidates[r] = s_cands;
+            // work counters (O(n + c)): windows probed, prefix-filter candidates, candidates
+            // through the full-hash pre-check, tokens their verification may compare
+            const int nwin_w = a.policy == 0 ? max(0, n - a.w + 1) : a.policy == 1 ? n / a.w : (n >= a.w ? 1 : 0);
+            atomicAdd(&a.hdr->match_work[0], (unsigned long long)nwin_w);
+            atomicAdd(&a.hdr->match_work[1], (unsigned long long)s_cands);
+            atomicAdd(&a.hdr->match_work[2], (unsigned long long)s_nc);
+            atomicAdd(&a.hdr->match_work[3], (unsigned long long)s_vtok);
         }
     } else if (tid == 0) {
         a.req_cnt[r] = 0;

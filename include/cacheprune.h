@@ -259,6 +259,10 @@ cp_status cp_gather_rerotate(cp_index* idx, const cp_batch* readers_h, const cp_
  * out_scores (device int64) receives m_s scores from score_offsets_h[s]; out_bits (device uint32)
  * receives ceil(m_s/32) words from bits_word_offsets_h[s]: the first ceil(rho_num*m/rho_den) tokens in
  * (score desc, index asc) order get bit 1 (R#15-16).  max_m bounds m_s (<= 16384).
+ * Fixed-point domain (the sums are exact int64): attention entries are probabilities, each head's row
+ * summing to at most 1 (softmax; a bf16 export may exceed 1 by rounding -- up to 2 is fine).  A score
+ * then sums at most heads * 2 * 2^40 < 2^49 in magnitude (heads <= 255): exact.  Rows summing past 2^22
+ * are outside the precondition and may wrap; that is not detected.
  * mode CP_SCORE_KVDEV takes KV caches, not attention: it returns CP_ERR_UNSUPPORTED here; the
  * CacheBlend selector is cp_score_kv_deviation below.
  */
@@ -347,6 +351,10 @@ size_t cp_annotate_workspace(int32_t num_reqs, const int32_t* n_h, int32_t max_s
  * segments (-1 if more than max_segments); for s < out_nseg[r], at [r * max_segments + s]:
  * out_l / out_r (0-based inclusive, -1 if the segment yields no reusable span) and out_diff.
  * workspace: device, >= cp_annotate_workspace(...) bytes, caller-owned.
+ * Fixed-point domain: the summed-area sums cover the whole causal triangle, so with the probabilities of
+ * cp_score_deviation (each head's row summing to at most 1, 2 with bf16 rounding) they stay below
+ * n * heads * 2 * 2^40: exact for n * heads < 2^22, checked (CP_ERR_INVALID_ARG).  Rows summing past 2
+ * are outside the precondition and may wrap (a uniform non-normalised matrix wraps near n = 4.5K).
  */
 cp_status cp_annotate_spans(int32_t num_reqs, const float* const* attn_h, const int32_t* n_h,
                             const int32_t* heads_h, const uint8_t* const* mask_h, int32_t min_len,

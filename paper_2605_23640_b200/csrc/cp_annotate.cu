@@ -398,7 +398,9 @@ extern "C" cp_status cp_annotate_spans(int32_t num_reqs, const float* const* att
         return CP_ERR_INVALID_ARG;
     if (workspace_bytes < cp_annotate_workspace(num_reqs, n_h, max_segments)) return CP_ERR_CAPACITY;
     for (int r = 0; r < num_reqs; ++r)
-        if (!attn_h[r] || !mask_h[r] || n_h[r] < 1 || heads_h[r] < 1 || n_h[r] > (1 << 20)) return CP_ERR_INVALID_ARG;
+        if (!attn_h[r] || !mask_h[r] || n_h[r] < 1 || heads_h[r] < 1 || n_h[r] > (1 << 20) ||
+            (int64_t)n_h[r] * heads_h[r] >= (1LL << 22))       // int64 domain of the 2^-40 sums (header)
+            return CP_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     std::vector<AnnArgs> hold(1);
     size_t off = 0;

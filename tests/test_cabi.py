@@ -69,6 +69,13 @@ def test_host_side_validation_without_gpu():
     assert lib.cp_score_kv_deviation(*args(3, 1, 3)) == L.CP_ERR_INVALID_ARG
     assert lib.cp_index_insert(None, None, None, 0, None, None, None, None, None, 0, None, None,
                                None) == L.CP_ERR_INVALID_ARG
+    # annotator: n * heads must stay inside the int64 domain of its 2^-40 sums (n * heads < 2^22)
+    dummy = (C.c_void_p * 1)(C.c_void_p(16))
+    outs = [C.c_void_p(16)] * 4
+    for n, h, want in [((1 << 20), 4, L.CP_ERR_INVALID_ARG), ((1 << 21), 1, L.CP_ERR_INVALID_ARG)]:
+        rc = lib.cp_annotate_spans(1, dummy, (C.c_int32 * 1)(n), (C.c_int32 * 1)(h), dummy, 128, 8,
+                                   C.c_void_p(16), C.c_size_t(2 ** 63), *outs, None)
+        assert rc == want, (n, h, rc)
     assert lib.cp_status_string(-2) == b"CP_ERR_SENSITIVE_SPAN"
 
 

@@ -81,3 +81,20 @@ def test_many_segments_beside_long_request(variant, monkeypatch):
         exp.append(O.annotate(A, m, 1))
     got = _run(mats, masks, heads, 1, max_segments=256)
     assert got == exp
+
+
+@pytest.mark.parametrize("n", [7500, 10000])
+def test_long_requests_at_the_timed_sizes(n):
+    """The 7.5K / 10K-token requests the annotator is timed at (M6 sizes): row-stochastic
+    segment-local attention plus a perturbation that makes the optimal span a strict sub-range of its
+    segment, two masked runs; bit exact against the oracle's summed-area-table search."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    segs = [(0, 1000), (1003, 4000), (4002, n)]
+    A = attention_torch(n, segs, 0.01, seed=n)
+    A = A * (1.0 + 0.5 * torch.rand(A.shape, generator=g, device="cuda")).tril()
+    A = (A / A.sum(-1, keepdim=True)).contiguous()                 # rows still sum to 1 (domain, header)
+    m = np.zeros(n, np.uint8); m[1000:1003] = 1; m[4000:4002] = 1
+    got = cp.annotate_spans([A], [torch.from_numpy(m).cuda()], [1], min_len=128)[0]
+    exp = O.annotate(A.cpu().numpy(), m, 128)
+    assert got == exp
+    assert len(got) == 3 and all(l >= 0 for l, _, _ in got)

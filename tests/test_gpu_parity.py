@@ -39,9 +39,10 @@ def test_msmarco_config2_reduced():
     assert res["covered"] / res["tokens"] > 0.9
 
 
-def test_msmarco_config2_full_size_sampled():
-    """Config 2 at its full size in the bench's launch configuration; sampled KV rows."""
-    case = Case(make_workload(2), sample_reqs=2, sample_layers=[0, 31])
+def test_msmarco_config2_full_size_every_request():
+    """Config 2 at its full size in the bench's launch configuration: every request's K and V rows of
+    the last layer (393K tokens, moved and unmoved hits, zero placeholders) against the oracle."""
+    case = Case(make_workload(2), sample_reqs=None, sample_layers=[31])
     wb, rb = case.wl.rounds[0]
     rep = ParityReport()
     case.insert(wb, rep)
@@ -249,11 +250,11 @@ def test_score_multihead_long_misaligned_rows():
         assert np.array_equal(bits[bo[q]:bo[q] + (m + 31) // 32], ob), q
 
 
-def test_multidoc_config3_full_size_sampled():
+def test_multidoc_config3_full_size_every_request():
     """Config 3 at full size (128 readers x ~4K, 512-passage pool, one GPU): all hits, plans and the
-    index bit exact; KV rows sampled (2 requests x 2 layers)."""
+    index bit exact; every request's K and V rows of one layer (533K tokens, 88% moved hits)."""
     wl = make_workload(3)
-    case = Case(wl, sample_reqs=2, sample_layers=[0, 31])
+    case = Case(wl, sample_reqs=None, sample_layers=[17])
     rep = ParityReport()
     wb, rb = wl.rounds[0]
     case.insert(wb, rep, sparse_kv=True)

@@ -19,7 +19,7 @@ def _gpu_index(wl):
     wb = wl.writers
     cfg = cp.IndexConfig(num_layers=1, num_kv_heads=1, head_dim=16, dtype="fp32", rope_theta=10000.0,
                          window_len=P.W, pool_capacity_tokens=1 << 16, max_entries=4096, max_span_len=256,
-                         max_req_tokens=256, max_batch_reqs=1 << 17, max_batch_tokens=1 << 21,
+                         max_req_tokens=256, max_batch_reqs=1 << 19, max_batch_tokens=1 << 23,
                          max_spans_per_insert=max(1, len(wb.span_len)))
     idx = cp.KVIndex(cfg)
     nb = [(int(n) + 15) // 16 for n in wb.lens]
@@ -69,8 +69,24 @@ def test_gpu_reuse_oracle_leaks_no_sensitive_token(block):
         rec, total, probes = P.attack(wl, both, "sensitive")
         assert total > 0 and probes > 0
         assert rec == 0, f"seed {seed}: {rec}/{total} sensitive tokens recovered through cp_match_spans"
-        pub, ptot, _ = P.attack(wl, Rg, "public", limit=24)
-        assert ptot == 0 or pub > 0, f"seed {seed}: the attack recovers no public token (positive control)"
+
+
+def test_gpu_positive_control_recovers_public_tokens():
+    """The same attack through cp_match_spans recovers public tokens inside stored segments (and the
+    GPU signal equals the oracle's on those probes too)."""
+    got = tot = 0
+    for seed in range(6):
+        wl = P.make_workload(seed)
+        idx, cp = _gpu_index(wl)
+        Rg, Ro = _reuse_gpu(idx, cp), _reuse_oracle(wl)
+
+        def both(batch):
+            g = Rg(batch)
+            assert np.array_equal(g, Ro(batch))
+            return g
+        rec, total, _ = P.attack(wl, both, "public")
+        got += rec; tot += total
+    assert tot > 0 and got / tot > 0.5, (got, tot)
 
 
 def test_gpu_false_negative_sweep_is_monotone():

@@ -39,7 +39,7 @@ def test_attack_recovers_public_tokens_positive_control():
     for seed in range(8):
         wl = P.make_workload(seed)
         idx = _oracle_index(wl)
-        rec, total, _ = P.attack(wl, _reuse(idx), "public", limit=40)
+        rec, total, _ = P.attack(wl, _reuse(idx), "public")
         got += rec; tot += total
     # not every covered public token is recoverable: a span stored only inside a longer entry of
     # another writer, or shadowed by a shorter entry inside every probe around it, gives no signal

@@ -64,6 +64,11 @@ def parse():
                          "multi-rank code path on one GPU")
     ap.add_argument("--rho", default="1/4", help="recompute fraction of N3 (paper: 25%%, P:L1032); 0/1 = no recompute "
                     "marks (e.g. same-user sessions, P:L719-722)")
+    ap.add_argument("--placeholders", default="both", choices=["both", "recompute", "none"],
+                    help="zero placeholders (P:L727, R#14): both = recompute-marked and unmatched positions get "
+                         "+0.0 K/V rows (paper-literal, default); recompute = only recompute-marked ones; none = "
+                         "the plan codes are the placeholders, those rows are left for the engine's prefill "
+                         "(CP_SKIP_RECOMPUTE)")
     ap.add_argument("--link", action="store_true",
                     help="NEXT-2: link page-aligned delta-0 recompute-free blocks (cp_link_blocks) instead of copying")
     return ap.parse_args()
@@ -275,6 +280,7 @@ def setup_ours(args, rank, world, device):
     S.bits = torch.zeros(max(bo[-1], 1), dtype=torch.int32, device=device)
     S.bits_off = torch.tensor(bo[:-1] or [0], dtype=torch.int64, device=device)
     S.link = bool(getattr(args, "link", False))
+    S.placeholders = getattr(args, "placeholders", "both")
     S.link_tab = torch.full((rb.num_reqs, max(nb)), -1, dtype=torch.int32, device=device)
     S.side = torch.cuda.Stream(device=device)
     S.overlap = int(getattr(args, "overlap", 3))
@@ -354,9 +360,12 @@ def run_step(S, torch, cp, world, events=None):
     if ev: ev[1].record()
     if S.link:                                                                     # NEXT-2
         S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
-    S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=True, skip_linked=S.link)   # N2
+    zr, zu, sk = S.placeholders in ("both", "recompute"), S.placeholders == "both", S.placeholders == "none"
+    S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
+                          skip_recompute=sk)                                                          # N2
     for v, dkv in zip(S.views, S.dsts[1:]):                                        # the rank's other rectangles
-        v.gather_rerotate(S.rdb, S.hits, dkv, zero_recompute=True, skip_linked=S.link, reuse_worklist=True)
+        v.gather_rerotate(S.rdb, S.hits, dkv, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
+                          skip_recompute=sk, reuse_worklist=True)
     if ev: ev[2].record()
     if S.overlap == 3:
         if scores:
@@ -438,7 +447,9 @@ def bench_ours(args):
     reused = cov - rec
     linked = int((S.link_tab >= 0).sum().item()) * 16 if S.link else 0   # reused without a copy
     reused_bytes = reused * 2 * row * 2                 # K + V, read + write
-    zero_bytes = rec * 2 * row                          # K + V zero placeholders (writes)
+    unc = S.rb.total_tokens - cov
+    zero_tok = {"both": rec + unc, "recompute": rec, "none": 0}[S.placeholders]
+    zero_bytes = zero_tok * 2 * row                     # K + V zero placeholders (writes)
     gather_bytes = (reused - linked) * 2 * row * 2 + zero_bytes
     # ---- timed region
     K = args.steps
@@ -496,6 +507,26 @@ def bench_ours(args):
         traffic = None                              # the capture was of a different workload
     value = reused_all / (ms_step * 1e-3) / 1e9
     achieved = gather_bytes / (gather_ms * 1e-3) / 1e9          # this rank's gather kernel
+    # ---- R#14 alternative, measured beside the paper-literal default: placeholders as plan codes only
+    alt = None
+    if world == 1 and not args.no_extra and S.placeholders != "none":
+        keep = S.placeholders
+        S.placeholders = "none"
+        for _ in range(2):
+            run_step(S, torch, cp, world)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(K):
+            run_step(S, torch, cp, world)
+        a1.record()
+        torch.cuda.synchronize()
+        S.placeholders = keep
+        ams = a0.elapsed_time(a1) / K
+        alt = {"placeholders": "none (CP_SKIP_RECOMPUTE: recompute-marked and unmatched rows left for the engine's "
+                               "prefill; the plan codes are the placeholders)",
+               "value": round(reused_bytes / (ams * 1e-3) / 1e9, 2), "ms_per_step": round(ams, 4),
+               "gather_bytes_per_step": int((reused - linked) * 2 * row * 2)}
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -521,6 +552,7 @@ def bench_ours(args):
                        "index_entries": len(S.wb.span_len), "insert_batch_spans": len(S.ib.span_len),
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
+                       "placeholders": S.placeholders,
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
                        **({"dist_backend": dist.get_backend()} if use_dist else {}),
                        "shard_rects": [[r.layer_lo, r.layer_hi, r.head_lo, r.head_hi] for r in S.rects],
@@ -546,8 +578,9 @@ def bench_ours(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "traffic_source": "profiles/r01/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
                          "algorithmic_bytes_per_launch": gather_bytes,
-                         "bytes_rule": "copied reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + recompute tokens x 2 (K,V) x L*H*d*e (zero writes); linked tokens (--link) move no bytes"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, **extras,
+                         "bytes_rule": "copied reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + zero-placeholder tokens (recompute-marked + unmatched with --placeholders both) x 2 (K,V) x L*H*d*e (writes); linked tokens (--link) move no bytes"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            **({"placeholders_untouched": alt} if alt else {}), **extras,
             "setup": {"insert_writers_ms": round(S.setup_insert_ms, 2), "setup_s": round(S.setup_s, 1)},
         }
         print(json.dumps(out), flush=True)

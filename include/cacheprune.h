@@ -58,7 +58,8 @@ enum { CP_MATCH_NO_TOUCH = 1,                     /* cp_match_spans flags       
 enum { CP_POLICY_FIXED_CHUNK = 1, CP_POLICY_PREFIX_ONLY = 2 };   /* cp_policy_spans              */
 enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2,  /* cp_gather_rerotate flags (R#14)            */
        CP_SKIP_LINKED = 4,                         /* NEXT-2: leave linkable blocks unwritten (R#31) */
-       CP_REUSE_WORKLIST = 8 };                    /* pool views: reuse the sibling's work list      */
+       CP_REUSE_WORKLIST = 8,                      /* pool views: reuse the sibling's work list      */
+       CP_SKIP_RECOMPUTE = 16 };                   /* leave plan-2 rows unwritten (R#14 alternative) */
 enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
 enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
 enum { CP_PLAN_UNCOVERED = 0, CP_PLAN_REUSED = 1, CP_PLAN_RECOMPUTE = 2 };              /* plan codes     */
@@ -243,7 +244,9 @@ cp_status cp_match_spans(cp_index* idx, const cp_batch* readers_h, uint64_t logi
  * (layer, head) of the shard: V_dst[q] <- V_pool[e][t] (bit copy); K_dst[q] <- R(delta) K_pool[e][t]
  * (fp32 products with cos/sin of delta*theta_i evaluated in fp64; delta == 0 is a bit copy).  With
  * CP_ZERO_RECOMPUTE, plan-2 positions get +0.0 in K and V (zero placeholders); with
- * CP_ZERO_UNCOVERED, plan-0 positions are zeroed too.  `hits` is the struct cp_match_spans wrote
+ * CP_ZERO_UNCOVERED, plan-0 positions are zeroed too (both flags = the paper-literal placeholders, R#14);
+ * with CP_SKIP_RECOMPUTE, plan-2 rows are neither copied nor zeroed (the plan codes are the placeholders
+ * and the engine's prefill writes those rows; CP_ZERO_RECOMPUTE is then ignored).  `hits` is the struct cp_match_spans wrote
  * (only num_hits, hit_* and plan are read).  readers_h must be the batch that was matched.
  * Device error: a block table narrower than a covered position (position >> 4 >= max_blocks_per_req)
  * -> CP_ERR_INVALID_ARG, and no row is written (the copy kernel sees the error word and exits).

@@ -17,7 +17,7 @@ CP_FP32, CP_BF16 = 0, 1
 CP_ROPE_NEOX, CP_ROPE_GPTJ = 0, 1
 CP_MATCH_NO_TOUCH, CP_MATCH_FIXED_CHUNK, CP_MATCH_PREFIX_ONLY = 1, 2, 4
 CP_POLICY_FIXED_CHUNK, CP_POLICY_PREFIX_ONLY = 1, 2
-CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED, CP_REUSE_WORKLIST = 1, 2, 4, 8
+CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED, CP_REUSE_WORKLIST, CP_SKIP_RECOMPUTE = 1, 2, 4, 8, 16
 CP_SCORE_INTER_INTRA, CP_SCORE_KVDEV = 0, 1
 CP_STORED, CP_SUPERSEDED, CP_DUPLICATE, CP_DROPPED_CONTAINED = 0, 1, 2, 3
 CP_WS_COUNT = 4

@@ -237,9 +237,12 @@ class KVIndex:
 
     def gather_rerotate(self, readers: DeviceBatch, hits: Hits, dst_kv: PagedKV,
                         zero_recompute: bool = True, zero_uncovered: bool = False, skip_linked: bool = False,
-                        reuse_worklist: bool = False, stream=None):
+                        reuse_worklist: bool = False, skip_recompute: bool = False, stream=None):
+        """Placeholders (R#14): zero_recompute + zero_uncovered = the paper's zero placeholders for both
+        kinds; skip_recompute leaves recompute-marked rows unwritten (plan codes as placeholders)."""
         flags = ((L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0) |
-                 (L.CP_SKIP_LINKED if skip_linked else 0) | (L.CP_REUSE_WORKLIST if reuse_worklist else 0))
+                 (L.CP_SKIP_LINKED if skip_linked else 0) | (L.CP_REUSE_WORKLIST if reuse_worklist else 0) |
+                 (L.CP_SKIP_RECOMPUTE if skip_recompute else 0))
         rb, hc, kv = readers.c(), hits.c(), dst_kv.c()
         L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
                 "cp_gather_rerotate")

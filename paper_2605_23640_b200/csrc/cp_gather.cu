@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_rows_prep2(RowsArgs a) {
         const long long pool_row = (long long)page * CP_BLOCK + (t & 15);
         const long long paged_row = (long long)blk * CP_BLOCK + (pos & 15);
         long long code = a.dir == 0 ? (long long)a.plan[a.req_off[r] + pos] : (long long)CP_PLAN_REUSED;
+        if (a.dir == 0 && (a.flags & CP_SKIP_RECOMPUTE) && code == CP_PLAN_RECOMPUTE) code = kCodeLinked;   // untouched
         if (a.dir == 0 && (a.flags & CP_SKIP_LINKED) && code == CP_PLAN_REUSED && a.l_delta[hh] == 0 && (k & 15) == 0) {
             const int b0 = pos & ~15;                                       // >= k: k is page aligned
             if (b0 + 16 <= k + a.l_len[hh]) {                               // the block lies inside the hit
@@ -507,22 +508,43 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rows_tma(RowsArgs a, int nst
     }
 }
 
-// CP_ZERO_UNCOVERED: zero K and V rows of plan-0 positions (one CTA per (token block of 32, layer))
+// CP_ZERO_UNCOVERED: zero K and V rows of plan-0 positions.  k_unc_list compacts the uncovered
+// positions (warp ballot + one atomic per warp; the order is irrelevant: zero stores commute); then
+// k_zero_uncovered walks items (32 listed positions x layer), so the work is proportional to the
+// uncovered tokens.  (The first version walked every 32-token block of the batch per layer: 1.78 ms on
+// config 2 for 1.5% uncovered tokens.)
+__global__ void k_unc_list(DevHeader* hdr, const uint8_t* plan, int64_t total, int64_t* list) {
+    if (cp_err_set(hdr)) return;
+    const int lane = threadIdx.x & 31;
+    for (int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; g0 < total;
+         g0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = g0 + lane;
+        const bool u = g < total && plan[g] == CP_PLAN_UNCOVERED;
+        const unsigned b = __ballot_sync(0xffffffffu, u);
+        if (!b) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&hdr->n_unc, __popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (u) list[base + __popc(b & ((1u << lane) - 1))] = g;
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int32_t R, int64_t total) {
+__global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int32_t R, const int64_t* list) {
     __shared__ int64_t s_dst[32];
     __shared__ int s_on[32];
     if (cp_err_set(a.hdr)) return;
     const int rowE = a.H * a.d;
-    const int64_t nblk = (total + 31) / 32;
-    const int64_t items = nblk * a.L;
+    const int nu = a.hdr->n_unc;
+    const int64_t items = (int64_t)((nu + 31) / 32) * a.L;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int64_t b = item / a.L;
         const int l = (int)(item % a.L);
         if (threadIdx.x < 32) {
-            const int64_t g = b * 32 + threadIdx.x;
+            const int64_t li = b * 32 + threadIdx.x;
             s_on[threadIdx.x] = 0;
-            if (g < total && a.plan[g] == CP_PLAN_UNCOVERED) {
+            if (li < nu) {
+                const int64_t g = list[li];
                 int lo = 0, hi = R - 1;
                 while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (a.req_off[mid] <= g) lo = mid; else hi = mid - 1; }
                 const int q = (int)(g - a.req_off[lo]);
@@ -647,7 +669,7 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     if (dir == 0 && !l_delta) return CP_ERR_INVALID_ARG;
     WorkKey key;
     key.valid = 1; key.dir = dir; key.cap = list_cap; key.max_blocks = kv->max_blocks_per_req;
-    key.skip_linked = dir == 0 && (flags & CP_SKIP_LINKED) ? 1 : 0;
+    key.skip_linked = dir == 0 ? (flags & (CP_SKIP_LINKED | CP_SKIP_RECOMPUTE)) : 0;
     const void* kp[9] = {d_count, l_req, l_slot, l_dst, l_len, l_delta, req_off, plan, kv->block_tables};
     for (int i = 0; i < 9; ++i) key.p[i] = kp[i];
     if (flags & CP_REUSE_WORKLIST) {
@@ -695,8 +717,12 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
         a.block_tables = kv->block_tables; a.max_blocks = kv->max_blocks_per_req;
         for (int l = 0; l < x->cfg.num_layers; ++l) { a.paged_k[l] = (char*)kv->k_layers_h[l]; a.paged_v[l] = (char*)kv->v_layers_h[l]; }
         a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim;
-        if (x->cfg.dtype == CP_BF16) k_zero_uncovered<__nv_bfloat16><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, b->total_tokens);
-        else k_zero_uncovered<float><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, b->total_tokens);
+        if (b->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
+        if (cudaMemsetAsync(&x->hdr->n_unc, 0, sizeof(x->hdr->n_unc), st) != cudaSuccess) return CP_ERR_CUDA;
+        k_unc_list<<<sm_count() * 4, 256, 0, st>>>(x->hdr, h->plan, b->total_tokens, x->unc_list);
+        CP_COUNT_LAUNCH();
+        if (x->cfg.dtype == CP_BF16) k_zero_uncovered<__nv_bfloat16><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, x->unc_list);
+        else k_zero_uncovered<float><<<rows_grid(), kRowsThreads, 0, st>>>(a, b->num_reqs, x->unc_list);
         CP_COUNT_LAUNCH();
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }

@@ -130,6 +130,7 @@ void compute_layout(const cp_config* c, Layout* L) {
     // 31 parallel-apply scratch: 12 int32 + 1 int64 arrays of MS + 1, 4 int32 arrays of S, 4 int32 + 1 int64 of 4097
     sput(4 * (size_t)(L->MS + 1) * 12 + 8 * (size_t)(L->MS + 1) + 4 * (size_t)S * 4 + 4 * 4097 * 4 + 8 * 4097 + 64);
     sput(4 * (size_t)(std::max<int64_t>(L->HS, L->MS) + 1));                 // 32 hit_coff (gather / copy-in)
+    sput(8 * (size_t)c->max_batch_tokens);                                   // 33 unc_list (CP_ZERO_UNCOVERED)
     L->scr_size = o;
 }
 
@@ -1594,6 +1595,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->match_g = cfg->max_req_tokens > CP_MATCH_SMEM_TOKENS ? s + L.scr_off[30] : nullptr;
     x->fscr = s + L.scr_off[31];
     x->hit_coff = (int32_t*)(s + L.scr_off[32]);
+    x->unc_list = (int64_t*)(s + L.scr_off[33]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;

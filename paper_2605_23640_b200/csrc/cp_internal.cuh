@@ -58,7 +58,7 @@ struct DevHeader {                   // first 256 B of META
     int32_t commits_parallel;        // insert commits applied by the parallel path (diagnostics)
     int32_t commits_serial;          // ... and by the sequential path
     int32_t commit_why;              // OR of the reasons the sequential path was taken (k_ins_commit bits)
-    int32_t pad0;
+    int32_t n_unc;                   // gather: uncovered positions listed for CP_ZERO_UNCOVERED
     unsigned long long match_work[4];   // matcher work counters (cp_index_match_work)
     int32_t pad[30];
 };
@@ -121,6 +121,7 @@ struct cp_index {
     // SCRATCH (gather / copy-in work lists)
     int64_t CH;          // chunk capacity
     int32_t *chunk_hit, *chunk_t0, *hit_coff;
+    int64_t* unc_list;   // [max_batch_tokens] uncovered positions (CP_ZERO_UNCOVERED)
     long long *row_src, *row_dst;   // [CH * CP_GATHER_CHUNK] element offsets; row_dst carries the plan code in bits 62-63
     float2* hit_cs;      // [hits][d/2] cos/sin
     int64_t CS_HITS;     // hits capacity of hit_cs

@@ -86,7 +86,8 @@ class Case:
 
     def __init__(self, wl: Workload, device="cuda", seed: int = 0, rho=(1, 4), layer_range=None,
                  head_range=None, sample_reqs: Optional[int] = None, sample_layers: Optional[Sequence[int]] = None,
-                 use_reader_mask: bool = True, hash_seed: int = 42, policy: Optional[str] = None):
+                 use_reader_mask: bool = True, hash_seed: int = 42, policy: Optional[str] = None,
+                 placeholders: str = "recompute"):
         import torch
         import paper_2605_23640_b200 as cp
         self.torch, self.cp = torch, cp
@@ -100,6 +101,9 @@ class Case:
         self.sample_reqs, self.sample_layers = sample_reqs, sample_layers
         self.use_reader_mask = use_reader_mask
         self.policy = policy                 # None: the method; "fixed_chunk" / "prefix_only": NEXT-3 baselines
+        # R#14 zero placeholders: "recompute" (CP_ZERO_RECOMPUTE), "both" (+ CP_ZERO_UNCOVERED: paper-literal),
+        # "none" (CP_SKIP_RECOMPUTE: recompute-marked rows left untouched)
+        self.placeholders = placeholders
         lens = [int(b.lens.max()) for wb, rb in wl.rounds for b in (wb, rb) if b is not None]
         spans = [len(wb.span_len) for wb, rb in wl.rounds if wb is not None]
         if policy is not None:
@@ -251,7 +255,9 @@ class Case:
         hits = self.dev.match_spans(db, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy)
         dst = self.dst_kv(rb) if check_kv else None
         if check_kv:
-            self.dev.gather_rerotate(db, hits, dst, zero_recompute=True)
+            ph = self.placeholders
+            self.dev.gather_rerotate(db, hits, dst, zero_recompute=ph != "none", zero_uncovered=ph == "both",
+                                     skip_recompute=ph == "none")
         err = self.dev.last_error()
         if err:
             rep.fail(f"match t={t}: device error {err}")
@@ -339,13 +345,20 @@ class Case:
                     krot = O.rerotate_rows(kraw, H, d, g.rope_theta, delta, g.dtype == "bf16", g.rope_style == "gptj")
                     expK[k0:k0 + m] = krot
                     expV[k0:k0 + m] = vraw
-                zero = plan == 2
+                zero = plan == 2 if self.placeholders != "none" else np.zeros_like(plan, bool)
+                if self.placeholders == "none":                       # recompute rows untouched
+                    expK[plan == 2] = SENTINEL
+                    expV[plan == 2] = SENTINEL
+                if self.placeholders == "both":                       # unmatched rows zeroed too
+                    zero = zero | (plan == 0)
                 expK[zero] = 0.0
                 expV[zero] = 0.0
                 if not np.array_equal(gotV.view(np.uint32), expV.view(np.uint32)):
                     bad = np.nonzero(np.any(gotV != expV, axis=(1, 2)))[0]
                     rep.fail(f"gather: V differs req {r} layer {l} at positions {bad[:8]}")
-                untouched = plan == 0
+                untouched = (plan == 0) if self.placeholders != "both" else np.zeros_like(plan, bool)
+                if self.placeholders == "none":
+                    untouched = untouched | (plan == 2)
                 if not np.array_equal(gotK[untouched], expK[untouched]) or not np.array_equal(
                         gotK[zero].view(np.uint32), expK[zero].view(np.uint32)):
                     rep.fail(f"gather: K placeholder / untouched rows differ req {r} layer {l}")

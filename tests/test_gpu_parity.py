@@ -539,3 +539,16 @@ def test_layer_and_head_shards_concatenate_to_the_full_gather():
             ls, hsl = sel
             assert torch.equal(sk.view(torch.int16), fk[ls, :, hsl].contiguous().view(torch.int16)), kw
             assert torch.equal(sv.view(torch.int16), fv[ls, :, hsl].contiguous().view(torch.int16)), kw
+
+
+@pytest.mark.parametrize("placeholders", ["both", "none"])
+def test_placeholder_modes_config2_every_request(placeholders):
+    """R#14 at full config-2 size, every request, one layer: 'both' = the paper-literal zero placeholders
+    (recompute-marked AND unmatched rows +0.0; the unmatched ones through the compacted uncovered list),
+    'none' = CP_SKIP_RECOMPUTE (recompute-marked rows left untouched, unmatched rows untouched)."""
+    case = Case(make_workload(2), sample_reqs=None, sample_layers=[5], placeholders=placeholders)
+    wb, rb = case.wl.rounds[0]
+    rep = ParityReport()
+    case.insert(wb, rep)
+    case.match_and_gather(rb, rep, check_kv=True)
+    assert rep.ok, rep.notes[:10]

@@ -77,7 +77,7 @@ def parse():
 def ncu_traffic(workload: str):
     """DRAM read+write bytes per launch of the gather from the committed ncu capture (or None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json")) as f:
             t = json.load(f)[workload]
         return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), int(t["algorithmic_bytes"])
     except Exception:
@@ -573,10 +573,10 @@ def bench_ours(args):
                                       2: "score (N3) on a side stream after the gather, beside the insert's read-only half",
                                       1: "score (N3) on a side stream concurrently with match + gather",
                                       0: "score (N3) serialized before match on the same stream"}[S.overlap]},
-            "roofline": {"kernel": "k_rows (cp_gather_rerotate: prep + rows)", "bound": "hbm",
+            "roofline": {"kernel": "k_rows (cp_gather_rerotate: prep + rows + uncovered zero placeholders)", "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "traffic_source": "profiles/r01/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
+                         "traffic_source": "profiles/r02/roofline_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of k_rows + k_zero_uncovered)",
                          "algorithmic_bytes_per_launch": gather_bytes,
                          "bytes_rule": "copied reused tokens x 2 (K,V) x L*H*d*e x 2 (read+write) + zero-placeholder tokens (recompute-marked + unmatched with --placeholders both) x 2 (K,V) x L*H*d*e (writes); linked tokens (--link) move no bytes"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,

@@ -37,7 +37,7 @@
 
 enum { ORC_OK = 0, ORC_ERR_INVALID_ARG = -1, ORC_ERR_SENSITIVE_SPAN = -2,
        ORC_ERR_SPAN_TOO_SHORT = -3, ORC_ERR_CAPACITY = -4 };
-enum { ORC_STORED = 0, ORC_SUPERSEDED = 1, ORC_DUPLICATE = 2, ORC_DROPPED_CONTAINED = 3 };
+enum { ORC_STORED = 0, ORC_SUPERSEDED = 1, ORC_DUPLICATE = 2, ORC_DROPPED_CONTAINED = 3, ORC_DEFERRED_PINNED = 4 };
 
 /* ------------------------------------------------------------------------- */
 /* hashing  ("polynomial rolling hash modulo 2^61-1 with a random base") */
@@ -149,6 +149,7 @@ void orc_sha256_tokens(const int32_t* t, int64_t m, uint8_t out[32]) {
 /* ------------------------------------------------------------------------- */
 typedef struct {
     int32_t id, live, len, origin_pos, origin_call, origin_req;
+    int32_t pin;          /* linked-block pins on its pages (R#32) */
     uint64_t prefix_hash, full_hash, last_used;
     uint8_t digest[32];
     int32_t* tokens;      /* [len] */
@@ -270,6 +271,20 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         for (int32_t i = 0; i < x->n_e && cont < 0; ++i)
             if (x->e[i].live && x->e[i].len > m && contains(x->e[i].tokens, x->e[i].len, tau, m)) cont = i;
         if (cont >= 0) { out_id[s] = cont; out_outcome[s] = ORC_DROPPED_CONTAINED; continue; }
+        /* R#32 (NEXT-2 lifetime of linked pages): a span may not remove a pinned entry, and the pinned
+           tokens plus the span must fit the budget (so that the LRU can always get back under it by
+           evicting unpinned entries) -- otherwise it is DEFERRED_PINNED: not stored, nothing changes */
+        int32_t blocked = -1;
+        int64_t pinned_tok = 0;
+        for (int32_t i = 0; i < x->n_e; ++i) {
+            if (!x->e[i].live || x->e[i].pin == 0) continue;
+            pinned_tok += x->e[i].len;
+            if (blocked < 0 && x->e[i].len < m && contains(tau, m, x->e[i].tokens, x->e[i].len)) blocked = i;
+        }
+        if (blocked >= 0 || pinned_tok + m > x->capacity) {
+            out_id[s] = blocked; out_outcome[s] = ORC_DEFERRED_PINNED;
+            continue;
+        }
         /* supersede live entries strictly contained in tau, ascending id */
         int32_t superseded = 0;
         for (int32_t i = 0; i < x->n_e; ++i)
@@ -301,11 +316,11 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         for (int32_t i = 0; i < e->npages; ++i) e->pages[i] = fifo_pop(x);
         x->live_tokens += m;
         out_id[s] = id; out_outcome[s] = superseded ? ORC_SUPERSEDED : ORC_STORED;
-        /* LRU eviction: victim = min (last_used, id) among live entries */
+        /* LRU eviction: victim = min (last_used, id) among live, unpinned entries (R#32) */
         while (x->live_tokens > x->capacity) {
             int32_t v = -1;
             for (int32_t i = 0; i < x->n_e; ++i) {
-                if (!x->e[i].live) continue;
+                if (!x->e[i].live || x->e[i].pin > 0) continue;
                 if (v < 0 || x->e[i].last_used < x->e[v].last_used) v = i;
             }
             remove_entry(x, &x->e[v]);
@@ -474,6 +489,38 @@ void orc_fifo_get(const orc_index* x, int32_t* out) {
  * every other entry of the first ceil(n_r / 16) blocks = -1 (entries beyond are left as they are).
  * The hits are the ones orc_match returned for this index state.
  */
+/* R#32: pin (delta > 0) or unpin (delta < 0) the entries owning the listed pool pages, once per listed
+ * page (entries < 0 are skipped: a link table can be passed as is).  Every page must belong to a live
+ * entry and no pin count may go negative; otherwise nothing changes and ORC_ERR_INVALID_ARG. */
+int32_t orc_pin_pages(orc_index* x, const int32_t* pages, int64_t n, int32_t delta) {
+    int32_t* owner = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t rc = ORC_OK;
+    for (int64_t q = 0; q < n && rc == ORC_OK; ++q) {
+        owner[q] = -1;
+        if (pages[q] < 0) continue;
+        for (int32_t i = 0; i < x->n_e && owner[q] < 0; ++i) {
+            if (!x->e[i].live) continue;
+            for (int32_t j = 0; j < x->e[i].npages; ++j)
+                if (x->e[i].pages[j] == pages[q]) { owner[q] = i; break; }
+        }
+        if (owner[q] < 0) rc = ORC_ERR_INVALID_ARG;
+    }
+    if (rc == ORC_OK && delta < 0) {            /* no count may go negative (counted over the whole list) */
+        for (int64_t q = 0; q < n && rc == ORC_OK; ++q) {
+            if (owner[q] < 0) continue;
+            int64_t uses = 0;
+            for (int64_t z = 0; z < n; ++z) uses += owner[z] == owner[q];
+            if (x->e[owner[q]].pin + delta * uses < 0) rc = ORC_ERR_INVALID_ARG;
+        }
+    }
+    if (rc == ORC_OK)
+        for (int64_t q = 0; q < n; ++q) if (owner[q] >= 0) x->e[owner[q]].pin += delta;
+    free(owner);
+    return rc;
+}
+
+int32_t orc_entry_pin(const orc_index* x, int32_t id) { return (id >= 0 && id < x->n_e) ? x->e[id].pin : -1; }
+
 int32_t orc_link_blocks(const orc_index* x, int32_t num_reqs, const int64_t* offsets, int32_t num_hits,
                         const int32_t* hit_req, const int32_t* hit_entry, const int32_t* hit_dst,
                         const int32_t* hit_len, const int32_t* hit_delta, const uint8_t* plan,

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "cp_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
-STORED, SUPERSEDED, DUPLICATE, DROPPED_CONTAINED = 0, 1, 2, 3
+STORED, SUPERSEDED, DUPLICATE, DROPPED_CONTAINED, DEFERRED_PINNED = 0, 1, 2, 3, 4
 OK, ERR_INVALID_ARG, ERR_SENSITIVE_SPAN, ERR_SPAN_TOO_SHORT, ERR_CAPACITY = 0, -1, -2, -3, -4
 
 
@@ -62,6 +62,8 @@ def lib():
             "orc_score": (i32, [vp, i64, i32, i32, i32, i32, i32, vp, vp]),
             "orc_kv_deviation": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp, vp]),
             "orc_link_blocks": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
+            "orc_pin_pages": (i32, [vp, vp, i64, i32]),
+            "orc_entry_pin": (i32, [vp, i32]),
             "orc_rerotate_rows": (None, [vp, i64, i32, i32, i32, C.c_double, i64, i32, vp]),
             "orc_annotate": (i32, [vp, i64, i32, vp, i32, i32, vp, vp, vp]),
             "orc_sat": (None, [vp, i64, i32, vp]),
@@ -313,6 +315,14 @@ class OracleIndex:
         if rc != OK:
             raise ValueError(f"orc_link_blocks rc={rc}")
         return link[:, :mb]
+
+    def pin_pages(self, pages, delta: int) -> int:
+        """R#32: pin (+1) / unpin (-1) the entries owning the listed pool pages (a link table; -1 skipped)."""
+        p = _c(np.asarray(pages).reshape(-1), np.int32)
+        return int(lib().orc_pin_pages(self.h, _p(p), len(p), int(delta)))
+
+    def entry_pin(self, eid: int) -> int:
+        return int(lib().orc_entry_pin(self.h, int(eid)))
 
     @property
     def num_ids(self) -> int:

@@ -61,7 +61,9 @@ enum { CP_ZERO_RECOMPUTE = 1, CP_ZERO_UNCOVERED = 2,  /* cp_gather_rerotate flag
        CP_REUSE_WORKLIST = 8,                      /* pool views: reuse the sibling's work list      */
        CP_SKIP_RECOMPUTE = 16 };                   /* leave plan-2 rows unwritten (R#14 alternative) */
 enum { CP_SCORE_INTER_INTRA = 0, CP_SCORE_KVDEV = 1 };
-enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3 }; /* insert outcomes */
+enum { CP_STORED = 0, CP_SUPERSEDED = 1, CP_DUPLICATE = 2, CP_DROPPED_CONTAINED = 3, /* insert outcomes */
+       CP_DEFERRED_PINNED = 4 };   /* not stored: it would supersede a pinned entry, or the pinned tokens plus it
+                                      exceed the budget (R#32); out id = the smallest pinned entry it contains, or -1 */
 enum { CP_PLAN_UNCOVERED = 0, CP_PLAN_REUSED = 1, CP_PLAN_RECOMPUTE = 2 };              /* plan codes     */
 
 typedef struct cp_index cp_index;                  /* opaque host handle */
@@ -313,12 +315,25 @@ cp_status cp_score_kv_deviation(int32_t num_spans, const int32_t* span_req_h, co
  * rows are the ones cp_gather_rerotate would copy (bit copies: delta 0), so an engine may point its
  * block table at the pool page (layer l's rows at pool_k + ((l * P + page) * 16) * H * d) instead
  * of copying; cp_gather_rerotate with CP_SKIP_LINKED then leaves those destination blocks unwritten.
- * Lifetime: a linked page stays valid until the next cp_index_insert on this index (which may evict
- * and recycle it).  `hits_h`: the cp_match_spans output for `readers_h` on this index state.
+ * Lifetime: unpinned, a linked page stays valid until the next cp_index_insert on this index (which may
+ * evict and recycle it); pinned with cp_pin_links it stays valid until released.  `hits_h`: the
+ * cp_match_spans output for `readers_h` on this index state.
  * Device error: max_blocks_per_req smaller than a request's block count -> CP_ERR_INVALID_ARG.
  */
 cp_status cp_link_blocks(cp_index* idx, const cp_batch* readers_h, const cp_hits* hits_h,
                          int32_t* link_table, int32_t max_blocks_per_req, void* stream);
+
+/*
+ * NEXT-2 lifetime of linked pages (R#32; vLLM-style block reference counts).  For each of the n
+ * entries of `pages` (device int32; entries < 0 skipped, so a cp_link_blocks table can be passed as is)
+ * the live entry owning that pool page gets `delta` pins (+1 when an engine links the block, -1 when it
+ * releases it).  While an entry has pins it is never evicted (LRU victims = min (last_used, id) among
+ * unpinned live entries) nor superseded: an insert span that would remove it, or whose length with the
+ * pinned tokens exceeds the budget, gets CP_DEFERRED_PINNED and changes nothing -- so a pinned page is
+ * never recycled and its rows stay exactly what the gather would copy.  Device error (nothing changes):
+ * a page that no live entry owns, or a count that would go negative -> CP_ERR_INVALID_ARG.
+ */
+cp_status cp_pin_links(cp_index* idx, const int32_t* pages, int64_t n, int32_t delta, void* stream);
 
 /*
  * NEXT-3: the spans a baseline policy stores for a writer batch (R#28-29), in
@@ -390,6 +405,7 @@ typedef struct {
     int32_t*  tokens;               /* [max_span_len] per entry, optional */
     uint8_t*  recompute;            /* [max_span_len] per entry, optional */
     int32_t*  fifo;                 /* free pages in pop order, optional */
+    int32_t*  pin;                  /* per entry: linked-block pins (R#32), optional */
 } cp_snapshot;
 cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
 

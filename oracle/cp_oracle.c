@@ -465,7 +465,7 @@ int32_t orc_entry_get(const orc_index* x, int32_t id, int32_t* info, uint64_t* h
     if (id < 0 || id >= x->n_e) return ORC_ERR_INVALID_ARG;
     const orc_entry* e = &x->e[id];
     info[0] = e->live; info[1] = e->len; info[2] = e->origin_pos; info[3] = e->origin_call;
-    info[4] = e->origin_req; info[5] = e->npages;
+    info[4] = e->origin_req; info[5] = e->npages; info[6] = e->pin;
     hashes[0] = e->prefix_hash; hashes[1] = e->full_hash; hashes[2] = e->last_used;
     if (digest) memcpy(digest, e->digest, 32);
     if (pages) memcpy(pages, e->pages, sizeof(int32_t) * (size_t)e->npages);

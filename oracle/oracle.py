@@ -351,7 +351,7 @@ class OracleIndex:
         return dict(id=eid, live=bool(info[0]), len=ln, origin_pos=int(info[2]), origin_call=int(info[3]),
                     origin_req=int(info[4]), prefix_hash=int(hs[0]), full_hash=int(hs[1]),
                     last_used=int(hs[2]), digest=dg.tobytes(), pages=pages[:npg].copy(),
-                    tokens=toks[:ln].copy(), recompute=rec[:ln].astype(bool))
+                    tokens=toks[:ln].copy(), recompute=rec[:ln].astype(bool), pin=int(info[6]))
 
     def live_entries(self):
         return [e for e in (self.entry(i) for i in range(self.num_ids)) if e["live"]]

@@ -19,7 +19,7 @@ CP_MATCH_NO_TOUCH, CP_MATCH_FIXED_CHUNK, CP_MATCH_PREFIX_ONLY = 1, 2, 4
 CP_POLICY_FIXED_CHUNK, CP_POLICY_PREFIX_ONLY = 1, 2
 CP_ZERO_RECOMPUTE, CP_ZERO_UNCOVERED, CP_SKIP_LINKED, CP_REUSE_WORKLIST, CP_SKIP_RECOMPUTE = 1, 2, 4, 8, 16
 CP_SCORE_INTER_INTRA, CP_SCORE_KVDEV = 0, 1
-CP_STORED, CP_SUPERSEDED, CP_DUPLICATE, CP_DROPPED_CONTAINED = 0, 1, 2, 3
+CP_STORED, CP_SUPERSEDED, CP_DUPLICATE, CP_DROPPED_CONTAINED, CP_DEFERRED_PINNED = 0, 1, 2, 3, 4
 CP_WS_COUNT = 4
 
 i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
@@ -54,7 +54,8 @@ class CpHits(C.Structure):
 class CpSnapshot(C.Structure):
     _fields_ = [("num_live", i32), ("next_id", i32), ("live_tokens", i64), ("fifo_count", i32), ("error", i32),
                 ("id", vp), ("len", vp), ("origin_pos", vp), ("prefix_hash", vp), ("full_hash", vp),
-                ("last_used", vp), ("digest", vp), ("pages", vp), ("tokens", vp), ("recompute", vp), ("fifo", vp)]
+                ("last_used", vp), ("digest", vp), ("pages", vp), ("tokens", vp), ("recompute", vp), ("fifo", vp),
+                ("pin", vp)]
 
 
 EXPORTS = {
@@ -78,6 +79,7 @@ EXPORTS = {
     "cp_score_kv_deviation": (i32, [i32, P_i32, P_i32, P_i32, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32,
                                     i32, i32, i32, vp, P_i64, vp, P_i64, vp]),
     "cp_link_blocks": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), vp, i32, vp]),
+    "cp_pin_links": (i32, [vp, vp, i64, i32, vp]),
     "cp_hash_prefix": (i32, [C.POINTER(CpBatch), u64, vp, vp]),
     "cp_policy_spans": (i32, [C.POINTER(CpBatch), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "cp_index_snapshot": (i32, [vp, C.POINTER(CpSnapshot), vp]),

@@ -271,6 +271,11 @@ class KVIndex:
         L.check(L.lib().cp_index_match_work(self.h, out, int(reset), _stream(stream)), "cp_index_match_work")
         return tuple(int(x) for x in out)
 
+    def pin_links(self, pages: torch.Tensor, delta: int, stream=None):
+        """cp_pin_links (R#32): +delta pins on the entries owning the listed pool pages (a link table)."""
+        p = pages.reshape(-1).contiguous()
+        L.check(L.lib().cp_pin_links(self.h, _ptr(p), int(p.numel()), int(delta), _stream(stream)), "cp_pin_links")
+
     def last_error(self, stream=None) -> int:
         return int(L.lib().cp_index_last_error(self.h, _stream(stream)))
 
@@ -283,6 +288,7 @@ class KVIndex:
             "prefix_hash": np.zeros(S, np.uint64), "full_hash": np.zeros(S, np.uint64),
             "last_used": np.zeros(S, np.uint64), "digest": np.zeros(S * 32, np.uint8),
             "pages": np.zeros(S * MP, np.int32), "fifo": np.zeros(self.num_pages, np.int32),
+            "pin": np.zeros(S, np.int32),
         }
         if with_tokens:
             arr["tokens"] = np.zeros(S * ML, np.int32)
@@ -290,7 +296,7 @@ class KVIndex:
         ptr = lambda k: arr[k].ctypes.data_as(C.c_void_p) if k in arr else None
         snap = L.CpSnapshot(0, 0, 0, 0, 0, ptr("id"), ptr("len"), ptr("origin_pos"), ptr("prefix_hash"),
                             ptr("full_hash"), ptr("last_used"), ptr("digest"), ptr("pages"), ptr("tokens"),
-                            ptr("recompute"), ptr("fifo"))
+                            ptr("recompute"), ptr("fifo"), ptr("pin"))
         L.check(L.lib().cp_index_snapshot(self.h, C.byref(snap), _stream(stream)), "cp_index_snapshot")
         n = snap.num_live
         out = dict(num_live=n, next_id=snap.next_id, live_tokens=snap.live_tokens, fifo_count=snap.fifo_count,
@@ -300,7 +306,7 @@ class KVIndex:
             e = dict(id=int(arr["id"][q]), len=ln, origin_pos=int(arr["origin_pos"][q]),
                      prefix_hash=int(arr["prefix_hash"][q]), full_hash=int(arr["full_hash"][q]),
                      last_used=int(arr["last_used"][q]), digest=arr["digest"][32 * q:32 * q + 32].tobytes(),
-                     pages=arr["pages"][q * MP:q * MP + (ln + 15) // 16].copy())
+                     pages=arr["pages"][q * MP:q * MP + (ln + 15) // 16].copy(), pin=int(arr["pin"][q]))
             if with_tokens:
                 e["tokens"] = arr["tokens"][q * ML:q * ML + ln].copy()
                 e["recompute"] = arr["recompute"][q * ML:q * ML + ln].astype(bool)

@@ -94,6 +94,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     put(2 * P);                                              // 13 page bits
     put(sizeof(HEntry) * L->T);                              // 14 htab
     put(8 * (size_t)(c->max_span_len + 1));                  // 15 pow table
+    put(4 * S);                                              // 16 slot pins (R#32)
+    put(4 * P);                                              // 17 page owner slot
     L->meta_size = o;
     // scratch
     L->HS = c->max_batch_tokens / c->window_len + c->max_batch_reqs + 1;
@@ -138,16 +140,18 @@ void compute_layout(const cp_config* c, Layout* L) {
 // kernels: initialisation
 // ------------------------------------------------------------------------------------------
 __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, int32_t* fifo, int32_t* slot_stack,
-                       HEntry* htab, int64_t P, int32_t S, int64_t T) {
+                       HEntry* htab, int64_t P, int32_t S, int64_t T, int32_t* slot_pin, int32_t* page_owner) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = tid; i < P; i += nt) fifo[i] = (int32_t)i;                 // FIFO: ascending page ids (R#22)
-    for (int64_t i = tid; i < S; i += nt) { slot_id[i] = -1; slot_state[i] = CP_SLOT_FREE; slot_stack[i] = S - 1 - (int32_t)i; }
+    for (int64_t i = tid; i < P; i += nt) { fifo[i] = (int32_t)i; page_owner[i] = -1; }   // FIFO: ascending (R#22)
+    for (int64_t i = tid; i < S; i += nt) {
+        slot_id[i] = -1; slot_state[i] = CP_SLOT_FREE; slot_stack[i] = S - 1 - (int32_t)i; slot_pin[i] = 0;
+    }
     for (int64_t i = tid; i < T; i += nt) { htab[i].key = CP_EMPTY_KEY; htab[i].full = 0; htab[i].slot = -1; htab[i].len = 0; }
     if (tid == 0) {
         hdr->error = 0; hdr->next_id = 0; hdr->num_live = 0; hdr->fifo_head = 0; hdr->fifo_count = (int32_t)P;
         hdr->slot_free_top = S; hdr->match_done = 0; hdr->table_used = 0; hdr->live_tokens = 0;
         hdr->first_err = CP_NO_ERR_KEY; hdr->rebuild = 0; hdr->n_cand = 0; hdr->n_copy = 0; hdr->n_removed = 0;
-        hdr->n_chunks = 0; hdr->n_new_live = 0; hdr->commits_parallel = 0; hdr->commits_serial = 0; hdr->commit_why = 0;
+        hdr->n_chunks = 0; hdr->n_new_live = 0; hdr->commits_parallel = 0; hdr->commits_serial = 0; hdr->commit_why = 0; hdr->pin_neg = 0;
         for (int i = 0; i < 4; ++i) hdr->match_work[i] = 0;
     }
 }
@@ -168,6 +172,7 @@ struct InsArgs {
     unsigned long long* slot_prefix; unsigned long long* slot_full; unsigned long long* slot_last;
     uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
     int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; int logT; int64_t T; const unsigned long long* pw;
+    const int32_t* slot_pin; int32_t* page_owner;     // R#32 pins, page -> owning slot
     // scratch
     unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed; int32_t* rm_pos;
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     int32_t* clen = (int32_t*)(smc + lay.clen);
     int2* srec = (int2*)(smc + lay.srec);
     __shared__ int s_abort, s_nrec;
-    __shared__ long long s_live_tokens, s_chunks;
+    __shared__ long long s_live_tokens, s_chunks, s_pinned_tok;
     __shared__ int s_fifo_head, s_fifo_count, s_next_id, s_free_top, s_num_live, s_nremoved;
     __shared__ int s_rm[kMaxSupersede];
     __shared__ unsigned long long s_red_key[kCommitThreads / 32];
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
 #endif
 
     if (tid == 0) {
-        s_abort = 0; s_chunks = 0;
+        s_abort = 0; s_chunks = 0; s_pinned_tok = 0;
         if (cp_err_set(a.hdr)) s_abort = 1;
         else if (a.hdr->first_err != CP_NO_ERR_KEY) {
             const unsigned code = (unsigned)(a.hdr->first_err & 0xffffffffu);
@@ -619,6 +624,13 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     // ---- load state
     for (int i = tid; i < a.nslots; i += blockDim.x) sflag[i] = a.slot_state[i] == CP_SLOT_LIVE ? 1 : 0;
+    {   // R#32: tokens of the live pinned entries (constant through the call: they can't be removed)
+        long long pt = 0;
+        for (int i = tid; i < a.nslots; i += blockDim.x)
+            if (a.slot_state[i] == CP_SLOT_LIVE && a.slot_pin[i] > 0) pt += a.slot_len[i];
+        for (int o = 16; o; o >>= 1) pt += __shfl_xor_sync(0xffffffffu, pt, o);
+        if ((tid & 31) == 0 && pt) atomicAdd((unsigned long long*)&s_pinned_tok, (unsigned long long)pt);
+    }
     for (int j = tid; j < a.S; j += blockDim.x) {
         snew[j] = -1; soff[j] = 0; srep[j] = a.span_rep[j]; seq[j] = -1; slen[j] = a.span_len[j]; sfpos[j] = -1;
     }
@@ -750,7 +762,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     if (a.candK > 0 && s_live_tokens + s_pending > a.capacity) {
         unsigned long long mn = ~0ULL, mx = 0;
         for (int sl = tid; sl < a.nslots; sl += blockDim.x)
-            if (sflag[sl] & 1) { const unsigned long long lu = a.slot_last[sl]; mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx; }
+            if ((sflag[sl] & 1) && a.slot_pin[sl] == 0) { const unsigned long long lu = a.slot_last[sl]; mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx; }
         for (int o = 16; o; o >>= 1) {
             const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, mn, o), b2 = __shfl_xor_sync(0xffffffffu, mx, o);
             mn = a2 < mn ? a2 : mn; mx = b2 > mx ? b2 : mx;
@@ -771,7 +783,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0;
                 __syncthreads();
                 for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
-                    if (!(sflag[sl] & 1)) continue;
+                    if (!(sflag[sl] & 1) || a.slot_pin[sl] > 0) continue;      // pinned: never evicted (R#32)
                     const unsigned long long k = keyof(sl);
                     if ((k & pmask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
                 }
@@ -791,7 +803,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             }
             const unsigned long long T = prefix;                   // K-th smallest (or the max if fewer live)
             for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
-                if (!(sflag[sl] & 1)) continue;
+                if (!(sflag[sl] & 1) || a.slot_pin[sl] > 0) continue;
                 const unsigned long long k = keyof(sl);
                 if (k <= T) { const int p = atomicAdd(&s_cn, 1); if (p < a.candK) { ckey[p] = k; cslot[p] = sl; clen[p] = a.slot_len[sl]; } }
             }
@@ -873,7 +885,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if (sfpos[j] < 0) continue;
             const int npg = (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
             int32_t* pl = a.slot_pages + (int64_t)snew[j] * a.MP;
-            for (int i = 0, pos = sfpos[j]; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
+            for (int i = 0, pos = sfpos[j]; i < npg; ++i, pos = wrap(pos + 1)) { pl[i] = fifo_at(pos); a.page_owner[pl[i]] = snew[j]; }
             sfpos[j] = -1;
         }
         s_defer = 0;
@@ -928,7 +940,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __shared__ long long s_s64[kCommitThreads / 32 + 1];
     __shared__ int s_why;                 // why the parallel apply was not taken (bit mask, diagnostics)
     const int Sn = a.S, NSl = a.nslots;
-    if (tid == 0) { s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0; }
+    if (tid == 0) {
+        s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0;
+        if (s_pinned_tok > 0) { s_fast = 0; s_why |= 1024; }      // pinned entries: the sequential rules (R#32)
+    }
     for (int i = tid; i < NSl; i += blockDim.x) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
     for (int j = tid; j < Sn; j += blockDim.x) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
     __syncthreads();
@@ -1162,6 +1177,15 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                                 if (sid < cont_id) { cont_id = sid; target = sx; }
                             }
                         kind = target >= 0 ? 1 : 2;
+                        if (kind == 2 && s_pinned_tok > 0) {      // R#32: it may not remove a pinned entry and
+                            int bid = 0x7fffffff;                 // must fit the budget beside the pinned tokens
+                            for (int q = b; q < e; ++q)
+                                if (rec[q].y == REL_CONTAINED && is_live(rec[q].x)) {
+                                    const int sx = resolve(rec[q].x);
+                                    if (a.slot_pin[sx] > 0 && a.slot_id[sx] < bid) { bid = a.slot_id[sx]; target = sx; }
+                                }
+                            if (target >= 0 || s_pinned_tok + slen[jj] > a.capacity) kind = 4;
+                        }
                     }
                 }
                 const unsigned need = __ballot_sync(0xffffffffu, kind == 2);
@@ -1173,6 +1197,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     a.out_tmp[jj] = target; a.out_oc[jj] = CP_DUPLICATE;
                 } else if (tid < f && kind == 1) {
                     a.out_tmp[jj] = target; a.out_oc[jj] = CP_DROPPED_CONTAINED;
+                } else if (tid < f && kind == 4) {
+                    a.out_tmp[jj] = target; a.out_oc[jj] = CP_DEFERRED_PINNED;
                 }
                 __syncwarp();
                 if (f == 32) { j += 32; continue; }
@@ -1204,7 +1230,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     if (s_defer) sfpos[js] = s_fifo_head;
                     else {
                         int32_t* pl = a.slot_pages + (int64_t)slot * a.MP;
-                        for (int i = 0, pos = s_fifo_head; i < npg; ++i, pos = wrap(pos + 1)) pl[i] = fifo_at(pos);
+                        for (int i = 0, pos = s_fifo_head; i < npg; ++i, pos = wrap(pos + 1)) { pl[i] = fifo_at(pos); a.page_owner[pl[i]] = slot; }
                     }
                     popped += npg;
                     s_fifo_head = wrap(s_fifo_head + npg); s_fifo_count -= npg;
@@ -1236,7 +1262,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         while (s_live_tokens > a.capacity) {
             unsigned long long best_last = ~0ULL; int best_id = 0x7fffffff, best_slot = -1;
             for (int sx = tid; sx < a.nslots; sx += blockDim.x) {
-                if (!(sflag[sx] & 1)) continue;
+                if (!(sflag[sx] & 1) || a.slot_pin[sx] > 0) continue;
                 const unsigned long long lu = a.slot_last[sx];
                 const int sid = a.slot_id[sx];
                 if (lu < best_last || (lu == best_last && sid < best_id)) { best_last = lu; best_id = sid; best_slot = sx; }
@@ -1255,7 +1281,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     if (s_red_slot[w] < 0) continue;
                     if (s_red_key[w] < bl || (s_red_key[w] == bl && s_wsum[w] < bi)) { bl = s_red_key[w]; bi = s_wsum[w]; bs = s_red_slot[w]; }
                 }
-                remove_serial(bs, a.slot_len[bs]);
+                if (bs >= 0) remove_serial(bs, a.slot_len[bs]);
+                else { cp_raise(a.hdr, CP_ERR_CAPACITY); s_live_tokens = 0; }   // unreachable: R#32 defers such stores
             }
             __syncthreads();
         }
@@ -1279,7 +1306,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if (sfpos[j] < 0) continue;
             const int npg = (slen[j] + CP_BLOCK - 1) / CP_BLOCK;
             int32_t* pl = a.slot_pages + (int64_t)snew[j] * a.MP;
-            for (int i = cl; i < npg; i += 32) pl[i] = a.fifo[wrap(sfpos[j] + i)];
+            for (int i = cl; i < npg; i += 32) { pl[i] = a.fifo[wrap(sfpos[j] + i)]; a.page_owner[pl[i]] = snew[j]; }
         }
     }
     __syncthreads();
@@ -1452,6 +1479,40 @@ __global__ void k_ins_publish(InsArgs a) {
 }
 
 // rebuild the prefix table when tombstones accumulate (live + tombstones > T/2)
+// ---- R#32 pins: validate every listed page (owned by a live entry), apply, undo if a count went negative
+__global__ void k_pin_check(DevHeader* hdr, const int32_t* pages, int64_t n, const int32_t* page_owner,
+                            const uint8_t* slot_state, const int32_t* slot_pages, int32_t MP, const int32_t* slot_len) {
+    if (cp_err_set(hdr)) return;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int p = pages[q];
+        if (p < 0) continue;
+        const int s = page_owner[p];
+        bool ok = s >= 0 && slot_state[s] == CP_SLOT_LIVE;
+        if (ok) {                                   // the page is in its owner's current page list
+            const int npg = (slot_len[s] + CP_BLOCK - 1) / CP_BLOCK;
+            bool in = false;
+            for (int i = 0; i < npg && !in; ++i) in = slot_pages[(int64_t)s * MP + i] == p;
+            ok = in;
+        }
+        if (!ok) cp_raise(hdr, CP_ERR_INVALID_ARG);
+    }
+}
+__global__ void k_pin_apply(DevHeader* hdr, const int32_t* pages, int64_t n, const int32_t* page_owner,
+                            int32_t* slot_pin, int32_t delta, int32_t undo) {
+    if (cp_err_set(hdr)) return;
+    if (undo && !hdr->pin_neg) return;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int p = pages[q];
+        if (p < 0) continue;
+        const int v = atomicAdd(&slot_pin[page_owner[p]], undo ? -delta : delta) + (undo ? -delta : delta);
+        if (!undo && v < 0) hdr->pin_neg = 1;
+    }
+}
+__global__ void k_pin_done(DevHeader* hdr) {
+    if (hdr->pin_neg && !cp_err_set(hdr)) cp_raise(hdr, CP_ERR_INVALID_ARG);   // after the undo
+    hdr->pin_neg = 0;
+}
+
 // SHA-256 digests of the published entries (thread per entry; launched on the index's side stream,
 // concurrently with the table rebuild and the copy-in, which do not read digests)
 __global__ void k_ins_digest(InsArgs a) {
@@ -1574,6 +1635,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->slot_stack = (int32_t*)(m + L.meta_off[11]); x->page_tokens = (int32_t*)(m + L.meta_off[12]);
     x->page_bits = (uint16_t*)(m + L.meta_off[13]); x->htab = (HEntry*)(m + L.meta_off[14]);
     x->pw = (unsigned long long*)(m + L.meta_off[15]);
+    x->slot_pin = (int32_t*)(m + L.meta_off[16]); x->page_owner = (int32_t*)(m + L.meta_off[17]);
     char* s = x->scratch;
     x->HS = L.HS; x->CH = L.CH; x->CS_HITS = L.CS_HITS; x->MS = L.MS; x->MAXC = L.MAXC; x->BT = L.BT; x->logBT = L.logBT;
     x->sp_entry = (int32_t*)(s + L.scr_off[0]); x->sp_slot = (int32_t*)(s + L.scr_off[1]);
@@ -1602,7 +1664,8 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     for (size_t k = 1; k < pw.size(); ++k) pw[k] = host_mulmod(pw[k - 1], x->B);
     x->Bw = pw[(size_t)cfg->window_len];
     if (cudaMemcpyAsync(x->pw, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
-    k_init<<<592, 256, 0, st>>>(x->hdr, x->slot_id, x->slot_state, x->fifo, x->slot_stack, x->htab, x->P, x->S, x->T);
+    k_init<<<592, 256, 0, st>>>(x->hdr, x->slot_id, x->slot_state, x->fifo, x->slot_stack, x->htab, x->P, x->S, x->T,
+                                x->slot_pin, x->page_owner);
     CP_COUNT_LAUNCH();
     if (cudaGetLastError() != cudaSuccess) { delete x; return CP_ERR_CUDA; }
     if (cudaStreamSynchronize(st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
@@ -1653,6 +1716,22 @@ cp_status cp_index_destroy(cp_index* x) {
 }
 
 uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
+
+cp_status cp_pin_links(cp_index* x, const int32_t* pages, int64_t n, int32_t delta, void* stream) {
+    if (!x || (n > 0 && !pages) || n < 0 || (delta != 1 && delta != -1)) return CP_ERR_INVALID_ARG;
+    if (n == 0) return CP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, cp_sm_count() * 4);
+    k_pin_check<<<grid, 256, 0, st>>>(x->hdr, pages, n, x->page_owner, x->slot_state, x->slot_pages, x->MP, x->slot_len);
+    CP_COUNT_LAUNCH();
+    k_pin_apply<<<grid, 256, 0, st>>>(x->hdr, pages, n, x->page_owner, x->slot_pin, delta, 0);
+    CP_COUNT_LAUNCH();
+    k_pin_apply<<<grid, 256, 0, st>>>(x->hdr, pages, n, x->page_owner, x->slot_pin, delta, 1);   // undo if negative
+    CP_COUNT_LAUNCH();
+    k_pin_done<<<1, 1, 0, st>>>(x->hdr);
+    CP_COUNT_LAUNCH();
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
+}
 
 cp_status cp_index_match_work(cp_index* x, uint64_t* out_h, int32_t reset, void* stream) {
     if (!x || !out_h) return CP_ERR_INVALID_ARG;
@@ -1751,6 +1830,11 @@ cp_status cp_index_snapshot(cp_index* x, cp_snapshot* o, void* stream) {
             if (o->recompute) o->recompute[(size_t)q * ML + t] = (pbits[page] >> (t % CP_BLOCK)) & 1;
         }
     }
+    if (o->pin) {
+        std::vector<int32_t> pins((size_t)S);
+        CP_CUDA_CHECK(cudaMemcpy(pins.data(), x->slot_pin, 4 * (size_t)S, cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < order.size(); ++q) o->pin[q] = pins[(size_t)order[q]];
+    }
     if (o->fifo) {
         std::vector<int32_t> f((size_t)x->P);
         CP_CUDA_CHECK(cudaMemcpy(f.data(), x->fifo, 4 * f.size(), cudaMemcpyDeviceToHost));
@@ -1799,7 +1883,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
     a.slot_prefix = x->slot_prefix; a.slot_full = x->slot_full; a.slot_last = x->slot_last;
     a.slot_digest = x->slot_digest; a.slot_pages = x->slot_pages; a.fifo = x->fifo; a.slot_stack = x->slot_stack;
     a.page_tokens = x->page_tokens; a.page_bits = x->page_bits; a.htab = x->htab; a.logT = x->logT; a.T = x->T;
-    a.pw = x->pw;
+    a.pw = x->pw; a.slot_pin = x->slot_pin; a.page_owner = x->page_owner;
     a.span_pre = x->span_pre; a.span_full = x->span_full; a.btab = x->btab; a.logBT = x->logBT; a.BT = x->BT;
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;

@@ -60,7 +60,8 @@ struct DevHeader {                   // first 256 B of META
     int32_t commit_why;              // OR of the reasons the sequential path was taken (k_ins_commit bits)
     int32_t n_unc;                   // gather: uncovered positions listed for CP_ZERO_UNCOVERED
     unsigned long long match_work[4];   // matcher work counters (cp_index_match_work)
-    int32_t pad[30];
+    int32_t pin_neg;                 // cp_pin_links: a count went negative (undone)
+    int32_t pad[29];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 
@@ -115,6 +116,7 @@ struct cp_index {
     unsigned long long* slot_prefix; unsigned long long* slot_full; unsigned long long* slot_last;
     uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
     int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; unsigned long long* pw;
+    int32_t* slot_pin; int32_t* page_owner;          // R#32: linked-page pins per slot, owning slot per page
     // SCRATCH (match)
     int64_t HS;          // sparse hit capacity
     int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;

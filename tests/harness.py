@@ -235,7 +235,7 @@ class Case:
         if not np.array_equal(snap["fifo"], self.orc.fifo()):
             rep.fail(f"{where}: free-page FIFO differs")
         for de, oe in zip(snap["entries"], live):
-            for k in ("id", "len", "origin_pos", "prefix_hash", "full_hash", "last_used", "digest"):
+            for k in ("id", "len", "origin_pos", "prefix_hash", "full_hash", "last_used", "digest", "pin"):
                 if de[k] != oe[k]:
                     rep.fail(f"{where}: entry {oe['id']} field {k}: {de[k]!r} != {oe[k]!r}")
             if not np.array_equal(de["pages"], oe["pages"]):

@@ -150,6 +150,7 @@ void orc_sha256_tokens(const int32_t* t, int64_t m, uint8_t out[32]) {
 typedef struct {
     int32_t id, live, len, origin_pos, origin_call, origin_req;
     int32_t pin;          /* linked-block pins on its pages (R#32) */
+    int32_t owner;        /* 0: shared (cross-user) entry; s >= 1: the private entry of session s (R#33) */
     uint64_t prefix_hash, full_hash, last_used;
     uint8_t digest[32];
     int32_t* tokens;      /* [len] */
@@ -260,7 +261,7 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         /* Duplicate (R#20: checked first) */
         int32_t dup = -1;
         for (int32_t i = 0; i < x->n_e; ++i)
-            if (x->e[i].live && memcmp(x->e[i].digest, dg, 32) == 0) { dup = i; break; }
+            if (x->e[i].live && !x->e[i].owner && memcmp(x->e[i].digest, dg, 32) == 0) { dup = i; break; }
         if (dup >= 0) {
             x->e[dup].last_used = t;
             out_id[s] = dup; out_outcome[s] = ORC_DUPLICATE;
@@ -269,7 +270,7 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         /* strictly contained in a live entry */
         int32_t cont = -1;
         for (int32_t i = 0; i < x->n_e && cont < 0; ++i)
-            if (x->e[i].live && x->e[i].len > m && contains(x->e[i].tokens, x->e[i].len, tau, m)) cont = i;
+            if (x->e[i].live && !x->e[i].owner && x->e[i].len > m && contains(x->e[i].tokens, x->e[i].len, tau, m)) cont = i;
         if (cont >= 0) { out_id[s] = cont; out_outcome[s] = ORC_DROPPED_CONTAINED; continue; }
         /* R#32 (NEXT-2 lifetime of linked pages): a span may not remove a pinned entry, and the pinned
            tokens plus the span must fit the budget (so that the LRU can always get back under it by
@@ -279,7 +280,7 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         for (int32_t i = 0; i < x->n_e; ++i) {
             if (!x->e[i].live || x->e[i].pin == 0) continue;
             pinned_tok += x->e[i].len;
-            if (blocked < 0 && x->e[i].len < m && contains(tau, m, x->e[i].tokens, x->e[i].len)) blocked = i;
+            if (blocked < 0 && !x->e[i].owner && x->e[i].len < m && contains(tau, m, x->e[i].tokens, x->e[i].len)) blocked = i;
         }
         if (blocked >= 0 || pinned_tok + m > x->capacity) {
             out_id[s] = blocked; out_outcome[s] = ORC_DEFERRED_PINNED;
@@ -288,7 +289,7 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
         /* supersede live entries strictly contained in tau, ascending id */
         int32_t superseded = 0;
         for (int32_t i = 0; i < x->n_e; ++i)
-            if (x->e[i].live && x->e[i].len < m && contains(tau, m, x->e[i].tokens, x->e[i].len)) {
+            if (x->e[i].live && !x->e[i].owner && x->e[i].len < m && contains(tau, m, x->e[i].tokens, x->e[i].len)) {
                 remove_entry(x, &x->e[i]);
                 superseded = 1;
             }
@@ -329,6 +330,71 @@ int32_t orc_index_insert(orc_index* x, const int32_t* tokens, const int64_t* off
     return ORC_OK;
 }
 
+/*
+ * Same-user sessions (R#33, "SameUserFull is modeled as exact-prefix reuse of
+ * the user's own last request").  For each request in order: its session's current private entry is
+ * replaced by the whole request [0, n) -- sensitive tokens included, no recompute marks -- stored at
+ * origin 0 with pages from the FIFO head (the old entry's pages go to the FIFO tail first), then LRU
+ * eviction as for shared entries (one budget; victims = min (last_used, id) among unpinned live entries of
+ * any owner).  A pinned old entry, or pinned tokens + n over the budget, defers the request (R#32).
+ * Private entries take part in no dedup / containment with shared ones; their prefix / full hashes are 0
+ * (they are found through the session, never through the prefix filter).
+ */
+int32_t orc_index_insert_session(orc_index* x, const int32_t* tokens, const int64_t* offsets, int32_t num_reqs,
+                                 const int32_t* sessions, uint64_t t, int32_t* out_id, int32_t* out_outcome) {
+    for (int32_t r = 0; r < num_reqs; ++r) {
+        const int64_t n = offsets[r + 1] - offsets[r];
+        if (sessions[r] < 1 || n < 1) return ORC_ERR_INVALID_ARG;
+        if (n > x->capacity) return ORC_ERR_CAPACITY;
+    }
+    int32_t call = x->calls++;
+    for (int32_t r = 0; r < num_reqs; ++r) {
+        const int32_t* tau = tokens + offsets[r];
+        const int32_t m = (int32_t)(offsets[r + 1] - offsets[r]);
+        int32_t old = -1;
+        int64_t pinned_tok = 0;
+        for (int32_t i = 0; i < x->n_e; ++i) {
+            if (!x->e[i].live) continue;
+            if (x->e[i].owner == sessions[r]) old = i;
+            if (x->e[i].pin > 0) pinned_tok += x->e[i].len;
+        }
+        if ((old >= 0 && x->e[old].pin > 0) || pinned_tok + m > x->capacity) {
+            out_id[r] = (old >= 0 && x->e[old].pin > 0) ? old : -1; out_outcome[r] = ORC_DEFERRED_PINNED;
+            continue;
+        }
+        if (old >= 0) remove_entry(x, &x->e[old]);
+        if (x->n_e == x->cap_e) {
+            x->cap_e *= 2;
+            x->e = (orc_entry*)realloc(x->e, sizeof(orc_entry) * (size_t)x->cap_e);
+        }
+        int32_t id = x->n_e++;
+        orc_entry* e = &x->e[id];
+        memset(e, 0, sizeof(*e));
+        e->id = id; e->live = 1; e->len = m; e->origin_pos = 0; e->origin_call = call; e->origin_req = r;
+        e->owner = sessions[r];
+        orc_sha256_tokens(tau, m, e->digest);
+        e->last_used = t;
+        e->tokens = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+        memcpy(e->tokens, tau, sizeof(int32_t) * (size_t)m);
+        e->recompute = (uint8_t*)calloc((size_t)m, 1);
+        e->npages = (m + x->block - 1) / x->block;
+        e->pages = (int32_t*)malloc(sizeof(int32_t) * (size_t)e->npages);
+        if (x->fifo_count < e->npages) return ORC_ERR_CAPACITY;
+        for (int32_t i = 0; i < e->npages; ++i) e->pages[i] = fifo_pop(x);
+        x->live_tokens += m;
+        out_id[r] = id; out_outcome[r] = ORC_STORED;
+        while (x->live_tokens > x->capacity) {
+            int32_t v = -1;
+            for (int32_t i = 0; i < x->n_e; ++i) {
+                if (!x->e[i].live || x->e[i].pin > 0) continue;
+                if (v < 0 || x->e[i].last_used < x->e[v].last_used) v = i;
+            }
+            remove_entry(x, &x->e[v]);
+        }
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* match (P:L663-704 C2; P:L724-727 plan with zero placeholders)              */
 /* ------------------------------------------------------------------------- */
@@ -356,12 +422,13 @@ static int cand_cmp(const void* a, const void* b) {       /* (k asc, m desc, id 
 #define ORC_MATCH_PREFIX_ONLY 4
 
 int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, const uint8_t* mask,
-                  int32_t num_reqs, uint64_t t, int32_t flags, int32_t max_hits,
+                  const int32_t* sessions, int32_t num_reqs, uint64_t t, int32_t flags, int32_t max_hits,
                   int32_t* req_hit_offsets, int32_t* hit_req, int32_t* hit_entry, int32_t* hit_dst,
                   int32_t* hit_len, int32_t* hit_delta, uint8_t* plan,
                   int32_t* req_covered, int32_t* req_recompute, int32_t* req_candidates) {
     const int fixed = (flags & ORC_MATCH_FIXED_CHUNK) != 0, prefix = (flags & ORC_MATCH_PREFIX_ONLY) != 0;
     if (fixed && prefix) return -2;
+    if (sessions && (fixed || prefix)) return -2;
     int32_t nh = 0;
     req_hit_offsets[0] = 0;
     for (int32_t r = 0; r < num_reqs; ++r) {
@@ -378,7 +445,7 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
             int32_t best = -1, bl = 0;
             for (int32_t i = 0; n >= x->w && i < x->n_e; ++i) {
                 orc_entry* e = &x->e[i];
-                if (!e->live) continue;
+                if (!e->live || e->owner) continue;
                 int64_t j = 0;
                 while (j < x->w && q[j] == e->tokens[j]) ++j;
                 if (j < x->w) continue;
@@ -400,13 +467,33 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
             req_covered[r] = cov; req_recompute[r] = rec; req_candidates[r] = cands;
             continue;
         }
+        /* same-user session reuse ("all KV cache can be reused without restriction", R#33): the
+           longest common prefix with the session's last request (its private entry), sensitive tokens
+           included, is one hit at 0 if >= w tokens; cross-user hits then start after it */
+        int64_t cursor = 0;
+        if (sessions && sessions[r] >= 1) {
+            for (int32_t i = 0; i < x->n_e; ++i) {
+                orc_entry* e = &x->e[i];
+                if (!e->live || e->owner != sessions[r]) continue;
+                int32_t l = 0;
+                while (l < e->len && l < n && q[l] == e->tokens[l]) ++l;
+                if (l >= x->w) {
+                    if (nh >= max_hits) return -1;
+                    hit_req[nh] = r; hit_entry[nh] = e->id; hit_dst[nh] = 0; hit_len[nh] = l; hit_delta[nh] = 0;
+                    nh++;
+                    for (int32_t z = 0; z < l; ++z) { pl[z] = 1; cov++; }
+                    cursor = l;
+                }
+                break;
+            }
+        }
         int64_t nc = 0, cap = 16;
         orc_cand* V = (orc_cand*)malloc(sizeof(orc_cand) * (size_t)cap);
         /* FixedChunk (Fig. 4-b): only chunk-aligned windows, only length-w entries (R#28) */
         for (int64_t k = 0; k + x->w <= n; k += fixed ? x->w : 1) {
             for (int32_t i = 0; i < x->n_e; ++i) {
                 orc_entry* e = &x->e[i];
-                if (!e->live) continue;
+                if (!e->live || e->owner) continue;              /* private entries: their session only */
                 int64_t j = 0;
                 while (j < x->w && q[k + j] == e->tokens[j]) ++j;
                 if (j < x->w) continue;
@@ -425,7 +512,6 @@ int32_t orc_match(orc_index* x, const int32_t* tokens, const int64_t* offsets, c
             }
         }
         qsort(V, (size_t)nc, sizeof(orc_cand), cand_cmp);
-        int64_t cursor = 0;
         for (int64_t c = 0; c < nc; ++c) {
             if (V[c].k < cursor) continue;
             if (nh >= max_hits) { free(V); return -1; }
@@ -465,7 +551,7 @@ int32_t orc_entry_get(const orc_index* x, int32_t id, int32_t* info, uint64_t* h
     if (id < 0 || id >= x->n_e) return ORC_ERR_INVALID_ARG;
     const orc_entry* e = &x->e[id];
     info[0] = e->live; info[1] = e->len; info[2] = e->origin_pos; info[3] = e->origin_call;
-    info[4] = e->origin_req; info[5] = e->npages; info[6] = e->pin;
+    info[4] = e->origin_req; info[5] = e->npages; info[6] = e->pin; info[7] = e->owner;
     hashes[0] = e->prefix_hash; hashes[1] = e->full_hash; hashes[2] = e->last_used;
     if (digest) memcpy(digest, e->digest, 32);
     if (pages) memcpy(pages, e->pages, sizeof(int32_t) * (size_t)e->npages);

@@ -52,7 +52,8 @@ def lib():
             "orc_index_free": (None, [vp]),
             "orc_index_base": (u64, [vp]),
             "orc_index_insert": (i32, [vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, u64, vp, vp]),
-            "orc_match": (i32, [vp, vp, vp, vp, i32, u64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "orc_match": (i32, [vp, vp, vp, vp, vp, i32, u64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "orc_index_insert_session": (i32, [vp, vp, vp, i32, vp, u64, vp, vp]),
             "orc_num_ids": (i32, [vp]),
             "orc_live_tokens": (i64, [vp]),
             "orc_fifo_count": (i32, [vp]),
@@ -281,8 +282,18 @@ class OracleIndex:
                                     _p(sr), _p(sb), _p(sl), _p(bw), _p(bo), t, _p(out_id), _p(out_oc))
         return rc, out_id[:S], out_oc[:S]
 
+    def insert_session(self, batch, sessions, t: int = 0):
+        """R#33: each request replaces its session's private entry (whole request, sensitive tokens too)."""
+        tok, off = _c(batch.tokens, np.int32), _c(batch.offsets, np.int64)
+        ss = _c(np.asarray(sessions), np.int32)
+        R = batch.num_reqs
+        out_id = np.full(max(R, 1), -1, np.int32)
+        out_oc = np.full(max(R, 1), -1, np.int32)
+        rc = lib().orc_index_insert_session(self.h, _p(tok), _p(off), R, _p(ss), t, _p(out_id), _p(out_oc))
+        return rc, out_id[:R], out_oc[:R]
+
     def match(self, batch, t: int = 0, no_touch: bool = False, use_mask: bool = True,
-              max_hits: Optional[int] = None, policy: Optional[str] = None) -> MatchResult:
+              max_hits: Optional[int] = None, policy: Optional[str] = None, sessions=None) -> MatchResult:
         """policy None: CrossUserSelective (the method); "fixed_chunk" / "prefix_only": NEXT-3
         baselines (R#28-29)."""
         R, T = batch.num_reqs, batch.total_tokens
@@ -295,7 +306,8 @@ class OracleIndex:
         plan = o(T, np.uint8)
         cov, rec, cand = o(R), o(R), o(R)
         flags = int(no_touch) | {None: 0, "fixed_chunk": 2, "prefix_only": 4}[policy]
-        nh = lib().orc_match(self.h, _p(tok), _p(off), _p(msk), R, t, flags, mh, _p(rho),
+        ss = None if sessions is None else _c(np.asarray(sessions), np.int32)
+        nh = lib().orc_match(self.h, _p(tok), _p(off), _p(msk), _p(ss), R, t, flags, mh, _p(rho),
                              _p(hr), _p(he), _p(hd), _p(hl), _p(hdl), _p(plan), _p(cov), _p(rec), _p(cand))
         if nh < 0:
             raise RuntimeError("oracle match: hit buffer overflow")
@@ -351,7 +363,7 @@ class OracleIndex:
         return dict(id=eid, live=bool(info[0]), len=ln, origin_pos=int(info[2]), origin_call=int(info[3]),
                     origin_req=int(info[4]), prefix_hash=int(hs[0]), full_hash=int(hs[1]),
                     last_used=int(hs[2]), digest=dg.tobytes(), pages=pages[:npg].copy(),
-                    tokens=toks[:ln].copy(), recompute=rec[:ln].astype(bool), pin=int(info[6]))
+                    tokens=toks[:ln].copy(), recompute=rec[:ln].astype(bool), pin=int(info[6]), owner=int(info[7]))
 
     def live_entries(self):
         return [e for e in (self.entry(i) for i in range(self.num_ids)) if e["live"]]

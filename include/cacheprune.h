@@ -86,6 +86,7 @@ typedef struct {
     int32_t  max_batch_reqs;        /* most requests per match / insert call                             */
     int64_t  max_batch_tokens;      /* most tokens per match / insert call                               */
     int32_t  max_spans_per_insert;  /* most spans per insert call                                        */
+    int32_t  max_sessions;          /* same-user sessions 1..max_sessions (R#33); 0 = no session store      */
 } cp_config;
 
 enum { CP_WS_POOL_K = 0, CP_WS_POOL_V = 1, CP_WS_META = 2, CP_WS_SCRATCH = 3, CP_WS_COUNT = 4 };
@@ -112,6 +113,8 @@ typedef struct {
     const int64_t* offsets;         /* [num_reqs + 1], offsets[0] = 0                                 */
     const uint8_t* mask;            /* [total_tokens] 1 = sensitive; NULL allowed for match (R#9)    */
     int32_t        max_req_len;     /* host hint: longest request in the batch (0 = cfg max)         */
+    const int32_t* session;         /* [num_reqs] same-user session of each request (R#33), or NULL:
+                                       1..max_sessions = that user's session, 0 = anonymous          */
 } cp_batch;
 
 /* A paged KV cache in vLLM NHD layout: per layer a K and a V tensor [num_blocks][16][H][d]. */
@@ -199,6 +202,30 @@ cp_status cp_index_insert_commit(cp_index* idx, const cp_batch* writers_h, const
                                  const int32_t* span_len, const uint32_t* recompute_bits,
                                  const int64_t* bits_word_offsets, uint64_t logical_time,
                                  int32_t* out_entry_id, int32_t* out_outcome, void* stream);
+
+/*
+ * Same-user session reuse (NEXT-2; "If the request belongs to the same user session,
+ * all KV cache can be reused without restriction.  If the request originates from a different user, it
+ * applies the selective cross-user sharing policy"; R#33: exact-prefix reuse of
+ * the user's own last request).  Needs cfg.max_sessions >= 1 and writers_h->session.  For each request r
+ * in input order, session s = writers_h->session[r] in 1..max_sessions: the session's private entry is
+ * replaced by the WHOLE request [0, n_r) -- sensitive tokens included, no recompute marks -- stored at
+ * origin 0 on pages from the FIFO head (the old entry's pages go to the FIFO tail first), with its K/V
+ * rows copied from writer_kv_h; then LRU eviction as for shared entries (one budget; victims = min
+ * (last_used, id) among unpinned live entries of any owner).  A pinned old entry, or pinned tokens + n_r
+ * over the budget, gives CP_DEFERRED_PINNED (R#32).  Private entries are never in the prefix filter:
+ * they take part in no dedup / containment with shared entries and are invisible to cp_match_spans
+ * except for requests of their own session.  out_entry_id / out_outcome: device int32 [num_reqs]
+ * (CP_STORED or CP_DEFERRED_PINNED).  Device errors (nothing changes; the first failing request decides):
+ * a session out of range, an empty request, a block table too narrow -> CP_ERR_INVALID_ARG; a request
+ * longer than the budget or max_span_len, more requests than free entry slots -> CP_ERR_CAPACITY.
+ * Matching: cp_match_spans with readers_h->session set gives each request of session s >= 1 the longest
+ * common prefix with s's private entry as its first hit (dst 0, delta 0, hit_len = that prefix) when it
+ * is >= window_len tokens, no reader-mask test (the user's own tokens), and cross-user hits only after
+ * it; session 0 = anonymous.  Only without CP_MATCH_FIXED_CHUNK / CP_MATCH_PREFIX_ONLY.
+ */
+cp_status cp_index_insert_session(cp_index* idx, const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
+                                  uint64_t logical_time, int32_t* out_entry_id, int32_t* out_outcome, void* stream);
 
 /* Outputs of cp_match_spans (all device buffers owned by the caller). */
 typedef struct {
@@ -406,6 +433,7 @@ typedef struct {
     uint8_t*  recompute;            /* [max_span_len] per entry, optional */
     int32_t*  fifo;                 /* free pages in pop order, optional */
     int32_t*  pin;                  /* per entry: linked-block pins (R#32), optional */
+    int32_t*  owner;                /* per entry: 0 shared, s = private entry of session s (R#33), optional */
 } cp_snapshot;
 cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
 

@@ -32,12 +32,12 @@ class CpConfig(C.Structure):
                 ("layer_offset", i32), ("head_offset", i32), ("dtype", i32), ("rope_style", i32),
                 ("rope_theta", C.c_double), ("pool_capacity_tokens", i64), ("max_entries", i32),
                 ("max_span_len", i32), ("max_req_tokens", i32), ("max_batch_reqs", i32),
-                ("max_batch_tokens", i64), ("max_spans_per_insert", i32)]
+                ("max_batch_tokens", i64), ("max_spans_per_insert", i32), ("max_sessions", i32)]
 
 
 class CpBatch(C.Structure):
     _fields_ = [("num_reqs", i32), ("total_tokens", i64), ("tokens", vp), ("offsets", vp), ("mask", vp),
-                ("max_req_len", i32)]
+                ("max_req_len", i32), ("session", vp)]
 
 
 class CpPagedKV(C.Structure):
@@ -55,7 +55,7 @@ class CpSnapshot(C.Structure):
     _fields_ = [("num_live", i32), ("next_id", i32), ("live_tokens", i64), ("fifo_count", i32), ("error", i32),
                 ("id", vp), ("len", vp), ("origin_pos", vp), ("prefix_hash", vp), ("full_hash", vp),
                 ("last_used", vp), ("digest", vp), ("pages", vp), ("tokens", vp), ("recompute", vp), ("fifo", vp),
-                ("pin", vp)]
+                ("pin", vp), ("owner", vp)]
 
 
 EXPORTS = {
@@ -80,6 +80,7 @@ EXPORTS = {
                                     i32, i32, i32, vp, P_i64, vp, P_i64, vp]),
     "cp_link_blocks": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), vp, i32, vp]),
     "cp_pin_links": (i32, [vp, vp, i64, i32, vp]),
+    "cp_index_insert_session": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), u64, vp, vp, vp]),
     "cp_hash_prefix": (i32, [C.POINTER(CpBatch), u64, vp, vp]),
     "cp_policy_spans": (i32, [C.POINTER(CpBatch), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "cp_index_snapshot": (i32, [vp, C.POINTER(CpSnapshot), vp]),

@@ -63,6 +63,7 @@ class IndexConfig:
     max_spans_per_insert: int = 4096
     layer_offset: int = 0
     head_offset: int = 0
+    max_sessions: int = 0                 # same-user session store (R#33); 0 = off
 
     def c(self) -> L.CpConfig:
         return L.CpConfig(self.window_len, self.block_size, self.hash_seed, self.num_layers, self.num_kv_heads,
@@ -70,7 +71,8 @@ class IndexConfig:
                           L.CP_BF16 if self.dtype == "bf16" else L.CP_FP32,
                           L.CP_ROPE_GPTJ if self.rope_style == "gptj" else L.CP_ROPE_NEOX,
                           float(self.rope_theta), self.pool_capacity_tokens, self.max_entries, self.max_span_len,
-                          self.max_req_tokens, self.max_batch_reqs, self.max_batch_tokens, self.max_spans_per_insert)
+                          self.max_req_tokens, self.max_batch_reqs, self.max_batch_tokens, self.max_spans_per_insert,
+                          self.max_sessions)
 
     @property
     def torch_dtype(self):
@@ -83,6 +85,7 @@ class DeviceBatch:
     offsets: torch.Tensor                 # int64 [R+1]
     mask: Optional[torch.Tensor]          # uint8 [T] or None
     max_req_len: int = 0
+    session: Optional[torch.Tensor] = None   # int32 [R]: same-user session per request (R#33), or None
 
     @property
     def num_reqs(self) -> int:
@@ -94,17 +97,19 @@ class DeviceBatch:
 
     def c(self, with_mask: bool = True) -> L.CpBatch:
         return L.CpBatch(self.num_reqs, self.total_tokens, _ptr(self.tokens), _ptr(self.offsets),
-                         _ptr(self.mask) if (with_mask and self.mask is not None) else None, int(self.max_req_len))
+                         _ptr(self.mask) if (with_mask and self.mask is not None) else None, int(self.max_req_len),
+                         _ptr(self.session))
 
     @staticmethod
-    def from_numpy(tokens, offsets, mask, device="cuda", pin: bool = False) -> "DeviceBatch":
+    def from_numpy(tokens, offsets, mask, device="cuda", pin: bool = False, session=None) -> "DeviceBatch":
         import numpy as np
         lens = np.diff(offsets)
         t = torch.from_numpy(np.ascontiguousarray(tokens, dtype=np.int32))
         o = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
         m = None if mask is None else torch.from_numpy(np.ascontiguousarray(mask, dtype=np.uint8))
+        ss = None if session is None else torch.from_numpy(np.ascontiguousarray(session, dtype=np.int32)).to(device)
         return DeviceBatch(t.to(device), o.to(device), None if m is None else m.to(device),
-                           int(lens.max()) if len(lens) else 0)
+                           int(lens.max()) if len(lens) else 0, ss)
 
 
 @dataclass
@@ -221,6 +226,17 @@ class KVIndex:
         L.check(rc, fn)
         return out_id[:S], out_oc[:S]
 
+    def insert_session(self, writers: DeviceBatch, writer_kv: PagedKV, t: int = 0, out=None, stream=None):
+        """cp_index_insert_session (R#33): each request replaces its session's private entry.  `writers.session`
+        (int32 [R], values 1..max_sessions) is required.  Returns (out_id, out_outcome) device tensors."""
+        R = writers.num_reqs
+        if out is None:
+            out = tuple(torch.full((max(R, 1),), -1, dtype=torch.int32, device=self.device) for _ in range(2))
+        wb, kv = writers.c(), writer_kv.c()
+        L.check(L.lib().cp_index_insert_session(self.h, C.byref(wb), C.byref(kv), int(t), _ptr(out[0]), _ptr(out[1]),
+                                                _stream(stream)), "cp_index_insert_session")
+        return out[0][:R], out[1][:R]
+
     def match_spans(self, readers: DeviceBatch, t: int = 0, no_touch: bool = False, use_mask: bool = True,
                     hits: Optional[Hits] = None, stream=None, policy: Optional[str] = None) -> Hits:
         """policy None: the method (cross-user selective); "fixed_chunk" / "prefix_only": the NEXT-3
@@ -288,7 +304,7 @@ class KVIndex:
             "prefix_hash": np.zeros(S, np.uint64), "full_hash": np.zeros(S, np.uint64),
             "last_used": np.zeros(S, np.uint64), "digest": np.zeros(S * 32, np.uint8),
             "pages": np.zeros(S * MP, np.int32), "fifo": np.zeros(self.num_pages, np.int32),
-            "pin": np.zeros(S, np.int32),
+            "pin": np.zeros(S, np.int32), "owner": np.zeros(S, np.int32),
         }
         if with_tokens:
             arr["tokens"] = np.zeros(S * ML, np.int32)
@@ -296,7 +312,7 @@ class KVIndex:
         ptr = lambda k: arr[k].ctypes.data_as(C.c_void_p) if k in arr else None
         snap = L.CpSnapshot(0, 0, 0, 0, 0, ptr("id"), ptr("len"), ptr("origin_pos"), ptr("prefix_hash"),
                             ptr("full_hash"), ptr("last_used"), ptr("digest"), ptr("pages"), ptr("tokens"),
-                            ptr("recompute"), ptr("fifo"), ptr("pin"))
+                            ptr("recompute"), ptr("fifo"), ptr("pin"), ptr("owner"))
         L.check(L.lib().cp_index_snapshot(self.h, C.byref(snap), _stream(stream)), "cp_index_snapshot")
         n = snap.num_live
         out = dict(num_live=n, next_id=snap.next_id, live_tokens=snap.live_tokens, fifo_count=snap.fifo_count,
@@ -306,7 +322,8 @@ class KVIndex:
             e = dict(id=int(arr["id"][q]), len=ln, origin_pos=int(arr["origin_pos"][q]),
                      prefix_hash=int(arr["prefix_hash"][q]), full_hash=int(arr["full_hash"][q]),
                      last_used=int(arr["last_used"][q]), digest=arr["digest"][32 * q:32 * q + 32].tobytes(),
-                     pages=arr["pages"][q * MP:q * MP + (ln + 15) // 16].copy(), pin=int(arr["pin"][q]))
+                     pages=arr["pages"][q * MP:q * MP + (ln + 15) // 16].copy(), pin=int(arr["pin"][q]),
+                     owner=int(arr["owner"][q]))
             if with_tokens:
                 e["tokens"] = arr["tokens"][q * ML:q * ML + ln].copy()
                 e["recompute"] = arr["recompute"][q * ML:q * ML + ln].astype(bool)

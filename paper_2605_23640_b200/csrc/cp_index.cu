@@ -69,6 +69,7 @@ bool valid_cfg(const cp_config* c) {
     // long requests keep the matcher arrays in 24 B/token of scratch: 20 n + 12 (n/w + 1) + 8 fits only for w >= 3
     if (c->max_req_tokens > CP_MATCH_SMEM_TOKENS && c->window_len < 3) return false;
     if (c->max_batch_reqs < 1 || c->max_batch_tokens < 1 || c->max_spans_per_insert < 1) return false;
+    if (c->max_sessions < 0 || c->max_sessions > (1 << 20)) return false;
     if (c->max_spans_per_insert > 16384) return false;
     if (!(c->rope_theta > 0)) return false;
     return true;
@@ -96,6 +97,8 @@ void compute_layout(const cp_config* c, Layout* L) {
     put(8 * (size_t)(c->max_span_len + 1));                  // 15 pow table
     put(4 * S);                                              // 16 slot pins (R#32)
     put(4 * P);                                              // 17 page owner slot
+    put(4 * S);                                              // 18 slot owner: 0 shared, s session (R#33)
+    put(4 * ((size_t)c->max_sessions + 1));                  // 19 session -> its private slot
     L->meta_size = o;
     // scratch
     L->HS = c->max_batch_tokens / c->window_len + c->max_batch_reqs + 1;
@@ -140,12 +143,15 @@ void compute_layout(const cp_config* c, Layout* L) {
 // kernels: initialisation
 // ------------------------------------------------------------------------------------------
 __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, int32_t* fifo, int32_t* slot_stack,
-                       HEntry* htab, int64_t P, int32_t S, int64_t T, int32_t* slot_pin, int32_t* page_owner) {
+                       HEntry* htab, int64_t P, int32_t S, int64_t T, int32_t* slot_pin, int32_t* page_owner,
+                       int32_t* slot_owner, int32_t* session_slot, int32_t nsess) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < P; i += nt) { fifo[i] = (int32_t)i; page_owner[i] = -1; }   // FIFO: ascending (R#22)
     for (int64_t i = tid; i < S; i += nt) {
         slot_id[i] = -1; slot_state[i] = CP_SLOT_FREE; slot_stack[i] = S - 1 - (int32_t)i; slot_pin[i] = 0;
+        slot_owner[i] = 0;
     }
+    for (int64_t i = tid; i <= nsess; i += nt) session_slot[i] = -1;
     for (int64_t i = tid; i < T; i += nt) { htab[i].key = CP_EMPTY_KEY; htab[i].full = 0; htab[i].slot = -1; htab[i].len = 0; }
     if (tid == 0) {
         hdr->error = 0; hdr->next_id = 0; hdr->num_live = 0; hdr->fifo_head = 0; hdr->fifo_count = (int32_t)P;
@@ -173,6 +179,8 @@ struct InsArgs {
     uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
     int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; int logT; int64_t T; const unsigned long long* pw;
     const int32_t* slot_pin; int32_t* page_owner;     // R#32 pins, page -> owning slot
+    int32_t* slot_owner;                              // R#33: 0 shared, s = private entry of session s
+    const int32_t* session; int32_t* session_slot; int32_t max_sessions;   // cp_index_insert_session
     // scratch
     unsigned long long* span_pre; unsigned long long* span_full; HEntry* btab; int logBT; int64_t BT;
     Cand* cand; int64_t MAXC; int32_t* rel_off; int2* rel_rec; int32_t* new_slot; int32_t* removed; int32_t* rm_pos;
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(kScanThreads) k_ins_scan(InsArgs a, int phase)
             if (a.span_rep[id] != id) continue;               // duplicates inherit their representative's relations
             m = a.span_len[id];
         } else {
-            if (a.slot_state[id] != CP_SLOT_LIVE) continue;
+            if (a.slot_state[id] != CP_SLOT_LIVE || a.slot_owner[id] != 0) continue;   // private: no relations (R#33)
             m = a.slot_len[id];
         }
         if (is_new) {
@@ -1326,6 +1334,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         if (slot < 0 || !(sflag[slot] & 1)) continue;
         const int q = soff[j];
         a.slot_origin[slot] = a.span_begin[j]; a.slot_prefix[slot] = a.span_pre[j]; a.slot_full[slot] = a.span_full[j];
+        a.slot_owner[slot] = 0;                              // a shared entry (the slot may have been private)
         a.cp_req[q] = a.span_req[j]; a.cp_slot[q] = slot; a.cp_dst[q] = a.span_begin[j];
         a.cp_len[q] = slen[j]; a.cp_delta[q] = j;            // cp_delta carries the span index
     }
@@ -1524,6 +1533,147 @@ __global__ void k_ins_digest(InsArgs a) {
     }
 }
 
+
+// ---- R#33 same-user sessions: cp_index_insert_session ----------------------------------------------
+// thread per request: session in range, 1 <= n <= budget / max_span_len, block table wide enough, and a
+// free slot for every request (the first failing request in input order decides; nothing changes)
+__global__ void k_sess_validate(InsArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) { a.hdr->n_removed = 0; a.hdr->n_copy = 0; a.hdr->n_new_live = 0; }
+    if (cp_err_set(a.hdr)) return;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.num_reqs; r += gridDim.x * blockDim.x) {
+        const int o = a.session[r];
+        const int64_t n = a.offsets[r + 1] - a.offsets[r];
+        int bad = -1;
+        if (o < 1 || o > a.max_sessions || n < 1 || ((n - 1) >> 4) >= a.max_blocks) bad = 0;
+        else if (n > a.capacity || n > a.max_span_len) bad = 2;
+        if (bad >= 0) atomicMin(&a.hdr->first_err, ((unsigned long long)r << 32) | (unsigned)bad);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.hdr->slot_free_top < a.num_reqs)
+        atomicMin(&a.hdr->first_err, ((unsigned long long)0x7FFFFFFF << 32) | 2u);
+}
+
+// one CTA: the requests in input order (thread 0 bookkeeping, block-wide LRU arg-min), the same rules as
+// the oracle's orc_index_insert_session.  Slots freed here go back to the free stack at the end (so an
+// evicted shared entry's slot keeps its prefix hash until k_ins_delete tombstones it).
+__global__ void __launch_bounds__(256) k_sess_commit(InsArgs a) {
+    __shared__ int s_abort, s_go, s_nfree, s_ncopy, s_nrm;
+    __shared__ long long s_live, s_pinned;
+    __shared__ unsigned long long s_bl[8]; __shared__ int s_bi[8], s_bs[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        s_abort = 0;
+        if (cp_err_set(a.hdr)) s_abort = 1;
+        else if (a.hdr->first_err != CP_NO_ERR_KEY) { cp_raise(a.hdr, code_of((int)(a.hdr->first_err & 0xffffffffu))); s_abort = 1; }
+        a.hdr->first_err = CP_NO_ERR_KEY;
+        s_live = a.hdr->live_tokens; s_pinned = 0; s_nfree = 0; s_ncopy = 0; s_nrm = 0;
+    }
+    __syncthreads();
+    if (s_abort) {
+        for (int r = tid; r < a.num_reqs; r += blockDim.x) { a.out_oc[r] = -1; a.out_tmp[r] = -1; }
+        return;
+    }
+    {
+        long long pt = 0;
+        for (int i = tid; i < a.nslots; i += blockDim.x)
+            if (a.slot_state[i] == CP_SLOT_LIVE && a.slot_pin[i] > 0) pt += a.slot_len[i];
+        for (int o = 16; o; o >>= 1) pt += __shfl_xor_sync(0xffffffffu, pt, o);
+        if (lane == 0 && pt) atomicAdd((unsigned long long*)&s_pinned, (unsigned long long)pt);
+    }
+    __syncthreads();
+    DevHeader* h = a.hdr;
+    const int P32 = (int)a.P;
+    auto remove = [&](int sl) {                     // thread 0: pages to the FIFO tail in page-list order
+        const int npg = (a.slot_len[sl] + CP_BLOCK - 1) / CP_BLOCK;
+        for (int i = 0; i < npg; ++i) {
+            a.fifo[(h->fifo_head + h->fifo_count) % P32] = a.slot_pages[(int64_t)sl * a.MP + i];
+            h->fifo_count++;
+        }
+        s_live -= a.slot_len[sl]; h->num_live--;
+        a.slot_state[sl] = CP_SLOT_FREE;
+        const int own = a.slot_owner[sl];
+        if (own > 0) { if (a.session_slot[own] == sl) a.session_slot[own] = -1; }
+        else a.removed[s_nrm++] = sl;                // shared: tombstone its prefix-table entry afterwards
+        a.rm_pos[s_nfree++] = sl;                    // freed slots, pushed at the end
+    };
+    for (int r = 0; r < a.num_reqs; ++r) {
+        const int o = a.session[r];
+        const int n = (int)(a.offsets[r + 1] - a.offsets[r]);
+        if (tid == 0) {
+            int old = a.session_slot[o];
+            if (old >= 0 && !(a.slot_state[old] == CP_SLOT_LIVE && a.slot_owner[old] == o)) old = -1;
+            s_go = 1;
+            if ((old >= 0 && a.slot_pin[old] > 0) || s_pinned + n > a.capacity) {        // R#32
+                s_go = 0;
+                a.out_tmp[r] = (old >= 0 && a.slot_pin[old] > 0) ? old : -1; a.out_oc[r] = CP_DEFERRED_PINNED;
+            } else {
+                if (old >= 0) remove(old);
+                const int slot = a.slot_stack[--h->slot_free_top];
+                const int id = h->next_id++;
+                const int npg = (n + CP_BLOCK - 1) / CP_BLOCK;
+                for (int i = 0; i < npg; ++i) {
+                    const int pg = a.fifo[h->fifo_head];
+                    h->fifo_head = (h->fifo_head + 1) % P32; h->fifo_count--;
+                    a.slot_pages[(int64_t)slot * a.MP + i] = pg; a.page_owner[pg] = slot;
+                }
+                a.slot_id[slot] = id; a.slot_len[slot] = n; a.slot_origin[slot] = 0; a.slot_last[slot] = a.t;
+                a.slot_prefix[slot] = 0; a.slot_full[slot] = 0; a.slot_owner[slot] = o;
+                a.slot_state[slot] = CP_SLOT_LIVE;
+                a.session_slot[o] = slot;
+                s_live += n; h->num_live++;
+                const int q = s_ncopy++;
+                a.cp_req[q] = r; a.cp_slot[q] = slot; a.cp_dst[q] = 0; a.cp_len[q] = n; a.cp_delta[q] = r;
+                a.out_tmp[r] = slot; a.out_oc[r] = CP_STORED;
+            }
+        }
+        __syncthreads();
+        // LRU (R#21, R#32): victim = min (last_used, id) among live unpinned entries of any owner
+        while (s_go && s_live > a.capacity) {
+            unsigned long long bl = ~0ULL; int bi = 0x7fffffff, bs = -1;
+            for (int sx = tid; sx < a.nslots; sx += blockDim.x) {
+                if (a.slot_state[sx] != CP_SLOT_LIVE || a.slot_pin[sx] > 0) continue;
+                const unsigned long long lu = a.slot_last[sx];
+                const int sid = a.slot_id[sx];
+                if (lu < bl || (lu == bl && sid < bi)) { bl = lu; bi = sid; bs = sx; }
+            }
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long ol = __shfl_xor_sync(0xffffffffu, bl, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off), os = __shfl_xor_sync(0xffffffffu, bs, off);
+                if (ol < bl || (ol == bl && oi < bi)) { bl = ol; bi = oi; bs = os; }
+            }
+            if (lane == 0) { s_bl[wid] = bl; s_bi[wid] = bi; s_bs[wid] = bs; }
+            __syncthreads();
+            if (tid == 0) {
+                int v = -1; unsigned long long vb = ~0ULL; int vi = 0x7fffffff;
+                for (int w = 0; w < 8; ++w)
+                    if (s_bs[w] >= 0 && (s_bl[w] < vb || (s_bl[w] == vb && s_bi[w] < vi))) { vb = s_bl[w]; vi = s_bi[w]; v = s_bs[w]; }
+                if (v >= 0) remove(v); else { cp_raise(h, CP_ERR_CAPACITY); s_live = 0; }   // unreachable (R#32)
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        for (int i = 0; i < s_nfree; ++i) a.slot_stack[h->slot_free_top++] = a.rm_pos[i];
+        h->live_tokens = s_live; h->n_removed = s_nrm; h->n_copy = s_ncopy; h->n_new_live = s_ncopy;
+    }
+}
+
+// warp per stored private entry: its tokens into the token store, no recompute marks, its SHA-256 digest
+__global__ void k_sess_publish(InsArgs a) {
+    if (cp_err_set(a.hdr)) return;
+    const int n = a.hdr->n_new_live;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int q = warp; q < n; q += nwarps) {
+        const int slot = a.cp_slot[q], r = a.cp_req[q], m = a.cp_len[q];
+        const int32_t* tau = a.tokens + a.offsets[r];
+        for (int t = lane; t < m; t += 32)
+            a.page_tokens[(int64_t)a.slot_pages[(int64_t)slot * a.MP + (t >> 4)] * CP_BLOCK + (t & 15)] = tau[t];
+        for (int pg = lane; pg < (m + CP_BLOCK - 1) / CP_BLOCK; pg += 32) a.page_bits[a.slot_pages[(int64_t)slot * a.MP + pg]] = 0;
+        if (lane == 0) sha256_tokens_dev(tau, m, a.slot_digest + (int64_t)slot * 32);
+    }
+}
+
 __global__ void k_rebuild_check(DevHeader* hdr, int64_t T) {
     hdr->rebuild = (hdr->error == 0 && (int64_t)hdr->table_used * 2 > T) ? 1 : 0;
 }
@@ -1536,13 +1686,13 @@ __global__ void k_rebuild_clear(DevHeader* hdr, HEntry* htab, int64_t T) {
 }
 __global__ void k_rebuild_fill(DevHeader* hdr, HEntry* htab, int logT, int64_t T, const uint8_t* state,
                                const unsigned long long* prefix, const unsigned long long* full,
-                               const int32_t* len, int32_t nslots) {
+                               const int32_t* len, int32_t nslots, const int32_t* owner) {
     if (!hdr->rebuild) return;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     for (int s = warp; s < nslots; s += nwarps) {
-        if (state[s] != CP_SLOT_LIVE) continue;
+        if (state[s] != CP_SLOT_LIVE || owner[s] != 0) continue;          // private entries are not probed
         HEntry v; v.key = prefix[s]; v.full = full[s]; v.slot = s; v.len = len[s]; v.pad = 0;
         cp_warp_insert(htab, (uint32_t)(T - 1), logT, v, false);
         if (lane == 0) atomicAdd(&hdr->table_used, 1);
@@ -1636,6 +1786,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->page_bits = (uint16_t*)(m + L.meta_off[13]); x->htab = (HEntry*)(m + L.meta_off[14]);
     x->pw = (unsigned long long*)(m + L.meta_off[15]);
     x->slot_pin = (int32_t*)(m + L.meta_off[16]); x->page_owner = (int32_t*)(m + L.meta_off[17]);
+    x->slot_owner = (int32_t*)(m + L.meta_off[18]); x->session_slot = (int32_t*)(m + L.meta_off[19]);
     char* s = x->scratch;
     x->HS = L.HS; x->CH = L.CH; x->CS_HITS = L.CS_HITS; x->MS = L.MS; x->MAXC = L.MAXC; x->BT = L.BT; x->logBT = L.logBT;
     x->sp_entry = (int32_t*)(s + L.scr_off[0]); x->sp_slot = (int32_t*)(s + L.scr_off[1]);
@@ -1665,7 +1816,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->Bw = pw[(size_t)cfg->window_len];
     if (cudaMemcpyAsync(x->pw, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
     k_init<<<592, 256, 0, st>>>(x->hdr, x->slot_id, x->slot_state, x->fifo, x->slot_stack, x->htab, x->P, x->S, x->T,
-                                x->slot_pin, x->page_owner);
+                                x->slot_pin, x->page_owner, x->slot_owner, x->session_slot, cfg->max_sessions);
     CP_COUNT_LAUNCH();
     if (cudaGetLastError() != cudaSuccess) { delete x; return CP_ERR_CUDA; }
     if (cudaStreamSynchronize(st) != cudaSuccess) { delete x; return CP_ERR_CUDA; }
@@ -1830,6 +1981,11 @@ cp_status cp_index_snapshot(cp_index* x, cp_snapshot* o, void* stream) {
             if (o->recompute) o->recompute[(size_t)q * ML + t] = (pbits[page] >> (t % CP_BLOCK)) & 1;
         }
     }
+    if (o->owner) {
+        std::vector<int32_t> own((size_t)S);
+        CP_CUDA_CHECK(cudaMemcpy(own.data(), x->slot_owner, 4 * (size_t)S, cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < order.size(); ++q) o->owner[q] = own[(size_t)order[q]];
+    }
     if (o->pin) {
         std::vector<int32_t> pins((size_t)S);
         CP_CUDA_CHECK(cudaMemcpy(pins.data(), x->slot_pin, 4 * (size_t)S, cudaMemcpyDeviceToHost));
@@ -1883,7 +2039,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
     a.slot_prefix = x->slot_prefix; a.slot_full = x->slot_full; a.slot_last = x->slot_last;
     a.slot_digest = x->slot_digest; a.slot_pages = x->slot_pages; a.fifo = x->fifo; a.slot_stack = x->slot_stack;
     a.page_tokens = x->page_tokens; a.page_bits = x->page_bits; a.htab = x->htab; a.logT = x->logT; a.T = x->T;
-    a.pw = x->pw; a.slot_pin = x->slot_pin; a.page_owner = x->page_owner;
+    a.pw = x->pw; a.slot_pin = x->slot_pin; a.page_owner = x->page_owner; a.slot_owner = x->slot_owner;
     a.span_pre = x->span_pre; a.span_full = x->span_full; a.btab = x->btab; a.logBT = x->logBT; a.BT = x->BT;
     a.cand = x->cand; a.MAXC = x->MAXC; a.rel_off = x->rel_off; a.rel_rec = (int2*)x->rel_rec;
     a.new_slot = x->new_slot; a.removed = x->removed; a.rm_pos = x->rm_pos;
@@ -1959,7 +2115,8 @@ cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp
     if (cudaEventRecord(x->ev_join, x->side) != cudaSuccess) return CP_ERR_CUDA;
     k_rebuild_check<<<1, 1, 0, st>>>(x->hdr, x->T); CP_COUNT_LAUNCH();
     k_rebuild_clear<<<256, 256, 0, st>>>(x->hdr, x->htab, x->T); CP_COUNT_LAUNCH();
-    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->slot_full, x->slot_len, x->S); CP_COUNT_LAUNCH();
+    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->slot_full, x->slot_len, x->S,
+                                        x->slot_owner); CP_COUNT_LAUNCH();
     if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     // copy the writer KV rows of the published entries into their pool pages
     const cp_status cs = cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
@@ -2008,6 +2165,47 @@ cp_status cp_index_insert_commit(cp_index* x, const cp_batch* wb, const cp_paged
     if (!x->insert_prepared) return CP_ERR_INVALID_ARG;          // commit without prepare
     x->insert_prepared = 0;
     return ins_commit(x, a, wb, kv, (cudaStream_t)stream);
+}
+
+
+cp_status cp_index_insert_session(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, uint64_t t,
+                                  int32_t* out_id, int32_t* out_oc, void* stream) {
+    if (!x || x->is_view || !wb || !kv || !out_id || !out_oc || x->cfg.max_sessions < 1) return CP_ERR_INVALID_ARG;
+    if (wb->num_reqs == 0) return CP_OK;
+    if (wb->num_reqs < 0 || wb->num_reqs > x->cfg.max_batch_reqs || wb->num_reqs > x->MS ||
+        wb->total_tokens > x->cfg.max_batch_tokens || !wb->tokens || !wb->offsets || !wb->session)
+        return CP_ERR_INVALID_ARG;
+    if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables || kv->max_blocks_per_req < 1) return CP_ERR_INVALID_ARG;
+    if (x->insert_prepared) return CP_ERR_INVALID_ARG;
+    InsArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.hdr = x->hdr; a.tokens = wb->tokens; a.offsets = wb->offsets; a.num_reqs = wb->num_reqs; a.S = wb->num_reqs;
+    a.t = t; a.w = x->cfg.window_len; a.B = x->B; a.capacity = x->cfg.pool_capacity_tokens;
+    a.max_span_len = x->cfg.max_span_len; a.out_id = out_id; a.out_oc = out_oc;
+    a.nslots = x->S; a.P = x->P; a.MP = x->MP;
+    a.slot_id = x->slot_id; a.slot_len = x->slot_len; a.slot_origin = x->slot_origin; a.slot_state = x->slot_state;
+    a.slot_prefix = x->slot_prefix; a.slot_full = x->slot_full; a.slot_last = x->slot_last;
+    a.slot_digest = x->slot_digest; a.slot_pages = x->slot_pages; a.fifo = x->fifo; a.slot_stack = x->slot_stack;
+    a.page_tokens = x->page_tokens; a.page_bits = x->page_bits; a.htab = x->htab; a.logT = x->logT; a.T = x->T;
+    a.pw = x->pw; a.slot_pin = x->slot_pin; a.page_owner = x->page_owner; a.slot_owner = x->slot_owner;
+    a.session = wb->session; a.session_slot = x->session_slot; a.max_sessions = x->cfg.max_sessions;
+    a.removed = x->removed; a.rm_pos = x->rm_pos; a.out_tmp = x->out_tmp;
+    a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
+    a.max_blocks = kv->max_blocks_per_req;
+    cudaStream_t st = (cudaStream_t)stream;
+    cp_invalidate_worklist(x);
+    k_sess_validate<<<std::max(1, std::min(148, (wb->num_reqs + 255) / 256)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_sess_commit<<<1, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_outids<<<(wb->num_reqs + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_sess_publish<<<std::max(1, std::min(1184, (wb->num_reqs + 7) / 8)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_rebuild_check<<<1, 1, 0, st>>>(x->hdr, x->T); CP_COUNT_LAUNCH();
+    k_rebuild_clear<<<256, 256, 0, st>>>(x->hdr, x->htab, x->T); CP_COUNT_LAUNCH();
+    k_rebuild_fill<<<256, 256, 0, st>>>(x->hdr, x->htab, x->logT, x->T, x->slot_state, x->slot_prefix, x->slot_full, x->slot_len, x->S,
+                                        x->slot_owner); CP_COUNT_LAUNCH();
+    if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
+    return cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
+                          x->MS, wb->offsets, nullptr, kv, 0, st);
 }
 
 cp_status cp_index_copy_in(cp_index* v, const cp_batch* wb, const cp_paged_kv* kv, int32_t flags, void* stream) {

@@ -117,6 +117,7 @@ struct cp_index {
     uint8_t* slot_digest; int32_t* slot_pages; int32_t* fifo; int32_t* slot_stack;
     int32_t* page_tokens; uint16_t* page_bits; HEntry* htab; unsigned long long* pw;
     int32_t* slot_pin; int32_t* page_owner;          // R#32: linked-page pins per slot, owning slot per page
+    int32_t* slot_owner; int32_t* session_slot;      // R#33: owner session per slot, private slot per session
     // SCRATCH (match)
     int64_t HS;          // sparse hit capacity
     int32_t *sp_entry, *sp_slot, *sp_dst, *sp_len, *sp_delta, *req_cnt;

@@ -49,6 +49,9 @@ struct MatchArgs {
     int32_t max_hits; int32_t* num_hits; int32_t* req_hit_offsets;
     int32_t *hit_req, *hit_entry, *hit_slot, *hit_dst, *hit_len, *hit_delta;
     uint8_t* plan; int32_t *req_covered, *req_recompute, *req_candidates;
+    // R#33 same-user sessions (session == nullptr: none)
+    const int32_t* session; const int32_t* session_slot; const int32_t* slot_owner; const uint8_t* slot_state;
+    int32_t max_sessions;
 };
 
 struct MatchSmem {
@@ -72,7 +75,7 @@ template <bool G>
 __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ uint64_t wtmp[2 * (kNT / 32)];
-    __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last, s_vtok;
+    __shared__ int s_nc, s_cands, s_nh, s_cov, s_rec, s_last, s_vtok, s_pslot, s_plen;
     __shared__ int s_scan[kNT / 32 + 1];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int r = blockIdx.x;
@@ -216,9 +219,42 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
         }
         __syncthreads();
         MPROF(2);
+        // ---- 3b. same-user session (R#33): the longest common prefix with the session's
+        //      private entry (its last request, sensitive tokens included: no mask test), one hit at 0 if
+        //      >= w tokens; the cross-user greedy then starts after it
+        if (wid == 0) {
+            int ps = -1, L = 0;
+            if (a.session) {
+                const int o = a.session[r];
+                if (o >= 1 && o <= a.max_sessions) {
+                    ps = a.session_slot[o];
+                    if (ps >= 0 && !(a.slot_state[ps] == CP_SLOT_LIVE && a.slot_owner[ps] == o)) ps = -1;
+                }
+                if (ps >= 0) {
+                    const int lim = min(__ldg(a.slot_len + ps), n);
+                    const int32_t* pg = a.slot_pages + (int64_t)ps * a.MP;
+                    L = lim;
+                    for (int i0 = 0; i0 < lim; i0 += 32) {
+                        const int i = i0 + lane;
+                        const bool stop = i < lim &&
+                            __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15)) != tok[i];
+                        const unsigned bs = __ballot_sync(0xffffffffu, stop);
+                        if (bs) { L = i0 + __ffs(bs) - 1; break; }
+                    }
+                    if (L < a.w) { ps = -1; L = 0; }
+                }
+            }
+            if (lane == 0) { s_pslot = ps; s_plen = L; }
+        }
+        __syncthreads();
         // ---- 4. greedy left-to-right assembly (warp 0)
         if (wid == 0) {
             int cursor = 0;
+            if (s_pslot >= 0) {
+                if (lane == 0) { hk[0] = 0; hs[0] = s_pslot; hm[0] = s_plen; }
+                nh = 1;
+                cursor = s_plen;
+            }
             while (cursor < nw) {
                 const int k = cursor + lane;
                 const int v = k < nw ? vslot[k] : -1;
@@ -397,6 +433,11 @@ extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, 
     a.hit_req = o->hit_req; a.hit_entry = o->hit_entry; a.hit_slot = o->hit_slot; a.hit_dst = o->hit_dst;
     a.hit_len = o->hit_len; a.hit_delta = o->hit_delta; a.plan = o->plan;
     a.req_covered = o->req_covered; a.req_recompute = o->req_recompute; a.req_candidates = o->req_candidates;
+    if (b->session) {                              // R#33: sessions only with the method's own policy
+        if (a.policy != 0 || x->cfg.max_sessions < 1) return CP_ERR_INVALID_ARG;
+        a.session = b->session; a.session_slot = x->session_slot; a.slot_owner = x->slot_owner;
+        a.slot_state = x->slot_state; a.max_sessions = x->cfg.max_sessions;
+    }
     static int attr_set = 0;
     if (!attr_set) {
         cudaFuncSetAttribute(k_match<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);

@@ -87,7 +87,7 @@ class Case:
     def __init__(self, wl: Workload, device="cuda", seed: int = 0, rho=(1, 4), layer_range=None,
                  head_range=None, sample_reqs: Optional[int] = None, sample_layers: Optional[Sequence[int]] = None,
                  use_reader_mask: bool = True, hash_seed: int = 42, policy: Optional[str] = None,
-                 placeholders: str = "recompute"):
+                 placeholders: str = "recompute", max_sessions: int = 0):
         import torch
         import paper_2605_23640_b200 as cp
         self.torch, self.cp = torch, cp
@@ -118,15 +118,39 @@ class Case:
             max_entries=min(131072, wl.pool_capacity_tokens // w + max(spans + [1]) + 64),
             max_span_len=wl.max_span_len, max_req_tokens=max(lens + [1]),
             max_batch_reqs=max(reqs + [1]), max_batch_tokens=max(toks + [1]),
-            max_spans_per_insert=max(spans + [1]), layer_offset=self.l0, head_offset=self.h0)
+            max_spans_per_insert=max(spans + [1]), layer_offset=self.l0, head_offset=self.h0,
+            max_sessions=max_sessions)
         self.dev = cp.KVIndex(self.cfg, self.device)
         self.orc = O.OracleIndex(w, hash_seed, wl.pool_capacity_tokens, self.dev.num_pages)
         self.calls: List[Batch] = []          # writer batch of each insert call (for payload identity)
         self.t = 0
 
     # ------------------------------------------------------------------ helpers
-    def _dev_batch(self, b: Batch, with_mask=True):
-        return self.cp.DeviceBatch.from_numpy(b.tokens, b.offsets, b.mask if with_mask else None, self.device)
+    def _dev_batch(self, b: Batch, with_mask=True, sessions=None):
+        return self.cp.DeviceBatch.from_numpy(b.tokens, b.offsets, b.mask if with_mask else None, self.device,
+                                              session=sessions)
+
+    def insert_session(self, wb: Batch, sessions, rep: ParityReport):
+        """R#33: every request of `wb` replaces its session's private entry, on the device and in the oracle."""
+        self.t += 1
+        t = self.t
+        kv = self.writer_kv(wb)
+        db = self._dev_batch(wb, sessions=np.asarray(sessions, np.int32))
+        ids, oc = self.dev.insert_session(db, kv, t)
+        err = self.dev.last_error()
+        rc, oids, ooc = self.orc.insert_session(wb, sessions, t)
+        if err != rc:
+            rep.fail(f"insert_session t={t}: device status {err} != oracle {rc}")
+            return
+        if rc != 0:
+            return
+        self.calls.append(wb)
+        ids, oc = ids.cpu().numpy(), oc.cpu().numpy()
+        if not np.array_equal(oc, ooc) or not np.array_equal(ids, oids):
+            rep.fail(f"insert_session t={t}: outcomes / ids differ: {oc[:6]} {ids[:6]} vs {ooc[:6]} {oids[:6]}")
+        rep.stats["session_stored"] = rep.stats.get("session_stored", 0) + int(np.sum(ooc == O.STORED))
+        del kv
+        self.compare_index(rep, f"after insert_session t={t}")
 
     def _tdt(self):
         return self.torch.bfloat16 if self.g.dtype == "bf16" else self.torch.float32
@@ -235,7 +259,7 @@ class Case:
         if not np.array_equal(snap["fifo"], self.orc.fifo()):
             rep.fail(f"{where}: free-page FIFO differs")
         for de, oe in zip(snap["entries"], live):
-            for k in ("id", "len", "origin_pos", "prefix_hash", "full_hash", "last_used", "digest", "pin"):
+            for k in ("id", "len", "origin_pos", "prefix_hash", "full_hash", "last_used", "digest", "pin", "owner"):
                 if de[k] != oe[k]:
                     rep.fail(f"{where}: entry {oe['id']} field {k}: {de[k]!r} != {oe[k]!r}")
             if not np.array_equal(de["pages"], oe["pages"]):
@@ -247,11 +271,12 @@ class Case:
                     rep.fail(f"{where}: entry {oe['id']} recompute bits differ")
         rep.stats["live_entries"] = len(live)
 
-    def match_and_gather(self, rb: Batch, rep: ParityReport, check_kv=True, no_touch=False):
+    def match_and_gather(self, rb: Batch, rep: ParityReport, check_kv=True, no_touch=False, sessions=None):
         torch = self.torch
         self.t += 1
         t = self.t
-        db = self._dev_batch(rb, with_mask=self.use_reader_mask)
+        db = self._dev_batch(rb, with_mask=self.use_reader_mask,
+                             sessions=None if sessions is None else np.asarray(sessions, np.int32))
         hits = self.dev.match_spans(db, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy)
         dst = self.dst_kv(rb) if check_kv else None
         if check_kv:
@@ -262,7 +287,8 @@ class Case:
         if err:
             rep.fail(f"match t={t}: device error {err}")
             return
-        res = self.orc.match(rb, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy)
+        res = self.orc.match(rb, t, no_touch=no_touch, use_mask=self.use_reader_mask, policy=self.policy,
+                             sessions=sessions)
         h = hits.to_host()
         if h["num_hits"] != res.num_hits:
             rep.fail(f"match t={t}: num_hits {h['num_hits']} != {res.num_hits}")

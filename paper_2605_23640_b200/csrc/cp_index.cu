@@ -1654,7 +1654,16 @@ __global__ void __launch_bounds__(256) k_sess_commit(InsArgs a) {
     }
     if (tid == 0) {
         for (int i = 0; i < s_nfree; ++i) a.slot_stack[h->slot_free_top++] = a.rm_pos[i];
-        h->live_tokens = s_live; h->n_removed = s_nrm; h->n_copy = s_ncopy; h->n_new_live = s_ncopy;
+        // entries stored and evicted again within this call are neither published nor copied (their pages
+        // may already belong to a later entry); freed slots are not reused within the call, so "still
+        // live" identifies the survivors
+        int q2 = 0;
+        for (int q = 0; q < s_ncopy; ++q) {
+            if (a.slot_state[a.cp_slot[q]] != CP_SLOT_LIVE) continue;
+            a.cp_req[q2] = a.cp_req[q]; a.cp_slot[q2] = a.cp_slot[q]; a.cp_dst[q2] = a.cp_dst[q];
+            a.cp_len[q2] = a.cp_len[q]; a.cp_delta[q2] = a.cp_delta[q]; ++q2;
+        }
+        h->live_tokens = s_live; h->n_removed = s_nrm; h->n_copy = q2; h->n_new_live = q2;
     }
 }
 

@@ -87,7 +87,7 @@ class Case:
     def __init__(self, wl: Workload, device="cuda", seed: int = 0, rho=(1, 4), layer_range=None,
                  head_range=None, sample_reqs: Optional[int] = None, sample_layers: Optional[Sequence[int]] = None,
                  use_reader_mask: bool = True, hash_seed: int = 42, policy: Optional[str] = None,
-                 placeholders: str = "recompute", max_sessions: int = 0):
+                 placeholders: str = "recompute", max_sessions: int = 0, batch_slack: int = 0):
         import torch
         import paper_2605_23640_b200 as cp
         self.torch, self.cp = torch, cp
@@ -116,8 +116,8 @@ class Case:
             rope_theta=g.rope_theta, rope_style=g.rope_style, window_len=w, hash_seed=hash_seed,
             pool_capacity_tokens=wl.pool_capacity_tokens,
             max_entries=min(131072, wl.pool_capacity_tokens // w + max(spans + [1]) + 64),
-            max_span_len=wl.max_span_len, max_req_tokens=max(lens + [1]),
-            max_batch_reqs=max(reqs + [1]), max_batch_tokens=max(toks + [1]),
+            max_span_len=wl.max_span_len, max_req_tokens=max(lens + [1]) + batch_slack,
+            max_batch_reqs=max(reqs + [1]) + batch_slack, max_batch_tokens=max(toks + [1]) + 64 * batch_slack,
             max_spans_per_insert=max(spans + [1]), layer_offset=self.l0, head_offset=self.h0,
             max_sessions=max_sessions)
         self.dev = cp.KVIndex(self.cfg, self.device)

@@ -21,19 +21,22 @@ from tests.test_gpu_fuzz_index import _request, _workload  # noqa: E402
 @pytest.mark.parametrize("seed", range(12))
 def test_sessions_gpu_vs_oracle(seed):
     wl = _workload(500 + seed, "bf16" if seed % 2 else "fp32", heavy=seed % 3 == 0, w=8)
-    case = Case(wl, seed=seed, sample_reqs=None, max_sessions=4)
+    case = Case(wl, seed=seed, sample_reqs=None, max_sessions=4, batch_slack=64)
     rep = ParityReport()
     rng = np.random.default_rng(seed)
     for wb, rb in wl.rounds:
         case.insert(wb, rep)
         assert rep.ok, rep.notes[:6]
-        sess = rng.integers(1, 5, wb.num_reqs).astype(np.int32)
-        case.insert_session(wb, sess, rep)                       # each writer is also its session's last turn
+        # each writer (that fits an entry's page list, max_span_len) is also its session's last turn
+        keep = [r for r in range(wb.num_reqs) if int(wb.lens[r]) <= wl.max_span_len]
+        sw = wb.subset(keep)
+        sess = rng.integers(1, 5, sw.num_reqs).astype(np.int32)
+        case.insert_session(sw, sess, rep)
         assert rep.ok, rep.notes[:6]
         # readers: follow-up turns of those sessions (a writer's prompt, then new tokens) and other readers
         follow = []
-        for r in range(min(wb.num_reqs, 3)):
-            base = wb.tokens[wb.offsets[r]:wb.offsets[r + 1]]
+        for r in range(min(sw.num_reqs, 3)):
+            base = sw.tokens[sw.offsets[r]:sw.offsets[r + 1]]
             cut = int(rng.integers(1, len(base) + 1))
             t = np.concatenate([base[:cut], rng.integers(0, 9, int(rng.integers(0, 30)))]).astype(np.int32)
             follow.append(Batch(tokens=t, offsets=np.array([0, len(t)], np.int64), mask=np.zeros(len(t), np.uint8),

@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-all-cores", action="store_true", help="cpu_baseline on one core only")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-3 and config-5 keys of the line")
+    ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of CUDA-graph replays")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
     ap.add_argument("--overlap", type=int, default=3, choices=[0, 1, 2, 3],
@@ -291,6 +292,9 @@ def setup_ours(args, rank, world, device):
                  torch.full((max(len(ib.span_len), 1),), -1, dtype=torch.int32, device=device))
     S.ev_insert_done = torch.cuda.Event()
     S.ev_insert_done.record()
+    S.ev_fork = torch.cuda.Event()
+    S.clock = None                         # device logical clock, set for CUDA-graph capture
+    S.graph = None
     S.setup_s = time.time() - t0
     return S
 
@@ -332,6 +336,11 @@ def run_step(S, torch, cp, world, events=None):
     ev = events
     main = torch.cuda.current_stream()
     scores = S.is_owner or S.use_dist
+    if S.clock is not None:
+        S.clock.add_(1)                    # the device logical clock (cp_index_set_clock), also in graph replays
+    # the side stream forks from the main stream at the step start: it then follows the previous step's
+    # insert (which read the bits N3 overwrites), and the fork stays inside a CUDA-graph capture
+    S.ev_fork.record(main)
 
     def score():
         if ev: ev[5].record()
@@ -347,12 +356,12 @@ def run_step(S, torch, cp, world, events=None):
         # the insert's read-only half on the side stream, beside match + gather (it needs only the
         # previous commit); N3 then runs on the main stream right after the gather (no cross-stream
         # hop on the critical path) and the commit waits for the prepare
-        S.side.wait_event(S.ev_insert_done)
+        S.side.wait_event(S.ev_fork)
         with torch.cuda.stream(S.side):
             S.idx.insert(*ins, out=S.ins_out, phase="prepare")
             S.ev_prep_done.record()
     if scores and S.overlap in (0, 1):
-        S.side.wait_event(S.ev_insert_done)
+        S.side.wait_event(S.ev_fork)
         with torch.cuda.stream(S.side if S.overlap == 1 else main):
             score()
     if ev: ev[0].record()
@@ -440,6 +449,29 @@ def bench_ours(args):
     S.warm_s_per_step = (time.perf_counter() - tw) / max(1, args.warmup)
     if S.idx.last_error():
         raise RuntimeError("device error during warm-up")
+    # ---- CUDA graph of one step: the ~40 launches of the control plane (match, prep, commit chain,
+    #      copy-ins) replay without host launch overhead or inter-kernel gaps; the logical time then
+    #      comes from a device clock the step itself advances (cp_index_set_clock)
+    use_graph = not args.no_graph and not (use_dist and backend == "gloo")
+    l_step0 = cp.kernel_launch_count()
+    run_step(S, torch, cp, world)
+    torch.cuda.synchronize()
+    launches_per_step = cp.kernel_launch_count() - l_step0
+    if use_graph:
+        S.clock = torch.full((1,), S.t, dtype=torch.int64, device=device)
+        S.idx.set_clock(S.clock)
+        run_step(S, torch, cp, world)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run_step(S, torch, cp, world)
+        S.graph = g
+        torch.cuda.synchronize()
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        if S.idx.last_error():
+            raise RuntimeError("device error in the CUDA-graph replays")
     cov = int(S.hits.req_covered.sum().item())
     rec = int(S.hits.req_recompute.sum().item())
     nh = int(S.hits.num_hits.item())
@@ -465,9 +497,10 @@ def bench_ours(args):
         nb_dev = n_busy.to(device) if backend == "nccl" else n_busy
         dist.all_reduce(nb_dev, op=dist.ReduceOp.MAX)
         n_busy = nb_dev.cpu()
+    step = (lambda: S.graph.replay()) if S.graph is not None else (lambda: run_step(S, torch, cp, world))
     clocks.start()
     for _ in range(int(n_busy.item())):
-        run_step(S, torch, cp, world)
+        step()
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -476,17 +509,26 @@ def bench_ours(args):
     torch.cuda.nvtx.range_push("timed")
     start.record()
     for k in range(K):
-        run_step(S, torch, cp, world, evs[k])
+        if S.graph is not None:
+            S.graph.replay()
+        else:
+            run_step(S, torch, cp, world, evs[k])
     end.record()
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
-    launches = cp.kernel_launch_count() - l0
+    launches = cp.kernel_launch_count() - l0 if S.graph is None else launches_per_step * K
+    if S.graph is not None:
+        # per-phase breakdown: a few eager steps with events (the timed steps are graph replays)
+        for k in range(min(K, 5)):
+            run_step(S, torch, cp, world, evs[k])
+        torch.cuda.synchronize()
     if use_dist:
         dist.barrier()
     ms_total = start.elapsed_time(end)
-    phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(K)])
-    score_ms = float(np.mean([evs[k][5].elapsed_time(evs[k][6]) for k in range(K)])) if (S.is_owner or S.use_dist) else 0.0
+    kph = K if S.graph is None else min(K, 5)
+    phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(kph)])
+    score_ms = float(np.mean([evs[k][5].elapsed_time(evs[k][6]) for k in range(kph)])) if (S.is_owner or S.use_dist) else 0.0
     if S.idx.last_error():
         raise RuntimeError("device error during timed steps")
     ms_step = ms_total / K
@@ -552,7 +594,7 @@ def bench_ours(args):
                        "index_entries": len(S.wb.span_len), "insert_batch_spans": len(S.ib.span_len),
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
-                       "placeholders": S.placeholders,
+                       "placeholders": S.placeholders, "cuda_graph": S.graph is not None,
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
                        **({"dist_backend": dist.get_backend()} if use_dist else {}),
                        "shard_rects": [[r.layer_lo, r.layer_hi, r.head_lo, r.head_hi] for r in S.rects],
@@ -764,7 +806,10 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
     for _ in range(K):
         for k in host:
             dev[k].copy_(host[k], non_blocking=True)
-        run_step(S, torch, cp, world)
+        if S.graph is not None:
+            S.graph.replay()                     # the captured step reads the same device buffers
+        else:
+            run_step(S, torch, cp, world)
         for src, dst in zip(outs, pinned_out):
             dst.copy_(src, non_blocking=True)
     t1.record()
@@ -783,7 +828,8 @@ def e2e_ours(S, torch, cp, world, K, reused_all, dist):
         ms = float(t[0])
     return {"value": round(reused_all / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "note": "per-step reader batch H2D from pinned host + results D2H, inside the timed region"}
+            "note": "per-step reader batch H2D from pinned host + results D2H, inside the timed region"
+                    + ("; the step is the captured CUDA graph" if S.graph is not None else "")}
 
 
 # ------------------------------------------------------------------------------ oracle (CPU)

@@ -437,6 +437,13 @@ typedef struct {
 } cp_snapshot;
 cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
 
+/* Device logical clock (for CUDA-graph capture of a serving step): with d_clock set (device uint64,
+ * caller-owned), cp_match_spans, the insert commit and cp_index_insert_session read the logical time
+ * from *d_clock when their kernels run and ignore their host `logical_time` argument -- so a captured
+ * step replays with the time the caller writes there before each replay (e.g. a captured copy from a
+ * pinned host scalar).  NULL restores the host argument. */
+cp_status cp_index_set_clock(cp_index* idx, const uint64_t* d_clock);
+
 /* Synchronizes, returns and clears the sticky device error word (CP_OK if none). */
 cp_status cp_index_last_error(cp_index* idx, void* stream);
 

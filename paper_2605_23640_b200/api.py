@@ -292,6 +292,11 @@ class KVIndex:
         p = pages.reshape(-1).contiguous()
         L.check(L.lib().cp_pin_links(self.h, _ptr(p), int(p.numel()), int(delta), _stream(stream)), "cp_pin_links")
 
+    def set_clock(self, clock: Optional[torch.Tensor]):
+        """cp_index_set_clock: read the logical time from a device uint64 (int64 storage) tensor, or None."""
+        self._clock = clock
+        L.check(L.lib().cp_index_set_clock(self.h, _ptr(clock)), "cp_index_set_clock")
+
     def last_error(self, stream=None) -> int:
         return int(L.lib().cp_index_last_error(self.h, _stream(stream)))
 

@@ -197,6 +197,7 @@ struct InsArgs {
     int32_t *f_vslot, *f_vlen, *f_vcpg, *f_vfc;
     long long* f_vcum;
     int32_t force_serial;   // CP_COMMIT_SERIAL=1: skip the parallel apply (A/B measurement, tests)
+    const unsigned long long* clock;   // cp_index_set_clock: logical time read on the device (else t)
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
     int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
@@ -587,6 +588,7 @@ __device__ unsigned long long g_commit_prof[16];
 // One CTA applies the spans in input order (exact sequential semantics of R#20-22).
 // sflag bit 0: live; bit 1: stored by this call.
 __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
+    const unsigned long long tnow = a.clock ? *a.clock : a.t;   // device clock (CUDA-graph replays advance it)
     extern __shared__ __align__(16) unsigned char smc[];
     const int tid = threadIdx.x;
     const CommitSmem lay(a.nslots, a.S, a.candK, a.rec_cap);
@@ -744,7 +746,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             else if (rr.y == REL_CONTAINER) { const int sid = a.slot_id[rr.x]; if (sid < cont_id) { cont_id = sid; cont = rr.x; } }
         }
         if (dup >= 0) {
-            a.slot_last[dup] = a.t; sflag[dup] |= 4; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
+            a.slot_last[dup] = tnow; sflag[dup] |= 4; a.out_tmp[j] = dup; a.out_oc[j] = CP_DUPLICATE;
             seq[rj] = dup;                        // the one live entry with this content (benign equal-value race)
         } else { a.out_tmp[j] = cont; a.out_oc[j] = CP_DROPPED_CONTAINED; }
     }
@@ -777,7 +779,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         }
         if ((tid & 31) == 0) { atomicMin(&s_minl, mn); atomicMax(&s_maxl, mx); }
         __syncthreads();
-        const bool ok = s_maxl >= s_minl && (s_maxl - s_minl) < (1ULL << 32) && a.t >= s_maxl;
+        const bool ok = s_maxl >= s_minl && (s_maxl - s_minl) < (1ULL << 32) && tnow >= s_maxl;
         if (ok) {
             const unsigned long long minl = s_minl;
             auto keyof = [&](int sl) -> unsigned long long {
@@ -929,7 +931,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         while (s_cp < s_cn) {
             const int sl = cslot[s_cp];
             const unsigned long long k = ckey[s_cp];
-            if ((k >> 32) + s_minl >= a.t) return -1;             // t-group: ordered by id with refreshed/new ones
+            if ((k >> 32) + s_minl >= tnow) return -1;             // t-group: ordered by id with refreshed/new ones
             len = clen[s_cp];
             ++s_cp;
             if ((sflag[sl] & 1) && !(sflag[sl] & 6)) return sl;    // live, not stored or refreshed in this call
@@ -1061,7 +1063,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             for (int q = tid; q < cn; q += blockDim.x) {
                 const int fc = a.f_vfc[q];
                 if (fc >= Vtot) continue;
-                if ((ckey[q] >> 32) + s_minl >= a.t) { s_fast = 0; atomicOr(&s_why, 64); continue; }
+                if ((ckey[q] >> 32) + s_minl >= tnow) { s_fast = 0; atomicOr(&s_why, 64); continue; }
                 int lo = 0, hi = ns - 1;                              // store whose eviction reaches q
                 while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.f_vk[mid] > fc) hi = mid; else lo = mid + 1; }
                 const int jk = a.f_sj[lo], sl = cslot[q];
@@ -1094,7 +1096,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             const int r = srep[j], kind = a.f_kind[r];
             if (kind == 0) {
                 const int X = a.f_target[r];
-                a.slot_last[X] = a.t; a.out_tmp[j] = X; a.out_oc[j] = CP_DUPLICATE;
+                a.slot_last[X] = tnow; a.out_tmp[j] = X; a.out_oc[j] = CP_DUPLICATE;
             } else if (kind == 1) {
                 a.out_tmp[j] = a.f_target[r]; a.out_oc[j] = CP_DROPPED_CONTAINED;
             }
@@ -1102,7 +1104,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         for (int k = tid; k < ns; k += blockDim.x) {
             const int j = a.f_sj[k], m = slen[j];
             const int slot = k < s_sc_n ? s_stack_cache[k] : a.slot_stack[free_top0 - 1 - k];
-            a.slot_id[slot] = s_next_id + k; a.slot_len[slot] = m; a.slot_last[slot] = a.t;
+            a.slot_id[slot] = s_next_id + k; a.slot_len[slot] = m; a.slot_last[slot] = tnow;
             snew[j] = slot; sfpos[j] = wrap(s_fifo_head0 + a.f_pgpref[k]);
             a.out_tmp[j] = slot; a.out_oc[j] = a.f_supcnt[j] > 0 ? CP_SUPERSEDED : CP_STORED;
             // removals of this store: its supersedes (ascending id), then its LRU victims
@@ -1200,7 +1202,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 const int f = need ? __ffs(need) - 1 : 32;
                 if (tid < f && kind == 0) {                        // Duplicate refreshes last_used (R#20)
                     seq[rjj] = target;
-                    a.slot_last[target] = a.t;
+                    a.slot_last[target] = tnow;
                     sflag[target] |= 4;                            // same value from every lane that writes it
                     a.out_tmp[jj] = target; a.out_oc[jj] = CP_DUPLICATE;
                 } else if (tid < f && kind == 1) {
@@ -1246,7 +1248,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     sflag[slot] = 3; snew[js] = slot; seq[rj] = slot;
                     // id / len / last_used are read by later decisions; origin and hashes are written by
                     // the parallel write-back (no global loads on this path)
-                    a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_last[slot] = a.t;
+                    a.slot_id[slot] = id; a.slot_len[slot] = m; a.slot_last[slot] = tnow;
                     a.out_tmp[js] = slot; a.out_oc[js] = n > 0 ? CP_SUPERSEDED : CP_STORED;
                     PROF_CNT(13, 1);
                     // LRU eviction: victim = min (last_used, id) among live entries (R#21)
@@ -1556,6 +1558,7 @@ __global__ void k_sess_validate(InsArgs a) {
 // the oracle's orc_index_insert_session.  Slots freed here go back to the free stack at the end (so an
 // evicted shared entry's slot keeps its prefix hash until k_ins_delete tombstones it).
 __global__ void __launch_bounds__(256) k_sess_commit(InsArgs a) {
+    const unsigned long long tnow = a.clock ? *a.clock : a.t;
     __shared__ int s_abort, s_go, s_nfree, s_ncopy, s_nrm;
     __shared__ long long s_live, s_pinned;
     __shared__ unsigned long long s_bl[8]; __shared__ int s_bi[8], s_bs[8];
@@ -1615,7 +1618,7 @@ __global__ void __launch_bounds__(256) k_sess_commit(InsArgs a) {
                     h->fifo_head = (h->fifo_head + 1) % P32; h->fifo_count--;
                     a.slot_pages[(int64_t)slot * a.MP + i] = pg; a.page_owner[pg] = slot;
                 }
-                a.slot_id[slot] = id; a.slot_len[slot] = n; a.slot_origin[slot] = 0; a.slot_last[slot] = a.t;
+                a.slot_id[slot] = id; a.slot_len[slot] = n; a.slot_origin[slot] = 0; a.slot_last[slot] = tnow;
                 a.slot_prefix[slot] = 0; a.slot_full[slot] = 0; a.slot_owner[slot] = o;
                 a.slot_state[slot] = CP_SLOT_LIVE;
                 a.session_slot[o] = slot;
@@ -1877,6 +1880,12 @@ cp_status cp_index_destroy(cp_index* x) {
 
 uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
 
+cp_status cp_index_set_clock(cp_index* x, const uint64_t* d_clock) {
+    if (!x || x->is_view) return CP_ERR_INVALID_ARG;
+    x->clock = reinterpret_cast<const unsigned long long*>(d_clock);
+    return CP_OK;
+}
+
 cp_status cp_pin_links(cp_index* x, const int32_t* pages, int64_t n, int32_t delta, void* stream) {
     if (!x || (n > 0 && !pages) || n < 0 || (delta != 1 && delta != -1)) return CP_ERR_INVALID_ARG;
     if (n == 0) return CP_OK;
@@ -2072,7 +2081,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
         if (fs < 0) { const char* e = getenv("CP_COMMIT_SERIAL"); fs = (e && atoi(e) != 0) ? 1 : 0; }
         a.force_serial = fs;
     }
-    a.CH = x->CH; a.max_blocks = kv->max_blocks_per_req;
+    a.CH = x->CH; a.max_blocks = kv->max_blocks_per_req; a.clock = x->clock;
     if (a.max_blocks < 1) return CP_ERR_INVALID_ARG;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
     // shared memory of the commit: flags + per-span arrays, then the LRU candidate list (4096 halved to
@@ -2200,7 +2209,7 @@ cp_status cp_index_insert_session(cp_index* x, const cp_batch* wb, const cp_page
     a.session = wb->session; a.session_slot = x->session_slot; a.max_sessions = x->cfg.max_sessions;
     a.removed = x->removed; a.rm_pos = x->rm_pos; a.out_tmp = x->out_tmp;
     a.cp_req = x->cp_req; a.cp_slot = x->cp_slot; a.cp_dst = x->cp_dst; a.cp_len = x->cp_len; a.cp_delta = x->cp_delta;
-    a.max_blocks = kv->max_blocks_per_req;
+    a.max_blocks = kv->max_blocks_per_req; a.clock = x->clock;
     cudaStream_t st = (cudaStream_t)stream;
     cp_invalidate_worklist(x);
     k_sess_validate<<<std::max(1, std::min(148, (wb->num_reqs + 255) / 256)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();

@@ -100,6 +100,7 @@ struct cp_index {
     int insert_prepared = 0;   // cp_index_insert_prepare issued, commit pending (host-side guard)
     int is_view = 0;           // a pool view (cp_index_create_view): own geometry + pool, the base's META/SCRATCH
     WorkKey* wk = nullptr;     // owned by the base, shared by its views
+    const unsigned long long* clock = nullptr;         // cp_index_set_clock (device logical time)
     cudaStream_t side = nullptr;                       // the insert's SHA-256 digests run here, beside the copy-in
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // (owned by the base)
     int32_t S;           // slots

@@ -52,6 +52,7 @@ struct MatchArgs {
     // R#33 same-user sessions (session == nullptr: none)
     const int32_t* session; const int32_t* session_slot; const int32_t* slot_owner; const uint8_t* slot_state;
     int32_t max_sessions;
+    const unsigned long long* clock;   // cp_index_set_clock: logical time read on the device (else t)
 };
 
 struct MatchSmem {
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             a.sp_dst[base + i] = hk[i];
             a.sp_len[base + i] = hm[i];
             a.sp_delta[base + i] = hk[i] - __ldg(a.slot_origin + slot);      // R#11
-            if (!a.no_touch) atomicMax(a.slot_last + slot, a.t);
+            if (!a.no_touch) atomicMax(a.slot_last + slot, a.clock ? *a.clock : a.t);
         }
         // ---- plan codes (0 uncovered / 1 reused / 2 recompute) and stats
         int cov = 0, rec = 0;
@@ -420,7 +421,7 @@ extern "C" cp_status cp_match_spans(cp_index* x, const cp_batch* b, uint64_t t, 
     MatchArgs a;
     std::memset(&a, 0, sizeof(a));
     a.hdr = x->hdr; a.tokens = b->tokens; a.offsets = b->offsets; a.mask = b->mask; a.R = b->num_reqs;
-    a.t = t; a.no_touch = (flags & CP_MATCH_NO_TOUCH) ? 1 : 0;
+    a.t = t; a.no_touch = (flags & CP_MATCH_NO_TOUCH) ? 1 : 0; a.clock = x->clock;
     a.policy = (flags & CP_MATCH_FIXED_CHUNK) ? 1 : (flags & CP_MATCH_PREFIX_ONLY) ? 2 : 0;
     a.w = x->cfg.window_len; a.B = x->B; a.Bw = x->Bw; a.pw = x->pw;
     a.htab = x->htab; a.logT = x->logT; a.T = x->T;

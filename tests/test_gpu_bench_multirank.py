@@ -81,3 +81,21 @@ def test_two_rank_balanced_bench_runs():
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "balanced-sharded x2"
+
+
+def test_cuda_graph_step_matches_the_eager_step():
+    """The timed steps are replays of one captured step (device clock, cp_index_set_clock): the same
+    hits, coverage and byte counts as eager steps, no device error; the line says which it used."""
+    outs = {}
+    for flag in ([], ["--no-graph"]):
+        cmd = [sys.executable, "bench.py", "--steps", "4", "--warmup", "3", "--scale", "0.1", "--no-cpu-baseline",
+               "--no-extra"] + flag
+        out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-3000:]
+        outs[bool(flag)] = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    g, e = outs[False], outs[True]
+    assert g["config"]["cuda_graph"] is True and e["config"]["cuda_graph"] is False
+    for k in ("covered_tokens", "reused_tokens", "recompute_tokens", "hits"):
+        assert g[k] == e[k], k
+    assert g["roofline"]["algorithmic_bytes_per_launch"] == e["roofline"]["algorithmic_bytes_per_launch"]
+    assert g["gpu_launches"] == e["gpu_launches"]

@@ -191,8 +191,12 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     const int tpr = rowE / (2 * VEC);                   // tasks per token row
     const bool zero_rec = (a.flags & CP_ZERO_RECOMPUTE) != 0;
     const int64_t pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
-    // CREG (tpr divides the block): a thread's column task, and so its cos/sin, is fixed
+    // CREG (tpr <= block): the block's first A = floor(256 / tpr) * tpr threads work with a task stride
+    // of A, so a thread's column task, and so its cos/sin, is fixed; the other 256 - A threads only
+    // stage the row table (A = 256 when tpr divides the block; 240 for the 3- and 6-head rectangles of
+    // the balanced layout, whose per-task column arithmetic cost ~10% per unit without this)
     constexpr bool creg = CREG;
+    const int A = creg ? (kRowsThreads / tpr) * tpr : kRowsThreads;
     auto task_geom = [&](int j, int& lo, int& hi, int& i0) {
         if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; hi = lo + half; i0 = sub * VEC; }
         else { lo = j * 2 * VEC; hi = lo + VEC; i0 = (lo % a.d) / 2; }
@@ -235,14 +239,14 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
         __syncthreads();
         // task = ((token g * nl) + layer ll) * tpr + column j  -> j = tid % tpr when tpr | block
         const int ntask = ntok * nl * tpr;
-        for (int base = 0; base < ntask; base += kRowsThreads * UNROLL) {
+        for (int base = 0; base < ntask; base += A * UNROLL) {
             uint4 klo[UNROLL], khi[UNROLL], vlo[UNROLL], vhi[UNROLL];
             int gl[UNROLL], code[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
-                const int task = base + u * kRowsThreads + tid;
+                const int task = base + u * A + tid;
                 code[u] = -1;
-                if (task < ntask) {
+                if (tid < A && task < ntask) {
                     const int row = task / tpr;                 // (g, ll) flattened
                     const int g = row / nl, ll = row - g * nl;
                     int lo = lo_t, hi = hi_t, i0 = i0_t;
@@ -630,7 +634,7 @@ cp_status launch_rows_t(const RowsArgs& a, int variant, cudaStream_t st) {
     const int tpr = a.H * a.d / (2 * VEC);
     if (variant == 4 && launch_rows_tma<T, G>(a, st)) return CP_OK;
     if (variant == 4) variant = 0;
-    return (kRowsThreads % tpr == 0) ? launch_rows_c<T, G, true>(a, variant, st) : launch_rows_c<T, G, false>(a, variant, st);
+    return (tpr <= kRowsThreads) ? launch_rows_c<T, G, true>(a, variant, st) : launch_rows_c<T, G, false>(a, variant, st);
 }
 
 int g_variant = -1;

@@ -758,9 +758,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     //      this list, skipping entries removed or refreshed since; the block-wide arg-min remains the
     //      fallback (list exhausted, non-monotone time, K = 0).
     __shared__ unsigned long long s_minl, s_maxl;
+    __shared__ unsigned s_idmin, s_idmax;
     __shared__ int s_cn, s_cp, s_heap, s_hist[256], s_digit, s_rem2;
     __shared__ long long s_pending;
-    if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_cn = 0; s_cp = 0; s_heap = 0; s_pending = 0; }
+    if (tid == 0) { s_minl = ~0ULL; s_maxl = 0; s_idmin = 0xffffffffu; s_idmax = 0; s_cn = 0; s_cp = 0; s_heap = 0; s_pending = 0; }
     __syncthreads();
     {   // upper bound of the tokens this call can still store: if it fits the budget, no eviction happens
         long long pend = 0;
@@ -770,32 +771,65 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     __syncthreads();
     if (a.candK > 0 && s_live_tokens + s_pending > a.capacity) {
+        // one pass: ranges of last_used and id over the evictable (live, unpinned) entries
         unsigned long long mn = ~0ULL, mx = 0;
+        unsigned idmn = 0xffffffffu, idmx = 0;
         for (int sl = tid; sl < a.nslots; sl += blockDim.x)
-            if ((sflag[sl] & 1) && a.slot_pin[sl] == 0) { const unsigned long long lu = a.slot_last[sl]; mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx; }
+            if ((sflag[sl] & 1) && a.slot_pin[sl] == 0) {
+                const unsigned long long lu = a.slot_last[sl];
+                const unsigned id = (unsigned)a.slot_id[sl];
+                mn = lu < mn ? lu : mn; mx = lu > mx ? lu : mx;
+                idmn = id < idmn ? id : idmn; idmx = id > idmx ? id : idmx;
+            }
         for (int o = 16; o; o >>= 1) {
             const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, mn, o), b2 = __shfl_xor_sync(0xffffffffu, mx, o);
             mn = a2 < mn ? a2 : mn; mx = b2 > mx ? b2 : mx;
+            const unsigned c2 = __shfl_xor_sync(0xffffffffu, idmn, o), d2 = __shfl_xor_sync(0xffffffffu, idmx, o);
+            idmn = c2 < idmn ? c2 : idmn; idmx = d2 > idmx ? d2 : idmx;
         }
-        if ((tid & 31) == 0) { atomicMin(&s_minl, mn); atomicMax(&s_maxl, mx); }
+        if ((tid & 31) == 0) { atomicMin(&s_minl, mn); atomicMax(&s_maxl, mx); atomicMin(&s_idmin, idmn); atomicMax(&s_idmax, idmx); }
         __syncthreads();
+        PROF_T(10);
         const bool ok = s_maxl >= s_minl && (s_maxl - s_minl) < (1ULL << 32) && tnow >= s_maxl;
         if (ok) {
             const unsigned long long minl = s_minl;
-            auto keyof = [&](int sl) -> unsigned long long {
-                return ((a.slot_last[sl] - minl) << 32) | (unsigned long long)(uint32_t)a.slot_id[sl];
+            const unsigned idmin = s_idmin;
+            // the radix select runs on a compact key with the same order: (last - minl) << idb | (id - idmin),
+            // idb = bits of the id range, so only the digits the keys can differ in are scanned (config-5
+            // churn: ~3 passes instead of 8 over the slot table)
+            const int idb = 32 - __clz((int)(s_idmax - idmin) | 1);
+            const int kb = idb + (64 - __clzll((long long)((s_maxl - minl) | 1)));
+            const int top = ((kb + 7) / 8 - 1) * 8;
+            auto ckeyof = [&](unsigned long long lu, unsigned id) -> unsigned long long {
+                return ((lu - minl) << idb) | (unsigned long long)(id - idmin);
             };
-            // radix-select the K-th smallest key (8-bit digits, MSB first)
             unsigned long long prefix = 0, pmask = 0;
             if (tid == 0) s_rem2 = a.candK;
             __syncthreads();
-            for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int shift = top; shift >= 0; shift -= 8) {
                 for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0;
                 __syncthreads();
-                for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
-                    if (!(sflag[sl] & 1) || a.slot_pin[sl] > 0) continue;      // pinned: never evicted (R#32)
-                    const unsigned long long k = keyof(sl);
-                    if ((k & pmask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+                // 4 slots per thread in flight (their loads are issued before any histogram update); the
+                // lanes of a warp that fall in one bin add once (most keys share the leading digits: plain
+                // shared atomics on one bin serialise 32-way)
+                for (int s0 = tid & ~31; s0 < a.nslots; s0 += 4 * blockDim.x) {     // warp-uniform trip count
+                    unsigned long long lu[4]; unsigned id[4]; bool on[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int sl = s0 + u * blockDim.x + (tid & 31);
+                        on[u] = sl < a.nslots && (sflag[sl] & 1);
+                        if (on[u]) { on[u] = a.slot_pin[sl] == 0; lu[u] = a.slot_last[sl]; id[u] = (unsigned)a.slot_id[sl]; }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        int bin = -1;                                           // pinned: never evicted (R#32)
+                        if (on[u]) {
+                            const unsigned long long k = ckeyof(lu[u], id[u]);
+                            if ((k & pmask) == prefix) bin = (int)((k >> shift) & 255);
+                        }
+                        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+                        if (bin >= 0 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
+                    }
                 }
                 __syncthreads();
                 if (tid == 0) {
@@ -812,15 +846,64 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 __syncthreads();
             }
             const unsigned long long T = prefix;                   // K-th smallest (or the max if fewer live)
-            for (int sl = tid; sl < a.nslots; sl += blockDim.x) {
-                if (!(sflag[sl] & 1) || a.slot_pin[sl] > 0) continue;
-                const unsigned long long k = keyof(sl);
-                if (k <= T) { const int p = atomicAdd(&s_cn, 1); if (p < a.candK) { ckey[p] = k; cslot[p] = sl; clen[p] = a.slot_len[sl]; } }
+            PROF_T(11);
+            for (int s0 = tid & ~31; s0 < a.nslots; s0 += blockDim.x) {       // warp-uniform trip count
+                const int sl = s0 + (tid & 31);
+                bool take = false;
+                unsigned long long lu = 0;
+                unsigned id = 0;
+                if (sl < a.nslots && (sflag[sl] & 1) && a.slot_pin[sl] == 0) {
+                    lu = a.slot_last[sl]; id = (unsigned)a.slot_id[sl];
+                    take = ckeyof(lu, id) <= T;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, take);            // one shared atomic per warp
+                int p0 = 0;
+                if ((tid & 31) == 0 && bal) p0 = atomicAdd(&s_cn, __popc(bal));
+                p0 = __shfl_sync(0xffffffffu, p0, 0);
+                if (take) {
+                    const int p = p0 + __popc(bal & ((1u << (tid & 31)) - 1));
+                    if (p < a.candK) {
+                        if (kb <= 32) ckey[p] = (ckeyof(lu, id) << 32) | (unsigned)sl;   // packed: one 64-bit sort key
+                        else { ckey[p] = ((lu - minl) << 32) | id; cslot[p] = sl; clen[p] = a.slot_len[sl]; }
+                    }
+                }
             }
             __syncthreads();
             const int cn = min(s_cn, a.candK);
+            if (kb <= 32) {
+                // (compact key, slot) packed in 64 bits; sort only the next power of two above cn; one
+                // thread per compare-exchange pair (the 3-array, thread-per-element form was ~140 us per
+                // evicting batch on config-5 churn)
+                int Kp = 2;
+                while (Kp < cn) Kp <<= 1;
+                for (int p = cn + tid; p < Kp; p += blockDim.x) ckey[p] = ~0ULL;
+                __syncthreads();
+                PROF_T(12);
+                for (int kk = 2; kk <= Kp; kk <<= 1)
+                    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                        for (int pr = tid; pr < Kp / 2; pr += blockDim.x) {
+                            const int i2 = 2 * jj * (pr / jj) + (pr % jj), ix = i2 + jj;
+                            const bool up = (i2 & kk) == 0;
+                            const unsigned long long x = ckey[i2], y = ckey[ix];
+                            if ((x > y) == up) { ckey[i2] = y; ckey[ix] = x; }
+                        }
+                        __syncthreads();
+                    }
+                // unpack to the list format the pops read: ((last - minl) << 32 | id, slot, length)
+                const unsigned long long idmask = (1ULL << idb) - 1;
+                for (int p = tid; p < a.candK; p += blockDim.x) {
+                    if (p < cn) {
+                        const unsigned long long sk = ckey[p], ck = sk >> 32;
+                        const int sl = (int)(sk & 0xffffffffu);
+                        ckey[p] = ((ck >> idb) << 32) | ((ck & idmask) + idmin);
+                        cslot[p] = sl; clen[p] = a.slot_len[sl];
+                    } else { ckey[p] = ~0ULL; cslot[p] = -1; clen[p] = 0; }
+                }
+                __syncthreads();
+            } else {
             for (int p = cn + tid; p < a.candK; p += blockDim.x) { ckey[p] = ~0ULL; cslot[p] = -1; clen[p] = 0; }
             __syncthreads();
+            PROF_T(12);
             // bitonic sort of the K candidates by key (keys are unique)
             for (int kk = 2; kk <= a.candK; kk <<= 1)
                 for (int jj = kk >> 1; jj > 0; jj >>= 1) {
@@ -838,6 +921,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                     }
                     __syncthreads();
                 }
+            }
             if (tid == 0) { s_cn = cn; s_heap = 1; }
         }
         __syncthreads();
@@ -959,6 +1043,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __syncthreads();
     for (int j = tid; j < Sn; j += blockDim.x) atomicMax(&a.f_last[srep[j]], j);
     __syncthreads();
+    PROF_T(5);
     for (int r = tid; r < Sn; r += blockDim.x) {                 // decision of each content vs the initial pool
         if (srep[r] != r) continue;
         int dup = -1, cont = -1, cont_id = INT_MAX, nsup = 0, suptok = 0, suppg = 0;
@@ -993,6 +1078,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __syncthreads();
     for (int i = tid; i < NSl; i += blockDim.x) if (a.f_supby[i] >= 0 && a.f_refs[i] > 1) { s_fast = 0; atomicOr(&s_why, 8); }
     __syncthreads();
+    PROF_T(6);
     if (s_fast) {
         // store order: exclusive scan of the storing contents (a content is stored by its first span)
         const int ns = block_excl_scan<kCommitThreads>(a.f_sidx, Sn, s_wsum);
@@ -1013,6 +1099,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         const long long totnet = block_excl_scan64<kCommitThreads>(a.f_netpref, ns, s_s64);
         (void)totpg; (void)totsup; (void)totsuppg; (void)totnet;
         __syncthreads();
+        PROF_T(7);
         // ---- LRU: the victims, in candidate-list order, that the sequential evictions would pop
         const long long L0 = s_live_tokens;
         bool evict = false;
@@ -1087,6 +1174,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if (end > s_count0 + app) { s_fast = 0; atomicOr(&s_why, 512); }
         }
         __syncthreads();
+        PROF_T(8);
     }
     if (s_fast) {
         // ---- apply (nothing above changed the index)
@@ -1153,6 +1241,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             atomicAdd(&a.hdr->commits_parallel, 1);
         }
         __syncthreads();
+        PROF_T(9);
     } else if (tid == 0) {
         atomicAdd(&a.hdr->commits_serial, 1);
         atomicOr(&a.hdr->commit_why, s_why);

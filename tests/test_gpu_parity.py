@@ -83,6 +83,21 @@ def test_70b_head_shard():
     assert rep.ok, rep.notes[:10]
 
 
+@pytest.mark.parametrize("h0,h1", [(0, 3), (2, 8), (1, 6), (4, 5)])
+def test_head_ranges_of_the_balanced_layout_config3(h0, h1):
+    """The balanced layout's partial-layer rectangles hold 1-7 KV heads: 3, 5 and 6 heads give 24, 40 and
+    48 column tasks per token row, which do not divide the 256-thread CTA (the copy kernel then runs on
+    its first 240 threads with a fixed column per thread).  Config 3 (moved hits: re-rotated K)."""
+    wl = make_workload(3, scale=0.05)
+    case = Case(wl, layer_range=(30, 32), head_range=(h0, h1), sample_reqs=3)
+    rep = ParityReport()
+    wb, rb = wl.rounds[0]
+    case.insert(wb, rep, sparse_kv=True)
+    case.match_and_gather(rb, rep)
+    assert rep.ok, rep.notes[:10]
+    assert rep.stats["moved_hits"] > 0
+
+
 def test_churn_config5_reduced_with_eviction():
     """Config 5 shape with a small token budget so LRU eviction, duplicates and supersedes happen."""
     wl = make_workload(5, scale=0.02)          # 1 batch... scale rounds up below

@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-3 and config-5 keys of the line")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of CUDA-graph replays")
+    ap.add_argument("--rects-launch", choices=["one", "per"], default="one",
+                    help="balanced layout: gather every rectangle of the rank in one launch (cp_gather_rerotate_rects) "
+                         "or one launch per rectangle (views with CP_REUSE_WORKLIST)")
     ap.add_argument("--out", default="")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (profiling runs only)")
     ap.add_argument("--overlap", type=int, default=3, choices=[0, 1, 2, 3],
@@ -285,6 +288,7 @@ def setup_ours(args, rank, world, device):
     S.link_tab = torch.full((rb.num_reqs, max(nb)), -1, dtype=torch.int32, device=device)
     S.side = torch.cuda.Stream(device=device)
     S.overlap = int(getattr(args, "overlap", 3))
+    S.rects_launch = getattr(args, "rects_launch", "one")
     S.ev_score_done = torch.cuda.Event()
     S.ev_gather_done = torch.cuda.Event()
     S.ev_prep_done = torch.cuda.Event()
@@ -371,11 +375,15 @@ def run_step(S, torch, cp, world, events=None):
     if S.link:                                                                     # NEXT-2
         S.idx.link_blocks(S.rdb, S.hits, S.link_tab.shape[1], out=S.link_tab)
     zr, zu, sk = S.placeholders in ("both", "recompute"), S.placeholders == "both", S.placeholders == "none"
-    S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
-                          skip_recompute=sk)                                                          # N2
-    for v, dkv in zip(S.views, S.dsts[1:]):                                        # the rank's other rectangles
-        v.gather_rerotate(S.rdb, S.hits, dkv, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
-                          skip_recompute=sk, reuse_worklist=True)
+    if S.views and S.rects_launch == "one":                                       # N2, every rectangle in one launch
+        S.idx.gather_rerotate_rects(S.views, S.rdb, S.hits, S.dsts, zero_recompute=zr, zero_uncovered=zu,
+                                    skip_linked=S.link, skip_recompute=sk)
+    else:
+        S.idx.gather_rerotate(S.rdb, S.hits, S.dst, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
+                              skip_recompute=sk)                                                      # N2
+        for v, dkv in zip(S.views, S.dsts[1:]):                                    # the rank's other rectangles
+            v.gather_rerotate(S.rdb, S.hits, dkv, zero_recompute=zr, zero_uncovered=zu, skip_linked=S.link,
+                              skip_recompute=sk, reuse_worklist=True)
     if ev: ev[2].record()
     if S.overlap == 3:
         if scores:
@@ -584,7 +592,7 @@ def bench_ours(args):
             del S.dst, S.dsts, S.ins_kvs, S.ins_kv, S.idx, S.views, S.attn
             torch.cuda.empty_cache()
             extras["config3"] = extra_config3(args, torch, cp, device)
-            extras["config5"] = extra_config5(torch, cp, device)
+            extras["config5"] = extra_config5_n8(torch, cp, device)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -596,6 +604,7 @@ def bench_ours(args):
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "placeholders": S.placeholders, "cuda_graph": S.graph is not None,
+                       **({"rects_launch": S.rects_launch} if S.views else {}),
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
                        **({"dist_backend": dist.get_backend()} if use_dist else {}),
                        "shard_rects": [[r.layer_lo, r.layer_hi, r.head_lo, r.head_hi] for r in S.rects],
@@ -767,9 +776,10 @@ def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000, re
             ev[7].record(side)
         hits = idx.match_spans(db, t)
         ev[1].record(main)
-        idx.gather_rerotate(db, hits, kvs[0], zero_recompute=True, zero_uncovered=True)
-        for v, kv in zip(views, kvs[1:]):
-            v.gather_rerotate(db, hits, kv, zero_recompute=True, zero_uncovered=True, reuse_worklist=True)
+        if views:
+            idx.gather_rerotate_rects(views, db, hits, kvs, zero_recompute=True, zero_uncovered=True)
+        else:
+            idx.gather_rerotate(db, hits, kvs[0], zero_recompute=True, zero_uncovered=True)
         ev[2].record(main)
         if owner:
             cp.score_deviation(*sargs, 1, 4, out_scores=scores, out_bits=bits)
@@ -829,6 +839,25 @@ def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000, re
     del idx, kvs, views
     torch.cuda.empty_cache()
     return out
+
+
+def extra_config5_n8(torch, cp, device):
+    """Config 5 at N = 8 in the balanced layout (tools/churn_scaling.py): the rank with the most
+    (layer, KV head) units and the N3 owner, each run alone on this GPU; the projected 8-GPU step is the
+    max of the two (the other ranks hold as many or fewer units and no N3)."""
+    from paper_2605_23640_b200.shard import balanced_units, make_layout
+    u = balanced_units(8, 32, 8, N3_UNITS[5])
+    big = max(range(7), key=lambda r: (u[r][1] - u[r][0], -r))
+    main = extra_config5(torch, cp, device, rects=make_layout(big, 8, 32, 8, "balanced", N3_UNITS[5]), owner=False)
+    own = extra_config5(torch, cp, device, rects=make_layout(7, 8, 32, 8, "balanced", N3_UNITS[5]), owner=True)
+    main["workload"] = (f"high_churn (BASELINE configs[4]) at N = 8, balanced layout (n3_units {N3_UNITS[5]}): rank "
+                        f"{big} ({main['units']} units, the most) and rank 7 (the N3 owner) of Llama-3-8B KV, each run "
+                        "alone on this GPU")
+    main["rank"] = big
+    main["owner_rank"] = {k: own[k] for k in ("rects", "units", "per_batch_median", "stored_per_batch",
+                                               "evicted_per_batch", "copy_in_bytes_per_batch")}
+    main["projected_step_ms_n8"] = round(max(main["per_batch_median"]["step_ms"], own["per_batch_median"]["step_ms"]), 4)
+    return main
 
 
 def e2e_ours(S, torch, cp, world, K, reused_all, dist):

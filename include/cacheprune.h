@@ -284,6 +284,22 @@ cp_status cp_gather_rerotate(cp_index* idx, const cp_batch* readers_h, const cp_
                              const cp_paged_kv* dst_kv_h, int32_t flags, void* stream);
 
 /*
+ * cp_gather_rerotate for every rectangle of a rank in ONE launch of the persistent copy kernel (and one
+ * of the zero-placeholder kernel): the base index `idx` and `num_views` (<= 3) of its pool views
+ * (cp_index_create_view), destination caches dst_kv_h[0] (the base's geometry) and dst_kv_h[1 + i]
+ * (views_h[i]'s geometry); the results are exactly those of one cp_gather_rerotate per rectangle (the
+ * same kernels, rows and rotations; only the work of all rectangles shares one grid, so the launch has
+ * one ramp and one tail instead of one per rectangle).  Same passages, hit list and flags as
+ * cp_gather_rerotate (CP_REUSE_WORKLIST is not accepted: the call builds the list itself).  Requirements
+ * (CP_ERR_INVALID_ARG, no side effects otherwise): idx is not a view, every views_h[i] is a view of idx,
+ * every dst_kv_h[i] has the SAME block_tables pointer and width, the rectangles' layers total at most
+ * 128.  Device errors as cp_gather_rerotate.
+ */
+cp_status cp_gather_rerotate_rects(cp_index* idx, int32_t num_views, cp_index* const* views_h,
+                                   const cp_batch* readers_h, const cp_hits* hits_h, const cp_paged_kv* dst_kv_h,
+                                   int32_t flags, void* stream);
+
+/*
  * Recompute scores and top-rho selection for `num_spans` spans.  Span s uses the
  * final-layer attention attn_h[s] (device, fp32 [heads_h[s]][n_h[s]][n_h[s]] row-major), span
  * [span_l_h[s], span_r_h[s]] (inclusive).  For i in the span, with q(x) = trunc(x * 2^40) (R#17):

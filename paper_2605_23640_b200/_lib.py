@@ -74,6 +74,8 @@ EXPORTS = {
                                      vp, vp, vp]),
     "cp_match_spans": (i32, [vp, C.POINTER(CpBatch), u64, i32, C.POINTER(CpHits), vp]),
     "cp_gather_rerotate": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), C.POINTER(CpPagedKV), i32, vp]),
+    "cp_gather_rerotate_rects": (i32, [vp, i32, C.POINTER(vp), C.POINTER(CpBatch), C.POINTER(CpHits),
+                                       C.POINTER(CpPagedKV), i32, vp]),
     "cp_score_deviation": (i32, [i32, C.POINTER(vp), P_i32, P_i32, P_i32, P_i32, i32, i32, i32, i32,
                                  vp, P_i64, vp, P_i64, vp]),
     "cp_score_kv_deviation": (i32, [i32, P_i32, P_i32, P_i32, vp, vp, vp, i32, vp, vp, vp, i32, i32, i32, i32,

@@ -263,6 +263,21 @@ class KVIndex:
         L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
                 "cp_gather_rerotate")
 
+    def gather_rerotate_rects(self, views: Sequence["KVIndexView"], readers: DeviceBatch, hits: Hits,
+                              dst_kvs: Sequence[PagedKV], zero_recompute: bool = True, zero_uncovered: bool = False,
+                              skip_linked: bool = False, skip_recompute: bool = False, stream=None):
+        """cp_gather_rerotate_rects: this index's rectangle (dst_kvs[0]) and its pool views' (dst_kvs[1:],
+        one per view, all on one block table) in one launch."""
+        flags = ((L.CP_ZERO_RECOMPUTE if zero_recompute else 0) | (L.CP_ZERO_UNCOVERED if zero_uncovered else 0) |
+                 (L.CP_SKIP_LINKED if skip_linked else 0) | (L.CP_SKIP_RECOMPUTE if skip_recompute else 0))
+        if len(dst_kvs) != len(views) + 1:
+            raise ValueError("one destination cache per rectangle")
+        vh = (C.c_void_p * max(1, len(views)))(*[v.h for v in views])
+        kvs = (L.CpPagedKV * len(dst_kvs))(*[k.c() for k in dst_kvs])
+        rb, hc = readers.c(), hits.c()
+        L.check(L.lib().cp_gather_rerotate_rects(self.h, len(views), vh, C.byref(rb), C.byref(hc), kvs, flags,
+                                                 _stream(stream)), "cp_gather_rerotate_rects")
+
     def link_blocks(self, readers: DeviceBatch, hits: Hits, max_blocks: int, out: Optional[torch.Tensor] = None,
                     stream=None) -> torch.Tensor:
         """NEXT-2 (cp_link_blocks, R#31): int32 [R, max_blocks] pool page per linkable request block, -1

@@ -21,6 +21,7 @@ namespace {
 constexpr int kRowsThreads = 256;
 constexpr int kPrepThreads = 512;
 constexpr int kCodeLinked = 3;       // row-table code of a token in a linked block (CP_SKIP_LINKED): no load, no store
+constexpr int kMaxRects = 4;         // rectangles per launch (a balanced-layout rank holds at most 3)
 
 struct RowsArgs {
     DevHeader* hdr;
@@ -39,6 +40,11 @@ struct RowsArgs {
     int32_t* hit_coff;                                 // [hits] first chunk of each hit (k_rows_prep)
     long long* row_src; long long* row_dst;
     float2* hit_cs; int64_t cs_hits;
+    // several (layer, head) rectangles of one rank in one launch (cp_gather_rerotate_rects): rectangle r
+    // covers items [rect[r].item0, rect[r + 1].item0), its layers are paged_k/v[layer0 + l]; nrect == 1:
+    // the index's own rectangle (L, H, LG, pool_k/v above)
+    int32_t nrect;
+    struct Rect { char* pool_k; char* pool_v; int64_t item0; int32_t L, H, LG, layer0; } rect[kMaxRects + 1];
 };
 
 // k_rows_prep (one block): per-hit first chunk = exclusive scan of ceil(len/32) over the hit list, a
@@ -182,27 +188,41 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
     __shared__ long long s_item;
     if (cp_err_set(a.hdr)) return;
     const int nchunks = a.hdr->n_chunks;
-    const int ngroups = ML ? (a.L + a.LG - 1) / a.LG : a.L;
-    const int64_t items = (int64_t)nchunks * ngroups;
     const int tid = threadIdx.x;
-    const int rowE = a.H * a.d;                        // elements per token row
     const int half = a.d / 2;
     const int hv = half / VEC;                          // vectors per half head
-    const int tpr = rowE / (2 * VEC);                   // tasks per token row
     const bool zero_rec = (a.flags & CP_ZERO_RECOMPUTE) != 0;
-    const int64_t pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
+    // the rectangle's geometry: fixed for nrect == 1, switched per item otherwise (items of one
+    // rectangle are contiguous, so a CTA switches rarely)
+    int cur = -1, L = 0, LG = 1, layer0 = 0, ngroups = 1, rowE = 0, tpr = 1, A = kRowsThreads;
+    int64_t item0 = 0, pool_layer = 0;
+    const char* poolk = nullptr; const char* poolv = nullptr;
+    const int64_t items = a.nrect > 1 ? a.rect[a.nrect].item0 * nchunks
+                                      : (int64_t)nchunks * (ML ? (a.L + a.LG - 1) / a.LG : a.L);
     // CREG (tpr <= block): the block's first A = floor(256 / tpr) * tpr threads work with a task stride
     // of A, so a thread's column task, and so its cos/sin, is fixed; the other 256 - A threads only
     // stage the row table (A = 256 when tpr divides the block; 240 for the 3- and 6-head rectangles of
     // the balanced layout, whose per-task column arithmetic cost ~10% per unit without this)
     constexpr bool creg = CREG;
-    const int A = creg ? (kRowsThreads / tpr) * tpr : kRowsThreads;
     auto task_geom = [&](int j, int& lo, int& hi, int& i0) {
         if (!GPTJ) { const int head = j / hv, sub = j - head * hv; lo = head * a.d + sub * VEC; hi = lo + half; i0 = sub * VEC; }
         else { lo = j * 2 * VEC; hi = lo + VEC; i0 = (lo % a.d) / 2; }
     };
     int lo_t = 0, hi_t = 0, i0_t = 0;
-    task_geom(tid % tpr, lo_t, hi_t, i0_t);
+    auto set_rect = [&](int r) {
+        cur = r;
+        if (a.nrect > 1) {
+            L = a.rect[r].L; LG = ML ? a.rect[r].LG : 1; layer0 = a.rect[r].layer0; rowE = a.rect[r].H * a.d;
+            poolk = a.rect[r].pool_k; poolv = a.rect[r].pool_v; item0 = a.rect[r].item0 * nchunks;
+        } else {
+            L = a.L; LG = ML ? a.LG : 1; layer0 = 0; rowE = a.H * a.d; poolk = a.pool_k; poolv = a.pool_v; item0 = 0;
+        }
+        ngroups = (L + LG - 1) / LG;
+        tpr = rowE / (2 * VEC);                                         // tasks per token row
+        A = creg ? (kRowsThreads / tpr) * tpr : kRowsThreads;
+        pool_layer = a.P * CP_BLOCK * (int64_t)rowE;
+        task_geom(tid % tpr, lo_t, hi_t, i0_t);
+    };
     // DYN: items are taken from a device counter (one atomic per item and CTA), so CTAs that drew
     // short items (hit tails, zero placeholders) take more -- no static round-robin tail imbalance
     int64_t item = blockIdx.x;
@@ -212,9 +232,15 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
         item = s_item;
     }
     while (item < items) {
-        const int c = (int)(item / ngroups), lg = (int)(item % ngroups);
-        const int l0 = lg * a.LG;
-        const int nl = ML ? min(a.LG, a.L - l0) : 1;        // compile-time 1 on the single-layer path
+        {
+            int r = 0;
+            if (a.nrect > 1) while (r + 1 < a.nrect && item >= a.rect[r + 1].item0 * nchunks) ++r;
+            if (r != cur) set_rect(r);
+        }
+        const int li = (int)(item - item0);
+        const int c = li / ngroups, lg = li - c * ngroups;
+        const int l0 = lg * LG;
+        const int nl = ML ? min(LG, L - l0) : 1;            // compile-time 1 on the single-layer path
         const int hh = a.chunk_hit[c], t0 = a.chunk_t0[c];
         const int len = a.l_len[hh];
         const int ntok = min(CP_GATHER_CHUNK, len - t0);
@@ -248,15 +274,15 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
                 code[u] = -1;
                 if (tid < A && task < ntask) {
                     const int row = task / tpr;                 // (g, ll) flattened
-                    const int g = row / nl, ll = row - g * nl;
+                    const int g = (ML && nl > 1) ? row / nl : row, ll = row - g * nl;
                     int lo = lo_t, hi = hi_t, i0 = i0_t;
                     if (!creg) task_geom(task - row * tpr, lo, hi, i0);
                     gl[u] = creg ? row : task;
                     code[u] = s_code[g] == kCodeLinked ? -1 : s_code[g];
                     if (code[u] >= 0 && !(code[u] == CP_PLAN_RECOMPUTE && zero_rec)) {
                         const int l = l0 + ll;
-                        const T* srcK = (const T*)(a.dir == 0 ? a.pool_k + l * pool_layer * sizeof(T) : a.paged_k[l]);
-                        const T* srcV = (const T*)(a.dir == 0 ? a.pool_v + l * pool_layer * sizeof(T) : a.paged_v[l]);
+                        const T* srcK = (const T*)(a.dir == 0 ? poolk + l * pool_layer * sizeof(T) : a.paged_k[layer0 + l]);
+                        const T* srcV = (const T*)(a.dir == 0 ? poolv + l * pool_layer * sizeof(T) : a.paged_v[layer0 + l]);
                         const int64_t so = s_src[g];
                         klo[u] = ld_stream(srcK + so + lo); khi[u] = ld_stream(srcK + so + hi);
                         vlo[u] = ld_stream(srcV + so + lo); vhi[u] = ld_stream(srcV + so + hi);
@@ -268,9 +294,9 @@ __global__ void __launch_bounds__(kRowsThreads, MINB) k_rows(RowsArgs a) {
                 if (code[u] < 0) continue;
                 int lo = lo_t, hi = hi_t, i0 = i0_t, row = gl[u];
                 if (!creg) { row = gl[u] / tpr; task_geom(gl[u] - row * tpr, lo, hi, i0); }
-                const int g = row / nl, l = l0 + (row - g * nl);
-                T* dstK = (T*)(a.dir == 0 ? a.paged_k[l] : a.pool_k + l * pool_layer * sizeof(T));
-                T* dstV = (T*)(a.dir == 0 ? a.paged_v[l] : a.pool_v + l * pool_layer * sizeof(T));
+                const int g = (ML && nl > 1) ? row / nl : row, l = l0 + (row - g * nl);
+                T* dstK = (T*)(a.dir == 0 ? a.paged_k[layer0 + l] : poolk + l * pool_layer * sizeof(T));
+                T* dstV = (T*)(a.dir == 0 ? a.paged_v[layer0 + l] : poolv + l * pool_layer * sizeof(T));
                 const int64_t dof = s_dst[g];
                 T* dk = dstK + dof;
                 T* dv = dstV + dof;
@@ -538,12 +564,16 @@ __global__ void __launch_bounds__(kRowsThreads) k_zero_uncovered(RowsArgs a, int
     __shared__ int64_t s_dst[32];
     __shared__ int s_on[32];
     if (cp_err_set(a.hdr)) return;
-    const int rowE = a.H * a.d;
+    // layers are flattened over the launch's rectangles (nrect > 1: paged_k/v[rect.layer0 + l])
+    const int Lt = a.nrect > 1 ? a.rect[a.nrect - 1].layer0 + a.rect[a.nrect - 1].L : a.L;
     const int nu = a.hdr->n_unc;
-    const int64_t items = (int64_t)((nu + 31) / 32) * a.L;
+    const int64_t items = (int64_t)((nu + 31) / 32) * Lt;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int64_t b = item / a.L;
-        const int l = (int)(item % a.L);
+        const int64_t b = item / Lt;
+        const int l = (int)(item % Lt);
+        int r = 0;
+        if (a.nrect > 1) while (r + 1 < a.nrect && l >= a.rect[r + 1].layer0) ++r;
+        const int rowE = (a.nrect > 1 ? a.rect[r].H : a.H) * a.d;
         if (threadIdx.x < 32) {
             const int64_t li = b * 32 + threadIdx.x;
             s_on[threadIdx.x] = 0;
@@ -632,7 +662,7 @@ template <typename T, bool G>
 cp_status launch_rows_t(const RowsArgs& a, int variant, cudaStream_t st) {
     constexpr int VEC = Vec<T>::N;
     const int tpr = a.H * a.d / (2 * VEC);
-    if (variant == 4 && launch_rows_tma<T, G>(a, st)) return CP_OK;
+    if (variant == 4 && a.nrect == 1 && launch_rows_tma<T, G>(a, st)) return CP_OK;
     if (variant == 4) variant = 0;
     return (tpr <= kRowsThreads) ? launch_rows_c<T, G, true>(a, variant, st) : launch_rows_c<T, G, false>(a, variant, st);
 }
@@ -648,7 +678,7 @@ int gather_variant() {
 cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int32_t* l_req, const int32_t* l_slot,
                          const int32_t* l_dst, const int32_t* l_len, const int32_t* l_delta, int64_t list_cap,
                          const int64_t* req_off, const uint8_t* plan, const cp_paged_kv* kv, int32_t flags,
-                         cudaStream_t st) {
+                         cudaStream_t st, int32_t nviews, cp_index* const* views, const cp_paged_kv* view_kvs) {
     RowsArgs a;
     std::memset(&a, 0, sizeof(a));
     a.hdr = x->hdr; a.dir = dir; a.count = d_count;
@@ -662,10 +692,41 @@ cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int
     a.pool_k = x->pool_k; a.pool_v = x->pool_v; a.P = x->P; a.slot_pages = x->slot_pages; a.MP = x->MP;
     a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim; a.theta = x->cfg.rope_theta;
     a.flags = flags; a.gptj = x->cfg.rope_style == CP_ROPE_GPTJ;
-    {
-        const int vec = x->cfg.dtype == CP_BF16 ? 8 : 4;
-        const int tpr = x->cfg.num_kv_heads * x->cfg.head_dim / (2 * vec);
-        a.LG = std::max(1, std::min(x->cfg.num_layers, 2048 / std::max(1, CP_GATHER_CHUNK * tpr)));
+    const int vec = x->cfg.dtype == CP_BF16 ? 8 : 4;
+    auto lg_of = [&](const cp_config& c) {
+        const int tpr = c.num_kv_heads * c.head_dim / (2 * vec);
+        return std::max(1, std::min(c.num_layers, 2048 / std::max(1, CP_GATHER_CHUNK * tpr)));
+    };
+    a.LG = lg_of(x->cfg);
+    a.nrect = 1;
+    if (nviews > 0) {
+        // the rank's other rectangles (pool views of x) in the same launch: one persistent grid, one tail
+        if (nviews + 1 > kMaxRects || !views || !view_kvs || x->is_view) return CP_ERR_INVALID_ARG;
+        int64_t groups = 0;
+        int layers = 0;
+        for (int r = 0; r <= nviews; ++r) {
+            const cp_index* v = r == 0 ? x : views[r - 1];
+            const cp_paged_kv* vk = r == 0 ? kv : &view_kvs[r - 1];
+            if (!v || (r > 0 && (!v->is_view || v->hdr != x->hdr))) return CP_ERR_INVALID_ARG;
+            if (v->cfg.head_dim != x->cfg.head_dim || v->cfg.dtype != x->cfg.dtype || v->cfg.rope_style != x->cfg.rope_style)
+                return CP_ERR_INVALID_ARG;
+            if (vk->block_tables != kv->block_tables || vk->max_blocks_per_req != kv->max_blocks_per_req ||
+                !vk->k_layers_h || !vk->v_layers_h) return CP_ERR_INVALID_ARG;
+            if (layers + v->cfg.num_layers > CP_MAX_LAYERS) return CP_ERR_INVALID_ARG;
+            auto& R = a.rect[r];
+            R.pool_k = v->pool_k; R.pool_v = v->pool_v; R.L = v->cfg.num_layers; R.H = v->cfg.num_kv_heads;
+            R.LG = lg_of(v->cfg); R.layer0 = layers; R.item0 = groups;
+            for (int l = 0; l < R.L; ++l) {
+                a.paged_k[layers + l] = (char*)vk->k_layers_h[l]; a.paged_v[layers + l] = (char*)vk->v_layers_h[l];
+                if (!a.paged_k[layers + l] || !a.paged_v[layers + l]) return CP_ERR_INVALID_ARG;
+            }
+            layers += R.L;
+            groups += (R.L + R.LG - 1) / R.LG;
+            a.LG = std::max(a.LG, R.LG);                    // the launch's template choice covers every rectangle
+            a.H = std::max(a.H, R.H);
+        }
+        a.rect[nviews + 1].item0 = groups;
+        a.nrect = nviews + 1;
     }
     a.chunk_hit = x->chunk_hit; a.chunk_t0 = x->chunk_t0; a.CH = x->CH; a.hit_coff = x->hit_coff;
     a.row_src = x->row_src; a.row_dst = x->row_dst;
@@ -702,8 +763,9 @@ extern "C" cp_status cp_set_gather_variant(int32_t v) {
     return CP_OK;
 }
 
-extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp_hits* h, const cp_paged_kv* kv,
-                                        int32_t flags, void* stream) {
+namespace {
+cp_status gather_rects(cp_index* x, const cp_batch* b, const cp_hits* h, const cp_paged_kv* kv, int32_t nviews,
+                       cp_index* const* views, const cp_paged_kv* view_kvs, int32_t flags, void* stream) {
     if (!x || !b || !h || !kv) return CP_ERR_INVALID_ARG;
     if (!kv->k_layers_h || !kv->v_layers_h || !kv->block_tables || !b->offsets) return CP_ERR_INVALID_ARG;
     if (!h->num_hits || !h->hit_req || !h->hit_slot || !h->hit_dst || !h->hit_len || !h->hit_delta || !h->plan)
@@ -712,7 +774,7 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
     if (b->num_reqs == 0) return CP_OK;
     cudaStream_t st = (cudaStream_t)stream;
     cp_status s = cp_launch_rows(x, 0, h->num_hits, h->hit_req, h->hit_slot, h->hit_dst, h->hit_len, h->hit_delta,
-                                 h->max_hits, b->offsets, h->plan, kv, flags, st);
+                                 h->max_hits, b->offsets, h->plan, kv, flags, st, nviews, views, view_kvs);
     if (s != CP_OK) return s;
     if (flags & CP_ZERO_UNCOVERED) {
         RowsArgs a;
@@ -721,6 +783,20 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
         a.block_tables = kv->block_tables; a.max_blocks = kv->max_blocks_per_req;
         for (int l = 0; l < x->cfg.num_layers; ++l) { a.paged_k[l] = (char*)kv->k_layers_h[l]; a.paged_v[l] = (char*)kv->v_layers_h[l]; }
         a.L = x->cfg.num_layers; a.H = x->cfg.num_kv_heads; a.d = x->cfg.head_dim;
+        a.nrect = 1;
+        if (nviews > 0) {                            // validated by cp_launch_rows above
+            int layers = 0;
+            for (int r = 0; r <= nviews; ++r) {
+                const cp_index* v = r == 0 ? x : views[r - 1];
+                const cp_paged_kv* vk = r == 0 ? kv : &view_kvs[r - 1];
+                a.rect[r].L = v->cfg.num_layers; a.rect[r].H = v->cfg.num_kv_heads; a.rect[r].layer0 = layers;
+                for (int l = 0; l < v->cfg.num_layers; ++l) {
+                    a.paged_k[layers + l] = (char*)vk->k_layers_h[l]; a.paged_v[layers + l] = (char*)vk->v_layers_h[l];
+                }
+                layers += v->cfg.num_layers;
+            }
+            a.nrect = nviews + 1;
+        }
         if (b->total_tokens > x->cfg.max_batch_tokens) return CP_ERR_INVALID_ARG;
         if (cudaMemsetAsync(&x->hdr->n_unc, 0, sizeof(x->hdr->n_unc), st) != cudaSuccess) return CP_ERR_CUDA;
         k_unc_list<<<sm_count() * 4, 256, 0, st>>>(x->hdr, h->plan, b->total_tokens, x->unc_list);
@@ -731,6 +807,19 @@ extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp
         if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     }
     return CP_OK;
+}
+}  // namespace
+
+extern "C" cp_status cp_gather_rerotate(cp_index* x, const cp_batch* b, const cp_hits* h, const cp_paged_kv* kv,
+                                        int32_t flags, void* stream) {
+    return gather_rects(x, b, h, kv, 0, nullptr, nullptr, flags, stream);
+}
+
+extern "C" cp_status cp_gather_rerotate_rects(cp_index* x, int32_t num_views, cp_index* const* views, const cp_batch* b,
+                                              const cp_hits* h, const cp_paged_kv* dst_kv, int32_t flags, void* stream) {
+    if (num_views < 0 || num_views + 1 > kMaxRects || (num_views > 0 && !views) || !dst_kv) return CP_ERR_INVALID_ARG;
+    if (!x || x->is_view || (flags & CP_REUSE_WORKLIST)) return CP_ERR_INVALID_ARG;
+    return gather_rects(x, b, h, &dst_kv[0], num_views, views, dst_kv + 1, flags, stream);
 }
 
 // ---- NEXT-2: zero-copy page linking (R#31) ---------------------------------------------------------

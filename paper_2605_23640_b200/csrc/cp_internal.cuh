@@ -168,7 +168,8 @@ inline int cp_sm_count() {
 cp_status cp_launch_rows(cp_index* x, int dir, const int32_t* d_count, const int32_t* l_req,
                          const int32_t* l_slot, const int32_t* l_dst, const int32_t* l_len,
                          const int32_t* l_delta, int64_t list_cap, const int64_t* req_off,
-                         const uint8_t* plan, const cp_paged_kv* kv, int32_t flags, cudaStream_t st);
+                         const uint8_t* plan, const cp_paged_kv* kv, int32_t flags, cudaStream_t st,
+                         int32_t nviews = 0, cp_index* const* views = nullptr, const cp_paged_kv* view_kvs = nullptr);
 inline void cp_invalidate_worklist(cp_index* x) { if (x && x->wk) x->wk->valid = 0; }
 
 // ---- device helpers ---------------------------------------------------------------------------

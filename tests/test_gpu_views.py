@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 from synth.gen import make_workload  # noqa: E402
-from tests.harness import Case  # noqa: E402
+from tests.harness import SENTINEL, Case  # noqa: E402
 
 
 def _slice_kv(cp, kv, l0, l1, h0, h1):
@@ -111,4 +111,27 @@ def test_balanced_rank_views_equal_slices_of_the_full_index(rank, world):
     with pytest.raises(L.CacheHitError):
         views[0].gather_rerotate(rdb, bh, other, reuse_worklist=True)       # a different block table
     views[0].gather_rerotate(rdb, bh, dsts[1], reuse_worklist=True)
+    assert base.last_error() == 0
+    # every rectangle in ONE launch (cp_gather_rerotate_rects): the same rows, bit for bit, with both
+    # placeholder modes
+    for zu in (False, True):
+        ref.gather_rerotate(rdb, fh, fdst, zero_uncovered=zu)
+        frows = _rows(fdst, bt, rb.lens)
+        d2 = []
+        for r in rects:
+            d = _slice_kv(cp, fdst, r.layer_lo, r.layer_hi, r.head_lo, r.head_hi)
+            d2.append(d)                             # sentinel-filled like fdst: rows no gather writes compare equal
+            for t in d.k + d.v:
+                t.fill_(SENTINEL)
+        base.gather_rerotate_rects(views, rdb, bh, d2, zero_uncovered=zu)
+        assert base.last_error() == 0
+        for d, r in zip(d2, rects):
+            for (fk_, fv_), (sk, sv) in zip(frows, _rows(d, bt, rb.lens)):
+                assert torch.equal(sk.view(torch.int16), fk_[r.layer_lo:r.layer_hi, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
+                assert torch.equal(sv.view(torch.int16), fv_[r.layer_lo:r.layer_hi, :, r.head_lo:r.head_hi].contiguous().view(torch.int16))
+    # refusals: a destination on another block table; a view passed as the base
+    with pytest.raises(L.CacheHitError):
+        base.gather_rerotate_rects(views, rdb, bh, [d2[0], other] + d2[2:])
+    with pytest.raises(L.CacheHitError):
+        views[0].gather_rerotate_rects([], rdb, bh, [d2[1]])
     assert base.last_error() == 0

@@ -604,7 +604,7 @@ def bench_ours(args):
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "placeholders": S.placeholders, "cuda_graph": S.graph is not None,
-                       **({"rects_launch": S.rects_launch} if S.views else {}),
+                       **({"rects_launch": S.rects_launch} if len(S.rects) > 1 else {}),
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
                        **({"dist_backend": dist.get_backend()} if use_dist else {}),
                        "shard_rects": [[r.layer_lo, r.layer_hi, r.head_lo, r.head_hi] for r in S.rects],

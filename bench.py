@@ -604,6 +604,7 @@ def bench_ours(args):
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "placeholders": S.placeholders, "cuda_graph": S.graph is not None,
+                       "build": cp._lib.lib().cp_build_info().decode(),
                        **({"rects_launch": S.rects_launch} if len(S.rects) > 1 else {}),
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
                        **({"dist_backend": dist.get_backend()} if use_dist else {}),

@@ -497,6 +497,10 @@ uint64_t cp_kernel_launch_count(void);
 
 const char* cp_status_string(cp_status s);
 
+/* Build provenance: "cp-src-sha256=<64 hex digits> arch=sm_100a" -- the SHA-256 of the sources and
+ * flags this library was compiled from (paper_2605_23640_b200/build.py source_hash()); static string. */
+const char* cp_build_info(void);
+
 #ifdef __cplusplus
 }
 #endif

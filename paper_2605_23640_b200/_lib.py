@@ -99,6 +99,7 @@ EXPORTS = {
     "cp_annotate_spans": (i32, [i32, C.POINTER(vp), P_i32, P_i32, C.POINTER(vp), i32, i32, vp, C.c_size_t,
                                 vp, vp, vp, vp, vp]),
     "cp_status_string": (C.c_char_p, [i32]),
+    "cp_build_info": (C.c_char_p, []),
 }
 
 _lib = None
@@ -115,6 +116,11 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        # provenance: the library must be the build of THESE sources (build.py source_hash)
+        from .build import source_hash
+        info = L.cp_build_info().decode()
+        if f"cp-src-sha256={source_hash()}" not in info:
+            raise RuntimeError(f"libcacheprune.so was built from other sources ({info}); run __graft_entry__.build()")
         _lib = L
     return _lib
 

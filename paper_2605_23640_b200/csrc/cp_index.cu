@@ -2015,6 +2015,11 @@ cp_status cp_index_commit_stats(cp_index* x, int32_t* out_h, void* stream) {
 
 uint64_t cp_kernel_launch_count(void) { return g_cp_launches.load(); }
 
+#ifndef CP_SRC_SHA256
+#define CP_SRC_SHA256 "unknown-unknown-unknown-unknown-unknown-unknown-unknown-unknown!"
+#endif
+const char* cp_build_info(void) { return "cp-src-sha256=" CP_SRC_SHA256 " arch=sm_100a"; }
+
 const char* cp_status_string(cp_status s) {
     switch (s) {
         case CP_OK: return "CP_OK";

@@ -32,6 +32,18 @@ def test_library_exports_every_declared_symbol():
         assert n in L.EXPORTS, f"binding does not declare {n}"
 
 
+def test_library_is_the_build_of_these_sources():
+    """Build provenance: the loaded library carries the SHA-256 of the current sources and flags."""
+    import __graft_entry__ as g
+    g.build()
+    from paper_2605_23640_b200 import _lib as L
+    from paper_2605_23640_b200.build import built_hash, source_hash
+    h = source_hash()
+    assert re.fullmatch(r"[0-9a-f]{64}", h)
+    assert built_hash() == h
+    assert L.lib().cp_build_info().decode() == f"cp-src-sha256={h} arch=sm_100a"
+
+
 def test_host_side_validation_without_gpu():
     from paper_2605_23640_b200 import _lib as L
     lib = L.lib()

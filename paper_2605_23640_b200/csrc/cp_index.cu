@@ -25,6 +25,8 @@ constexpr int kValThreads = 256;
 constexpr int kScanThreads = 256;
 constexpr int kCommitThreads = 1024;
 constexpr int kCommitRecCap = 8192;
+constexpr int kLruK = 4096;            // prepared LRU candidates (the commit's list capacity, candK <= this)
+constexpr int kLruBins = 2048;         // 11-bit radix digits; at most 3 passes (compact keys <= 33 bits)
 
 int64_t next_pow2(int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; }
 int ilog2(int64_t v) { int l = 0; while ((1LL << l) < v) ++l; return l; }
@@ -136,6 +138,9 @@ void compute_layout(const cp_config* c, Layout* L) {
     sput(4 * (size_t)(L->MS + 1) * 12 + 8 * (size_t)(L->MS + 1) + 4 * (size_t)S * 4 + 4 * 4097 * 4 + 8 * 4097 + 64);
     sput(4 * (size_t)(std::max<int64_t>(L->HS, L->MS) + 1));                 // 32 hit_coff (gather / copy-in)
     sput(8 * (size_t)c->max_batch_tokens);                                   // 33 unc_list (CP_ZERO_UNCOVERED)
+    // 34 prepared LRU list (k_lru_*): header, per-slot key snapshot, 3 x 2048-bin histograms, list /
+    // rank / sorted of kLruK candidates
+    sput(64 + 8 * (size_t)S + 4 * 3 * kLruBins + 8 * kLruK + 4 * kLruK + 8 * kLruK + 64);
     L->scr_size = o;
 }
 
@@ -165,6 +170,17 @@ __global__ void k_init(DevHeader* hdr, int32_t* slot_id, uint8_t* slot_state, in
 // ------------------------------------------------------------------------------------------
 // kernels: insert
 // ------------------------------------------------------------------------------------------
+// LRU candidate list prepared beside match + gather (k_lru_*, cp_index_insert_prepare): the K smallest
+// (last_used, id) keys of the live unpinned entries of a snapshot, sorted
+struct LruHdr {
+    unsigned long long minl, maxl;   // last_used range of the snapshot's evictable entries
+    unsigned idmin, idmax;           // their id range
+    int valid;                       // 1: the list below is usable by the commit that follows
+    int count;                       // entries with compact key <= the K-th smallest (<= K)
+    int all;                         // fewer evictable entries than K: all of them are listed
+    uint32_t pin_epoch;              // hdr->pin_epoch at the snapshot
+};
+
 struct InsArgs {
     DevHeader* hdr;
     const int32_t* tokens; const int64_t* offsets; const uint8_t* mask; int32_t num_reqs;
@@ -199,6 +215,8 @@ struct InsArgs {
     int32_t force_serial;   // CP_COMMIT_SERIAL=1: skip the parallel apply (A/B measurement, tests)
     const unsigned long long* clock;   // cp_index_set_clock: logical time read on the device (else t)
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
+    LruHdr* lru; unsigned long long* lru_key; unsigned* lru_hist; unsigned long long* lru_list;
+    unsigned* lru_rank; unsigned long long* lru_sorted;
     int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
 
@@ -587,6 +605,194 @@ __device__ unsigned long long g_commit_prof[16];
 
 // One CTA applies the spans in input order (exact sequential semantics of R#20-22).
 // sflag bit 0: live; bit 1: stored by this call.
+// ---- LRU candidate list, prepared beside match + gather (cp_index_insert_prepare, R#21) ----
+// The commit evicts in (last_used, id) order.  Instead of selecting the K smallest keys with one CTA
+// inside the commit (a radix select over the slot table and a K-element sort: ~135 us per evicting
+// config-5 batch), the prepare snapshots the evictable keys and selects + sorts them with the whole
+// grid: 11-bit MSB digits of the compact key ((last - minl) << idb | (id - idmin), <= 33 bits), a global
+// histogram per digit, then a rank-by-count sort.  The snapshot may precede this step's match, whose
+// touches only RAISE keys: the commit pops an entry only if its last_used still equals the listed one,
+// so the entries it accepts are exactly the smallest current keys below the list's threshold, in order
+// (an entry whose key rose is skipped; a pin since the snapshot, or a non-monotone clock, discards the
+// list and the commit selects in-kernel as before).
+struct LruGeom {
+    unsigned long long minl; unsigned idmin; int idb, kb, digits;
+    __device__ bool load(const LruHdr* h) {
+        if (!h->valid || h->minl > h->maxl || h->maxl - h->minl >= (1ULL << 32)) return false;
+        minl = h->minl; idmin = h->idmin;
+        idb = 32 - __clz((int)(h->idmax - h->idmin) | 1);
+        kb = idb + (64 - __clzll((long long)((h->maxl - h->minl) | 1)));
+        digits = (kb + 10) / 11;
+        return kb <= 33;
+    }
+    __device__ int hi(int p) const { return kb - 11 * p; }
+    __device__ int lo(int p) const { return max(0, kb - 11 * (p + 1)); }
+    __device__ unsigned long long ckey(unsigned long long last, int id) const {
+        return ((last - minl) << idb) | (unsigned long long)((unsigned)id - idmin);
+    }
+};
+
+// digits 0..upto-1 of the K-th smallest compact key, from the global histograms (every CTA computes the
+// same result; 256 threads); all = 1 when there are no more than K evictable entries
+__device__ void lru_select(const InsArgs& a, const LruGeom& g, int upto, unsigned long long& prefix, int& all) {
+    __shared__ int s_w[8], s_bin, s_rem, s_tot;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int rem = a.candK;
+    prefix = 0; all = 0;
+    for (int p = 0; p < upto; ++p) {
+        const unsigned* hist = a.lru_hist + p * kLruBins;
+        const int nb = 1 << (g.hi(p) - g.lo(p));
+        int own = 0;
+        for (int b = tid * 8; b < min(nb, tid * 8 + 8); ++b) own += hist[b];
+        int inc = own;
+        for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (lane == 31) s_w[wid] = inc;
+        __syncthreads();
+        int base = 0;
+        for (int w = 0; w < wid; ++w) base += s_w[w];
+        if (tid == 255) s_tot = base + inc;
+        const int excl = base + inc - own;
+        if (own > 0 && excl < rem && rem <= excl + own) {
+            int c = excl;
+            for (int b = tid * 8; b < min(nb, tid * 8 + 8); ++b) {
+                if (c + (int)hist[b] >= rem) { s_bin = b; s_rem = rem - c; break; }
+                c += hist[b];
+            }
+        }
+        __syncthreads();
+        if (p == 0 && s_tot <= a.candK) { all = 1; __syncthreads(); return; }
+        prefix = (prefix << (g.hi(p) - g.lo(p))) | (unsigned long long)s_bin;
+        rem = s_rem;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lru_init(InsArgs a) {
+    __shared__ unsigned long long s_sum;
+    if (threadIdx.x == 0) s_sum = 0;
+    __syncthreads();
+    unsigned long long sum = 0;
+    for (int j = threadIdx.x; j < a.S; j += blockDim.x) sum += (unsigned long long)max(0, a.span_len[j]);
+    atomicAdd(&s_sum, sum);
+    for (int i = threadIdx.x; i < 3 * kLruBins; i += blockDim.x) a.lru_hist[i] = 0;
+    for (int i = threadIdx.x; i < kLruK; i += blockDim.x) a.lru_rank[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LruHdr* h = a.lru;
+        h->minl = ~0ULL; h->maxl = 0; h->idmin = 0xffffffffu; h->idmax = 0; h->count = 0; h->all = 0;
+        h->pin_epoch = a.hdr->pin_epoch;
+        // only when this call may evict (the commit's own test is tighter: spans after its duplicates)
+        h->valid = (a.candK > 0 && a.candK <= kLruK && !cp_err_set(a.hdr) &&
+                    a.hdr->live_tokens + (long long)s_sum > a.capacity) ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lru_snap(InsArgs a) {
+    if (!a.lru->valid) return;
+    unsigned long long mn = ~0ULL, mx = 0;
+    unsigned imn = 0xffffffffu, imx = 0;
+    for (int sl = blockIdx.x * blockDim.x + threadIdx.x; sl < a.nslots; sl += gridDim.x * blockDim.x) {
+        unsigned long long k = ~0ULL;
+        if (a.slot_state[sl] == CP_SLOT_LIVE && a.slot_pin[sl] == 0) {
+            k = a.slot_last[sl];
+            const unsigned id = (unsigned)a.slot_id[sl];
+            mn = k < mn ? k : mn; mx = k > mx ? k : mx; imn = id < imn ? id : imn; imx = id > imx ? id : imx;
+        }
+        a.lru_key[sl] = k;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, mn, o), b2 = __shfl_xor_sync(0xffffffffu, mx, o);
+        const unsigned c2 = __shfl_xor_sync(0xffffffffu, imn, o), d2 = __shfl_xor_sync(0xffffffffu, imx, o);
+        mn = a2 < mn ? a2 : mn; mx = b2 > mx ? b2 : mx; imn = c2 < imn ? c2 : imn; imx = d2 > imx ? d2 : imx;
+    }
+    if ((threadIdx.x & 31) == 0 && mn <= mx) {
+        atomicMin(&a.lru->minl, mn); atomicMax(&a.lru->maxl, mx);
+        atomicMin(&a.lru->idmin, imn); atomicMax(&a.lru->idmax, imx);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lru_hist(InsArgs a, int p) {
+    __shared__ unsigned s_h[kLruBins];
+    LruGeom g;
+    if (!g.load(a.lru)) { if (p == 0 && blockIdx.x == 0 && threadIdx.x == 0) a.lru->valid = 0; return; }
+    if (p >= g.digits) return;
+    unsigned long long prefix; int all;
+    lru_select(a, g, p, prefix, all);
+    if (all) return;
+    const int hi = g.hi(p), lo = g.lo(p);
+    const unsigned long long bmask = (1ULL << (hi - lo)) - 1;
+    for (int b = threadIdx.x; b < kLruBins; b += blockDim.x) s_h[b] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int s0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; s0 < a.nslots; s0 += gridDim.x * blockDim.x) {
+        const int sl = s0 + lane;                              // warp-uniform trip count
+        int bin = -1;
+        if (sl < a.nslots) {
+            const unsigned long long k = a.lru_key[sl];
+            if (k != ~0ULL) {
+                const unsigned long long ck = g.ckey(k, a.slot_id[sl]);
+                if ((ck >> hi) == prefix) bin = (int)((ck >> lo) & bmask);
+            }
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_h[bin], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b <= (int)bmask; b += blockDim.x)
+        if (s_h[b]) atomicAdd(&a.lru_hist[p * kLruBins + b], s_h[b]);
+}
+
+__global__ void __launch_bounds__(256) k_lru_collect(InsArgs a) {
+    LruGeom g;
+    if (!g.load(a.lru)) return;
+    unsigned long long T; int all;
+    lru_select(a, g, g.digits, T, all);
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.lru->all = all;
+    const int lane = threadIdx.x & 31;
+    for (int s0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; s0 < a.nslots; s0 += gridDim.x * blockDim.x) {
+        const int sl = s0 + lane;
+        bool take = false;
+        unsigned long long ck = 0;
+        if (sl < a.nslots) {
+            const unsigned long long k = a.lru_key[sl];
+            if (k != ~0ULL) { ck = g.ckey(k, a.slot_id[sl]); take = all || ck <= T; }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        int p0 = 0;
+        if (lane == 0 && bal) p0 = atomicAdd(&a.lru->count, __popc(bal));
+        p0 = __shfl_sync(0xffffffffu, p0, 0);
+        if (take) {
+            const int pos = p0 + __popc(bal & ((1u << lane) - 1));
+            if (pos < kLruK) a.lru_list[pos] = (ck << 32) | (unsigned)sl;
+        }
+    }
+}
+
+// rank by count: element e's position = the number of listed keys below it (keys are unique); a CTA
+// compares 256 elements against one quarter of the list
+__global__ void __launch_bounds__(256) k_lru_rank(InsArgs a) {
+    __shared__ unsigned long long s_k[kLruK / 4];
+    if (!a.lru->valid) return;
+    const int n = min(a.lru->count, kLruK);
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c0 = blockIdx.y * (kLruK / 4), c1 = min(n, c0 + kLruK / 4);
+    if (blockIdx.x * blockDim.x >= n || c0 >= n) return;
+    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) s_k[i - c0] = a.lru_list[i];
+    __syncthreads();
+    if (e >= n) return;
+    const unsigned long long k = a.lru_list[e];
+    unsigned cnt = 0;
+    for (int i = 0; i < c1 - c0; ++i) cnt += s_k[i] < k;
+    atomicAdd(&a.lru_rank[e], cnt);
+}
+
+__global__ void __launch_bounds__(256) k_lru_scatter(InsArgs a) {
+    if (!a.lru->valid) return;
+    const int n = min(a.lru->count, kLruK);
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) a.lru_sorted[a.lru_rank[e]] = a.lru_list[e];
+}
+
 __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     const unsigned long long tnow = a.clock ? *a.clock : a.t;   // device clock (CUDA-graph replays advance it)
     extern __shared__ __align__(16) unsigned char smc[];
@@ -770,7 +976,25 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         if ((tid & 31) == 0 && pend) atomicAdd((unsigned long long*)&s_pending, (unsigned long long)pend);
     }
     __syncthreads();
-    if (a.candK > 0 && s_live_tokens + s_pending > a.capacity) {
+    // the list the prepare built (k_lru_*), if it is usable: no pin since its snapshot, a monotone clock
+    const bool prepared = a.candK > 0 && a.lru->valid && a.lru->pin_epoch == a.hdr->pin_epoch && tnow >= a.lru->maxl;
+    if (prepared && s_live_tokens + s_pending > a.capacity) {
+        const unsigned long long minl = a.lru->minl;
+        const unsigned idmin = a.lru->idmin;
+        const int idb = 32 - __clz((int)(a.lru->idmax - idmin) | 1);
+        const unsigned long long idmask = (1ULL << idb) - 1;
+        const int cn = min(a.lru->count, a.candK);
+        for (int p = tid; p < a.candK; p += blockDim.x) {
+            if (p < cn) {
+                const unsigned long long sk = a.lru_sorted[p], ck = sk >> 32;
+                const int sl = (int)(sk & 0xffffffffu);
+                ckey[p] = ((ck >> idb) << 32) | ((ck & idmask) + idmin);   // (last - minl) << 32 | id
+                cslot[p] = sl; clen[p] = a.slot_len[sl];
+            } else { ckey[p] = ~0ULL; cslot[p] = -1; clen[p] = 0; }
+        }
+        if (tid == 0) { s_minl = minl; s_maxl = a.lru->maxl; s_cn = cn; s_heap = 1; }
+        __syncthreads();
+    } else if (a.candK > 0 && s_live_tokens + s_pending > a.capacity) {
         // one pass: ranges of last_used and id over the evictable (live, unpinned) entries
         unsigned long long mn = ~0ULL, mx = 0;
         unsigned idmn = 0xffffffffu, idmx = 0;
@@ -1018,7 +1242,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             if ((k >> 32) + s_minl >= tnow) return -1;             // t-group: ordered by id with refreshed/new ones
             len = clen[s_cp];
             ++s_cp;
-            if ((sflag[sl] & 1) && !(sflag[sl] & 6)) return sl;    // live, not stored or refreshed in this call
+            // live, not stored or refreshed in this call, last_used still the listed one (a prepared list
+            // predates this step's match touches)
+            if ((sflag[sl] & 1) && !(sflag[sl] & 6) && a.slot_last[sl] == (k >> 32) + s_minl) return sl;
         }
         return -1;
     };
@@ -1112,7 +1338,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
             // kept = live old entries not refreshed / superseded in this call (the pop test of the loop)
             for (int q = tid; q < cn; q += blockDim.x) {
                 const int sl = cslot[q];
-                a.f_vfc[q] = (sl >= 0 && (sflag[sl] & 1) && !(sflag[sl] & 4) && a.f_evpos[sl] == INT_MAX) ? 1 : 0;
+                a.f_vfc[q] = (sl >= 0 && (sflag[sl] & 1) && !(sflag[sl] & 4) && a.f_evpos[sl] == INT_MAX &&
+                              a.slot_last[sl] == (ckey[q] >> 32) + s_minl) ? 1 : 0;
             }
             __syncthreads();
             for (int q = tid; q < cn; q += blockDim.x) a.f_vlen[q] = a.f_vfc[q];      // keep flags
@@ -1155,7 +1382,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
                 while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.f_vk[mid] > fc) hi = mid; else lo = mid + 1; }
                 const int jk = a.f_sj[lo], sl = cslot[q];
                 if (a.f_vlen[q]) { if (a.f_maxpos[sl] > jk) { s_fast = 0; atomicOr(&s_why, 128); } }
-                else if ((sflag[sl] & 1) && !(sflag[sl] & 4) && !(a.f_evpos[sl] < jk)) { s_fast = 0; atomicOr(&s_why, 256); }
+                else if ((sflag[sl] & 1) && !(sflag[sl] & 4) && a.slot_last[sl] == (ckey[q] >> 32) + s_minl &&
+                         !(a.f_evpos[sl] < jk)) { s_fast = 0; atomicOr(&s_why, 256); }
             }
         } else if (s_fast) {
             for (int k = tid; k < ns; k += blockDim.x) a.f_vk[k] = 0;
@@ -1611,6 +1839,7 @@ __global__ void k_pin_apply(DevHeader* hdr, const int32_t* pages, int64_t n, con
 __global__ void k_pin_done(DevHeader* hdr) {
     if (hdr->pin_neg && !cp_err_set(hdr)) cp_raise(hdr, CP_ERR_INVALID_ARG);   // after the undo
     hdr->pin_neg = 0;
+    hdr->pin_epoch += 1;
 }
 
 // SHA-256 digests of the published entries (thread per entry; launched on the index's side stream,
@@ -1910,6 +2139,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->fscr = s + L.scr_off[31];
     x->hit_coff = (int32_t*)(s + L.scr_off[32]);
     x->unc_list = (int64_t*)(s + L.scr_off[33]);
+    x->lru_scr = s + L.scr_off[34];
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -2178,6 +2408,15 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
     a.CH = x->CH; a.max_blocks = kv->max_blocks_per_req; a.clock = x->clock;
     if (a.max_blocks < 1) return CP_ERR_INVALID_ARG;
     a.out_tmp = x->out_tmp; a.eq_old = x->eq_old; a.dtab = x->dtab; a.span_rep = x->span_rep; a.precs = x->precs;
+    {
+        char* q = x->lru_scr;
+        a.lru = (LruHdr*)q; q += 64;
+        a.lru_key = (unsigned long long*)q; q += 8 * (size_t)x->S;
+        a.lru_hist = (unsigned*)q; q += 4 * 3 * (size_t)kLruBins;
+        a.lru_list = (unsigned long long*)q; q += 8 * (size_t)kLruK;
+        a.lru_rank = (unsigned*)q; q += 4 * (size_t)kLruK;
+        a.lru_sorted = (unsigned long long*)q;
+    }
     // shared memory of the commit: flags + per-span arrays, then the LRU candidate list (4096 halved to
     // fit), then as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)
     int candK = 4096;
@@ -2208,6 +2447,13 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, sms * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
+    // the commit's LRU candidate list (exits at once when this call cannot evict)
+    k_lru_init<<<1, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_lru_snap<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    for (int p = 0; p < 3; ++p) { k_lru_hist<<<sms, 256, 0, st>>>(a, p); CP_COUNT_LAUNCH(); }
+    k_lru_collect<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_lru_rank<<<dim3(kLruK / 256, 4), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_lru_scatter<<<kLruK / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
 

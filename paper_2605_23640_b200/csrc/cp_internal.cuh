@@ -61,7 +61,8 @@ struct DevHeader {                   // first 256 B of META
     int32_t n_unc;                   // gather: uncovered positions listed for CP_ZERO_UNCOVERED
     unsigned long long match_work[4];   // matcher work counters (cp_index_match_work)
     int32_t pin_neg;                 // cp_pin_links: a count went negative (undone)
-    int32_t pad[29];
+    uint32_t pin_epoch;              // cp_pin_links calls so far (a prepared LRU list is stale after one)
+    int32_t pad[28];
 };
 static_assert(sizeof(DevHeader) == 256, "DevHeader must be 256 B");
 
@@ -142,6 +143,7 @@ struct cp_index {
     HEntry* dtab;        // unique table keyed by full hash -> smallest span index (batch dedup)
     int32_t* span_rep;   // [MS] representative (smallest equal span) of each span
     char* fscr;          // parallel-apply scratch of the commit
+    char* lru_scr;       // LRU candidate list prepared by cp_index_insert_prepare (k_lru_*)
     Rec16* precs;        // [MS] bucket records of the batch prefix table
 };
 

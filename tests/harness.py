@@ -193,10 +193,14 @@ class Case:
         rep.stats["policy_spans"] = rep.stats.get("policy_spans", 0) + len(o_sr)
         return dataclasses.replace(wb, span_req=o_sr, span_begin=o_sb, span_len=o_sl), (d_sr, d_sb, d_sl)
 
-    def insert(self, wb: Batch, rep: ParityReport, bits_flags=None, sparse_kv=False, concurrent_readers=None):
+    def insert(self, wb: Batch, rep: ParityReport, bits_flags=None, sparse_kv=False, concurrent_readers=None,
+               between=None):
         """concurrent_readers: a reader batch matched (NO_TOUCH) and gathered on the main stream while
         the device insert's read-only half (cp_index_insert_prepare) runs on a side stream; the commit
-        follows both.  The oracle inserts sequentially (the NO_TOUCH match changes no state)."""
+        follows both.  The oracle inserts sequentially (the NO_TOUCH match changes no state).
+        between: a callable run after the device prepare and before the commit (it applies the same
+        operation to the device and the oracle, e.g. a touching match or a pin); the oracle's insert
+        follows it, so the device commit must decide as if the prepare had come after it."""
         torch = self.torch
         dev_spans = None
         if self.policy is not None:
@@ -214,7 +218,11 @@ class Case:
         dwords = torch.from_numpy(words.view(np.int32).copy() if len(words) else np.zeros(1, np.int32)).to(self.device)
         doffs = torch.from_numpy(offs.astype(np.int64)).to(self.device)
         dsp = dev_spans if dev_spans is not None else (sp(wb.span_req), sp(wb.span_begin), sp(wb.span_len))
-        if concurrent_readers is None:
+        if between is not None:
+            self.dev.insert(db, kv, *dsp, dwords, doffs, t, phase="prepare")
+            between()
+            ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t, phase="commit")
+        elif concurrent_readers is None:
             ids, oc = self.dev.insert(db, kv, *dsp, dwords, doffs, t)
         else:
             side, main = torch.cuda.Stream(), torch.cuda.current_stream()

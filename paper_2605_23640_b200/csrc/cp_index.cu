@@ -141,6 +141,7 @@ void compute_layout(const cp_config* c, Layout* L) {
     // 34 prepared LRU list (k_lru_*): header, per-slot key snapshot, 3 x 2048-bin histograms, list /
     // rank / sorted of kLruK candidates
     sput(64 + 8 * (size_t)S + 4 * 3 * kLruBins + 8 * kLruK + 4 * kLruK + 8 * kLruK + 64);
+    sput(4 * (size_t)(L->MS + 1));                                           // 35 rel_cur (relation CSR fill cursors)
     L->scr_size = o;
 }
 
@@ -217,6 +218,7 @@ struct InsArgs {
     int32_t candK;          // LRU candidate list size in the commit's shared memory (power of two, or 0)
     LruHdr* lru; unsigned long long* lru_key; unsigned* lru_hist; unsigned long long* lru_list;
     unsigned* lru_rank; unsigned long long* lru_sorted;
+    int32_t* rel_cur;       // relation CSR fill cursors (k_ins_rel_*)
     int32_t rec_cap;        // relation records cached in the commit's shared memory
 };
 
@@ -605,6 +607,53 @@ __device__ unsigned long long g_commit_prof[16];
 
 // One CTA applies the spans in input order (exact sequential semantics of R#20-22).
 // sflag bit 0: live; bit 1: stored by this call.
+// ---- relation CSR and the parallel apply's scratch, built by the grid at the end of the prepare: they
+//      depend only on the verified candidates, the span lengths and the lengths of live entries, none of
+//      which change before the commit (the one CTA of the commit used to build them: ~25 us per batch)
+__global__ void k_ins_rel_init(InsArgs a) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
+    for (int j = g; j <= a.S; j += ng) a.rel_off[j] = 0;
+    for (int j = g; j < a.S; j += ng) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
+    for (int i = g; i < a.nslots; i += ng) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
+}
+
+__global__ void k_ins_rel_count(InsArgs a) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
+    const int nc = (int)min((int64_t)a.hdr->n_cand, a.MAXC);     // more: the commit aborts (CP_ERR_CAPACITY)
+    for (int c = g; c < nc; c += ng) {
+        const Cand cd = a.cand[c];
+        if (!cd.ok) continue;
+        if (cd.needle < 0) atomicAdd(&a.rel_off[-1 - cd.needle], 1);
+        if (cd.hay < 0) atomicAdd(&a.rel_off[-1 - cd.hay], 1);
+    }
+    for (int j = g; j < a.S; j += ng) atomicMax(&a.f_last[a.span_rep[j]], j);   // a content's last span
+}
+
+__global__ void __launch_bounds__(1024) k_ins_rel_scan(InsArgs a) {
+    __shared__ int32_t s_w[1024 / 32 + 1];
+    block_excl_scan<1024>(a.rel_off, a.S + 1, s_w);             // rel_off[S] = the record count
+    for (int j = threadIdx.x; j <= a.S; j += blockDim.x) a.rel_cur[j] = a.rel_off[j];
+}
+
+__global__ void k_ins_rel_fill(InsArgs a) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
+    const int nc = (int)min((int64_t)a.hdr->n_cand, a.MAXC);
+    auto len_of = [&](int code) { return code < 0 ? a.span_len[-1 - code] : a.slot_len[code]; };
+    for (int c = g; c < nc; c += ng) {
+        const Cand cd = a.cand[c];
+        if (!cd.ok) continue;
+        const bool eq = len_of(cd.needle) == len_of(cd.hay);
+        if (cd.needle < 0) {       // the new span (needle) occurs inside hay
+            const int p = atomicAdd(&a.rel_cur[-1 - cd.needle], 1);
+            a.rel_rec[p] = make_int2(cd.hay, eq ? REL_EQ : REL_CONTAINER);
+        }
+        if (cd.hay < 0) {          // the new span (hay) contains needle
+            const int p = atomicAdd(&a.rel_cur[-1 - cd.hay], 1);
+            a.rel_rec[p] = make_int2(cd.needle, eq ? REL_EQ : REL_CONTAINED);
+        }
+    }
+}
+
 // ---- LRU candidate list, prepared beside match + gather (cp_index_insert_prepare, R#21) ----
 // The commit evicts in (last_used, id) order.  Instead of selecting the K smallest keys with one CTA
 // inside the commit (a radix select over the slot table and a K-element sort: ~135 us per evicting
@@ -857,35 +906,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         s_nremoved = 0;
     }
     __syncthreads();
-    // ---- relation CSR over new spans: (other, kind) records per span
-    const int nc = a.hdr->n_cand;
-    auto len_of = [&](int code) { return code < 0 ? slen[-1 - code] : a.slot_len[code]; };
-    for (int c = tid; c < nc; c += blockDim.x) {
-        const Cand cd = a.cand[c];
-        if (!cd.ok) continue;
-        if (cd.needle < 0) atomicAdd(&soff[-1 - cd.needle], 1);
-        if (cd.hay < 0) atomicAdd(&soff[-1 - cd.hay], 1);
-    }
-    __syncthreads();
-    const int nrec = block_excl_scan<kCommitThreads>(soff, a.S + 1, s_wsum);
-    for (int j = tid; j <= a.S; j += blockDim.x) a.rel_off[j] = soff[j];
-    __syncthreads();
-    for (int c = tid; c < nc; c += blockDim.x) {
-        const Cand cd = a.cand[c];
-        if (!cd.ok) continue;
-        const bool eq = len_of(cd.needle) == len_of(cd.hay);
-        if (cd.needle < 0) {       // the new span (needle) occurs inside hay
-            const int p = atomicAdd(&soff[-1 - cd.needle], 1);
-            a.rel_rec[p] = make_int2(cd.hay, eq ? REL_EQ : REL_CONTAINER);
-        }
-        if (cd.hay < 0) {          // the new span (hay) contains needle
-            const int p = atomicAdd(&soff[-1 - cd.hay], 1);
-            a.rel_rec[p] = make_int2(cd.needle, eq ? REL_EQ : REL_CONTAINED);
-        }
-    }
-    __syncthreads();
+    // ---- relation CSR over new spans: (other, kind) records per span, built by the prepare (k_ins_rel_*)
     for (int j = tid; j <= a.S; j += blockDim.x) soff[j] = a.rel_off[j];
-    if (tid == 0) s_nrec = nrec;
+    if (tid == 0) s_nrec = a.rel_off[a.S];
     __syncthreads();
     // ---- capacity checks before any mutation (an insert that fails changes nothing): the supersede
     //      list of one span (its CONTAINED records bound it) and the copy-in chunk list (stored spans
@@ -1264,10 +1287,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0;
         if (s_pinned_tok > 0) { s_fast = 0; s_why |= 1024; }      // pinned entries: the sequential rules (R#32)
     }
-    for (int i = tid; i < NSl; i += blockDim.x) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
-    for (int j = tid; j < Sn; j += blockDim.x) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
-    __syncthreads();
-    for (int j = tid; j < Sn; j += blockDim.x) atomicMax(&a.f_last[srep[j]], j);
+    // f_refs / f_evpos / f_maxpos / f_supby / f_sidx come initialised and f_last (each content's last
+    // span) filled from the prepare (k_ins_rel_init / k_ins_rel_count)
     __syncthreads();
     PROF_T(5);
     for (int r = tid; r < Sn; r += blockDim.x) {                 // decision of each content vs the initial pool
@@ -2140,6 +2161,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->hit_coff = (int32_t*)(s + L.scr_off[32]);
     x->unc_list = (int64_t*)(s + L.scr_off[33]);
     x->lru_scr = s + L.scr_off[34];
+    x->rel_cur = (int32_t*)(s + L.scr_off[35]);
     // power table B^k, k = 0..max_span_len (host, exact)
     std::vector<unsigned long long> pw((size_t)cfg->max_span_len + 1);
     pw[0] = 1;
@@ -2417,6 +2439,7 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
         a.lru_rank = (unsigned*)q; q += 4 * (size_t)kLruK;
         a.lru_sorted = (unsigned long long*)q;
     }
+    a.rel_cur = x->rel_cur;
     // shared memory of the commit: flags + per-span arrays, then the LRU candidate list (4096 halved to
     // fit), then as many relation records as the rest of the 180 KB holds (up to kCommitRecCap; beyond: global)
     int candK = 4096;
@@ -2447,6 +2470,11 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, sms * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
+    // the commit's relation CSR and parallel-apply scratch
+    k_ins_rel_init<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_rel_count<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_rel_scan<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_rel_fill<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     // the commit's LRU candidate list (exits at once when this call cannot evict)
     k_lru_init<<<1, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_lru_snap<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();

@@ -236,6 +236,13 @@ __global__ void k_ins_validate(InsArgs a) {
         a.hdr->n_cand0 = 0; a.hdr->n_need = 0;
     }
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.S; j += gridDim.x * blockDim.x) a.eq_old[j] = 0;
+    {   // the commit's relation-CSR counts and parallel-apply scratch (filled by k_ins_rep / k_ins_verify /
+        // k_ins_rel_fill below; the commit's one CTA used to build them)
+        const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
+        for (int j = g; j <= a.S; j += ng) a.rel_off[j] = 0;
+        for (int j = g; j < a.S; j += ng) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
+        for (int i = g; i < a.nslots; i += ng) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
+    }
     // clear the batch prefix table
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.BT; i += (int64_t)gridDim.x * blockDim.x) {
         a.btab[i].key = CP_EMPTY_KEY; a.btab[i].slot = 0; a.btab[i].len = 0; a.btab[i].full = 0;      // prefix buckets
@@ -323,6 +330,7 @@ __global__ void k_ins_rep(InsArgs a) {
         }
         if (lane == 0) {
             a.span_rep[s] = r;
+            atomicMax(&a.f_last[r], s);                   // the content's last span (parallel apply)
             if (r == s) {
                 HEntry* b = cp_find_or_insert(a.btab, (uint32_t)(a.BT - 1), a.logBT, a.span_pre[s]);
                 atomicAdd(&b->len, 1);
@@ -490,7 +498,13 @@ __global__ void k_ins_verify(InsArgs a, int from_phase1) {
             for (int u = 0; u < U; ++u) bad |= (x[u] != y[u]);
         }
         bad = __any_sync(0xffffffffu, bad);
-        if (lane == 0) a.cand[c].ok = !bad;
+        if (lane == 0) {
+            a.cand[c].ok = !bad;
+            if (!bad) {                               // relation-CSR counts per new span
+                if (cd.needle < 0) atomicAdd(&a.rel_off[-1 - cd.needle], 1);
+                if (cd.hay < 0) atomicAdd(&a.rel_off[-1 - cd.hay], 1);
+            }
+        }
     }
 }
 
@@ -607,39 +621,18 @@ __device__ unsigned long long g_commit_prof[16];
 
 // One CTA applies the spans in input order (exact sequential semantics of R#20-22).
 // sflag bit 0: live; bit 1: stored by this call.
-// ---- relation CSR and the parallel apply's scratch, built by the grid at the end of the prepare: they
-//      depend only on the verified candidates, the span lengths and the lengths of live entries, none of
-//      which change before the commit (the one CTA of the commit used to build them: ~25 us per batch)
-__global__ void k_ins_rel_init(InsArgs a) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
-    for (int j = g; j <= a.S; j += ng) a.rel_off[j] = 0;
-    for (int j = g; j < a.S; j += ng) { a.f_last[j] = -1; a.f_sidx[j] = 0; }
-    for (int i = g; i < a.nslots; i += ng) { a.f_refs[i] = 0; a.f_evpos[i] = INT_MAX; a.f_maxpos[i] = -1; a.f_supby[i] = -1; }
-}
-
-__global__ void k_ins_rel_count(InsArgs a) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
-    const int nc = (int)min((int64_t)a.hdr->n_cand, a.MAXC);     // more: the commit aborts (CP_ERR_CAPACITY)
-    for (int c = g; c < nc; c += ng) {
-        const Cand cd = a.cand[c];
-        if (!cd.ok) continue;
-        if (cd.needle < 0) atomicAdd(&a.rel_off[-1 - cd.needle], 1);
-        if (cd.hay < 0) atomicAdd(&a.rel_off[-1 - cd.hay], 1);
-    }
-    for (int j = g; j < a.S; j += ng) atomicMax(&a.f_last[a.span_rep[j]], j);   // a content's last span
-}
-
-__global__ void __launch_bounds__(1024) k_ins_rel_scan(InsArgs a) {
+// ---- relation CSR of the commit, finished at the end of the prepare: k_ins_verify counted the verified
+//      relations per new span; one CTA scans the counts and places the records (they depend only on the
+//      verified candidates and on lengths, none of which change before the commit)
+__global__ void __launch_bounds__(1024) k_ins_rel_fill(InsArgs a) {
     __shared__ int32_t s_w[1024 / 32 + 1];
+    if (cp_err_set(a.hdr) || a.hdr->first_err != CP_NO_ERR_KEY) return;   // the commit aborts
     block_excl_scan<1024>(a.rel_off, a.S + 1, s_w);             // rel_off[S] = the record count
     for (int j = threadIdx.x; j <= a.S; j += blockDim.x) a.rel_cur[j] = a.rel_off[j];
-}
-
-__global__ void k_ins_rel_fill(InsArgs a) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x, ng = gridDim.x * blockDim.x;
-    const int nc = (int)min((int64_t)a.hdr->n_cand, a.MAXC);
+    __syncthreads();
+    const int nc = (int)min((int64_t)a.hdr->n_cand, a.MAXC);     // more: the commit aborts (CP_ERR_CAPACITY)
     auto len_of = [&](int code) { return code < 0 ? a.span_len[-1 - code] : a.slot_len[code]; };
-    for (int c = g; c < nc; c += ng) {
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
         const Cand cd = a.cand[c];
         if (!cd.ok) continue;
         const bool eq = len_of(cd.needle) == len_of(cd.hay);
@@ -906,7 +899,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         s_nremoved = 0;
     }
     __syncthreads();
-    // ---- relation CSR over new spans: (other, kind) records per span, built by the prepare (k_ins_rel_*)
+    // ---- relation CSR over new spans: (other, kind) records per span, built by the prepare (counts in
+    //      k_ins_verify, offsets and records in k_ins_rel_fill)
     for (int j = tid; j <= a.S; j += blockDim.x) soff[j] = a.rel_off[j];
     if (tid == 0) s_nrec = a.rel_off[a.S];
     __syncthreads();
@@ -1287,8 +1281,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0;
         if (s_pinned_tok > 0) { s_fast = 0; s_why |= 1024; }      // pinned entries: the sequential rules (R#32)
     }
-    // f_refs / f_evpos / f_maxpos / f_supby / f_sidx come initialised and f_last (each content's last
-    // span) filled from the prepare (k_ins_rel_init / k_ins_rel_count)
+    // f_refs / f_evpos / f_maxpos / f_supby / f_sidx come initialised (k_ins_validate) and f_last (each
+    // content's last span) filled (k_ins_rep) by the prepare
     __syncthreads();
     PROF_T(5);
     for (int r = tid; r < Sn; r += blockDim.x) {                 // decision of each content vs the initial pool
@@ -2182,7 +2176,9 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->wk = new WorkKey();
     if (cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_pfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_pjoin, cudaEventDisableTiming) != cudaSuccess) {
         delete x->wk; delete x; return CP_ERR_CUDA;
     }
     *out = x;
@@ -2213,6 +2209,8 @@ cp_status cp_index_destroy(cp_index* x) {
         delete x->wk;
         if (x->ev_fork) cudaEventDestroy(x->ev_fork);
         if (x->ev_join) cudaEventDestroy(x->ev_join);
+        if (x->ev_pfork) cudaEventDestroy(x->ev_pfork);
+        if (x->ev_pjoin) cudaEventDestroy(x->ev_pjoin);
         if (x->side) cudaStreamDestroy(x->side);
     }
     delete x;
@@ -2456,6 +2454,21 @@ cp_status ins_args(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, int32
 cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     const int num_spans = a.S;
     cp_invalidate_worklist(x);
+    const int sms = cp_sm_count();
+    // The prepare runs beside the step's match; it must end before the gather starts, whose persistent
+    // grid holds every SM's registers until it ends (kernels queued behind it land on the critical path).
+    // First the work that needs only the index as the previous commit left it: the commit's LRU
+    // candidate list (it exits at once when this call cannot evict).  The LRU chain runs on the index's side stream, a branch beside the containment scans (it reads
+    // only index state no prepare kernel writes), joined before the prepare returns
+    if (cudaEventRecord(x->ev_pfork, st) != cudaSuccess || cudaStreamWaitEvent(x->side, x->ev_pfork, 0) != cudaSuccess)
+        return CP_ERR_CUDA;
+    k_lru_init<<<1, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    k_lru_snap<<<sms, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    for (int p = 0; p < 3; ++p) { k_lru_hist<<<sms, 256, 0, x->side>>>(a, p); CP_COUNT_LAUNCH(); }
+    k_lru_collect<<<sms, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    k_lru_rank<<<dim3(kLruK / 256, 4), 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    k_lru_scatter<<<kLruK / 256, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    if (cudaEventRecord(x->ev_pjoin, x->side) != cudaSuccess) return CP_ERR_CUDA;
     const int wblocks = std::max(1, std::min(1184, (num_spans + 7) / 8));
     k_ins_validate<<<std::max<int64_t>(wblocks, std::min<int64_t>(1184, (x->BT + 255) / 256)), kValThreads, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_hash<<<wblocks, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
@@ -2463,25 +2476,15 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     k_ins_bucket_offsets<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_bucket_fill<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     const size_t scan_smem = 8 * ((size_t)x->cfg.max_span_len + 1);
-    const int sms = cp_sm_count();
     k_ins_scan<<<(int)std::min<int64_t>(num_spans, sms * 6), kScanThreads, scan_smem, st>>>(a, 0); CP_COUNT_LAUNCH();
     k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 0); CP_COUNT_LAUNCH();
     k_ins_flag_eq<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_count_need<<<64, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_scan<<<(int)std::min<int64_t>(x->S, sms * 6), kScanThreads, scan_smem, st>>>(a, 1); CP_COUNT_LAUNCH();
     k_ins_verify<<<sms * 4, 256, 0, st>>>(a, 1); CP_COUNT_LAUNCH();
-    // the commit's relation CSR and parallel-apply scratch
-    k_ins_rel_init<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_rel_count<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_rel_scan<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_rel_fill<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    // the commit's LRU candidate list (exits at once when this call cannot evict)
-    k_lru_init<<<1, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_lru_snap<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    for (int p = 0; p < 3; ++p) { k_lru_hist<<<sms, 256, 0, st>>>(a, p); CP_COUNT_LAUNCH(); }
-    k_lru_collect<<<sms, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_lru_rank<<<dim3(kLruK / 256, 4), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
-    k_lru_scatter<<<kLruK / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    // the commit's relation CSR over the verified candidates
+    k_ins_rel_fill<<<1, 1024, 0, st>>>(a); CP_COUNT_LAUNCH();
+    if (cudaStreamWaitEvent(st, x->ev_pjoin, 0) != cudaSuccess) return CP_ERR_CUDA;   // the LRU branch
     return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ERR_CUDA;
 }
 

@@ -104,6 +104,7 @@ struct cp_index {
     const unsigned long long* clock = nullptr;         // cp_index_set_clock (device logical time)
     cudaStream_t side = nullptr;                       // the insert's SHA-256 digests run here, beside the copy-in
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // (owned by the base)
+    cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;  // the prepare's LRU branch on `side` (owned by the base)
     int32_t S;           // slots
     int64_t T;           // prefix-table entries (pow2)
     int32_t logT;

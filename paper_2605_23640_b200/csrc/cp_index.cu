@@ -1276,7 +1276,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     __shared__ int s_fast, s_ns;
     __shared__ long long s_s64[kCommitThreads / 32 + 1];
     __shared__ int s_why;                 // why the parallel apply was not taken (bit mask, diagnostics)
-    const int Sn = a.S, NSl = a.nslots;
+    const int Sn = a.S;
     if (tid == 0) {
         s_fast = a.force_serial ? 0 : 1; s_why = a.force_serial ? 1 : 0;
         if (s_pinned_tok > 0) { s_fast = 0; s_why |= 1024; }      // pinned entries: the sequential rules (R#32)
@@ -1317,7 +1317,15 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
         }
     }
     __syncthreads();
-    for (int i = tid; i < NSl; i += blockDim.x) if (a.f_supby[i] >= 0 && a.f_refs[i] > 1) { s_fast = 0; atomicOr(&s_why, 8); }
+    // a live segment superseded by one span and referenced by another (f_supby >= 0 marks exactly the live
+    // CONTAINED records of storing contents: walk those records, not the whole slot table)
+    for (int r = tid; r < Sn; r += blockDim.x) {
+        if (srep[r] != r || a.f_kind[r] != 2) continue;
+        for (int q = soff[r]; q < soff[r + 1]; ++q) {
+            const int2 rr = rec[q];
+            if (rr.y == REL_CONTAINED && rr.x >= 0 && (sflag[rr.x] & 1) && a.f_refs[rr.x] > 1) { s_fast = 0; atomicOr(&s_why, 8); }
+        }
+    }
     __syncthreads();
     PROF_T(6);
     if (s_fast) {

@@ -188,35 +188,60 @@ __global__ void __launch_bounds__(kNT) k_match(MatchArgs a) {
             }
             __syncthreads();
         } else {
-        // ---- 3. exact verification, one warp per candidate
+        // ---- 3. exact verification.  Few candidates (the usual case: the full-hash pre-check leaves the
+        //      true occurrences): work items are (candidate, 256-token chunk), dealt round-robin over the
+        //      warps, so one long segment no longer runs on one warp while the others idle; a chunk that
+        //      differs or covers a masked token marks its candidate (sign bit of clist).  Many candidates:
+        //      one warp per candidate, stopping at the first difference.  8 tokens per lane in flight (the
+        //      page-list and token-store loads of a step are issued before any compare).
         const int nc = s_nc;
-        for (int c = wid; c < nc; c += kNT / 32) {
-            const int k = clist[c];
-            const int slot = vslot[k];
-            const int m = __ldg(a.slot_len + slot);
-            const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
-            if (lane == 0) atomicAdd(&s_vtok, m);                 // work counter: tokens a verification may compare
-            // 8 tokens per lane in flight per step (the page-list and token-store loads of a step are
-            // issued before any compare): one round trip per 256 tokens instead of per 32
-            constexpr int U = 8;
+        constexpr int U = 8, CHK = 32 * U, NW = kNT / 32;
+        auto chunk_bad = [&](int k, const int32_t* pg, int m, int i0) -> int {
+            int32_t et[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + 32 * u + lane;
+                et[u] = i < m ? __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15)) : 0;
+            }
             int bad = 0;
-            for (int i0 = 0; i0 < m && !__any_sync(0xffffffffu, bad); i0 += 32 * U) {
-                int32_t et[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + 32 * u + lane;
-                    et[u] = i < m ? __ldg(a.page_tokens + (int64_t)__ldg(pg + (i >> 4)) * CP_BLOCK + (i & 15)) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + 32 * u + lane;
-                    if (i < m) {
-                        bad |= (et[u] != tok[k + i]);
-                        if (mk) bad |= mk[k + i];
-                    }
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + 32 * u + lane;
+                if (i < m) {
+                    bad |= (et[u] != tok[k + i]);
+                    if (mk) bad |= mk[k + i];
                 }
             }
-            if (__any_sync(0xffffffffu, bad) && lane == 0) vslot[k] = -1;
+            return __any_sync(0xffffffffu, bad);
+        };
+        if (nc <= 4 * NW) {
+            int gbase = 0;                                  // global index of candidate c's first chunk
+            for (int c = 0; c < nc; ++c) {
+                const int k = clist[c] & 0x7fffffff;
+                const int slot = vslot[k];
+                const int m = __ldg(a.slot_len + slot);
+                const int nch = (m + CHK - 1) / CHK;
+                const int first = gbase % NW;               // the warp of chunk 0
+                if (wid == first && lane == 0) atomicAdd(&s_vtok, m);   // work counter: tokens a verification may compare
+                const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+                for (int ch = (wid - first + NW) % NW; ch < nch; ch += NW)
+                    if (chunk_bad(k, pg, m, ch * CHK) && lane == 0) atomicOr(&clist[c], (int)0x80000000);
+                gbase += nch;
+            }
+            __syncthreads();
+            for (int c = tid; c < nc; c += kNT)
+                if (clist[c] < 0) vslot[clist[c] & 0x7fffffff] = -1;
+        } else {
+            for (int c = wid; c < nc; c += NW) {
+                const int k = clist[c];
+                const int slot = vslot[k];
+                const int m = __ldg(a.slot_len + slot);
+                const int32_t* pg = a.slot_pages + (int64_t)slot * a.MP;
+                if (lane == 0) atomicAdd(&s_vtok, m);             // work counter: tokens a verification may compare
+                int bad = 0;
+                for (int i0 = 0; i0 < m && !bad; i0 += CHK) bad = chunk_bad(k, pg, m, i0);
+                if (bad && lane == 0) vslot[k] = -1;
+            }
         }
         __syncthreads();
         MPROF(2);

@@ -74,6 +74,12 @@ def test_host_side_validation_without_gpu():
                                   None, None) == L.CP_ERR_UNSUPPORTED
     assert lib.cp_score_deviation(1, None, None, None, None, None, 5, 4, 0, 1, None, None, None, None,
                                   None) == L.CP_ERR_INVALID_ARG
+    # one-launch rectangles gather: no index, too many views, a views list missing -- before any device call
+    kv = (L.CpPagedKV * 2)()
+    assert lib.cp_gather_rerotate_rects(None, 0, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_gather_rerotate_rects(None, 4, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_gather_rerotate_rects(None, -1, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_gather_rerotate_rects(None, 1, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
     # KV deviation (NEXT-4): bad rho, a row that is not a whole number of 16-B vectors
     args = lambda rn, H, d: (1, None, None, None, None, None, None, 1, None, None, None, 1, H, d, L.CP_BF16, rn, 20,
                              16, None, None, None, None, None)

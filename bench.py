@@ -325,6 +325,16 @@ def copy_in_views(S):
         v.copy_in(S.ins_db, kv, reuse_worklist=True)
 
 
+def commit(S, ins):
+    """The insert's mutating half; with pool views, the commit whose copy-in fills every rectangle in one
+    launch (cp_index_insert_commit_rects) unless --rects-launch per."""
+    if S.views and S.rects_launch == "one":
+        S.idx.insert_commit_rects(S.views, S.ins_db, S.ins_kvs, *ins[2:], out=S.ins_out)
+    else:
+        S.idx.insert(*ins, out=S.ins_out, phase="commit")
+        copy_in_views(S)
+
+
 def run_step(S, torch, cp, world, events=None):
     """One pass of the hot path.  Scheduling (--overlap):
       3 (default): the insert's read-only half (cp_index_insert_prepare: validation, hashing, dedup,
@@ -390,8 +400,7 @@ def run_step(S, torch, cp, world, events=None):
             score()                                                                # N3 (+ C1), main stream
         main.wait_event(S.ev_prep_done)
         if ev: ev[3].record()
-        S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
-        copy_in_views(S)
+        commit(S, ins)                                                             # N4, mutating half
     elif S.overlap == 2:
         if scores:
             S.ev_gather_done.record()
@@ -402,8 +411,7 @@ def run_step(S, torch, cp, world, events=None):
         if scores:
             main.wait_event(S.ev_score_done)
         if ev: ev[3].record()
-        S.idx.insert(*ins, out=S.ins_out, phase="commit")                          # N4, mutating half
-        copy_in_views(S)
+        commit(S, ins)                                                             # N4, mutating half
     else:
         if scores:
             main.wait_event(S.ev_score_done)
@@ -787,9 +795,10 @@ def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000, re
         ev[3].record(main)
         main.wait_stream(side)
         ev[4].record(main)
-        ids, oc = idx.insert(db, kvs[0], *sp, bits, boff, t, phase="commit")
-        for v, kv in zip(views, kvs[1:]):
-            v.copy_in(db, kv, reuse_worklist=True)
+        if views:
+            ids, oc = idx.insert_commit_rects(views, db, kvs, *sp, bits, boff, t)
+        else:
+            ids, oc = idx.insert(db, kvs[0], *sp, bits, boff, t, phase="commit")
         ev[5].record(main)
         torch.cuda.nvtx.range_pop()
         host_ms = (time.perf_counter() - h0) * 1e3

@@ -204,6 +204,20 @@ cp_status cp_index_insert_commit(cp_index* idx, const cp_batch* writers_h, const
                                  int32_t* out_entry_id, int32_t* out_outcome, void* stream);
 
 /*
+ * cp_index_insert_commit whose copy-in also fills `num_views` (<= 3) pool views of idx, all in ONE launch
+ * of the copy kernel: writer_kv_h[0] is the writer KV in idx's geometry, writer_kv_h[1 + i] in
+ * views_h[i]'s (all on the SAME block_tables pointer and width).  Equivalent to the commit followed by
+ * cp_index_copy_in on every view (same rows, bit for bit).  Requirements as cp_gather_rerotate_rects
+ * (CP_ERR_INVALID_ARG with no side effects otherwise); the rest as cp_index_insert_commit.
+ */
+cp_status cp_index_insert_commit_rects(cp_index* idx, int32_t num_views, cp_index* const* views_h,
+                                       const cp_batch* writers_h, const cp_paged_kv* writer_kv_h,
+                                       int32_t num_spans, const int32_t* span_req, const int32_t* span_begin,
+                                       const int32_t* span_len, const uint32_t* recompute_bits,
+                                       const int64_t* bits_word_offsets, uint64_t logical_time,
+                                       int32_t* out_entry_id, int32_t* out_outcome, void* stream);
+
+/*
  * Same-user session reuse (NEXT-2; "If the request belongs to the same user session,
  * all KV cache can be reused without restriction.  If the request originates from a different user, it
  * applies the selective cross-user sharing policy"; R#33: exact-prefix reuse of

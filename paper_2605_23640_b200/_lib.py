@@ -72,6 +72,8 @@ EXPORTS = {
                                       vp, vp, vp]),
     "cp_index_insert_commit": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32, vp, vp, vp, vp, vp, u64,
                                      vp, vp, vp]),
+    "cp_index_insert_commit_rects": (i32, [vp, i32, C.POINTER(vp), C.POINTER(CpBatch), C.POINTER(CpPagedKV), i32,
+                                           vp, vp, vp, vp, vp, u64, vp, vp, vp]),
     "cp_match_spans": (i32, [vp, C.POINTER(CpBatch), u64, i32, C.POINTER(CpHits), vp]),
     "cp_gather_rerotate": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), C.POINTER(CpPagedKV), i32, vp]),
     "cp_gather_rerotate_rects": (i32, [vp, i32, C.POINTER(vp), C.POINTER(CpBatch), C.POINTER(CpHits),

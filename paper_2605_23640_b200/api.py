@@ -226,6 +226,28 @@ class KVIndex:
         L.check(rc, fn)
         return out_id[:S], out_oc[:S]
 
+    def insert_commit_rects(self, views: Sequence["KVIndexView"], writers: DeviceBatch, writer_kvs: Sequence[PagedKV],
+                            span_req, span_begin, span_len, recompute_bits=None, bits_word_offsets=None, t: int = 0,
+                            stream=None, out=None):
+        """cp_index_insert_commit_rects: the commit half of a split insert whose copy-in fills this index's
+        pool (writer_kvs[0]) and its views' (writer_kvs[1:], one per view, one block table) in one launch."""
+        S = int(span_req.numel())
+        if out is None:
+            out = (torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device),
+                   torch.full((max(S, 1),), -1, dtype=torch.int32, device=self.device))
+        if len(writer_kvs) != len(views) + 1:
+            raise ValueError("one writer cache per rectangle")
+        out_id, out_oc = out
+        vh = (C.c_void_p * max(1, len(views)))(*[v.h for v in views])
+        kvs = (L.CpPagedKV * len(writer_kvs))(*[k.c() for k in writer_kvs])
+        wb = writers.c()
+        rc = L.lib().cp_index_insert_commit_rects(self.h, len(views), vh, C.byref(wb), kvs, S, _ptr(span_req),
+                                                  _ptr(span_begin), _ptr(span_len), _ptr(recompute_bits),
+                                                  _ptr(bits_word_offsets), int(t), _ptr(out_id), _ptr(out_oc),
+                                                  _stream(stream))
+        L.check(rc, "cp_index_insert_commit_rects")
+        return out_id[:S], out_oc[:S]
+
     def insert_session(self, writers: DeviceBatch, writer_kv: PagedKV, t: int = 0, out=None, stream=None):
         """cp_index_insert_session (R#33): each request replaces its session's private entry.  `writers.session`
         (int32 [R], values 1..max_sessions) is required.  Returns (out_id, out_outcome) device tensors."""

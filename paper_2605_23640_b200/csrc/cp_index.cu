@@ -2497,7 +2497,8 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
 }
 
 // mutating phases: sequential apply, table updates, copy-in of the writer KV
-cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp_paged_kv* kv, cudaStream_t st) {
+cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp_paged_kv* kv, cudaStream_t st,
+                     int32_t nviews = 0, cp_index* const* views = nullptr, const cp_paged_kv* view_kvs = nullptr) {
     const int num_spans = a.S;
     cp_invalidate_worklist(x);
     const size_t csm = CommitSmem(x->S, num_spans, a.candK, a.rec_cap).total;
@@ -2517,7 +2518,7 @@ cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp
     if (cudaGetLastError() != cudaSuccess) return CP_ERR_CUDA;
     // copy the writer KV rows of the published entries into their pool pages
     const cp_status cs = cp_launch_rows(x, 1, &x->hdr->n_copy, x->cp_req, x->cp_slot, x->cp_dst, x->cp_len, nullptr,
-                                        x->MS, wb->offsets, nullptr, kv, 0, st);
+                                        x->MS, wb->offsets, nullptr, kv, 0, st, nviews, views, view_kvs);
     if (cudaStreamWaitEvent(st, x->ev_join, 0) != cudaSuccess) return CP_ERR_CUDA;   // digests done
     return cs;
 }
@@ -2564,6 +2565,31 @@ cp_status cp_index_insert_commit(cp_index* x, const cp_batch* wb, const cp_paged
     return ins_commit(x, a, wb, kv, (cudaStream_t)stream);
 }
 
+
+cp_status cp_index_insert_commit_rects(cp_index* x, int32_t num_views, cp_index* const* views, const cp_batch* wb,
+                                       const cp_paged_kv* kvs, int32_t num_spans, const int32_t* span_req,
+                                       const int32_t* span_begin, const int32_t* span_len, const uint32_t* bits,
+                                       const int64_t* bits_off, uint64_t t, int32_t* out_id, int32_t* out_oc,
+                                       void* stream) {
+    if (!kvs || num_views < 0 || num_views > 3 || (num_views > 0 && !views)) return CP_ERR_INVALID_ARG;
+    int layers = x ? x->cfg.num_layers : 0;
+    for (int i = 0; i < num_views; ++i) {      // checked before any state changes (cp_launch_rows re-checks)
+        const cp_index* v = views[i];
+        if (v) layers += v->cfg.num_layers;
+        if (layers > CP_MAX_LAYERS) return CP_ERR_INVALID_ARG;
+        const cp_paged_kv* vk = &kvs[1 + i];
+        if (!v || !v->is_view || !x || v->hdr != x->hdr || vk->block_tables != kvs[0].block_tables ||
+            vk->max_blocks_per_req != kvs[0].max_blocks_per_req || !vk->k_layers_h || !vk->v_layers_h)
+            return CP_ERR_INVALID_ARG;
+    }
+    InsArgs a;
+    const cp_status s = ins_args(x, wb, &kvs[0], num_spans, span_req, span_begin, span_len, bits, bits_off, t, out_id,
+                                 out_oc, a);
+    if (s != CP_OK || num_spans == 0) return s;
+    if (!x->insert_prepared) return CP_ERR_INVALID_ARG;          // commit without prepare
+    x->insert_prepared = 0;
+    return ins_commit(x, a, wb, &kvs[0], (cudaStream_t)stream, num_views, views, kvs + 1);
+}
 
 cp_status cp_index_insert_session(cp_index* x, const cp_batch* wb, const cp_paged_kv* kv, uint64_t t,
                                   int32_t* out_id, int32_t* out_oc, void* stream) {

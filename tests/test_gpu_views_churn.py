@@ -1,7 +1,8 @@
 """A balanced-layout rank (one index + pool views) under the config-5 churn shape: every
 batch is matched, gathered into every rectangle in ONE launch (cp_gather_rerotate_rects, placeholders
 for recompute-marked and unmatched rows) and then inserted under a small LRU budget (stores, evictions,
-copy-in into the base and every view).  Composition pin: after every batch the rank's hits equal a
+copy-in into the base and every view -- alternately by cp_index_insert_commit_rects in one launch and
+by cp_index_copy_in per view).  Composition pin: after every batch the rank's hits equal a
 one-index run's over the full geometry, and every rectangle's gathered K/V rows and pool rows are the
 slices of that run's, bit for bit."""
 import dataclasses
@@ -69,9 +70,16 @@ def test_balanced_rank_under_churn_equals_one_index(rank, world):
         db = full._dev_batch(wb)
         wkv = full.writer_kv(wb)
         ref.insert(db, wkv, *spans, dwords, doffs, t)
-        base.insert(db, _slice_kv(cp, wkv, r0.layer_lo, r0.layer_hi, r0.head_lo, r0.head_hi), *spans, dwords, doffs, t)
-        for v, r in zip(views, rects[1:]):
-            v.copy_in(db, _slice_kv(cp, wkv, r.layer_lo, r.layer_hi, r.head_lo, r.head_hi), reuse_worklist=True)
+        wkvs = [_slice_kv(cp, wkv, r.layer_lo, r.layer_hi, r.head_lo, r.head_hi) for r in rects]
+        for x in wkvs[1:]:
+            x.block_tables = wkvs[0].block_tables               # one block table object for the rects calls
+        if t % 4 == 0:                                          # commit + copy-in of every rectangle in one launch
+            base.insert(db, wkvs[0], *spans, dwords, doffs, t, phase="prepare")
+            base.insert_commit_rects(views, db, wkvs, *spans, dwords, doffs, t)
+        else:                                                   # insert, then each view's share of the copy-in
+            base.insert(db, wkvs[0], *spans, dwords, doffs, t)
+            for v, x in zip(views, wkvs[1:]):
+                v.copy_in(db, x, reuse_worklist=True)
         assert ref.last_error() == 0 and base.last_error() == 0
         fs, bs = ref.snapshot(with_tokens=False), base.snapshot(with_tokens=False)
         assert [(e["id"], e["pages"].tolist(), e["last_used"]) for e in fs["entries"]] == \

@@ -80,6 +80,10 @@ def test_host_side_validation_without_gpu():
     assert lib.cp_gather_rerotate_rects(None, 4, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
     assert lib.cp_gather_rerotate_rects(None, -1, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
     assert lib.cp_gather_rerotate_rects(None, 1, None, None, None, kv, 0, None) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_index_insert_commit_rects(None, 4, None, None, kv, 1, None, None, None, None, None, 1, None, None,
+                                            None) == L.CP_ERR_INVALID_ARG
+    assert lib.cp_index_insert_commit_rects(None, 0, None, None, None, 1, None, None, None, None, None, 1, None, None,
+                                            None) == L.CP_ERR_INVALID_ARG
     # KV deviation (NEXT-4): bad rho, a row that is not a whole number of 16-B vectors
     args = lambda rn, H, d: (1, None, None, None, None, None, None, 1, None, None, None, 1, H, d, L.CP_BF16, rn, 20,
                              16, None, None, None, None, None)

@@ -600,6 +600,9 @@ def bench_ours(args):
             del S.dst, S.dsts, S.ins_kvs, S.ins_kv, S.idx, S.views, S.attn
             torch.cuda.empty_cache()
             extras["config3"] = extra_config3(args, torch, cp, device)
+            extras["config4"] = {f"rank{r}": extra_config3(args, torch, cp, device, config=4, shard_world=8, shard_rank=r)
+                                 for r in (0, 7)}
+            extras["config4"]["projected_step_ms_n8"] = max(v["ms_per_step"] for v in extras["config4"].values())
             extras["config5"] = extra_config5_n8(torch, cp, device)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": K,
@@ -654,12 +657,14 @@ def bench_ours(args):
     return out
 
 
-def extra_config3(args, torch, cp, device, steps=5, warmup=3):
+def extra_config3(args, torch, cp, device, steps=5, warmup=3, config=3, shard_world=0, shard_rank=0):
     """BASELINE configs[2] on this GPU (multi-document RAG, passages reused at shifted positions: heavy
-    RoPE re-rotation), the same step and schedule as the headline, layer layout x1."""
+    RoPE re-rotation), the same step and schedule as the headline, layer layout x1.  config=4 with
+    shard_world=8: one rank of BASELINE configs[3] (Llama-3-70B KV, 8K prompts, 8-GPU layer layout)."""
     import copy
     a3 = copy.copy(args)
-    a3.config, a3.by, a3.link, a3.shard_world, a3.scale = 3, "layer", False, 0, 1.0
+    a3.config, a3.by, a3.link, a3.shard_world, a3.scale = config, "layer", False, shard_world, 1.0
+    a3.shard_rank = shard_rank
     S = setup_ours(a3, 0, 1, device)
     S.use_dist = False
     for _ in range(warmup):
@@ -681,15 +686,21 @@ def extra_config3(args, torch, cp, device, steps=5, warmup=3):
     moved = int(np.sum(h["hit_delta"] != 0))
     row = S.shard.num_layers * S.shard.num_heads * S.g.head_dim * (2 if S.g.dtype == "bf16" else 4)
     reused_b = (cov - rec) * 2 * row * 2
-    gather_b = reused_b + rec * 2 * row
-    out = {"workload": S.wl.name + " (BASELINE configs[2])", "requests": S.rb.num_reqs,
+    unc = S.rb.total_tokens - cov if S.placeholders == "both" else 0       # unmatched rows: zero placeholders
+    gather_b = reused_b + (rec + unc) * 2 * row
+    out = {"workload": S.wl.name + f" (BASELINE configs[{config - 1}])", "requests": S.rb.num_reqs,
            "request_tokens": S.rb.total_tokens, "steps": steps, "warmup": warmup, "ms_per_step": round(ms, 4),
            "value_GBps": round(reused_b / (ms * 1e-3) / 1e9, 1), "gather_GBps": round(gather_b / (ph[1] * 1e-3) / 1e9, 1),
            "gather_frac_of_peak": round(gather_b / (ph[1] * 1e-3) / 1e9 / peaks()[0], 4),
            "breakdown_ms": {"match": round(float(ph[0]), 4), "gather": round(float(ph[1]), 4),
                             "score_and_wait_prepare": round(float(ph[2]), 4), "insert_commit": round(float(ph[3]), 4)},
            "covered_tokens": cov, "hits": int(h["num_hits"]), "moved_hits": moved,
-           "matched_tokens_per_s": round(cov / (ms * 1e-3), 1)}
+           "matched_tokens_per_s": round(cov / (ms * 1e-3), 1),
+           "gather_bytes_rule": "reused rows read + written, zero placeholders (recompute-marked" +
+                                (" and unmatched" if unc else "") + ") written",
+           **({"shard": f"rank {shard_rank} of the {shard_world}-GPU layer layout: layers "
+                        f"[{S.shard.layer_lo}, {S.shard.layer_hi})" + (" (holds the final layer: runs N3)" if S.is_owner else "")}
+              if shard_world else {})}
     del S
     torch.cuda.empty_cache()
     return out

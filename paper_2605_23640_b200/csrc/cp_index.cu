@@ -994,7 +994,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     __syncthreads();
     // the list the prepare built (k_lru_*), if it is usable: no pin since its snapshot, a monotone clock
-    const bool prepared = a.candK > 0 && a.lru->valid && a.lru->pin_epoch == a.hdr->pin_epoch && tnow >= a.lru->maxl;
+    // (count <= candK: the list holds EVERY snapshot key up to its threshold -- a complete prefix of the
+    // LRU order, which is what makes its pops exact; a longer list would have been truncated)
+    const bool prepared = a.candK > 0 && a.lru->valid && a.lru->pin_epoch == a.hdr->pin_epoch && tnow >= a.lru->maxl &&
+                          a.lru->count <= a.candK;
     if (prepared && s_live_tokens + s_pending > a.capacity) {
         const unsigned long long minl = a.lru->minl;
         const unsigned idmin = a.lru->idmin;

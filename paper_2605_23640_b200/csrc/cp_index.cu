@@ -1690,6 +1690,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_ins_commit(InsArgs a) {
     }
     __syncthreads();
     for (int i = tid; i < a.nslots; i += blockDim.x) a.slot_state[i] = (sflag[i] & 1) ? CP_SLOT_LIVE : CP_SLOT_FREE;
+    // entry ids of the outcomes (the block's slot_id writes are visible after the barrier above; this was
+    // the separate k_ins_outids launch)
+    for (int j = tid; j < a.S; j += blockDim.x) { const int sx = a.out_tmp[j]; a.out_id[j] = sx >= 0 ? a.slot_id[sx] : -1; }
     __syncthreads();
     PROF_T(4);
 }
@@ -2505,8 +2508,7 @@ cp_status ins_commit(cp_index* x, const InsArgs& a, const cp_batch* wb, const cp
     const int num_spans = a.S;
     cp_invalidate_worklist(x);
     const size_t csm = CommitSmem(x->S, num_spans, a.candK, a.rec_cap).total;
-    k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();
-    k_ins_outids<<<(num_spans + 255) / 256, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
+    k_ins_commit<<<1, kCommitThreads, csm, st>>>(a); CP_COUNT_LAUNCH();   // writes out_id too
     k_ins_delete<<<128, 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     k_ins_publish<<<std::max(1, std::min(1184, (num_spans + 7) / 8)), 256, 0, st>>>(a); CP_COUNT_LAUNCH();
     // digests beside the rest of the commit (rebuild, copy-in): fork onto the side stream, join at the end

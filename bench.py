@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-3 and config-5 keys of the line")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of CUDA-graph replays")
+    ap.add_argument("--no-l2-persist", action="store_true",
+                    help="do not keep the index metadata L2-resident (cp_index_l2_persist) in the captured step")
     ap.add_argument("--rects-launch", choices=["one", "per"], default="one",
                     help="balanced layout: gather every rectangle of the rank in one launch (cp_gather_rerotate_rects) "
                          "or one launch per rectangle (views with CP_REUSE_WORKLIST)")
@@ -289,6 +291,7 @@ def setup_ours(args, rank, world, device):
     S.side = torch.cuda.Stream(device=device)
     S.overlap = int(getattr(args, "overlap", 3))
     S.rects_launch = getattr(args, "rects_launch", "one")
+    S.l2_persist = not getattr(args, "no_l2_persist", False)
     S.ev_score_done = torch.cuda.Event()
     S.ev_gather_done = torch.cuda.Event()
     S.ev_prep_done = torch.cuda.Event()
@@ -480,7 +483,11 @@ def bench_ours(args):
         run_step(S, torch, cp, world)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        cap = torch.cuda.Stream(device)
+        if S.l2_persist:                               # the metadata window rides into the captured kernels
+            S.idx.l2_persist(cap)
+            S.idx.l2_persist(S.side)
+        with torch.cuda.graph(g, stream=cap):
             run_step(S, torch, cp, world)
         S.graph = g
         torch.cuda.synchronize()
@@ -615,6 +622,7 @@ def bench_ours(args):
                        "parallelism": (f"one rank ({args.shard_rank}) of a {args.by}-sharded x{args.shard_world} layout"
                                        if args.shard_world and world == 1 else f"{args.by}-sharded x{world}"),
                        "placeholders": S.placeholders, "cuda_graph": S.graph is not None,
+                       "l2_persist_metadata": bool(S.l2_persist and S.graph is not None),
                        "build": cp._lib.lib().cp_build_info().decode(),
                        **({"rects_launch": S.rects_launch} if len(S.rects) > 1 else {}),
                        "shard_layers": L, "shard_heads": H, "shard_units": units,
@@ -748,6 +756,9 @@ def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000, re
     units = sum(r.num_layers * r.num_heads for r in rects)
     side = torch.cuda.Stream(device)
     main = torch.cuda.current_stream(device)
+    if os.environ.get("CP_L2_PERSIST", "1") != "0":     # the index metadata L2-resident beside the gather's stream
+        idx.l2_persist(main)
+        idx.l2_persist(side)
     rows = []
     row = units * 128 * 2                                # bytes of one token's K (or V) over the rank's units
     for bi, (wb, rb) in enumerate(wl.rounds):
@@ -834,6 +845,9 @@ def extra_config5(torch, cp, device, prefill=26, timed=6, capacity=1_500_000, re
                      "copy_in_bytes": stored_tok * 2 * row * 2, "covered": cov, "parallel_commit": bool(par_commit)})
         if owner:
             del attn
+    if os.environ.get("CP_L2_PERSIST", "1") != "0":
+        idx.l2_persist(main, 0.0)                        # clear the windows (the carve-out stays)
+        idx.l2_persist(side, 0.0)
     par, ser, why = idx.commit_stats()
     med = {k: round(float(np.median([r[k] for r in rows])), 4) for k in rows[0] if k.endswith("_ms") or k.endswith("GBps")}
     cin = float(np.mean([r["copy_in_bytes"] for r in rows]))

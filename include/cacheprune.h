@@ -474,6 +474,16 @@ cp_status cp_index_snapshot(cp_index* idx, cp_snapshot* out_h, void* stream);
  * pinned host scalar).  NULL restores the host argument. */
 cp_status cp_index_set_clock(cp_index* idx, const uint64_t* d_clock);
 
+/* L2 residency of the index metadata (B200: 126 MB L2 with a persisting carve-out).  Sets `stream`'s (and
+ * the index's internal side stream's) access-policy window to the index's META workspace with
+ * persisting hits (hit_ratio in [0, 1]; 0 clears the window) and raises the device's persisting-L2 limit
+ * to the window size (capped by the device maxima) if it is lower.  The gather streams ~100 GB per step
+ * through L2 with evict-first hints; without this the control-plane kernels (match, commit) find about
+ * half of the entry table in DRAM.  Kernels launched in the stream afterwards (and captured into a CUDA
+ * graph from it) carry the window.  Device-wide side effect: the persisting carve-out.  Returns
+ * CP_ERR_UNSUPPORTED where the device has no persisting L2. */
+cp_status cp_index_l2_persist(cp_index* idx, void* stream, float hit_ratio);
+
 /* Synchronizes, returns and clears the sticky device error word (CP_OK if none). */
 cp_status cp_index_last_error(cp_index* idx, void* stream);
 

@@ -85,6 +85,7 @@ EXPORTS = {
     "cp_link_blocks": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpHits), vp, i32, vp]),
     "cp_pin_links": (i32, [vp, vp, i64, i32, vp]),
     "cp_index_set_clock": (i32, [vp, vp]),
+    "cp_index_l2_persist": (i32, [vp, vp, C.c_float]),
     "cp_index_insert_session": (i32, [vp, C.POINTER(CpBatch), C.POINTER(CpPagedKV), u64, vp, vp, vp]),
     "cp_hash_prefix": (i32, [C.POINTER(CpBatch), u64, vp, vp]),
     "cp_policy_spans": (i32, [C.POINTER(CpBatch), i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),

@@ -285,6 +285,10 @@ class KVIndex:
         L.check(L.lib().cp_gather_rerotate(self.h, C.byref(rb), C.byref(hc), C.byref(kv), flags, _stream(stream)),
                 "cp_gather_rerotate")
 
+    def l2_persist(self, stream=None, hit_ratio: float = 1.0):
+        """cp_index_l2_persist: keep this index's metadata L2-resident for kernels launched in `stream`."""
+        L.check(L.lib().cp_index_l2_persist(self.h, _stream(stream), float(hit_ratio)), "cp_index_l2_persist")
+
     def gather_rerotate_rects(self, views: Sequence["KVIndexView"], readers: DeviceBatch, hits: Hits,
                               dst_kvs: Sequence[PagedKV], zero_recompute: bool = True, zero_uncovered: bool = False,
                               skip_linked: bool = False, skip_recompute: bool = False, stream=None):

@@ -2134,6 +2134,7 @@ cp_status cp_index_create(const cp_config* cfg, void* const* ws, void* stream, c
     x->elem = cfg->dtype == CP_FP32 ? 4 : 2;
     x->pool_k = (char*)ws[CP_WS_POOL_K]; x->pool_v = (char*)ws[CP_WS_POOL_V];
     x->meta = (char*)ws[CP_WS_META]; x->scratch = (char*)ws[CP_WS_SCRATCH];
+    x->meta_bytes = L.meta_size;
     char* m = x->meta;
     x->hdr = (DevHeader*)(m + L.meta_off[0]);
     x->slot_id = (int32_t*)(m + L.meta_off[1]); x->slot_len = (int32_t*)(m + L.meta_off[2]);
@@ -2232,6 +2233,31 @@ cp_status cp_index_destroy(cp_index* x) {
 }
 
 uint64_t cp_index_hash_base(const cp_index* x) { return x ? x->B : 0; }
+
+cp_status cp_index_l2_persist(cp_index* x, void* stream, float hit_ratio) {
+    if (!x || !(hit_ratio >= 0.0f && hit_ratio <= 1.0f)) return CP_ERR_INVALID_ARG;
+    int dev = 0;
+    CP_CUDA_CHECK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CP_CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0) return CP_ERR_UNSUPPORTED;
+    const size_t meta = x->meta_bytes;
+    const size_t win = std::min<size_t>(meta, (size_t)prop.accessPolicyMaxWindowSize);
+    const size_t carve = std::min<size_t>(win, (size_t)prop.persistingL2CacheMaxSize);
+    size_t cur = 0;
+    CP_CUDA_CHECK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (hit_ratio > 0.0f && cur < carve) CP_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+    cudaStreamAttrValue v;
+    std::memset(&v, 0, sizeof(v));
+    v.accessPolicyWindow.base_ptr = x->meta;
+    v.accessPolicyWindow.num_bytes = hit_ratio > 0.0f ? win : 0;
+    v.accessPolicyWindow.hitRatio = hit_ratio > 0.0f ? std::min(hit_ratio, (float)carve / (float)std::max<size_t>(win, 1)) : 0.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CP_CUDA_CHECK(cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    if (x->side) CP_CUDA_CHECK(cudaStreamSetAttribute(x->side, cudaStreamAttributeAccessPolicyWindow, &v));
+    return CP_OK;
+}
 
 cp_status cp_index_set_clock(cp_index* x, const uint64_t* d_clock) {
     if (!x || x->is_view) return CP_ERR_INVALID_ARG;

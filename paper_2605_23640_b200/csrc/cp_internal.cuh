@@ -145,6 +145,7 @@ struct cp_index {
     int32_t* span_rep;   // [MS] representative (smallest equal span) of each span
     char* fscr;          // parallel-apply scratch of the commit
     char* lru_scr;       // LRU candidate list prepared by cp_index_insert_prepare (k_lru_*)
+    size_t meta_bytes = 0;   // size of META (cp_index_l2_persist)
     int32_t* rel_cur;    // relation CSR fill cursors (k_ins_rel_*)
     Rec16* precs;        // [MS] bucket records of the batch prefix table
 };

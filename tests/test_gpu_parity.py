@@ -25,6 +25,21 @@ def test_toy_config1_all_rounds():
     assert res["moved_hits"] > 0 and res["covered"] > 0
 
 
+def test_l2_persist_window_changes_no_result():
+    """cp_index_l2_persist only sets a cache policy: the rounds with the metadata window on the stream give
+    the oracle's results; a hit ratio outside [0, 1] is refused; 0 clears the window."""
+    from paper_2605_23640_b200 import _lib as L
+    case = Case(make_workload(1))
+    st = torch.cuda.current_stream()
+    case.dev.l2_persist(st, 1.0)
+    with pytest.raises(L.CacheHitError):
+        case.dev.l2_persist(st, 1.5)
+    res = run_round_parity(case)
+    case.dev.l2_persist(st, 0.0)
+    _assert(res)
+    assert res["covered"] > 0
+
+
 def test_toy_gptj_and_no_reader_mask():
     wl = make_workload(1, seed=11)
     wl.geometry.rope_style = "gptj"

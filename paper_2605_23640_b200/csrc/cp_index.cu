@@ -709,24 +709,29 @@ __device__ void lru_select(const InsArgs& a, const LruGeom& g, int upto, unsigne
     }
 }
 
-__global__ void __launch_bounds__(256) k_lru_init(InsArgs a) {
+__global__ void __launch_bounds__(1024) k_lru_init(InsArgs a) {
     __shared__ unsigned long long s_sum;
+    __shared__ int s_valid;
     if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
     unsigned long long sum = 0;
     for (int j = threadIdx.x; j < a.S; j += blockDim.x) sum += (unsigned long long)max(0, a.span_len[j]);
-    atomicAdd(&s_sum, sum);
-    for (int i = threadIdx.x; i < 3 * kLruBins; i += blockDim.x) a.lru_hist[i] = 0;
-    for (int i = threadIdx.x; i < kLruK; i += blockDim.x) a.lru_rank[i] = 0;
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&s_sum, sum);
     __syncthreads();
     if (threadIdx.x == 0) {
         LruHdr* h = a.lru;
         h->minl = ~0ULL; h->maxl = 0; h->idmin = 0xffffffffu; h->idmax = 0; h->count = 0; h->all = 0;
         h->pin_epoch = a.hdr->pin_epoch;
         // only when this call may evict (the commit's own test is tighter: spans after its duplicates)
-        h->valid = (a.candK > 0 && a.candK <= kLruK && !cp_err_set(a.hdr) &&
-                    a.hdr->live_tokens + (long long)s_sum > a.capacity) ? 1 : 0;
+        s_valid = (a.candK > 0 && a.candK <= kLruK && !cp_err_set(a.hdr) &&
+                   a.hdr->live_tokens + (long long)s_sum > a.capacity) ? 1 : 0;
+        h->valid = s_valid;
     }
+    __syncthreads();
+    if (!s_valid) return;                      // steady state without eviction: nothing else to do
+    for (int i = threadIdx.x; i < 3 * kLruBins; i += blockDim.x) a.lru_hist[i] = 0;
+    for (int i = threadIdx.x; i < kLruK; i += blockDim.x) a.lru_rank[i] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_lru_snap(InsArgs a) {
@@ -2502,7 +2507,7 @@ cp_status ins_prepare(cp_index* x, const InsArgs& a, cudaStream_t st) {
     // only index state no prepare kernel writes), joined before the prepare returns
     if (cudaEventRecord(x->ev_pfork, st) != cudaSuccess || cudaStreamWaitEvent(x->side, x->ev_pfork, 0) != cudaSuccess)
         return CP_ERR_CUDA;
-    k_lru_init<<<1, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
+    k_lru_init<<<1, 1024, 0, x->side>>>(a); CP_COUNT_LAUNCH();
     k_lru_snap<<<sms, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
     for (int p = 0; p < 3; ++p) { k_lru_hist<<<sms, 256, 0, x->side>>>(a, p); CP_COUNT_LAUNCH(); }
     k_lru_collect<<<sms, 256, 0, x->side>>>(a); CP_COUNT_LAUNCH();
